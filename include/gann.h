@@ -1,0 +1,195 @@
+/* gann.h — C ABI of the B200-native Vamana batch build + batched beam search.
+ *
+ * This is the drop-in boundary for the hot path of the reference (graphann,
+ * arXiv 2305.04359). Every entry point takes plain pointers and sizes; no
+ * torch or CUDA types cross it. Each function cites the reference interface it
+ * replaces (paths relative to the reference's proj/ directory).
+ *
+ * Conventions
+ *   elem     GANN_U8 / GANN_I8 / GANN_F32         (graphann::ElemKind, include/graphann/core.hpp:23)
+ *   metric   GANN_L2 (squared) / GANN_IP (negated) (graphann::Metric, include/graphann/metric.hpp:13)
+ *   rule     GANN_SCALE_CANDIDATE / GANN_SCALE_SELECTED (graphann::PruneRule, include/graphann/prune.hpp:19)
+ *   graph    n rows of R uint32 ids; unused slots hold GANN_NONE and the
+ *            degree of a row is the length of its non-GANN_NONE prefix
+ *            (graphann::NeighborGraph, include/graphann/graph.hpp:16-59).
+ *   results  ids padded with GANN_NONE, distances with +inf.
+ *   errors   return GANN_OK (0); GANN_EINVAL (1) where the reference throws
+ *            std::invalid_argument; GANN_EIO (2) for io_error/format_error;
+ *            GANN_ECUDA (3) for a CUDA failure. gann_last_error() returns the
+ *            calling thread's message.
+ *   threads  calls on one gann_index are serialised by the caller (the index
+ *            owns one CUDA stream); different indexes may be used from
+ *            different host threads.
+ *   host vs device: functions without a _device suffix take HOST buffers and
+ *            are synchronous, like the reference's by-value returns. The
+ *            _device variants take device pointers and enqueue on `stream`
+ *            (NULL = the index's stream) without synchronising.
+ */
+#ifndef GANN_H
+#define GANN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GANN_NONE 0xFFFFFFFFu
+
+enum { GANN_U8 = 0, GANN_I8 = 1, GANN_F32 = 2 };
+enum { GANN_L2 = 0, GANN_IP = 1 };
+enum { GANN_SCALE_CANDIDATE = 0, GANN_SCALE_SELECTED = 1 };
+/* Visited filter of the search kernel. FAST: a bounded shared-memory hash
+ * with no false positives (ids, visit order and |V| are identical to the
+ * reference; dist_comps counts this kernel's own evaluations). REF: the
+ * reference's L*L-slot ApproxVisitedSet (include/graphann/search.hpp:24-38)
+ * held in global memory, so dist_comps matches the reference too. */
+enum { GANN_VISITED_FAST = 0, GANN_VISITED_REF = 1 };
+enum { GANN_OK = 0, GANN_EINVAL = 1, GANN_EIO = 2, GANN_ECUDA = 3 };
+
+typedef struct gann_index gann_index;
+
+const char* gann_last_error(void);
+/* Library/ABI version string, e.g. "gann 0.1 sm_100a". */
+const char* gann_version(void);
+
+/* ---- index lifetime -------------------------------------------------------
+ * Replaces graphann::VectorDataset (include/graphann/dataset.hpp:16) +
+ * NeighborGraph(n, cap) (include/graphann/graph.hpp:20): uploads the points
+ * into an HBM-resident, 16-byte-padded row layout and allocates an empty graph
+ * of capacity R. */
+int gann_index_create(const void* points, uint64_t n, uint32_t d, int elem, int metric,
+                      uint32_t R, int device, gann_index** out);
+/* Same, from points already resident on `device` (row-major, d*elem bytes). */
+int gann_index_create_device(const void* d_points, uint64_t n, uint32_t d, int elem,
+                             int metric, uint32_t R, int device, gann_index** out);
+void gann_index_free(gann_index* idx);
+int gann_index_info(const gann_index* idx, uint64_t* n, uint32_t* d, int* elem, int* metric,
+                    uint32_t* R, uint32_t* start);
+
+/* ---- build ----------------------------------------------------------------
+ * Replaces graphann::build_diskann(ds, metric, DiskannParams{R, L, alpha, rule,
+ * seed}, workers) (include/graphann/diskann.hpp:36-37, src/diskann.cpp:31-70).
+ * max_batch = 0 reproduces the reference's uncapped prefix-doubling schedule
+ * (src/builder_common.cpp:13-20); max_batch > 0 caps every batch at
+ * hi = min(2*lo, lo + max_batch, n). */
+int gann_build(gann_index* idx, uint32_t L, float alpha, int rule, uint64_t seed,
+               uint32_t max_batch);
+/* create + build in one call: the reference's build(points, R, L, alpha). */
+int gann_build_diskann(const void* points, uint64_t n, uint32_t d, int elem, int metric,
+                       uint32_t R, uint32_t L, float alpha, int rule, uint64_t seed,
+                       uint32_t max_batch, int device, gann_index** out);
+
+/* Graph transfer (NeighborGraph::out_neighbors/set_neighbors/start,
+ * include/graphann/graph.hpp:29-45; the ANNG payload of src/graph.cpp:96-178).
+ * import validates ids (< n, no self loops) like set_neighbors
+ * (src/graph.cpp:42-59). deg may be NULL on export. */
+int gann_import_graph(gann_index* idx, const uint32_t* adj, uint32_t start);
+int gann_export_graph(const gann_index* idx, uint32_t* adj, uint32_t* deg, uint32_t* start);
+
+/* ---- search ---------------------------------------------------------------
+ * Replaces graphann::beam_search(g, ds, metric, q, SearchParams{L, k_gate, eps},
+ * counter, start_override) (include/graphann/search.hpp:57-60,
+ * src/search.cpp:62-131) for a batch of nq queries. k_gate is the
+ * reference's SearchParams::k (expansion gate); k_gate = L is the plain
+ * Alg. 1 drain used by insert_point. Outputs the k_out best of the visited
+ * set (k_out <= L), |V| and dist_comps per query (both nullable), and
+ * optionally the visited sequence (vis_ids/vis_dists, vcap per query,
+ * nullable). start_override (nullable) gives one start per query. */
+int gann_search(gann_index* idx, const void* queries, uint32_t nq, uint32_t k_out, uint32_t L,
+                uint32_t k_gate, float eps, int visited_mode, const uint32_t* start_override,
+                uint32_t* ids, float* dists, uint32_t* n_visited, uint64_t* dist_comps,
+                uint32_t* vis_ids, float* vis_dists, uint32_t vcap);
+/* Device-pointer variant (queries row-major d*elem bytes on the device). */
+int gann_search_device(gann_index* idx, const void* d_queries, uint32_t nq, uint32_t k_out,
+                       uint32_t L, uint32_t k_gate, float eps, int visited_mode,
+                       uint32_t* d_ids, float* d_dists, uint32_t* d_n_visited,
+                       uint64_t* d_dist_comps, void* stream);
+/* Stage a query batch once (padded device layout) so repeated
+ * gann_search_staged calls time only the search kernel. */
+int gann_stage_queries(gann_index* idx, const void* d_queries, uint32_t nq);
+int gann_search_staged(gann_index* idx, uint32_t k_out, uint32_t L, uint32_t k_gate, float eps,
+                       uint32_t* d_ids, float* d_dists, void* stream);
+
+/* ---- the build's internals, individually (parity + reuse) ------------------
+ * alpha_prune: graphann::alpha_prune (include/graphann/prune.hpp:31-33,
+ * src/prune.cpp:8-44) over `count` candidate lists at once. List i has point
+ * p[i] and candidates cand_ids/cand_dists[offsets[i] .. offsets[i+1]). The
+ * kept ids of list i go to out[i*R ..] (GANN_NONE padded); n_out[i] = count. */
+int gann_alpha_prune(gann_index* idx, const uint32_t* p, const uint64_t* offsets,
+                     uint32_t count, const uint32_t* cand_ids, const float* cand_dists,
+                     float alpha, int rule, uint32_t* out, uint32_t* n_out);
+/* group_by_key: graphann::group_by_key (include/graphann/semisort.hpp:21-22,
+ * src/semisort.cpp:15-73) on the GPU. Equal keys are contiguous, input order is
+ * kept inside a group; group order is unspecified (as in the reference, where it
+ * is hash-bucket order). offsets has n_groups+1 entries. */
+int gann_group_by_key(const uint32_t* keys, const uint32_t* vals, uint64_t m, int device,
+                      uint32_t* out_keys, uint32_t* out_vals, uint64_t* offsets,
+                      uint64_t* n_groups);
+/* choose_start: graphann::choose_start (src/builder_common.cpp:58-97). */
+int gann_choose_start(gann_index* idx, uint32_t* start);
+/* insert_point over a batch: graphann::insert_point (src/diskann.cpp:12-29) for
+ * points ids[0..count) against the current graph (all read the same
+ * snapshot, as in one build batch). Writes each out-list into the graph and,
+ * if back != NULL, copies it to back[i*R ..] (the reverse-edge targets). */
+int gann_insert_batch(gann_index* idx, const uint32_t* ids, uint32_t count, uint32_t L,
+                      float alpha, int rule, uint32_t* back);
+/* apply_back_edges: graphann::apply_back_edges (src/builder_common.cpp:109-140). */
+int gann_apply_back_edges(gann_index* idx, const uint32_t* targets, const uint32_t* sources,
+                          uint64_t m, float alpha, int rule);
+
+/* Host helpers of the build schedule (no device work):
+ * shuffled_order — graphann::shuffled_order (src/builder_common.cpp:99-107),
+ *   the same libstdc++ std::mt19937_64 + std::shuffle draw;
+ * batch_ranges — graphann::batch_ranges (src/builder_common.cpp:13-20) with the
+ *   optional cap; returns the number of ranges (writes at most max_ranges). */
+void gann_shuffled_order(uint32_t n, uint64_t seed, uint32_t front, uint32_t* out);
+uint32_t gann_batch_ranges(uint64_t n, uint32_t max_batch, uint32_t* lo, uint32_t* hi,
+                           uint32_t max_ranges);
+/* The seed build_diskann derives for shuffled_order: mix64(seed, "insert"). */
+uint64_t gann_insert_seed(uint64_t seed);
+
+/* ---- next-row helpers --------------------------------------
+ * Exact top-k by (dist, id): graphann::compute_groundtruth (src/dataset.cpp:172-217). */
+int gann_groundtruth(gann_index* idx, const void* queries, uint32_t nq, uint32_t k,
+                     uint32_t* ids, float* dists);
+int gann_groundtruth_device(gann_index* idx, const void* d_queries, uint32_t nq, uint32_t k,
+                            uint32_t* d_ids, float* d_dists, void* stream);
+
+/* Seeded synthetic u8 Gaussian-mixture rows (BASELINE configs 0-2, 4) written
+ * straight into device memory: rows [row0, row0+n) of the stream `stream_seed`,
+ * cluster centres from `center_seed`. Pure function of its arguments. */
+int gann_generate_u8(void* d_out, uint64_t n, uint32_t d, uint32_t clusters, float sigma,
+                     float noise_frac, uint64_t center_seed, uint64_t stream_seed, uint64_t row0,
+                     int device);
+
+/* ---- counters (roofline) ----------------------------------------------------
+ * Totals accumulated by the kernels since the last reset. */
+typedef struct gann_stats {
+  uint64_t queries;         /* searches run (queries + build inserts) */
+  uint64_t expansions;      /* sum |V| */
+  uint64_t evaluations;     /* distance evaluations by the search kernel */
+  uint64_t filter_drops;    /* visited-filter inserts that did not fit */
+  uint64_t adj_entries;     /* sum over expanded v of deg(v) */
+  uint64_t prune_lists;     /* alpha_prune calls (insert + back-edge) */
+  uint64_t prune_candidates;/* sum of prune list lengths */
+  uint64_t prune_evals;     /* distances evaluated inside alpha_prune */
+  uint64_t back_pairs;      /* reverse pairs grouped */
+  uint64_t back_groups;     /* distinct targets */
+  uint64_t back_pruned;     /* targets re-pruned */
+  double build_ms[6];       /* start, search, prune, group, merge, reprune */
+} gann_stats;
+int gann_get_stats(const gann_index* idx, gann_stats* out);
+int gann_reset_stats(gann_index* idx);
+
+/* Device pointers of the resident index (points: padded rows of `stride`
+ * bytes; adj: n*R uint32). For in-process callers that move the index with
+ * NCCL; not needed for ordinary use. */
+int gann_index_device_ptrs(const gann_index* idx, void** points, uint64_t* stride,
+                           uint32_t** adj);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GANN_H */

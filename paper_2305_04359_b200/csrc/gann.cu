@@ -1,0 +1,1092 @@
+// gann.cu — host side of the C ABI (include/gann.h): HBM-resident index,
+// batch-build driver and search front end. Plain C++ + CUDA runtime; no torch.
+//
+// Build driver = graphann::build_diskann (src/diskann.cpp:31-70) re-planned
+// for one GPU: the start vertex is chosen on the device, the insertion order
+// is drawn on the host with the same libstdc++ std::mt19937_64 + std::shuffle
+// call as the reference (src/builder_common.cpp:99-107), and every prefix-
+// doubling batch runs as
+//   search  (one warp per inserted point, drained beam {L, L, 0})
+//   prune   (one CTA per point: alpha_prune of its visited list, written
+//            straight into its out-row — the point is unreachable until its
+//            back-edges land, src/diskann.cpp:56-59)
+//   group   (count / bump-offsets / scatter of the batch's reverse pairs)
+//   merge   (one CTA per target: restore pair order, append, dedupe; rows
+//            that overflow R are staged with fresh distances)
+//   reprune (alpha_prune of the staged rows)
+// on one stream, with one host read-back per phase-2 step for grid sizes.
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/gann.h"
+#include "common.cuh"
+#include "internal.h"
+
+using namespace gann;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Error {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw Error{code, msg}; }
+
+void cu(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(GANN_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return GANN_OK;
+  } catch (const Error& e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return GANN_ECUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return GANN_ECUDA;
+  }
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  void ensure(size_t bytes) {
+    if (bytes <= cap) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = std::max<size_t>(bytes, 256);
+    cu(cudaMalloc(&p, want), "cudaMalloc scratch");
+    cap = want;
+  }
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+size_t elem_bytes(int elem) { return elem == GANN_F32 ? 4 : 1; }
+
+uint32_t env_u32(const char* name, uint32_t dflt) {
+  const char* v = std::getenv(name);
+  return v && *v ? static_cast<uint32_t>(std::strtoul(v, nullptr, 10)) : dflt;
+}
+
+// Shared-memory visited table size of the fast search mode. Distinct
+// evaluations per query run ~500-2000 at L = 10..200 (SURVEY.md §A probe 1).
+uint32_t hash_log2_for(uint32_t L) {
+  const uint32_t forced = env_u32("GANN_HASH_LOG2", 0);
+  if (forced) return std::min<uint32_t>(std::max<uint32_t>(forced, 5), 15);
+  if (L <= 64) return 10;
+  if (L <= 256) return 11;
+  return 12;
+}
+
+}  // namespace
+
+struct gann_index {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  uint64_t n = 0;
+  uint32_t d = 0;
+  int elem = 0, metric = 0;
+  uint32_t R = 0;
+  uint32_t start = 0;
+  uint32_t row_bytes = 0;
+  uint64_t stride = 0;
+  Geometry geom{};
+  uint8_t* points = nullptr;
+  uint32_t* adj = nullptr;
+  uint32_t* tcount = nullptr;
+  uint32_t* tgroup = nullptr;
+  unsigned long long* stats = nullptr;  // kStCount
+  unsigned long long* counters = nullptr;  // kCntNum
+  uint32_t* flags = nullptr;  // [0] overflow, [1] too_long
+  double build_ms[6] = {0, 0, 0, 0, 0, 0};
+  uint64_t back_pairs = 0, back_groups = 0, back_pruned = 0;
+  // scratch
+  DevBuf q, qids, qdists, qnvis, qdc, qvids, qvd, qstart, table;
+  DevBuf order, vis_ids, vis_d, nvis;
+  DevBuf gtarget, gcnt, goff, gcursor, gsrc, poff, plen, pid, pdist, bigg, pls, plb;
+  DevBuf pt, ps, ok, ov, misc, gt;
+  uint32_t staged_nq = 0;
+};
+
+namespace {
+
+void set_device(const gann_index* idx) { cu(cudaSetDevice(idx->device), "cudaSetDevice"); }
+
+gann_index* new_index(uint64_t n, uint32_t d, int elem, int metric, uint32_t R, int device) {
+  if (elem < GANN_U8 || elem > GANN_F32) fail(GANN_EINVAL, "unknown element kind");
+  if (metric != GANN_L2 && metric != GANN_IP) fail(GANN_EINVAL, "unknown metric");
+  if (d == 0) fail(GANN_EINVAL, "dimension must be positive");
+  if (n > 0 && R == 0) fail(GANN_EINVAL, "graph capacity must be positive");
+  if (n >= 0xFFFFFFFFull) fail(GANN_EINVAL, "ids are uint32: n must be below 2^32-1");
+  if (R > 1024) fail(GANN_EINVAL, "degree bound above 1024 is not supported");
+  auto* idx = new gann_index();
+  try {
+    idx->device = device;
+    idx->n = n;
+    idx->d = d;
+    idx->elem = elem;
+    idx->metric = metric;
+    idx->R = R;
+    idx->row_bytes = static_cast<uint32_t>(d * elem_bytes(elem));
+    idx->stride = (uint64_t(idx->row_bytes) + 15) & ~uint64_t(15);
+    if (idx->stride > 2048) fail(GANN_EINVAL, "rows above 2048 bytes are not supported");
+    idx->geom = make_geometry(static_cast<uint32_t>(idx->stride / 16));
+    set_device(idx);
+    cu(cudaStreamCreateWithFlags(&idx->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    const uint64_t nn = std::max<uint64_t>(n, 1);
+    cu(cudaMalloc(&idx->points, nn * idx->stride), "cudaMalloc points");
+    cu(cudaMalloc(&idx->adj, nn * std::max<uint32_t>(R, 1) * 4), "cudaMalloc graph");
+    cu(cudaMalloc(&idx->tcount, nn * 4), "cudaMalloc tcount");
+    cu(cudaMalloc(&idx->tgroup, nn * 4), "cudaMalloc tgroup");
+    cu(cudaMalloc(&idx->stats, sizeof(unsigned long long) * kStCount), "cudaMalloc stats");
+    cu(cudaMalloc(&idx->counters, sizeof(unsigned long long) * kCntNum), "cudaMalloc counters");
+    cu(cudaMalloc(&idx->flags, 16), "cudaMalloc flags");
+    cu(cudaMemsetAsync(idx->points, 0, nn * idx->stride, idx->stream), "memset");
+    cu(cudaMemsetAsync(idx->adj, 0xFF, nn * std::max<uint32_t>(R, 1) * 4, idx->stream), "memset");
+    cu(cudaMemsetAsync(idx->tcount, 0, nn * 4, idx->stream), "memset");
+    cu(cudaMemsetAsync(idx->stats, 0, sizeof(unsigned long long) * kStCount, idx->stream), "memset");
+    cu(cudaMemsetAsync(idx->flags, 0, 16, idx->stream), "memset");
+  } catch (...) {
+    gann_index_free(idx);
+    throw;
+  }
+  return idx;
+}
+
+void sync(gann_index* idx) { cu(cudaStreamSynchronize(idx->stream), "stream sync"); }
+
+template <class T>
+T read_dev(gann_index* idx, const T* p) {
+  T v;
+  cu(cudaMemcpyAsync(&v, p, sizeof(T), cudaMemcpyDeviceToHost, idx->stream), "read back");
+  sync(idx);
+  return v;
+}
+
+// Stage nq rows (row_bytes each, host or device) into a padded device buffer.
+const uint8_t* stage_rows(gann_index* idx, DevBuf& buf, const void* src, uint32_t nq, bool device) {
+  buf.ensure(size_t(nq) * idx->stride);
+  if (nq == 0) return buf.as<uint8_t>();
+  if (idx->stride != idx->row_bytes)
+    cu(cudaMemsetAsync(buf.p, 0, size_t(nq) * idx->stride, idx->stream), "memset staging");
+  cu(cudaMemcpy2DAsync(buf.p, idx->stride, src, idx->row_bytes, idx->row_bytes, nq,
+                       device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, idx->stream),
+     "copy rows");
+  return buf.as<uint8_t>();
+}
+
+void validate_search(const gann_index* idx, uint32_t k_out, uint32_t L, uint32_t k_gate,
+                     float eps, int mode) {
+  // validate_search_args — src/search.cpp:32-48
+  if (L == 0 || k_gate == 0) fail(GANN_EINVAL, "beam and k must be positive");
+  if (k_gate > L)
+    fail(GANN_EINVAL, "k=" + std::to_string(k_gate) + " exceeds beam=" + std::to_string(L));
+  if (!(eps >= 0.0f && eps <= 0.25f)) fail(GANN_EINVAL, "epsilon must lie in [0, 0.25]");
+  if (k_out > k_gate) fail(GANN_EINVAL, "k_out must not exceed k (the expansion gate)");
+  if (mode != GANN_VISITED_FAST && mode != GANN_VISITED_REF) fail(GANN_EINVAL, "unknown visited mode");
+  if (idx->n > 0 && idx->start >= idx->n) fail(GANN_EINVAL, "start vertex out of range");
+}
+
+SearchArgs base_search_args(gann_index* idx, uint32_t L, uint32_t k_gate, uint32_t k_out, float eps,
+                            int mode) {
+  SearchArgs a{};
+  a.data = idx->points;
+  a.stride = idx->stride;
+  a.n = static_cast<uint32_t>(idx->n);
+  a.adj = idx->adj;
+  a.R = idx->R;
+  a.start = idx->start;
+  a.L = L;
+  a.k_gate = k_gate;
+  a.k_out = k_out;
+  a.eps = eps;
+  a.visited_mode = mode;
+  a.hash_log2 = hash_log2_for(L);
+  a.dim = idx->d;
+  a.row_bytes = idx->row_bytes;
+  a.overflow = idx->flags;
+  a.stats = idx->stats;
+  return a;
+}
+
+// Launch the search over nq queries, chunking in REF mode so the L*L tables
+// stay under ~1 GiB.
+void run_search(gann_index* idx, SearchArgs a, cudaStream_t s) {
+  if (a.visited_mode == GANN_VISITED_REF) {
+    const uint64_t per = uint64_t(a.L) * a.L * 4;
+    const uint32_t chunk = static_cast<uint32_t>(std::max<uint64_t>(1, (1ull << 30) / per));
+    idx->table.ensure(std::min<uint64_t>(chunk, std::max<uint32_t>(a.nq, 1)) * per);
+    const uint32_t nq = a.nq;
+    for (uint32_t q0 = 0; q0 < nq; q0 += chunk) {
+      SearchArgs c = a;
+      c.nq = std::min(chunk, nq - q0);
+      c.ref_table = idx->table.as<uint32_t>();
+      if (c.queries) c.queries += uint64_t(q0) * a.stride;
+      if (c.query_rows) c.query_rows += q0;
+      if (c.start_override) c.start_override += q0;
+      if (c.out_ids) c.out_ids += uint64_t(q0) * a.k_out, c.out_dists += uint64_t(q0) * a.k_out;
+      if (c.n_visited) c.n_visited += q0;
+      if (c.dist_comps) c.dist_comps += q0;
+      if (c.vis_ids) c.vis_ids += uint64_t(q0) * a.vcap, c.vis_dists += uint64_t(q0) * a.vcap;
+      cu(launch_search(c, idx->elem, idx->metric, idx->geom, s), "search kernel");
+    }
+    return;
+  }
+  cu(launch_search(a, idx->elem, idx->metric, idx->geom, s), "search kernel");
+}
+
+constexpr uint32_t kPruneSmallCap = 512;
+constexpr uint32_t kPruneBigCap = 16384;
+constexpr uint32_t kSmallGroupCap = 256;
+constexpr uint32_t kBigGroupCap = 32768;
+
+PruneArgs base_prune_args(gann_index* idx, float alpha, int rule) {
+  PruneArgs p{};
+  p.data = idx->points;
+  p.stride = idx->stride;
+  p.R = idx->R;
+  p.alpha = alpha;
+  p.rule = rule;
+  p.too_long = idx->flags + 1;
+  p.stats = idx->stats;
+  return p;
+}
+
+void check_prune_params(float alpha, int rule) {
+  if (!(alpha > 0.0f)) fail(GANN_EINVAL, "alpha must be positive");  // prune.cpp:12
+  if (rule != GANN_SCALE_CANDIDATE && rule != GANN_SCALE_SELECTED) fail(GANN_EINVAL, "unknown prune rule");
+}
+
+struct Timer {
+  cudaEvent_t a, b;
+  cudaStream_t s;
+  explicit Timer(cudaStream_t st) : s(st) {
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, s);
+  }
+  double stop() {
+    cudaEventRecord(b, s);
+    cudaEventSynchronize(b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return ms;
+  }
+};
+
+// Insert points order[lo..hi) (device ids) against the current graph:
+// search {L, L, 0} + alpha_prune of each visited list into its row.
+void insert_batch(gann_index* idx, const uint32_t* d_ids, uint32_t B, uint32_t L, float alpha,
+                  int rule, bool timed) {
+  if (B == 0) return;
+  const uint32_t vcap = std::max<uint32_t>(64, 3 * L);
+  idx->vis_ids.ensure(size_t(B) * vcap * 4);
+  idx->vis_d.ensure(size_t(B) * vcap * 4);
+  idx->nvis.ensure(size_t(B) * 4);
+  cu(cudaMemsetAsync(idx->flags, 0, 8, idx->stream), "memset flags");
+  SearchArgs a = base_search_args(idx, L, L, 0, 0.0f, GANN_VISITED_FAST);
+  a.query_rows = d_ids;
+  a.nq = B;
+  a.n_visited = idx->nvis.as<uint32_t>();
+  a.vis_ids = idx->vis_ids.as<uint32_t>();
+  a.vis_dists = idx->vis_d.as<float>();
+  a.vcap = vcap;
+  Timer ts(idx->stream);
+  run_search(idx, a, idx->stream);
+  if (timed) idx->build_ms[1] += ts.stop(); else ts.stop();
+  PruneArgs p = base_prune_args(idx, alpha, rule);
+  p.count = B;
+  p.points = d_ids;
+  p.fixed_stride = vcap;
+  p.lengths = idx->nvis.as<uint32_t>();
+  p.cand_ids = idx->vis_ids.as<uint32_t>();
+  p.cand_dists = idx->vis_d.as<float>();
+  p.out_adj = idx->adj;
+  p.mcap = vcap;
+  Timer tp(idx->stream);
+  cu(launch_prune(p, idx->elem, idx->metric, idx->geom, 32, idx->stream), "prune kernel");
+  if (timed) idx->build_ms[2] += tp.stop(); else tp.stop();
+  uint32_t fl[2];
+  cu(cudaMemcpyAsync(fl, idx->flags, 8, cudaMemcpyDeviceToHost, idx->stream), "read flags");
+  sync(idx);
+  if (fl[0] || fl[1])
+    fail(GANN_ECUDA, "visited list exceeded its capacity (" + std::to_string(vcap) + ") in " +
+                         std::to_string(fl[0]) + " insert searches");
+}
+
+// Phase 2: group reverse pairs by target and merge (apply_back_edges).
+// Batch form (bsrc != nullptr): the pairs are the out-rows of bsrc[0..B).
+void apply_back(gann_index* idx, const uint32_t* bsrc, uint32_t B, const uint32_t* ptarget,
+                const uint32_t* psource, uint64_t npairs, float alpha, int rule, bool timed,
+                uint32_t* out_keys = nullptr, uint32_t* out_vals = nullptr,
+                uint64_t* ngroups_out = nullptr, const uint32_t* key_of_target = nullptr) {
+  if (npairs == 0) {
+    if (ngroups_out) *ngroups_out = 0;
+    return;
+  }
+  if (npairs >= 0xFFFFFFFFull) fail(GANN_EINVAL, "too many reverse pairs in one batch");
+  const uint32_t R = idx->R;
+  BackEdgeArgs b{};
+  b.data = idx->points;
+  b.stride = idx->stride;
+  b.adj = idx->adj;
+  b.R = R;
+  b.bsrc = bsrc;
+  b.B = B;
+  b.ptarget = ptarget;
+  b.psource = psource;
+  b.npairs = npairs;
+  b.sources_distinct = bsrc != nullptr;
+  b.tcount = idx->tcount;
+  b.tgroup = idx->tgroup;
+  b.counters = idx->counters;
+  b.small_group_cap = kSmallGroupCap;
+  b.big_group_cap = kBigGroupCap;
+  b.prune_small_cap = kPruneSmallCap;
+  b.key_of_target = key_of_target;
+  cu(cudaMemsetAsync(idx->counters, 0, sizeof(unsigned long long) * kCntNum, idx->stream), "memset");
+  const uint64_t gmax = npairs;  // groups <= pairs
+  idx->gtarget.ensure(gmax * 4);
+  b.gtarget = idx->gtarget.as<uint32_t>();
+  Timer tg(idx->stream);
+  cu(backedge_count(b, idx->stream), "back-edge count");
+  const uint32_t ng = static_cast<uint32_t>(read_dev(idx, idx->counters + kCntGroups));
+  idx->gcnt.ensure(size_t(ng) * 4);
+  idx->goff.ensure(size_t(ng) * 8);
+  idx->gcursor.ensure(size_t(ng) * 4);
+  idx->gsrc.ensure(npairs * 4);
+  idx->poff.ensure(size_t(ng) * 8);
+  idx->plen.ensure(size_t(ng) * 4);
+  idx->bigg.ensure(size_t(ng) * 4);
+  idx->pls.ensure(size_t(ng) * 4);
+  idx->plb.ensure(size_t(ng) * 4);
+  const uint64_t ptotal = uint64_t(ng) * R + npairs;
+  idx->pid.ensure(ptotal * 4);
+  idx->pdist.ensure(ptotal * 4);
+  b.gcnt = idx->gcnt.as<uint32_t>();
+  b.goff = idx->goff.as<uint64_t>();
+  b.gcursor = idx->gcursor.as<uint32_t>();
+  b.gsrc = idx->gsrc.as<uint32_t>();
+  b.poff = idx->poff.as<uint64_t>();
+  b.plen = idx->plen.as<uint32_t>();
+  b.pid = idx->pid.as<uint32_t>();
+  b.pdist = idx->pdist.as<float>();
+  b.big_groups = idx->bigg.as<uint32_t>();
+  b.plist_small = idx->pls.as<uint32_t>();
+  b.plist_big = idx->plb.as<uint32_t>();
+  cu(backedge_offsets(b, ng, idx->stream), "back-edge offsets");
+  cu(backedge_scatter(b, idx->stream), "back-edge scatter");
+  unsigned long long cnt[kCntNum];
+  cu(cudaMemcpyAsync(cnt, idx->counters, sizeof(cnt), cudaMemcpyDeviceToHost, idx->stream), "read");
+  sync(idx);
+  const uint32_t nbig = static_cast<uint32_t>(cnt[kCntBig]);
+  if (cnt[kCntMaxGroup] > kBigGroupCap)
+    fail(GANN_ECUDA, "a back-edge group of " + std::to_string(cnt[kCntMaxGroup]) +
+                         " sources exceeds the device cap " + std::to_string(kBigGroupCap) +
+                         "; cap the batch size (max_batch)");
+  if (timed) idx->build_ms[3] += tg.stop(); else tg.stop();
+  if (out_keys) {  // group_by_key mode
+    cu(backedge_write_groups(b, ng, nbig, out_keys, out_vals, idx->stream), "group write");
+    sync(idx);
+    if (ngroups_out) *ngroups_out = ng;
+    return;
+  }
+  Timer tm(idx->stream);
+  cu(backedge_merge(b, ng, nbig, idx->elem, idx->metric, idx->geom, idx->stream), "back-edge merge");
+  cu(cudaMemcpyAsync(cnt, idx->counters, sizeof(cnt), cudaMemcpyDeviceToHost, idx->stream), "read");
+  sync(idx);
+  if (timed) idx->build_ms[4] += tm.stop(); else tm.stop();
+  if (cnt[kCntTooBig]) fail(GANN_ECUDA, "back-edge group exceeded the merge capacity");
+  const uint32_t nps = static_cast<uint32_t>(cnt[kCntPruneSmall]);
+  const uint32_t npb = static_cast<uint32_t>(cnt[kCntPruneBig]);
+  if (cnt[kCntMaxMerged] > kPruneBigCap)
+    fail(GANN_ECUDA, "a merged list of " + std::to_string(cnt[kCntMaxMerged]) +
+                         " candidates exceeds the device prune cap " + std::to_string(kPruneBigCap));
+  idx->back_pairs += npairs;
+  idx->back_groups += ng;
+  idx->back_pruned += nps + npb;
+  Timer tp(idx->stream);
+  PruneArgs p = base_prune_args(idx, alpha, rule);
+  p.points = b.gtarget;
+  p.begins = b.poff;
+  p.lengths = b.plen;
+  p.cand_ids = b.pid;
+  p.cand_dists = b.pdist;
+  p.out_adj = idx->adj;
+  if (nps) {
+    p.count = nps;
+    p.list_index = b.plist_small;
+    p.mcap = kPruneSmallCap;
+    cu(launch_prune(p, idx->elem, idx->metric, idx->geom, 32, idx->stream), "reprune small");
+  }
+  if (npb) {
+    p.count = npb;
+    p.list_index = b.plist_big;
+    p.mcap = kPruneBigCap;
+    cu(launch_prune(p, idx->elem, idx->metric, idx->geom, 256, idx->stream), "reprune big");
+  }
+  sync(idx);
+  if (timed) idx->build_ms[5] += tp.stop(); else tp.stop();
+}
+
+std::vector<std::pair<uint32_t, uint32_t>> batch_ranges(uint64_t n, uint32_t cap) {
+  // src/builder_common.cpp:13-20, + the optional cap hi = min(2 lo, lo + cap, n)
+  std::vector<std::pair<uint32_t, uint32_t>> r;
+  for (uint64_t lo = 1; lo < n;) {
+    uint64_t hi = std::min<uint64_t>(lo << 1, n);
+    if (cap) hi = std::min<uint64_t>(hi, lo + cap);
+    r.emplace_back(static_cast<uint32_t>(lo), static_cast<uint32_t>(hi));
+    lo = hi;
+  }
+  return r;
+}
+
+uint32_t choose_start_dev(gann_index* idx) {
+  if (idx->n == 0) fail(GANN_EINVAL, "cannot pick a start point of an empty dataset");
+  idx->misc.ensure(sizeof(double) * idx->d + sizeof(float) * idx->d + 16);
+  double* colsum = idx->misc.as<double>();
+  float* centroid = reinterpret_cast<float*>(colsum + idx->d);
+  unsigned long long* best = reinterpret_cast<unsigned long long*>(
+      (reinterpret_cast<uintptr_t>(centroid + idx->d) + 15) & ~uintptr_t(15));
+  idx->misc.ensure(reinterpret_cast<uint8_t*>(best + 1) - idx->misc.as<uint8_t>());
+  colsum = idx->misc.as<double>();
+  centroid = reinterpret_cast<float*>(colsum + idx->d);
+  best = reinterpret_cast<unsigned long long*>(
+      (reinterpret_cast<uintptr_t>(centroid + idx->d) + 15) & ~uintptr_t(15));
+  cu(launch_choose_start(idx->points, idx->stride, idx->n, idx->d, idx->elem, idx->metric, colsum,
+                         centroid, best, idx->stream),
+     "choose_start");
+  const unsigned long long k = read_dev(idx, best);
+  return static_cast<uint32_t>(k & 0xFFFFFFFFu);
+}
+
+// Brute force over padded query rows — compute_groundtruth (src/dataset.cpp:172-217).
+void run_groundtruth(gann_index* idx, const uint8_t* q, uint32_t nq, uint32_t k, uint32_t* d_ids,
+                     float* d_dists, cudaStream_t s) {
+  if (k == 0 || k > 16) fail(GANN_EINVAL, "groundtruth: k must lie in [1, 16]");
+  if (k > idx->n) fail(GANN_EINVAL, "groundtruth: k=" + std::to_string(k) + " exceeds n");
+  if (idx->stride > 256) fail(GANN_EINVAL, "groundtruth: rows above 256 bytes are not supported");
+  if (nq == 0) return;
+  const uint32_t splits = groundtruth_splits(idx->n, nq);
+  idx->gt.ensure(size_t(nq) * splits * 16 * 8);
+  cu(launch_groundtruth(idx->points, idx->stride, idx->n, q, nq, k, idx->elem, idx->metric,
+                        static_cast<uint32_t>(idx->stride / 16), idx->gt.as<unsigned long long>(),
+                        splits, d_ids, d_dists, s),
+     "groundtruth kernel");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* gann_last_error(void) { return g_err.c_str(); }
+const char* gann_version(void) { return "gann 0.1 sm_100a"; }
+
+int gann_index_create(const void* points, uint64_t n, uint32_t d, int elem, int metric, uint32_t R,
+                      int device, gann_index** out) {
+  return guarded([&] {
+    if (!out) fail(GANN_EINVAL, "out is NULL");
+    if (n && !points) fail(GANN_EINVAL, "points is NULL");
+    gann_index* idx = new_index(n, d, elem, metric, R, device);
+    try {
+      if (n) {
+        cu(cudaMemcpy2DAsync(idx->points, idx->stride, points, idx->row_bytes, idx->row_bytes, n,
+                             cudaMemcpyHostToDevice, idx->stream),
+           "upload points");
+      }
+      sync(idx);
+    } catch (...) {
+      gann_index_free(idx);
+      throw;
+    }
+    *out = idx;
+  });
+}
+
+int gann_index_create_device(const void* d_points, uint64_t n, uint32_t d, int elem, int metric,
+                             uint32_t R, int device, gann_index** out) {
+  return guarded([&] {
+    if (!out) fail(GANN_EINVAL, "out is NULL");
+    gann_index* idx = new_index(n, d, elem, metric, R, device);
+    try {
+      if (n) {
+        cu(cudaMemcpy2DAsync(idx->points, idx->stride, d_points, idx->row_bytes, idx->row_bytes, n,
+                             cudaMemcpyDeviceToDevice, idx->stream),
+           "copy points");
+      }
+      sync(idx);
+    } catch (...) {
+      gann_index_free(idx);
+      throw;
+    }
+    *out = idx;
+  });
+}
+
+void gann_index_free(gann_index* idx) {
+  if (!idx) return;
+  cudaSetDevice(idx->device);
+  if (idx->stream) cudaStreamSynchronize(idx->stream);
+  for (void* p : {static_cast<void*>(idx->points), static_cast<void*>(idx->adj),
+                  static_cast<void*>(idx->tcount), static_cast<void*>(idx->tgroup),
+                  static_cast<void*>(idx->stats), static_cast<void*>(idx->counters),
+                  static_cast<void*>(idx->flags)})
+    if (p) cudaFree(p);
+  for (DevBuf* b : {&idx->q, &idx->qids, &idx->qdists, &idx->qnvis, &idx->qdc, &idx->qvids,
+                    &idx->qvd, &idx->qstart, &idx->table, &idx->order, &idx->vis_ids, &idx->vis_d,
+                    &idx->nvis, &idx->gtarget, &idx->gcnt, &idx->goff, &idx->gcursor, &idx->gsrc,
+                    &idx->poff, &idx->plen, &idx->pid, &idx->pdist, &idx->bigg, &idx->pls,
+                    &idx->plb, &idx->pt, &idx->ps, &idx->ok, &idx->ov, &idx->misc, &idx->gt})
+    b->release();
+  if (idx->stream) cudaStreamDestroy(idx->stream);
+  delete idx;
+}
+
+int gann_index_info(const gann_index* idx, uint64_t* n, uint32_t* d, int* elem, int* metric,
+                    uint32_t* R, uint32_t* start) {
+  return guarded([&] {
+    if (!idx) fail(GANN_EINVAL, "index is NULL");
+    if (n) *n = idx->n;
+    if (d) *d = idx->d;
+    if (elem) *elem = idx->elem;
+    if (metric) *metric = idx->metric;
+    if (R) *R = idx->R;
+    if (start) *start = idx->start;
+  });
+}
+
+int gann_build(gann_index* idx, uint32_t L, float alpha, int rule, uint64_t seed, uint32_t max_batch) {
+  return guarded([&] {
+    if (!idx) fail(GANN_EINVAL, "index is NULL");
+    // src/diskann.cpp:33-42
+    if (idx->n == 0) fail(GANN_EINVAL, "cannot build over an empty dataset");
+    if (L == 0 || idx->R == 0) fail(GANN_EINVAL, "build beam and degree bound must be positive");
+    check_prune_params(alpha, rule);
+    if (L < idx->R)
+      std::fprintf(stderr, "warning: build beam %u below degree bound %u; lists will be thin\n", L,
+                   idx->R);
+    set_device(idx);
+    for (double& m : idx->build_ms) m = 0;
+    idx->back_pairs = idx->back_groups = idx->back_pruned = 0;
+    const uint64_t n = idx->n;
+    cu(cudaMemsetAsync(idx->adj, 0xFF, n * idx->R * 4, idx->stream), "clear graph");
+    cu(cudaMemsetAsync(idx->tcount, 0, n * 4, idx->stream), "clear counts");
+    Timer t0(idx->stream);
+    const uint32_t start = choose_start_dev(idx);
+    idx->start = start;
+    // shuffled_order — src/builder_common.cpp:99-107 (same libstdc++ calls)
+    std::vector<uint32_t> order(n);
+    gann_shuffled_order(static_cast<uint32_t>(n), mix64(seed, 0x696e73657274ULL), start, order.data());
+    idx->order.ensure(n * 4);
+    cu(cudaMemcpyAsync(idx->order.p, order.data(), n * 4, cudaMemcpyHostToDevice, idx->stream),
+       "upload order");
+    idx->build_ms[0] += t0.stop();
+    const uint32_t* d_order = idx->order.as<uint32_t>();
+    for (auto [lo, hi] : batch_ranges(n, max_batch)) {
+      const uint32_t B = hi - lo;
+      insert_batch(idx, d_order + lo, B, L, alpha, rule, true);
+      apply_back(idx, d_order + lo, B, nullptr, nullptr, uint64_t(B) * idx->R, alpha, rule, true);
+    }
+    sync(idx);
+  });
+}
+
+int gann_build_diskann(const void* points, uint64_t n, uint32_t d, int elem, int metric, uint32_t R,
+                       uint32_t L, float alpha, int rule, uint64_t seed, uint32_t max_batch,
+                       int device, gann_index** out) {
+  gann_index* idx = nullptr;
+  int rc = gann_index_create(points, n, d, elem, metric, R, device, &idx);
+  if (rc != GANN_OK) return rc;
+  rc = gann_build(idx, L, alpha, rule, seed, max_batch);
+  if (rc != GANN_OK) {
+    gann_index_free(idx);
+    return rc;
+  }
+  *out = idx;
+  return GANN_OK;
+}
+
+int gann_import_graph(gann_index* idx, const uint32_t* adj, uint32_t start) {
+  return guarded([&] {
+    if (!idx) fail(GANN_EINVAL, "index is NULL");
+    const uint64_t n = idx->n;
+    const uint32_t R = idx->R;
+    if (n && start >= n) fail(GANN_EINVAL, "start vertex out of range");
+    for (uint64_t v = 0; v < n; v++) {  // set_neighbors checks, src/graph.cpp:42-59
+      const uint32_t* r = adj + v * R;
+      bool ended = false;
+      for (uint32_t t = 0; t < R; t++) {
+        if (r[t] == GANN_NONE) {
+          ended = true;
+          continue;
+        }
+        if (ended) fail(GANN_EINVAL, "row " + std::to_string(v) + ": id after GANN_NONE padding");
+        if (r[t] >= n) fail(GANN_EINVAL, "neighbor id " + std::to_string(r[t]) + " out of range at vertex " + std::to_string(v));
+        if (r[t] == v) fail(GANN_EINVAL, "self loop at vertex " + std::to_string(v));
+      }
+    }
+    set_device(idx);
+    if (n) cu(cudaMemcpyAsync(idx->adj, adj, n * R * 4, cudaMemcpyHostToDevice, idx->stream), "upload graph");
+    idx->start = start;
+    sync(idx);
+  });
+}
+
+int gann_export_graph(const gann_index* cidx, uint32_t* adj, uint32_t* deg, uint32_t* start) {
+  return guarded([&] {
+    gann_index* idx = const_cast<gann_index*>(cidx);
+    if (!idx) fail(GANN_EINVAL, "index is NULL");
+    set_device(idx);
+    const uint64_t n = idx->n;
+    const uint32_t R = idx->R;
+    if (adj && n) {
+      cu(cudaMemcpyAsync(adj, idx->adj, n * R * 4, cudaMemcpyDeviceToHost, idx->stream), "download graph");
+      sync(idx);
+      if (deg)
+        for (uint64_t v = 0; v < n; v++) {
+          uint32_t k = 0;
+          while (k < R && adj[v * R + k] != GANN_NONE) k++;
+          deg[v] = k;
+        }
+    } else if (deg && n) {
+      std::vector<uint32_t> tmp(n * R);
+      cu(cudaMemcpyAsync(tmp.data(), idx->adj, n * R * 4, cudaMemcpyDeviceToHost, idx->stream), "download graph");
+      sync(idx);
+      for (uint64_t v = 0; v < n; v++) {
+        uint32_t k = 0;
+        while (k < R && tmp[v * R + k] != GANN_NONE) k++;
+        deg[v] = k;
+      }
+    }
+    if (start) *start = idx->start;
+  });
+}
+
+int gann_search(gann_index* idx, const void* queries, uint32_t nq, uint32_t k_out, uint32_t L,
+                uint32_t k_gate, float eps, int visited_mode, const uint32_t* start_override,
+                uint32_t* ids, float* dists, uint32_t* n_visited, uint64_t* dist_comps,
+                uint32_t* vis_ids, float* vis_dists, uint32_t vcap) {
+  return guarded([&] {
+    if (!idx) fail(GANN_EINVAL, "index is NULL");
+    validate_search(idx, k_out, L, k_gate, eps, visited_mode);
+    if (nq == 0) return;
+    if (!queries) fail(GANN_EINVAL, "queries is NULL");
+    set_device(idx);
+    if (idx->n == 0) {  // src/search.cpp:67 — empty graph, empty result
+      for (uint64_t i = 0; i < uint64_t(nq) * k_out; i++) {
+        if (ids) ids[i] = GANN_NONE;
+        if (dists) dists[i] = __builtin_inff();
+      }
+      for (uint32_t i = 0; i < nq; i++) {
+        if (n_visited) n_visited[i] = 0;
+        if (dist_comps) dist_comps[i] = 0;
+      }
+      return;
+    }
+    if (start_override)
+      for (uint32_t i = 0; i < nq; i++)
+        if (start_override[i] >= idx->n) fail(GANN_EINVAL, "start vertex out of range");
+    SearchArgs a = base_search_args(idx, L, k_gate, k_out, eps, visited_mode);
+    a.queries = stage_rows(idx, idx->q, queries, nq, false);
+    a.nq = nq;
+    if (start_override) {
+      idx->qstart.ensure(size_t(nq) * 4);
+      cu(cudaMemcpyAsync(idx->qstart.p, start_override, size_t(nq) * 4, cudaMemcpyHostToDevice, idx->stream), "upload starts");
+      a.start_override = idx->qstart.as<uint32_t>();
+    }
+    if (k_out) {
+      idx->qids.ensure(size_t(nq) * k_out * 4);
+      idx->qdists.ensure(size_t(nq) * k_out * 4);
+      a.out_ids = idx->qids.as<uint32_t>();
+      a.out_dists = idx->qdists.as<float>();
+    }
+    idx->qnvis.ensure(size_t(nq) * 4);
+    idx->qdc.ensure(size_t(nq) * 8);
+    a.n_visited = idx->qnvis.as<uint32_t>();
+    a.dist_comps = idx->qdc.as<uint64_t>();
+    if (vis_ids && vcap) {
+      idx->qvids.ensure(size_t(nq) * vcap * 4);
+      idx->qvd.ensure(size_t(nq) * vcap * 4);
+      cu(cudaMemsetAsync(idx->qvids.p, 0xFF, size_t(nq) * vcap * 4, idx->stream), "memset");
+      a.vis_ids = idx->qvids.as<uint32_t>();
+      a.vis_dists = idx->qvd.as<float>();
+      a.vcap = vcap;
+    }
+    run_search(idx, a, idx->stream);
+    auto d2h = [&](void* dst, const void* src, size_t bytes) {
+      if (dst) cu(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, idx->stream), "download results");
+    };
+    if (k_out) {
+      d2h(ids, a.out_ids, size_t(nq) * k_out * 4);
+      d2h(dists, a.out_dists, size_t(nq) * k_out * 4);
+    }
+    d2h(n_visited, a.n_visited, size_t(nq) * 4);
+    d2h(dist_comps, a.dist_comps, size_t(nq) * 8);
+    if (a.vis_ids) {
+      d2h(vis_ids, a.vis_ids, size_t(nq) * vcap * 4);
+      d2h(vis_dists, a.vis_dists, size_t(nq) * vcap * 4);
+    }
+    sync(idx);
+  });
+}
+
+int gann_search_device(gann_index* idx, const void* d_queries, uint32_t nq, uint32_t k_out,
+                       uint32_t L, uint32_t k_gate, float eps, int visited_mode, uint32_t* d_ids,
+                       float* d_dists, uint32_t* d_n_visited, uint64_t* d_dist_comps, void* stream) {
+  return guarded([&] {
+    if (!idx) fail(GANN_EINVAL, "index is NULL");
+    validate_search(idx, k_out, L, k_gate, eps, visited_mode);
+    if (nq == 0) return;
+    if (idx->n == 0) fail(GANN_EINVAL, "search over an empty index");
+    set_device(idx);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : idx->stream;
+    SearchArgs a = base_search_args(idx, L, k_gate, k_out, eps, visited_mode);
+    if (idx->stride == idx->row_bytes) {
+      a.queries = static_cast<const uint8_t*>(d_queries);
+    } else {
+      idx->q.ensure(size_t(nq) * idx->stride);
+      cu(cudaMemsetAsync(idx->q.p, 0, size_t(nq) * idx->stride, s), "memset");
+      cu(cudaMemcpy2DAsync(idx->q.p, idx->stride, d_queries, idx->row_bytes, idx->row_bytes, nq,
+                           cudaMemcpyDeviceToDevice, s), "stage queries");
+      a.queries = idx->q.as<uint8_t>();
+    }
+    a.nq = nq;
+    a.out_ids = k_out ? d_ids : nullptr;
+    a.out_dists = k_out ? d_dists : nullptr;
+    a.n_visited = d_n_visited;
+    a.dist_comps = d_dist_comps;
+    run_search(idx, a, s);
+  });
+}
+
+int gann_stage_queries(gann_index* idx, const void* d_queries, uint32_t nq) {
+  return guarded([&] {
+    if (!idx) fail(GANN_EINVAL, "index is NULL");
+    set_device(idx);
+    stage_rows(idx, idx->q, d_queries, nq, true);
+    idx->staged_nq = nq;
+    sync(idx);
+  });
+}
+
+int gann_search_staged(gann_index* idx, uint32_t k_out, uint32_t L, uint32_t k_gate, float eps,
+                       uint32_t* d_ids, float* d_dists, void* stream) {
+  return guarded([&] {
+    if (!idx) fail(GANN_EINVAL, "index is NULL");
+    validate_search(idx, k_out, L, k_gate, eps, GANN_VISITED_FAST);
+    if (idx->n == 0) fail(GANN_EINVAL, "search over an empty index");
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : idx->stream;
+    SearchArgs a = base_search_args(idx, L, k_gate, k_out, eps, GANN_VISITED_FAST);
+    a.queries = idx->q.as<uint8_t>();
+    a.nq = idx->staged_nq;
+    a.out_ids = d_ids;
+    a.out_dists = d_dists;
+    cu(launch_search(a, idx->elem, idx->metric, idx->geom, s), "search kernel");
+  });
+}
+
+int gann_alpha_prune(gann_index* idx, const uint32_t* p, const uint64_t* offsets, uint32_t count,
+                     const uint32_t* cand_ids, const float* cand_dists, float alpha, int rule,
+                     uint32_t* out, uint32_t* n_out) {
+  return guarded([&] {
+    if (!idx) fail(GANN_EINVAL, "index is NULL");
+    if (idx->R == 0) fail(GANN_EINVAL, "degree bound must be positive");  // prune.cpp:11
+    check_prune_params(alpha, rule);
+    if (count == 0) return;
+    set_device(idx);
+    const uint64_t total = offsets[count];
+    std::vector<uint32_t> len(count), small, big;
+    std::vector<uint64_t> beg(count);
+    for (uint32_t i = 0; i < count; i++) {
+      if (offsets[i + 1] < offsets[i]) fail(GANN_EINVAL, "offsets must be non-decreasing");
+      beg[i] = offsets[i];
+      const uint64_t m = offsets[i + 1] - offsets[i];
+      if (m > kPruneBigCap) fail(GANN_EINVAL, "candidate list longer than " + std::to_string(kPruneBigCap));
+      len[i] = static_cast<uint32_t>(m);
+      if (p[i] >= idx->n) fail(GANN_EINVAL, "point id out of range");
+      (m <= kPruneSmallCap ? small : big).push_back(i);
+    }
+    for (uint64_t i = 0; i < total; i++)
+      if (cand_ids[i] >= idx->n) fail(GANN_EINVAL, "candidate id out of range");
+    // one scratch block: p | beg | len | small | big | ids | dists | out | nout
+    idx->pt.ensure(size_t(count) * 4 * 4 + size_t(count) * 8 + total * 8 + size_t(count) * idx->R * 4 + 64);
+    uint8_t* base = idx->pt.as<uint8_t>();
+    uint64_t* d_beg = reinterpret_cast<uint64_t*>(base);
+    uint32_t* d_p = reinterpret_cast<uint32_t*>(d_beg + count);
+    uint32_t* d_len = d_p + count;
+    uint32_t* d_small = d_len + count;
+    uint32_t* d_big = d_small + count;
+    uint32_t* d_ids = d_big + count;
+    float* d_d = reinterpret_cast<float*>(d_ids + total);
+    uint32_t* d_out = reinterpret_cast<uint32_t*>(d_d + total);
+    idx->ps.ensure(size_t(count) * 4);
+    uint32_t* d_nout = idx->ps.as<uint32_t>();
+    auto h2d = [&](void* dst, const void* src, size_t bytes) {
+      if (bytes) cu(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, idx->stream), "upload");
+    };
+    h2d(d_beg, beg.data(), size_t(count) * 8);
+    h2d(d_p, p, size_t(count) * 4);
+    h2d(d_len, len.data(), size_t(count) * 4);
+    h2d(d_small, small.data(), small.size() * 4);
+    h2d(d_big, big.data(), big.size() * 4);
+    h2d(d_ids, cand_ids, total * 4);
+    h2d(d_d, cand_dists, total * 4);
+    cu(cudaMemsetAsync(idx->flags, 0, 8, idx->stream), "memset");
+    PruneArgs a = base_prune_args(idx, alpha, rule);
+    a.points = d_p;
+    a.begins = d_beg;
+    a.lengths = d_len;
+    a.cand_ids = d_ids;
+    a.cand_dists = d_d;
+    a.out_rows = d_out;
+    a.n_out = d_nout;
+    if (!small.empty()) {
+      a.count = static_cast<uint32_t>(small.size());
+      a.list_index = d_small;
+      a.mcap = kPruneSmallCap;
+      cu(launch_prune(a, idx->elem, idx->metric, idx->geom, 32, idx->stream), "prune kernel");
+    }
+    if (!big.empty()) {
+      a.count = static_cast<uint32_t>(big.size());
+      a.list_index = d_big;
+      a.mcap = kPruneBigCap;
+      cu(launch_prune(a, idx->elem, idx->metric, idx->geom, 256, idx->stream), "prune kernel");
+    }
+    cu(cudaMemcpyAsync(out, d_out, size_t(count) * idx->R * 4, cudaMemcpyDeviceToHost, idx->stream), "download");
+    if (n_out) cu(cudaMemcpyAsync(n_out, d_nout, size_t(count) * 4, cudaMemcpyDeviceToHost, idx->stream), "download");
+    sync(idx);
+  });
+}
+
+int gann_group_by_key(const uint32_t* keys, const uint32_t* vals, uint64_t m, int device,
+                      uint32_t* out_keys, uint32_t* out_vals, uint64_t* offsets, uint64_t* n_groups) {
+  return guarded([&] {
+    if (n_groups) *n_groups = 0;
+    if (m == 0) {
+      if (offsets) offsets[0] = 0;
+      return;
+    }
+    if (m >= 0x7FFFFFFFull) fail(GANN_EINVAL, "group_by_key: too many pairs");
+    for (uint64_t i = 0; i < m; i++)
+      if (keys[i] == GANN_NONE) fail(GANN_EINVAL, "key 0xFFFFFFFF is reserved");
+    uint32_t tbits = 6;
+    while ((uint64_t(1) << tbits) < 2 * m) tbits++;
+    // keys -> dense slots of a device hash table; the slots play the role of
+    // target vertices for the counting group-by
+    gann_index* idx = new_index(uint64_t(1) << tbits, 1, GANN_U8, GANN_L2, 1, device);
+    try {
+      idx->pt.ensure(m * 4);
+      idx->ps.ensure(m * 4);
+      idx->ok.ensure(m * 4);
+      idx->ov.ensure(m * 4);
+      idx->misc.ensure((size_t(1) << tbits) * 4);
+      idx->qids.ensure(m * 4);
+      cu(cudaMemcpyAsync(idx->qids.p, keys, m * 4, cudaMemcpyHostToDevice, idx->stream), "upload");
+      cu(cudaMemcpyAsync(idx->ps.p, vals, m * 4, cudaMemcpyHostToDevice, idx->stream), "upload");
+      cu(launch_hash_keys(idx->qids.as<uint32_t>(), m, idx->misc.as<uint32_t>(), tbits,
+                          idx->pt.as<uint32_t>(), idx->stream), "hash keys");
+      uint64_t ng = 0;
+      apply_back(idx, nullptr, 0, idx->pt.as<uint32_t>(), idx->ps.as<uint32_t>(), m, 1.0f, 0, false,
+                 idx->ok.as<uint32_t>(), idx->ov.as<uint32_t>(), &ng, idx->misc.as<uint32_t>());
+      cu(cudaMemcpyAsync(out_keys, idx->ok.p, m * 4, cudaMemcpyDeviceToHost, idx->stream), "download");
+      cu(cudaMemcpyAsync(out_vals, idx->ov.p, m * 4, cudaMemcpyDeviceToHost, idx->stream), "download");
+      sync(idx);
+      uint64_t g = 0;
+      for (uint64_t i = 0; i < m; i++)
+        if (i == 0 || out_keys[i] != out_keys[i - 1]) {
+          if (offsets) offsets[g] = i;
+          g++;
+        }
+      if (offsets) offsets[g] = m;
+      if (g != ng) fail(GANN_ECUDA, "group count mismatch");
+      if (n_groups) *n_groups = g;
+    } catch (...) {
+      gann_index_free(idx);
+      throw;
+    }
+    gann_index_free(idx);
+  });
+}
+
+int gann_choose_start(gann_index* idx, uint32_t* start) {
+  return guarded([&] {
+    if (!idx) fail(GANN_EINVAL, "index is NULL");
+    set_device(idx);
+    *start = choose_start_dev(idx);
+  });
+}
+
+int gann_insert_batch(gann_index* idx, const uint32_t* ids, uint32_t count, uint32_t L, float alpha,
+                      int rule, uint32_t* back) {
+  return guarded([&] {
+    if (!idx) fail(GANN_EINVAL, "index is NULL");
+    if (L == 0 || idx->R == 0) fail(GANN_EINVAL, "build beam and degree bound must be positive");
+    check_prune_params(alpha, rule);
+    if (count == 0) return;
+    for (uint32_t i = 0; i < count; i++)
+      if (ids[i] >= idx->n) fail(GANN_EINVAL, "point id out of range");
+    set_device(idx);
+    idx->pt.ensure(size_t(count) * 4);
+    cu(cudaMemcpyAsync(idx->pt.p, ids, size_t(count) * 4, cudaMemcpyHostToDevice, idx->stream), "upload");
+    insert_batch(idx, idx->pt.as<uint32_t>(), count, L, alpha, rule, false);
+    if (back) {
+      for (uint32_t i = 0; i < count; i++)
+        cu(cudaMemcpyAsync(back + size_t(i) * idx->R, idx->adj + uint64_t(ids[i]) * idx->R,
+                           size_t(idx->R) * 4, cudaMemcpyDeviceToHost, idx->stream), "download");
+      sync(idx);
+    }
+  });
+}
+
+int gann_apply_back_edges(gann_index* idx, const uint32_t* targets, const uint32_t* sources,
+                          uint64_t m, float alpha, int rule) {
+  return guarded([&] {
+    if (!idx) fail(GANN_EINVAL, "index is NULL");
+    check_prune_params(alpha, rule);
+    if (m == 0) return;
+    for (uint64_t i = 0; i < m; i++) {
+      if (targets[i] >= idx->n || sources[i] >= idx->n) fail(GANN_EINVAL, "pair id out of range");
+      if (targets[i] == sources[i]) fail(GANN_EINVAL, "self loop at vertex " + std::to_string(targets[i]));
+    }
+    set_device(idx);
+    idx->pt.ensure(m * 4);
+    idx->ps.ensure(m * 4);
+    cu(cudaMemcpyAsync(idx->pt.p, targets, m * 4, cudaMemcpyHostToDevice, idx->stream), "upload");
+    cu(cudaMemcpyAsync(idx->ps.p, sources, m * 4, cudaMemcpyHostToDevice, idx->stream), "upload");
+    apply_back(idx, nullptr, 0, idx->pt.as<uint32_t>(), idx->ps.as<uint32_t>(), m, alpha, rule, false);
+  });
+}
+
+int gann_groundtruth_device(gann_index* idx, const void* d_queries, uint32_t nq, uint32_t k,
+                            uint32_t* d_ids, float* d_dists, void* stream) {
+  return guarded([&] {
+    if (!idx) fail(GANN_EINVAL, "index is NULL");
+    set_device(idx);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : idx->stream;
+    const uint8_t* q = static_cast<const uint8_t*>(d_queries);
+    if (idx->stride != idx->row_bytes) {
+      idx->q.ensure(size_t(nq) * idx->stride);
+      cu(cudaMemsetAsync(idx->q.p, 0, size_t(nq) * idx->stride, s), "memset");
+      cu(cudaMemcpy2DAsync(idx->q.p, idx->stride, d_queries, idx->row_bytes, idx->row_bytes, nq,
+                           cudaMemcpyDeviceToDevice, s), "stage queries");
+      q = idx->q.as<uint8_t>();
+    }
+    run_groundtruth(idx, q, nq, k, d_ids, d_dists, s);
+  });
+}
+
+int gann_groundtruth(gann_index* idx, const void* queries, uint32_t nq, uint32_t k, uint32_t* ids,
+                     float* dists) {
+  return guarded([&] {
+    if (!idx) fail(GANN_EINVAL, "index is NULL");
+    if (nq == 0) return;
+    set_device(idx);
+    idx->qids.ensure(size_t(nq) * k * 4);
+    idx->qdists.ensure(size_t(nq) * k * 4);
+    const uint8_t* q = stage_rows(idx, idx->q, queries, nq, false);
+    run_groundtruth(idx, q, nq, k, idx->qids.as<uint32_t>(), idx->qdists.as<float>(), idx->stream);
+    cu(cudaMemcpyAsync(ids, idx->qids.p, size_t(nq) * k * 4, cudaMemcpyDeviceToHost, idx->stream), "download");
+    cu(cudaMemcpyAsync(dists, idx->qdists.p, size_t(nq) * k * 4, cudaMemcpyDeviceToHost, idx->stream), "download");
+    sync(idx);
+  });
+}
+
+int gann_generate_u8(void* d_out, uint64_t n, uint32_t d, uint32_t clusters, float sigma,
+                     float noise_frac, uint64_t center_seed, uint64_t stream_seed, uint64_t row0,
+                     int device) {
+  return guarded([&] {
+    if (clusters == 0 || d == 0) fail(GANN_EINVAL, "gen: d and clusters must be positive");
+    cu(cudaSetDevice(device), "cudaSetDevice");
+    cu(launch_generate_u8(static_cast<uint8_t*>(d_out), d, n, d, clusters, sigma, noise_frac,
+                          center_seed, stream_seed, row0, nullptr),
+       "generate");
+    cu(cudaDeviceSynchronize(), "generate sync");
+  });
+}
+
+void gann_shuffled_order(uint32_t n, uint64_t seed, uint32_t front, uint32_t* out) {
+  std::vector<uint32_t> order(n);
+  for (uint32_t i = 0; i < n; i++) order[i] = i;
+  std::mt19937_64 rng(seed);
+  std::shuffle(order.begin(), order.end(), rng);
+  if (n) std::iter_swap(order.begin(), std::find(order.begin(), order.end(), front));
+  std::copy(order.begin(), order.end(), out);
+}
+
+uint32_t gann_batch_ranges(uint64_t n, uint32_t max_batch, uint32_t* lo, uint32_t* hi,
+                           uint32_t max_ranges) {
+  auto r = batch_ranges(n, max_batch);
+  for (size_t i = 0; i < r.size() && i < max_ranges; i++) {
+    lo[i] = r[i].first;
+    hi[i] = r[i].second;
+  }
+  return static_cast<uint32_t>(r.size());
+}
+
+uint64_t gann_insert_seed(uint64_t seed) { return mix64(seed, 0x696e73657274ULL); }
+
+int gann_get_stats(const gann_index* idx, gann_stats* out) {
+  return guarded([&] {
+    if (!idx || !out) fail(GANN_EINVAL, "NULL argument");
+    cudaSetDevice(idx->device);
+    unsigned long long s[kStCount];
+    cu(cudaMemcpy(s, idx->stats, sizeof(s), cudaMemcpyDeviceToHost), "read stats");
+    out->queries = s[kStQueries];
+    out->expansions = s[kStExpansions];
+    out->evaluations = s[kStEvals];
+    out->filter_drops = s[kStDrops];
+    out->adj_entries = s[kStAdj];
+    out->prune_lists = s[kStPruneLists];
+    out->prune_candidates = s[kStPruneCands];
+    out->prune_evals = s[kStPruneEvals];
+    out->back_pairs = idx->back_pairs;
+    out->back_groups = idx->back_groups;
+    out->back_pruned = idx->back_pruned;
+    for (int i = 0; i < 6; i++) out->build_ms[i] = idx->build_ms[i];
+  });
+}
+
+int gann_reset_stats(gann_index* idx) {
+  return guarded([&] {
+    if (!idx) fail(GANN_EINVAL, "index is NULL");
+    set_device(idx);
+    cu(cudaMemsetAsync(idx->stats, 0, sizeof(unsigned long long) * kStCount, idx->stream), "memset");
+    sync(idx);
+  });
+}
+
+int gann_index_device_ptrs(const gann_index* idx, void** points, uint64_t* stride, uint32_t** adj) {
+  return guarded([&] {
+    if (!idx) fail(GANN_EINVAL, "index is NULL");
+    if (points) *points = idx->points;
+    if (stride) *stride = idx->stride;
+    if (adj) *adj = idx->adj;
+  });
+}
+
+}  // extern "C"

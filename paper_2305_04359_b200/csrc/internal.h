@@ -1,0 +1,144 @@
+// internal.h — argument blocks and launchers shared between the kernel
+// translation units and the C-ABI host code (gann.cu). Not installed.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace gann {
+
+// Row geometry: LPR lanes per row, up to CPL 16-byte chunks per lane.
+struct Geometry {
+  uint32_t nch;  // 16-byte chunks per (padded) row
+  int lpr;       // 1, 2, 4, 8, 16 or 32
+  int cpl;       // 1..4 (only with lpr == 32)
+};
+Geometry make_geometry(uint32_t nch);
+
+enum StatIdx {
+  kStQueries = 0, kStExpansions, kStEvals, kStDrops, kStAdj,
+  kStPruneLists, kStPruneCands, kStPruneEvals, kStCount
+};
+
+struct SearchArgs {
+  const uint8_t* data;       // n rows of `stride` bytes
+  uint64_t stride;
+  uint32_t n;
+  const uint32_t* adj;       // n * R, kNone padded
+  uint32_t R;
+  uint32_t start;
+  const uint8_t* queries;    // nq rows of `stride` bytes (when query_rows == nullptr)
+  const uint32_t* query_rows;// build mode: query i is data row query_rows[i]
+  const uint32_t* start_override;
+  uint32_t nq;
+  uint32_t L, k_gate, k_out;
+  float eps;
+  int visited_mode;          // 0 fast (shared hash), 1 reference L*L table
+  uint32_t hash_log2;        // fast mode table size
+  uint32_t* ref_table;       // mode 1: nq * L * L words, filled by the kernel
+  uint32_t dim;              // real dimension (search_seed)
+  uint32_t row_bytes;        // real bytes per row (search_seed)
+  uint32_t* out_ids;         // nq * k_out (nullable)
+  float* out_dists;
+  uint32_t* n_visited;       // nq (nullable)
+  uint64_t* dist_comps;      // nq (nullable)
+  uint32_t* vis_ids;         // nq * vcap (nullable)
+  float* vis_dists;
+  uint32_t vcap;
+  uint32_t* overflow;        // count of searches whose |V| exceeded vcap
+  unsigned long long* stats; // kStCount counters (nullable)
+};
+size_t search_smem_per_warp(uint32_t L, uint32_t R, uint32_t hash_log2);
+cudaError_t launch_search(const SearchArgs& a, int elem, int metric, const Geometry& g,
+                          cudaStream_t s);
+
+struct PruneArgs {
+  const uint8_t* data;
+  uint64_t stride;
+  uint32_t count;              // lists
+  const uint32_t* list_index;  // nullable: list i of this launch is list_index[i]
+  const uint32_t* points;      // p per list
+  const uint64_t* begins;      // list l starts at begins[l] (nullable => l*fixed_stride)
+  uint64_t fixed_stride;
+  const uint32_t* lengths;     // list l has lengths[l] candidates
+  const uint32_t* cand_ids;
+  const float* cand_dists;
+  uint32_t R;
+  float alpha;
+  int rule;                    // 0 scale_candidate, 1 scale_selected
+  uint32_t* out_adj;           // write to out_adj[p * R] (when out_rows == nullptr)
+  uint32_t* out_rows;          // or to out_rows[l * R]
+  uint32_t* n_out;             // nullable, per list l
+  uint32_t mcap;               // max list length this launch supports
+  uint32_t* too_long;          // lists longer than mcap are counted here
+  unsigned long long* stats;
+};
+// threads = 32 for short lists, larger for hubs; smem from prune_smem_bytes.
+size_t prune_smem_bytes(uint32_t mcap, uint32_t R);
+cudaError_t launch_prune(const PruneArgs& a, int elem, int metric, const Geometry& g, int threads,
+                         cudaStream_t s);
+
+// ---- back-edge grouping (phase 2) -----------------------------------------
+// Pairs (target, source) come either from the out-rows of the batch's points
+// (batch form: pair e = (adj[bsrc[e/R]*R + e%R], bsrc[e/R]), the reference's
+// concatenation order, src/diskann.cpp:61-65) or from explicit arrays.
+struct BackEdgeArgs {
+  const uint8_t* data;
+  uint64_t stride;
+  uint32_t* adj;            // n * R
+  uint32_t R;
+  const uint32_t* bsrc;     // batch form: B source points
+  uint32_t B;
+  const uint32_t* ptarget;  // explicit form (nullable): targets
+  const uint32_t* psource;  //                           sources
+  uint64_t npairs;          // B*R (batch form) or explicit count
+  int sources_distinct;     // batch form: every source appears once per target
+  uint32_t* tcount;         // n, all zero on entry and on exit
+  uint32_t* tgroup;         // n
+  uint32_t* gtarget;        // per group
+  uint32_t* gcnt;
+  uint64_t* goff;           // ordinal slots of group g: [goff[g], goff[g]+gcnt[g])
+  uint32_t* gcursor;
+  uint32_t* gsrc;           // npairs ordinals
+  uint64_t* poff;           // merged-list region of group g (R + gcnt[g] slots)
+  uint32_t* plen;           // merged length
+  uint32_t* pid;            // merged ids
+  float* pdist;             // d(target, id)
+  unsigned long long* counters;  // see kCnt*
+  uint32_t* big_groups;     // groups with more than small_group_cap sources
+  uint32_t* plist_small;    // groups to re-prune, merged length <= prune_small_cap
+  uint32_t* plist_big;
+  const uint32_t* key_of_target; // group_by_key: real key of a dense target slot
+  uint32_t small_group_cap;
+  uint32_t big_group_cap;
+  uint32_t prune_small_cap;
+};
+enum { kCntGroups = 0, kCntPairsCursor, kCntPruneCursor, kCntBig, kCntMaxGroup,
+       kCntPruneSmall, kCntPruneBig, kCntMaxMerged, kCntTooBig, kCntNum };
+cudaError_t backedge_count(const BackEdgeArgs& a, cudaStream_t s);
+cudaError_t backedge_offsets(const BackEdgeArgs& a, uint32_t ngroups, cudaStream_t s);
+cudaError_t backedge_scatter(const BackEdgeArgs& a, cudaStream_t s);
+cudaError_t backedge_merge(const BackEdgeArgs& a, uint32_t ngroups, uint32_t nbig, int elem,
+                           int metric, const Geometry& g, cudaStream_t s);
+size_t backedge_merge_smem(uint32_t cap, uint32_t R);
+// group_by_key: map arbitrary u32 keys to dense slots of a 2^k-entry table.
+cudaError_t launch_hash_keys(const uint32_t* keys, uint64_t m, uint32_t* table, uint32_t tbits,
+                             uint32_t* slots, cudaStream_t s);
+// group_by_key output: pairs of group g written at [goff[g], goff[g]+gcnt[g]).
+cudaError_t backedge_write_groups(const BackEdgeArgs& a, uint32_t ngroups, uint32_t nbig,
+                                  uint32_t* out_keys, uint32_t* out_vals, cudaStream_t s);
+
+// ---- misc -------------------------------------------------------------------
+cudaError_t launch_choose_start(const uint8_t* data, uint64_t stride, uint64_t n, uint32_t d,
+                                int elem, int metric, double* colsum, float* centroid,
+                                unsigned long long* best, cudaStream_t s);
+cudaError_t launch_generate_u8(uint8_t* out, uint64_t out_stride, uint64_t n, uint32_t d,
+                               uint32_t clusters, float sigma, float noise_frac,
+                               uint64_t center_seed, uint64_t stream_seed, uint64_t row0,
+                               cudaStream_t s);
+cudaError_t launch_groundtruth(const uint8_t* data, uint64_t stride, uint64_t n,
+                               const uint8_t* queries, uint32_t nq, uint32_t k, int elem,
+                               int metric, uint32_t nch, unsigned long long* partial,
+                               uint32_t splits, uint32_t* ids, float* dists, cudaStream_t s);
+uint32_t groundtruth_splits(uint64_t n, uint32_t nq);
+
+}  // namespace gann

@@ -1,0 +1,286 @@
+// misc.cu — start vertex, synthetic data generator, brute-force ground truth.
+#include <algorithm>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace gann {
+
+namespace {
+
+template <int E>
+__device__ __forceinline__ float elem_at(const uint8_t* row, uint32_t j) {
+  if (E == kU8) return static_cast<float>(row[j]);
+  if (E == kI8) return static_cast<float>(reinterpret_cast<const int8_t*>(row)[j]);
+  return reinterpret_cast<const float*>(row)[j];
+}
+
+// Column sums in double — builder_common.cpp:65-74. Exact for integer kinds
+// whatever the summation order.
+template <int E>
+__global__ void colsum_kernel(const uint8_t* data, uint64_t stride, uint64_t n, uint32_t d,
+                              double* colsum) {
+  constexpr uint32_t kRows = 512;
+  const uint64_t r0 = uint64_t(blockIdx.x) * kRows;
+  const uint64_t r1 = min(n, r0 + kRows);
+  for (uint32_t j = threadIdx.x; j < d; j += blockDim.x) {
+    double acc = 0.0;
+    for (uint64_t r = r0; r < r1; r++) acc += static_cast<double>(elem_at<E>(data + r * stride, j));
+    atomicAdd(colsum + j, acc);
+  }
+}
+
+__global__ void centroid_kernel(const double* colsum, uint64_t n, uint32_t d, float* c) {
+  for (uint32_t j = threadIdx.x; j < d; j += blockDim.x)
+    c[j] = __double2float_rn(__ddiv_rn(colsum[j], static_cast<double>(n)));  // :76-80
+}
+
+// dist_to_centroid — builder_common.cpp:24-38: sequential float, no FMA.
+template <int E, int M>
+__global__ void start_dist_kernel(const uint8_t* data, uint64_t stride, uint64_t n, uint32_t d,
+                                  const float* centroid, unsigned long long* best) {
+  extern __shared__ float cs[];
+  for (uint32_t j = threadIdx.x; j < d; j += blockDim.x) cs[j] = centroid[j];
+  __syncthreads();
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  uint64_t key = kMaxKey;
+  if (i < n) {
+    const uint8_t* row = data + i * stride;
+    float acc = 0.0f;
+    for (uint32_t j = 0; j < d; j++) {
+      const float x = elem_at<E>(row, j);
+      if (M == kL2) {
+        const float diff = __fsub_rn(x, cs[j]);
+        acc = __fadd_rn(acc, __fmul_rn(diff, diff));
+      } else {
+        acc = __fadd_rn(acc, __fmul_rn(x, cs[j]));
+      }
+    }
+    key = make_key(M == kL2 ? acc : -acc, static_cast<uint32_t>(i));
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t other = __shfl_xor_sync(0xFFFFFFFFu, key, o);
+    key = other < key ? other : key;
+  }
+  if ((threadIdx.x & 31) == 0 && key != kMaxKey) atomicMin(best, static_cast<unsigned long long>(key));
+}
+
+// ---- synthetic data ---------------------------------------------------------
+// A pure function of (seeds, row, column), restated bit-for-bit in numpy by
+// paper_2305_04359_b200/datagen.py. Gaussian noise is Irwin-Hall(4) over
+// 16-bit uniforms (unit variance), i.e. integer arithmetic plus three IEEE f32
+// ops, so host and device agree exactly.
+constexpr uint64_t kKCenter = 0xC3A5C85C97CB3127ull;
+constexpr uint64_t kKCluster = 0x2545F4914F6CDD1Dull;
+constexpr uint64_t kKNoiseRow = 0x9E3779B97F4A7C15ull;
+constexpr uint64_t kKUniform = 0xD6E8FEB86659FD93ull;
+constexpr uint64_t kKNormal = 0xA0761D6478BD642Full;
+
+__global__ void gen_u8_kernel(uint8_t* out, uint64_t out_stride, uint64_t n, uint32_t d,
+                              uint32_t clusters, float sigma, uint32_t noise_thr,
+                              uint64_t cseed, uint64_t sseed, uint64_t row0) {
+  const uint64_t total = n * d;
+  const uint64_t step = uint64_t(gridDim.x) * blockDim.x;
+  const float inv_sd = 1.0f / 37837.2227f;
+  for (uint64_t idx = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total; idx += step) {
+    const uint64_t i = idx / d;
+    const uint32_t j = static_cast<uint32_t>(idx - i * d);
+    const uint64_t r = row0 + i;
+    const uint64_t el = r * d + j;
+    uint32_t v;
+    if ((mix64(sseed ^ kKNoiseRow, r) >> 40) < noise_thr) {
+      v = static_cast<uint32_t>(mix64(sseed ^ kKUniform, el) >> 56);
+    } else {
+      const uint64_t c = mix64(sseed ^ kKCluster, r) % clusters;
+      const uint32_t center = static_cast<uint32_t>(mix64(cseed ^ kKCenter, c * d + j) >> 56);
+      const uint64_t h = mix64(sseed ^ kKNormal, el);
+      const int s = static_cast<int>((h & 0xFFFF) + ((h >> 16) & 0xFFFF) + ((h >> 32) & 0xFFFF) +
+                                     ((h >> 48) & 0xFFFF)) - 131070;
+      const float z = __fmul_rn(static_cast<float>(s), inv_sd);
+      const float x = __fadd_rn(static_cast<float>(center), __fmul_rn(sigma, z));
+      const float rx = rintf(x);
+      v = rx < 0.0f ? 0u : (rx > 255.0f ? 255u : static_cast<uint32_t>(rx));
+    }
+    out[i * out_stride + j] = static_cast<uint8_t>(v);
+  }
+}
+
+// ---- brute-force ground truth ---------------------------------------------
+// compute_groundtruth (src/dataset.cpp:172-217): exact top-k by (dist, id).
+// One thread per query (its row in registers), a shared-memory tile of points
+// broadcast to the block; the point range is split across blockIdx.y and the
+// per-split top-16 lists are merged by gt_merge_kernel.
+constexpr int kGtK = 16;
+constexpr int kGtThreads = 128;
+constexpr int kGtTile = 128;
+
+template <int E, int M, int NCH>
+__global__ void __launch_bounds__(kGtThreads)
+    gt_kernel(const uint8_t* data, uint64_t stride, uint64_t n, const uint8_t* queries,
+              uint32_t nq, uint32_t nch, uint32_t splits, unsigned long long* partial) {
+  using Op = DistOp<E, M>;
+  extern __shared__ __align__(16) uint4 tile[];
+  const uint32_t q = blockIdx.x * kGtThreads + threadIdx.x;
+  const uint64_t lo = n * blockIdx.y / splits, hi = n * (blockIdx.y + 1) / splits;
+  uint4 qr[NCH];
+#pragma unroll
+  for (int c = 0; c < NCH; c++)
+    qr[c] = (q < nq && c < static_cast<int>(nch))
+                ? __ldg(reinterpret_cast<const uint4*>(queries + uint64_t(q) * stride) + c)
+                : make_uint4(0, 0, 0, 0);
+  uint64_t top[kGtK];
+#pragma unroll
+  for (int i = 0; i < kGtK; i++) top[i] = kMaxKey;
+  for (uint64_t p0 = lo; p0 < hi; p0 += kGtTile) {
+    const uint32_t cnt = static_cast<uint32_t>((hi - p0) < kGtTile ? (hi - p0) : uint64_t(kGtTile));
+    __syncthreads();
+    for (uint32_t t = threadIdx.x; t < cnt * nch; t += kGtThreads) {
+      const uint32_t pp = t / nch, c = t - pp * nch;
+      tile[pp * NCH + c] = __ldg(reinterpret_cast<const uint4*>(data + (p0 + pp) * stride) + c);
+    }
+    __syncthreads();
+    for (uint32_t pp = 0; pp < cnt; pp++) {
+      typename Op::acc_t acc = Op::zero();
+#pragma unroll
+      for (int c = 0; c < NCH; c++)
+        if (c < static_cast<int>(nch)) acc = Op::chunk(qr[c], tile[pp * NCH + c], acc);
+      const uint64_t key = make_key(Op::finish(acc), static_cast<uint32_t>(p0 + pp));
+      if (key < top[kGtK - 1]) {
+        top[kGtK - 1] = key;
+#pragma unroll
+        for (int i = kGtK - 1; i > 0; i--) {
+          if (top[i] < top[i - 1]) {
+            const uint64_t t = top[i];
+            top[i] = top[i - 1];
+            top[i - 1] = t;
+          }
+        }
+      }
+    }
+  }
+  if (q < nq) {
+    unsigned long long* out = partial + (uint64_t(q) * splits + blockIdx.y) * kGtK;
+#pragma unroll
+    for (int i = 0; i < kGtK; i++) out[i] = top[i];
+  }
+}
+
+__global__ void gt_merge_kernel(const unsigned long long* partial, uint32_t nq, uint32_t splits,
+                                uint32_t k, uint32_t* ids, float* dists) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  uint64_t top[kGtK];
+#pragma unroll
+  for (int i = 0; i < kGtK; i++) top[i] = kMaxKey;
+  const unsigned long long* in = partial + uint64_t(q) * splits * kGtK;
+  for (uint32_t t = 0; t < splits * kGtK; t++) {
+    const uint64_t key = in[t];
+    if (key < top[kGtK - 1]) {
+      top[kGtK - 1] = key;
+#pragma unroll
+      for (int i = kGtK - 1; i > 0; i--) {
+        if (top[i] < top[i - 1]) {
+          const uint64_t x = top[i];
+          top[i] = top[i - 1];
+          top[i - 1] = x;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kGtK; i++) {
+    if (static_cast<uint32_t>(i) < k) {
+      ids[uint64_t(q) * k + i] = top[i] == kMaxKey ? kNone : key_id(top[i]);
+      dists[uint64_t(q) * k + i] = top[i] == kMaxKey ? __int_as_float(0x7f800000) : key_dist(top[i]);
+    }
+  }
+}
+
+template <int E, int M, int NCH>
+cudaError_t gt_launch(const uint8_t* data, uint64_t stride, uint64_t n, const uint8_t* queries,
+                      uint32_t nq, uint32_t nch, uint32_t splits, unsigned long long* partial,
+                      cudaStream_t s) {
+  const size_t smem = size_t(kGtTile) * NCH * 16;
+  auto k = gt_kernel<E, M, NCH>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return e;
+  dim3 grid((nq + kGtThreads - 1) / kGtThreads, splits);
+  k<<<grid, kGtThreads, smem, s>>>(data, stride, n, queries, nq, nch, splits, partial);
+  return cudaGetLastError();
+}
+
+template <int E, int M>
+cudaError_t gt_dispatch(const uint8_t* data, uint64_t stride, uint64_t n, const uint8_t* queries,
+                        uint32_t nq, uint32_t nch, uint32_t splits, unsigned long long* partial,
+                        cudaStream_t s) {
+  if (nch <= 1) return gt_launch<E, M, 1>(data, stride, n, queries, nq, nch, splits, partial, s);
+  if (nch <= 2) return gt_launch<E, M, 2>(data, stride, n, queries, nq, nch, splits, partial, s);
+  if (nch <= 4) return gt_launch<E, M, 4>(data, stride, n, queries, nq, nch, splits, partial, s);
+  if (nch <= 8) return gt_launch<E, M, 8>(data, stride, n, queries, nq, nch, splits, partial, s);
+  return gt_launch<E, M, 16>(data, stride, n, queries, nq, nch, splits, partial, s);
+}
+
+}  // namespace
+
+cudaError_t launch_choose_start(const uint8_t* data, uint64_t stride, uint64_t n, uint32_t d,
+                                int elem, int metric, double* colsum, float* centroid,
+                                unsigned long long* best, cudaStream_t s) {
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(colsum, 0, sizeof(double) * d, s)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(best, 0xFF, sizeof(unsigned long long), s)) != cudaSuccess) return e;
+  const uint32_t cb = static_cast<uint32_t>((n + 511) / 512);
+  const uint32_t ct = d < 256 ? ((d + 31) / 32) * 32 : 256;
+  if (elem == kU8) colsum_kernel<kU8><<<cb, ct, 0, s>>>(data, stride, n, d, colsum);
+  else if (elem == kI8) colsum_kernel<kI8><<<cb, ct, 0, s>>>(data, stride, n, d, colsum);
+  else colsum_kernel<kF32><<<cb, ct, 0, s>>>(data, stride, n, d, colsum);
+  centroid_kernel<<<1, 256, 0, s>>>(colsum, n, d, centroid);
+  const uint32_t db = static_cast<uint32_t>((n + 255) / 256);
+  const size_t smem = sizeof(float) * d;
+#define GANN_SD(E, M) start_dist_kernel<E, M><<<db, 256, smem, s>>>(data, stride, n, d, centroid, best)
+  if (metric == kL2) {
+    if (elem == kU8) GANN_SD(kU8, kL2); else if (elem == kI8) GANN_SD(kI8, kL2); else GANN_SD(kF32, kL2);
+  } else {
+    if (elem == kU8) GANN_SD(kU8, kIP); else if (elem == kI8) GANN_SD(kI8, kIP); else GANN_SD(kF32, kIP);
+  }
+#undef GANN_SD
+  return cudaGetLastError();
+}
+
+cudaError_t launch_generate_u8(uint8_t* out, uint64_t out_stride, uint64_t n, uint32_t d,
+                               uint32_t clusters, float sigma, float noise_frac,
+                               uint64_t center_seed, uint64_t stream_seed, uint64_t row0,
+                               cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  const uint32_t thr = static_cast<uint32_t>(static_cast<double>(noise_frac) * 16777216.0);
+  gen_u8_kernel<<<148 * 16, 256, 0, s>>>(out, out_stride, n, d, clusters, sigma, thr, center_seed,
+                                         stream_seed, row0);
+  return cudaGetLastError();
+}
+
+uint32_t groundtruth_splits(uint64_t n, uint32_t nq) {
+  const uint32_t qb = (nq + kGtThreads - 1) / kGtThreads;
+  uint32_t s = (148 * 8 + qb - 1) / qb;
+  s = std::max<uint32_t>(1, std::min<uint32_t>(s, 256));
+  while (s > 1 && n / s < 4096) s--;
+  return s;
+}
+
+cudaError_t launch_groundtruth(const uint8_t* data, uint64_t stride, uint64_t n,
+                               const uint8_t* queries, uint32_t nq, uint32_t k, int elem,
+                               int metric, uint32_t nch, unsigned long long* partial,
+                               uint32_t splits, uint32_t* ids, float* dists, cudaStream_t s) {
+  if (nq == 0) return cudaSuccess;
+  cudaError_t e;
+#define GANN_GT(E, M) e = gt_dispatch<E, M>(data, stride, n, queries, nq, nch, splits, partial, s)
+  if (metric == kL2) {
+    if (elem == kU8) GANN_GT(kU8, kL2); else if (elem == kI8) GANN_GT(kI8, kL2); else GANN_GT(kF32, kL2);
+  } else {
+    if (elem == kU8) GANN_GT(kU8, kIP); else if (elem == kI8) GANN_GT(kI8, kIP); else GANN_GT(kF32, kIP);
+  }
+#undef GANN_GT
+  if (e != cudaSuccess) return e;
+  gt_merge_kernel<<<(nq + 127) / 128, 128, 0, s>>>(partial, nq, splits, k, ids, dists);
+  return cudaGetLastError();
+}
+
+}  // namespace gann

@@ -1,0 +1,251 @@
+// prune.cu — robustPrune (alpha_prune) for many lists at once, one CTA per list.
+//
+// Behaviour contract: graphann::alpha_prune (src/prune.cpp:8-44):
+// drop p, sort the candidates by (dist, id), then walk them in order; a
+// candidate that is still alive is selected, and unless its distance is 0 it
+// culls every later alive candidate j with alpha*d(sel, j) <= d(p, j)
+// (scale_candidate) or d(sel, j) < alpha*d(p, sel) (scale_selected); stop at R.
+//
+// GPU shape. The candidate keys sit in shared memory and are bitonic-sorted
+// by the CTA. The alive list is a compacted index array in key order; every
+// selection computes its distances to all alive candidates in parallel (LPR
+// lanes per row, 16-byte gathers of rows that the preceding search just pulled
+// into L2) and stable-compacts the survivors. Each alpha*via is one IEEE f32
+// multiply (__fmul_rn) so the comparison is bit-identical to the reference;
+// integer distances are exact. 32-thread CTAs serve the insert-time lists
+// (|V| ~ L); 256-thread CTAs with up to 16k candidates serve back-edge hubs.
+#include "common.cuh"
+#include "internal.h"
+
+namespace gann {
+
+size_t prune_smem_bytes(uint32_t mcap, uint32_t R) {
+  uint32_t M = 32;
+  while (M < mcap) M <<= 1;
+  size_t b = size_t(M) * 8 + 2 * size_t(M) * 2 + size_t(M) + size_t(R) * 4;
+  return (b + 15) & ~size_t(15);
+}
+
+template <int NT>
+__device__ __forceinline__ void cta_sync() {
+  if (NT == 32) __syncwarp(); else __syncthreads();
+}
+
+// Stable compaction of src[0..n) into dst by flags kf[0..n); returns count.
+template <int NT>
+__device__ __forceinline__ uint32_t cta_compact(const uint16_t* src, const uint8_t* kf, uint32_t n,
+                                                uint16_t* dst, uint32_t* warp_tot) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  uint32_t total = 0;
+  for (uint32_t b0 = 0; b0 < n; b0 += NT) {
+    const uint32_t i = b0 + tid;
+    const bool keep = i < n && kf[i];
+    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, keep);
+    uint32_t off = __popc(bal & ((1u << lane) - 1u));
+    if (NT == 32) {
+      if (keep) dst[total + off] = src[i];
+      total += __popc(bal);
+    } else {
+      if (lane == 0) warp_tot[w] = __popc(bal);
+      __syncthreads();
+      uint32_t before = 0, all = 0;
+      for (int t = 0; t < NT / 32; t++) {
+        const uint32_t c = warp_tot[t];
+        if (t < w) before += c;
+        all += c;
+      }
+      if (keep) dst[total + before + off] = src[i];
+      total += all;
+      __syncthreads();
+    }
+  }
+  return total;
+}
+
+template <int E, int M, int LPR, int CPL, int NT>
+__global__ void __launch_bounds__(NT) prune_kernel(const PruneArgs a, const uint32_t Mcap) {
+  using Op = DistOp<E, M>;
+  constexpr int GROUPS = NT / LPR;
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ uint32_t warp_tot[NT / 32];
+  uint64_t* keys = reinterpret_cast<uint64_t*>(smem);
+  uint16_t* alA = reinterpret_cast<uint16_t*>(keys + Mcap);
+  uint16_t* alB = alA + Mcap;
+  uint8_t* kf = reinterpret_cast<uint8_t*>(alB + Mcap);
+  uint32_t* sel = reinterpret_cast<uint32_t*>(kf + Mcap);
+  const int tid = threadIdx.x;
+  const int sub = tid & (LPR - 1);
+  const int grp = tid / LPR;
+  const uint32_t nch = static_cast<uint32_t>(a.stride >> 4);
+  const uint32_t R = a.R;
+
+  for (uint32_t li = blockIdx.x; li < a.count; li += gridDim.x) {
+    const uint32_t l = a.list_index ? a.list_index[li] : li;
+    const uint32_t p = a.points[l];
+    uint64_t beg, m;
+    beg = a.begins ? a.begins[l] : uint64_t(l) * a.fixed_stride;
+    m = a.lengths[l];
+    uint32_t* orow = a.out_rows ? a.out_rows + uint64_t(l) * R : a.out_adj + uint64_t(p) * R;
+    if (m > a.mcap) {  // caller routes long lists elsewhere; never truncate silently
+      if (tid == 0) atomicAdd(a.too_long, 1u);
+      continue;
+    }
+    uint32_t Mp = 32;
+    while (Mp < m) Mp <<= 1;
+    for (uint32_t i = tid; i < Mp; i += NT) {
+      uint64_t k = kMaxKey;
+      if (i < m) {
+        const uint32_t id = a.cand_ids[beg + i];
+        if (id != p) k = make_key(a.cand_dists[beg + i], id);  // prune.cpp:18-20 drops p
+      }
+      keys[i] = k;
+    }
+    cta_sync<NT>();
+    // bitonic sort by (dist, id) — prune.cpp:21
+    for (uint32_t k = 2; k <= Mp; k <<= 1) {
+      for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+        for (uint32_t i = tid; i < Mp; i += NT) {
+          const uint32_t ixj = i ^ j;
+          if (ixj > i) {
+            const uint64_t x = keys[i], y = keys[ixj];
+            const bool up = (i & k) == 0;
+            if ((x > y) == up) {
+              keys[i] = y;
+              keys[ixj] = x;
+            }
+          }
+        }
+        cta_sync<NT>();
+      }
+    }
+    const uint32_t m2 = lower_bound_u64(keys, Mp, kMaxKey);
+    for (uint32_t i = tid; i < m2; i += NT) alA[i] = static_cast<uint16_t>(i);
+    cta_sync<NT>();
+
+    uint16_t* alive = alA;
+    uint32_t nalive = m2, nsel = 0;
+    uint64_t evals = 0;
+    while (nsel < R && nalive > 0) {  // prune.cpp:25-43
+      const uint64_t sk = keys[alive[0]];
+      if (tid == 0) sel[nsel] = key_id(sk);
+      nsel++;
+      if (nsel == R) break;
+      if (key_dist(sk) == 0.0f) {  // :32 a zero-distance pick culls nothing
+        alive++;
+        nalive--;
+        continue;
+      }
+      const uint32_t sid = key_id(sk);
+      const float sdist = key_dist(sk);
+      uint4 sr[CPL];
+      const uint8_t* srow = a.data + uint64_t(sid) * a.stride;
+#pragma unroll
+      for (int c = 0; c < CPL; c++) {
+        const uint32_t ch = sub + c * LPR;
+        sr[c] = ch < nch ? __ldg(reinterpret_cast<const uint4*>(srow) + ch) : make_uint4(0, 0, 0, 0);
+      }
+      const uint32_t rest = nalive - 1;  // candidates after the selection
+      evals += rest;
+      constexpr int U = 4;
+      for (uint32_t b0 = 0; b0 < rest; b0 += GROUPS * U) {
+        uint4 x[U][CPL];
+        uint32_t idx[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+          const uint32_t t = b0 + u * GROUPS + grp;
+          idx[u] = t < rest ? alive[1 + t] : 0xFFFFu;
+          const uint32_t id = t < rest ? key_id(keys[idx[u]]) : 0u;
+          const uint8_t* rp = a.data + uint64_t(id) * a.stride;
+#pragma unroll
+          for (int c = 0; c < CPL; c++) {
+            const uint32_t ch = sub + c * LPR;
+            x[u][c] = (t < rest && ch < nch) ? __ldg(reinterpret_cast<const uint4*>(rp) + ch)
+                                             : make_uint4(0, 0, 0, 0);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+          typename Op::acc_t acc = Op::zero();
+#pragma unroll
+          for (int c = 0; c < CPL; c++) acc = Op::chunk(sr[c], x[u][c], acc);
+          acc = group_sum<LPR>(acc);
+          const uint32_t t = b0 + u * GROUPS + grp;
+          if (sub == 0 && t < rest) {
+            const float via = Op::finish(acc);
+            const float dj = key_dist(keys[idx[u]]);
+            // prune.cpp:37-39, one IEEE multiply, never contracted
+            const bool drop = a.rule == 0 ? (__fmul_rn(a.alpha, via) <= dj)
+                                          : (via < __fmul_rn(a.alpha, sdist));
+            kf[t] = drop ? 0 : 1;
+          }
+        }
+      }
+      cta_sync<NT>();
+      uint16_t* dst = (alive >= alA && alive < alA + Mcap) ? alB : alA;
+      nalive = cta_compact<NT>(alive + 1, kf, rest, dst, warp_tot);
+      alive = dst;
+      cta_sync<NT>();
+    }
+    cta_sync<NT>();
+    for (uint32_t i = tid; i < R; i += NT) orow[i] = i < nsel ? sel[i] : kNone;
+    if (tid == 0) {
+      if (a.n_out) a.n_out[l] = nsel;
+      if (a.stats) {
+        atomicAdd(a.stats + kStPruneLists, 1ull);
+        atomicAdd(a.stats + kStPruneCands, static_cast<unsigned long long>(m));
+        atomicAdd(a.stats + kStPruneEvals, static_cast<unsigned long long>(evals));
+      }
+    }
+    cta_sync<NT>();
+  }
+}
+
+namespace {
+template <int E, int M, int LPR, int CPL>
+cudaError_t launch_nt(const PruneArgs& a, int threads, cudaStream_t s) {
+  uint32_t Mcap = 32;
+  while (Mcap < a.mcap) Mcap <<= 1;
+  const size_t smem = prune_smem_bytes(a.mcap, a.R);
+  if (a.count == 0) return cudaSuccess;
+  if (threads <= 32) {
+    auto k = prune_kernel<E, M, LPR, CPL, 32>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    k<<<a.count, 32, smem, s>>>(a, Mcap);
+  } else {
+    auto k = prune_kernel<E, M, LPR, CPL, 256>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    k<<<a.count, 256, smem, s>>>(a, Mcap);
+  }
+  return cudaGetLastError();
+}
+template <int E, int M>
+cudaError_t dispatch(const PruneArgs& a, const Geometry& g, int threads, cudaStream_t s) {
+  switch (g.lpr) {
+    case 1: return launch_nt<E, M, 1, 1>(a, threads, s);
+    case 2: return launch_nt<E, M, 2, 1>(a, threads, s);
+    case 4: return launch_nt<E, M, 4, 1>(a, threads, s);
+    case 8: return launch_nt<E, M, 8, 1>(a, threads, s);
+    case 16: return launch_nt<E, M, 16, 1>(a, threads, s);
+    default:
+      if (g.cpl == 1) return launch_nt<E, M, 32, 1>(a, threads, s);
+      if (g.cpl == 2) return launch_nt<E, M, 32, 2>(a, threads, s);
+      return launch_nt<E, M, 32, 4>(a, threads, s);
+  }
+}
+}  // namespace
+
+cudaError_t launch_prune(const PruneArgs& a, int elem, int metric, const Geometry& g, int threads,
+                         cudaStream_t s) {
+  if (metric == kL2) {
+    if (elem == kU8) return dispatch<kU8, kL2>(a, g, threads, s);
+    if (elem == kI8) return dispatch<kI8, kL2>(a, g, threads, s);
+    return dispatch<kF32, kL2>(a, g, threads, s);
+  }
+  if (elem == kU8) return dispatch<kU8, kIP>(a, g, threads, s);
+  if (elem == kI8) return dispatch<kI8, kIP>(a, g, threads, s);
+  return dispatch<kF32, kIP>(a, g, threads, s);
+}
+
+}  // namespace gann

@@ -1,0 +1,380 @@
+// search.cu — batched greedy beam search, one warp per query (sm_100a).
+//
+// Behaviour contract: graphann::beam_search (src/search.cpp:62-131), restated
+// in SURVEY.md §B.1. Per warp:
+//   * the beam (<= L keys, sorted) and its expanded flags live in shared
+//     memory, double-buffered so a merge is one parallel scatter;
+//   * exactly one vertex is expanded per step (the first unexpanded key,
+//     src/search.cpp:96-103), gated by the k-th best key with epsilon slack
+//     (:105-107) — the only order the reference's visit sequence allows;
+//   * the expanded vertex's adjacency row (R ids, one coalesced load) is run
+//     through the visited filter, the surviving ids' rows are gathered with
+//     16-byte loads (LPR lanes per row, several rows in flight per lane) and
+//     reduced with xor-shuffles into exact int32 (u8/i8) or f32 distances;
+//   * the new keys are merged into the beam as top-L of the union with exact
+//     (dist, id) duplicates dropped — equal to the reference's sequential
+//     push (:83-90) because the L-th key only ever decreases.
+// Visited filter. FAST: an open-addressing hash in shared memory with a
+// bounded probe; an id that does not fit is simply not remembered, so the
+// filter never reports a false positive and ids / |V| / visit order are the
+// reference's. REF: the reference's own ApproxVisitedSet
+// (L*L slots, mix64(id ^ seed) % L^2, include/graphann/search.hpp:24-38,
+// seed from src/search.cpp:52-58) in global memory, applied per expansion
+// with the order-exact warp rule of SURVEY.md §0.4 (first lane of a slot
+// tests, last lane writes), so dist_comps matches the reference too.
+#include <cstdio>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace gann {
+
+namespace {
+
+constexpr int kWarpsPerBlock = 4;
+constexpr int kProbes = 4;
+
+template <int LPR, int CPL>
+struct Unroll {
+  static constexpr int RPP = 32 / LPR;
+  static constexpr int raw = (32 / RPP) > 8 ? 8 : (32 / RPP);
+  static constexpr int U = (raw / CPL) < 1 ? 1 : (raw / CPL);
+};
+
+// Distances from the lane's query chunks qr to rows ids[0..m) -> keys out[].
+template <class Op, int LPR, int CPL>
+__device__ __forceinline__ void eval_rows(const uint8_t* __restrict__ data, uint64_t stride,
+                                          uint32_t nch, const uint32_t* ids, uint32_t m,
+                                          uint64_t* out, const uint4 (&qr)[CPL], int lane) {
+  constexpr int RPP = 32 / LPR;
+  constexpr int U = Unroll<LPR, CPL>::U;
+  const int sub = lane & (LPR - 1);
+  const int grp = lane / LPR;
+  for (uint32_t base = 0; base < m; base += RPP * U) {
+    uint4 x[U][CPL];
+    uint32_t id[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const uint32_t r = base + u * RPP + grp;
+      id[u] = r < m ? ids[r] : kNone;
+      const uint8_t* rp = data + static_cast<uint64_t>(id[u] == kNone ? 0u : id[u]) * stride;
+#pragma unroll
+      for (int c = 0; c < CPL; c++) {
+        const uint32_t ch = sub + c * LPR;
+        x[u][c] = (id[u] != kNone && ch < nch) ? __ldg(reinterpret_cast<const uint4*>(rp) + ch)
+                                               : make_uint4(0, 0, 0, 0);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      typename Op::acc_t acc = Op::zero();
+#pragma unroll
+      for (int c = 0; c < CPL; c++) acc = Op::chunk(qr[c], x[u][c], acc);
+      acc = group_sum<LPR>(acc);
+      const uint32_t r = base + u * RPP + grp;
+      if (sub == 0 && r < m) out[r] = make_key(Op::finish(acc), id[u]);
+    }
+  }
+}
+
+__device__ __forceinline__ bool hash_insert(volatile uint32_t* hash, uint32_t log2, uint32_t id,
+                                            uint32_t& drops) {
+  const uint32_t mask = (1u << log2) - 1u;
+  const uint32_t h = (id * 0x9E3779B1u) >> (32 - log2);
+#pragma unroll 1
+  for (int p = 0; p < kProbes; p++) {
+    const uint32_t s = (h + p) & mask;
+    const uint32_t v = hash[s];
+    if (v == id) return false;
+    if (v == kNone) {
+      const uint32_t old = atomicCAS(const_cast<uint32_t*>(hash + s), kNone, id);
+      if (old == kNone) return true;
+      if (old == id) return false;
+    }
+  }
+  drops++;
+  return true;  // not remembered: may be evaluated again later, never wrongly skipped
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt(int lane) { return (1u << lane) - 1u; }
+
+}  // namespace
+
+size_t search_smem_per_warp(uint32_t L, uint32_t R, uint32_t hash_log2) {
+  const size_t Lp = (L + 31) & ~31u, Rp = (R + 31) & ~31u;
+  size_t b = 2 * Lp * 8 + 3 * Rp * 8 + 2 * Rp * 4 + (size_t(1) << hash_log2) * 4 + 2 * Lp;
+  return (b + 15) & ~size_t(15);
+}
+
+template <int E, int M, int LPR, int CPL>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+    search_kernel(const SearchArgs a, const uint32_t per_warp) {
+  using Op = DistOp<E, M>;
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const uint32_t L = a.L, R = a.R;
+  const uint32_t Lp = (L + 31) & ~31u, Rp = (R + 31) & ~31u;
+  const uint32_t H = 1u << a.hash_log2;
+  const uint32_t nch = static_cast<uint32_t>(a.stride >> 4);
+  uint8_t* base = smem + wib * per_warp;
+  uint64_t* beamA = reinterpret_cast<uint64_t*>(base);
+  uint64_t* beamB = beamA + Lp;
+  uint64_t* ck = beamB + Lp;
+  uint64_t* srt = ck + Rp;
+  uint64_t* tmpk = srt + Rp;
+  uint32_t* cid = reinterpret_cast<uint32_t*>(tmpk + Rp);
+  uint32_t* posb = cid + Rp;
+  uint32_t* hash = posb + Rp;
+  uint8_t* flA = reinterpret_cast<uint8_t*>(hash + H);
+  uint8_t* flB = flA + Lp;
+  const uint32_t FULL = 0xFFFFFFFFu;
+
+  const uint32_t nw = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t q = blockIdx.x * (blockDim.x >> 5) + wib; q < a.nq; q += nw) {
+    const uint8_t* qp = a.query_rows ? a.data + static_cast<uint64_t>(a.query_rows[q]) * a.stride
+                                     : a.queries + static_cast<uint64_t>(q) * a.stride;
+    const int sub = lane & (LPR - 1);
+    uint4 qr[CPL];
+#pragma unroll
+    for (int c = 0; c < CPL; c++) {
+      const uint32_t ch = sub + c * LPR;
+      qr[c] = ch < nch ? __ldg(reinterpret_cast<const uint4*>(qp) + ch) : make_uint4(0, 0, 0, 0);
+    }
+    const uint32_t start = a.start_override ? a.start_override[q] : a.start;
+    uint32_t* table = nullptr;
+    uint64_t seed = 0;
+    const uint32_t LL = L * L;
+    if (a.visited_mode == 1) {
+      table = a.ref_table + static_cast<uint64_t>(q) * LL;
+      for (uint32_t i = lane; i < LL; i += 32) table[i] = kNone;
+      // search_seed — src/search.cpp:52-58 (rows are zero padded to >= 16 bytes,
+      // which equals the reference's zero-filled copy of the first min(16, bytes))
+      const uint64_t* q64 = reinterpret_cast<const uint64_t*>(qp);
+      const uint64_t h = mix64(start, a.dim);
+      seed = mix64(h ^ q64[0], q64[1]);
+    } else {
+      for (uint32_t i = lane; i < H; i += 32) hash[i] = kNone;
+    }
+    if (lane == 0) cid[0] = start;
+    __syncwarp();
+    eval_rows<Op, LPR, CPL>(a.data, a.stride, nch, cid, 1, ck, qr, lane);
+    uint32_t drops = 0;
+    __syncwarp();
+    if (lane == 0) {
+      beamA[0] = ck[0];
+      flA[0] = 0;
+      if (a.visited_mode == 1)
+        table[mix64(static_cast<uint64_t>(start) ^ seed) % LL] = start;
+      else
+        hash_insert(hash, a.hash_log2, start, drops);
+    }
+    uint64_t* beam = beamA;
+    uint64_t* nbeam = beamB;
+    uint8_t* fl = flA;
+    uint8_t* nfl = flB;
+    uint32_t size = 1, nvis = 0;
+    uint64_t evals = 1, adjsum = 0;
+    __syncwarp();
+
+    while (true) {
+      __syncwarp();
+      int fu = -1;
+      for (uint32_t b0 = 0; b0 < size; b0 += 32) {
+        const uint32_t i = b0 + lane;
+        const uint32_t bal = __ballot_sync(FULL, i < size && fl[i] == 0);
+        if (bal) {
+          fu = static_cast<int>(b0 + __ffs(bal) - 1);
+          break;
+        }
+      }
+      if (fu < 0) break;
+      const uint64_t fk = beam[fu];
+      if (a.k_gate <= size) {  // k-gate + epsilon, src/search.cpp:105-107
+        const float bk = key_dist(beam[a.k_gate - 1]);
+        const float lim = __fadd_rn(bk, __fmul_rn(a.eps, fabsf(bk)));
+        if (key_dist(fk) > lim) break;
+      }
+      const uint32_t cur = key_id(fk);
+      __syncwarp();
+      if (lane == 0) {
+        fl[fu] = 1;
+        if (a.vis_ids && nvis < a.vcap) {
+          a.vis_ids[static_cast<uint64_t>(q) * a.vcap + nvis] = cur;
+          a.vis_dists[static_cast<uint64_t>(q) * a.vcap + nvis] = key_dist(fk);
+        }
+      }
+      nvis++;
+
+      // ---- neighbours through the visited filter (adjacency order kept) ----
+      uint32_t m = 0;
+      const uint32_t* row = a.adj + static_cast<uint64_t>(cur) * R;
+      for (uint32_t t0 = 0; t0 < R; t0 += 32) {
+        const uint32_t t = t0 + lane;
+        const uint32_t nb = t < R ? __ldg(row + t) : kNone;
+        const bool valid = nb != kNone;
+        adjsum += __popc(__ballot_sync(FULL, valid));
+        bool fresh;
+        if (a.visited_mode == 1) {
+          const uint32_t slot =
+              valid ? static_cast<uint32_t>(mix64(static_cast<uint64_t>(nb) ^ seed) % LL) : kNone;
+          const uint32_t peers = __match_any_sync(FULL, slot);
+          const bool first = (__ffs(peers) - 1) == lane;
+          const bool last = (31 - __clz(peers)) == lane;
+          const uint32_t tv = valid ? table[slot] : 0u;
+          const bool seen = valid && first && tv == nb;
+          __syncwarp();
+          if (valid && last) table[slot] = nb;
+          __syncwarp();
+          fresh = valid && !seen;
+        } else {
+          fresh = valid && hash_insert(hash, a.hash_log2, nb, drops);
+        }
+        const uint32_t bal = __ballot_sync(FULL, fresh);
+        if (fresh) cid[m + __popc(bal & lanemask_lt(lane))] = nb;
+        m += __popc(bal);
+      }
+      if (m == 0) continue;
+      __syncwarp();
+      evals += m;
+      eval_rows<Op, LPR, CPL>(a.data, a.stride, nch, cid, m, ck, qr, lane);
+      __syncwarp();
+
+      // ---- merge: top-L of beam U new, exact duplicates dropped ----
+      const uint64_t worst = size == L ? beam[L - 1] : kMaxKey;
+      uint32_t s = 0;
+      for (uint32_t i0 = 0; i0 < m; i0 += 32) {
+        const uint32_t i = i0 + lane;
+        const uint64_t k = i < m ? ck[i] : kMaxKey;
+        bool keep = k < worst;
+        uint32_t pb = 0;
+        if (keep) {
+          pb = lower_bound_u64(beam, size, k);
+          if (pb < size && beam[pb] == k) keep = false;
+        }
+        const uint32_t bal = __ballot_sync(FULL, keep);
+        if (keep) {
+          const uint32_t o = s + __popc(bal & lanemask_lt(lane));
+          tmpk[o] = k;
+          posb[o] = pb;
+        }
+        s += __popc(bal);
+      }
+      if (s == 0) continue;
+      __syncwarp();
+      for (uint32_t j0 = 0; j0 < s; j0 += 32) {
+        const uint32_t j = j0 + lane;
+        if (j < s) {
+          const uint64_t k = tmpk[j];
+          uint32_t r = 0;
+          for (uint32_t t = 0; t < s; t++) r += tmpk[t] < k ? 1u : 0u;
+          srt[r] = k;
+          const uint32_t fin = posb[j] + r;
+          if (fin < L) {
+            nbeam[fin] = k;
+            nfl[fin] = 0;
+          }
+        }
+      }
+      __syncwarp();
+      for (uint32_t i0 = 0; i0 < size; i0 += 32) {
+        const uint32_t i = i0 + lane;
+        if (i < size) {
+          const uint64_t k = beam[i];
+          const uint32_t fin = i + lower_bound_u64(srt, s, k);
+          if (fin < L) {
+            nbeam[fin] = k;
+            nfl[fin] = fl[i];
+          }
+        }
+      }
+      size = min(L, size + s);
+      uint64_t* tb = beam; beam = nbeam; nbeam = tb;
+      uint8_t* tf = fl; fl = nfl; nfl = tf;
+    }
+
+    __syncwarp();
+    // neighbors = top-k of V == beam prefix (every key above the first
+    // unexpanded one has been expanded; k_out <= k_gate is enforced by the host)
+    if (a.out_ids) {
+      for (uint32_t i = lane; i < a.k_out; i += 32) {
+        const bool have = i < size;
+        a.out_ids[static_cast<uint64_t>(q) * a.k_out + i] = have ? key_id(beam[i]) : kNone;
+        a.out_dists[static_cast<uint64_t>(q) * a.k_out + i] =
+            have ? key_dist(beam[i]) : __int_as_float(0x7f800000);
+      }
+    }
+    if (lane == 0) {
+      if (a.n_visited) a.n_visited[q] = nvis;
+      if (a.dist_comps) a.dist_comps[q] = evals;
+      if (a.vis_ids && nvis > a.vcap) atomicAdd(a.overflow, 1u);
+      if (a.stats) {
+        atomicAdd(a.stats + kStQueries, 1ull);
+        atomicAdd(a.stats + kStExpansions, static_cast<unsigned long long>(nvis));
+        atomicAdd(a.stats + kStEvals, static_cast<unsigned long long>(evals));
+        atomicAdd(a.stats + kStDrops, static_cast<unsigned long long>(drops));
+        atomicAdd(a.stats + kStAdj, static_cast<unsigned long long>(adjsum));
+      }
+    }
+    __syncwarp();
+  }
+}
+
+namespace {
+template <int E, int M, int LPR, int CPL>
+cudaError_t launch_one(const SearchArgs& a, cudaStream_t s) {
+  const uint32_t per_warp = static_cast<uint32_t>(search_smem_per_warp(a.L, a.R, a.hash_log2));
+  const size_t smem = size_t(per_warp) * kWarpsPerBlock;
+  auto k = search_kernel<E, M, LPR, CPL>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  const uint32_t blocks = (a.nq + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  if (blocks == 0) return cudaSuccess;
+  k<<<blocks, kWarpsPerBlock * 32, smem, s>>>(a, per_warp);
+  return cudaGetLastError();
+}
+
+template <int E, int M>
+cudaError_t dispatch_geom(const SearchArgs& a, const Geometry& g, cudaStream_t s) {
+  switch (g.lpr) {
+    case 1: return launch_one<E, M, 1, 1>(a, s);
+    case 2: return launch_one<E, M, 2, 1>(a, s);
+    case 4: return launch_one<E, M, 4, 1>(a, s);
+    case 8: return launch_one<E, M, 8, 1>(a, s);
+    case 16: return launch_one<E, M, 16, 1>(a, s);
+    default:
+      if (g.cpl == 1) return launch_one<E, M, 32, 1>(a, s);
+      if (g.cpl == 2) return launch_one<E, M, 32, 2>(a, s);
+      return launch_one<E, M, 32, 4>(a, s);
+  }
+}
+}  // namespace
+
+Geometry make_geometry(uint32_t nch) {
+  Geometry g{nch, 32, 1};
+  if (nch <= 32) {
+    int l = 1;
+    while (static_cast<uint32_t>(l) < nch) l <<= 1;
+    g.lpr = l;
+    g.cpl = 1;
+  } else {
+    g.lpr = 32;
+    g.cpl = nch <= 64 ? 2 : 4;
+  }
+  return g;
+}
+
+cudaError_t launch_search(const SearchArgs& a, int elem, int metric, const Geometry& g,
+                          cudaStream_t s) {
+  if (metric == kL2) {
+    if (elem == kU8) return dispatch_geom<kU8, kL2>(a, g, s);
+    if (elem == kI8) return dispatch_geom<kI8, kL2>(a, g, s);
+    return dispatch_geom<kF32, kL2>(a, g, s);
+  }
+  if (elem == kU8) return dispatch_geom<kU8, kIP>(a, g, s);
+  if (elem == kI8) return dispatch_geom<kI8, kIP>(a, g, s);
+  return dispatch_geom<kF32, kIP>(a, g, s);
+}
+
+}  // namespace gann
