@@ -1,0 +1,441 @@
+#!/usr/bin/env python
+"""Benchmark: batched beam-search QPS at recall@10 >= 0.95 over a B200-built
+Vamana graph (BASELINE config 1: 10M x 128 u8, R64 L128 alpha 1.2), plus the
+build's points/s, the search kernel's HBM roofline, the end-to-end QPS through
+the C ABI with host buffers, and the reference's CPU search timed beside it.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1] [--n N]
+  python bench.py --impl reference ...     # the reference's own CPU path
+
+A step is one search launch over one batch of 10,000 queries per GPU (the
+config's query set); the index (1.28 GB vectors + 2.56 GB graph) is larger
+than L2, so no flush is needed between steps (smaller indexes are flushed).
+Multi-GPU: one process per GPU, the index is rebuilt identically on every rank
+(the build is deterministic; a checksum all-gather verifies the replicas) and
+each rank searches its own 10k-query shard — no data-path collective
+("scaling": "weak"). Timing: CUDA events on the launching stream, barrier +
+synchronize on both sides, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import importlib.util
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+L_CANDIDATES = [10, 12, 14, 16, 20, 24, 28, 32, 40, 48, 56, 64, 80, 96, 128, 160, 200]
+GT_DEPTH = 16
+
+
+def load_module(name, rel):
+    spec = importlib.util.spec_from_file_location(name, ROOT / rel)
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules[name] = mod
+    spec.loader.exec_module(mod)
+    return mod
+
+
+# datagen / evalutil are plain numpy: load them without importing the package
+# (which loads libgann_b200.so) so the reference arm never touches our library.
+datagen = load_module("gann_datagen", "paper_2305_04359_b200/datagen.py")
+evalutil = load_module("gann_evalutil", "paper_2305_04359_b200/evalutil.py")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c1")
+    ap.add_argument("--n", type=int, default=0, help="override the config's n (debug)")
+    ap.add_argument("--nq", type=int, default=0, help="queries per GPU (default: the config's)")
+    ap.add_argument("--target-recall", type=float, default=0.95)
+    ap.add_argument("--L", type=int, default=0, help="force the search beam")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="CPU baseline sample length")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--ref-n", type=int, default=100_000, help="reference arm: points in its CPU build sample")
+    return ap.parse_args()
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    FIELDS = ["clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.active",
+              "clocks_event_reasons.hw_slowdown", "clocks_event_reasons.hw_thermal_slowdown",
+              "clocks_event_reasons.sw_thermal_slowdown", "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = Path(f"/tmp/gann_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        time.sleep(0.2)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.1)
+        self.proc.terminate()
+        self.proc.wait()
+        rows = [l.split(", ") for l in self.path.read_text().strip().splitlines() if l.count(",") >= 7]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        sm = []
+        smax = None
+        for r in rows:
+            try:
+                sm.append(float(r[0]))
+                smax = float(r[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, r[4:8]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        loaded = [s for s in sm if smax and s > 0.5 * smax] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def search_bytes(stats: dict, row_bytes: int, nq: int, k: int) -> float:
+    """Algorithmic bytes of the search: every distinct evaluated
+    row once (evaluations - filter drops, a lower bound on the distinct count),
+    every expanded adjacency row (deg + 1 words), the queries and the results."""
+    distinct = stats["evaluations"] - stats["filter_drops"]
+    return (distinct * row_bytes + 4.0 * (stats["expansions"] + stats["adj_entries"])
+            + nq * row_bytes + 8.0 * k * nq)
+
+
+def traffic_from_profile(name: str):
+    p = ROOT / "profiles" / "traffic.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d.get(name)
+    return None
+
+
+# ---------------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    # a dedicated stream: torch's legacy default stream has handle 0, which the C
+    # ABI reads as "the index's own stream"
+    torch.cuda.set_stream(torch.cuda.Stream())
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2305_04359_b200 as g
+    from paper_2305_04359_b200._lib import check, lib
+
+    cfg = datagen.CONFIGS[args.config]
+    if args.n:
+        cfg = cfg.scaled(args.n)
+    nq = args.nq or cfg.n_queries
+    n, d, k = cfg.n, cfg.d, cfg.k
+    dev = local
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def allreduce(x, op="max"):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+        return float(t.item())
+
+    # ---- data: generated straight into HBM ------------------------------------------
+    base = torch.empty(n * d, dtype=torch.uint8, device="cuda")
+    check(lib().gann_generate_u8(base.data_ptr(), n, d, cfg.clusters, cfg.sigma, cfg.noise_frac,
+                                 cfg.center_seed, cfg.base_seed, 0, dev))
+    qdev = torch.empty(nq * d, dtype=torch.uint8, device="cuda")
+    check(lib().gann_generate_u8(qdev.data_ptr(), nq, d, cfg.clusters, cfg.sigma, cfg.noise_frac,
+                                 cfg.center_seed, cfg.query_seed, rank * nq, dev))
+    idx = g.Index.from_device(base.data_ptr(), n, d, np.uint8, cfg.metric, cfg.R, dev)
+
+    # ---- build (timed once) ---------------------------------------------------------------
+    params = g.DiskannParams(cfg.R, cfg.L, cfg.alpha, seed=42, max_batch=cfg.max_batch)
+    idx.reset_stats()
+    barrier()
+    t0 = time.perf_counter()
+    idx.build(params)
+    torch.cuda.synchronize()
+    build_s = allreduce(time.perf_counter() - t0)
+    bstats = idx.stats()
+    adj_t = _tensor_from_ptr(idx.device_ptrs()[2], n * cfg.R * 4).view(torch.int32)  # a view, no copy
+    checksum = int(adj_t.to(torch.int64).mul_(1 + torch.arange(n * cfg.R, device="cuda") % 7919).sum().item())
+    replicas_identical = True
+    if world > 1:
+        sums = [None] * world
+        dist.all_gather_object(sums, checksum)
+        replicas_identical = len(set(sums)) == 1
+    deg_mean = float((adj_t != -1).sum().item()) / n
+    del adj_t
+
+    # ---- ground truth (GPU brute force) and the beam giving recall >= target -----------------
+    gt_ids = torch.empty(nq * GT_DEPTH, dtype=torch.int32, device="cuda")
+    gt_d = torch.empty(nq * GT_DEPTH, dtype=torch.float32, device="cuda")
+    idx.groundtruth_device(qdev.data_ptr(), nq, GT_DEPTH, gt_ids.data_ptr(), gt_d.data_ptr())
+    torch.cuda.synchronize()
+    gt_ids_h = gt_ids.cpu().numpy().view(np.uint32).reshape(nq, GT_DEPTH)
+    gt_d_h = gt_d.cpu().numpy().reshape(nq, GT_DEPTH)
+    idx.stage_queries(qdev.data_ptr(), nq)
+    out_ids = torch.empty(nq * k, dtype=torch.int32, device="cuda")
+    out_d = torch.empty(nq * k, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream().cuda_stream
+
+    def search_L(L):
+        idx.search_staged(g.SearchParams(L, L, 0.0), k, out_ids.data_ptr(), out_d.data_ptr(), stream)
+
+    curve = []
+    chosen = args.L
+    for L in ([args.L] if args.L else L_CANDIDATES):
+        search_L(L)
+        torch.cuda.synchronize()
+        res = out_ids.cpu().numpy().view(np.uint32).reshape(nq, k)
+        rec = float(evalutil.recall_at_k(gt_ids_h, gt_d_h, res, k).mean())
+        rec = allreduce(rec, "sum") / world
+        curve.append({"L": L, "recall@10": round(rec, 5)})
+        if not args.L and rec >= args.target_recall:
+            chosen = L
+            break
+    if not chosen:
+        chosen = L_CANDIDATES[-1]
+    recall = curve[-1]["recall@10"]
+    sp = g.SearchParams(chosen, chosen, 0.0)
+
+    # ---- timed search steps --------------------------------------------------------
+    l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
+    index_bytes = n * (d + 4 * cfg.R)
+    flush = index_bytes < 2 * l2_bytes
+    flush_buf = torch.empty(max(4 * l2_bytes, 1), dtype=torch.uint8, device="cuda") if flush else None
+    for _ in range(args.warmup):
+        search_L(chosen)
+    idx.reset_stats()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    sampler = ClockSampler(dev)
+    sampler.start()
+    barrier()
+    for e0, e1 in evs:
+        if flush:
+            flush_buf.fill_(1)
+        e0.record()
+        idx.search_staged(sp, k, out_ids.data_ptr(), out_d.data_ptr(), stream)
+        e1.record()
+    barrier()
+    clocks = sampler.stop()
+    step_ms = [e0.elapsed_time(e1) for e0, e1 in evs]
+    total_ms = allreduce(sum(step_ms))
+    sstats = idx.stats()
+    qps = world * nq * args.steps / (total_ms / 1e3)
+    per_launch_bytes = search_bytes(sstats, d, nq * args.steps, k) / args.steps
+    avg_launch_s = statistics.mean(step_ms) / 1e3
+    peak, peak_src = peaks()
+    achieved = per_launch_bytes / avg_launch_s / 1e9
+
+    # ---- end to end through the C ABI with host buffers -------------------------------------
+    import ctypes as C
+    qh = torch.empty((nq, d), dtype=torch.uint8).pin_memory()
+    qh.copy_(qdev.view(nq, d).cpu())
+    ih = torch.empty((nq, k), dtype=torch.int32).pin_memory()
+    dh = torch.empty((nq, k), dtype=torch.float32).pin_memory()
+    L_ = lib()
+
+    def e2e_step():
+        check(L_.gann_search(idx.handle, C.c_void_p(qh.data_ptr()), nq, k, chosen, chosen, 0.0, 0, None,
+                             C.c_void_p(ih.data_ptr()), C.c_void_p(dh.data_ptr()), None, None, None, None, 0))
+
+    for _ in range(args.warmup):
+        e2e_step()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        e2e_step()
+    barrier()
+    e2e_s = allreduce(time.perf_counter() - t0)
+    e2e_match = bool((ih.numpy().view(np.uint32) == out_ids.cpu().numpy().view(np.uint32).reshape(nq, k)).all())
+
+    # ---- CPU baseline: the reference's beam_search over the same graph, rank 0 at N=1 ------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline_search(idx, base, qh.numpy(), chosen, k, args.cpu_seconds, out_ids, nq)
+
+    build_bytes = search_bytes(bstats, d, bstats["queries"], 0)
+    build_search_ms = bstats["build_ms"]["search"]
+    line = {
+        "metric": "search QPS at recall@10>=0.95 (Alg.1 beam {L,L,0}, top-10) over a B200-built Vamana graph",
+        "value": round(qps, 1),
+        "unit": "queries/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(total_ms / args.steps, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u8",
+        "data": "synthetic: seeded Gaussian mixture with BASELINE config shapes (datagen.py), generated in HBM",
+        "config": {
+            "workload": f"BASELINE configs[1]: {cfg.name}",
+            "n": n, "d": d, "R": cfg.R, "L_build": cfg.L, "alpha": cfg.alpha,
+            "max_batch": cfg.max_batch, "queries_per_gpu": nq, "k": k,
+            "L_search": chosen, "recall@10": recall, "target_recall": args.target_recall,
+            "l2": "flushed between steps" if flush else f"inputs larger than L2 ({index_bytes / 1e9:.2f} GB index)",
+        },
+        "roofline": {
+            "bound": "hbm", "kernel": "search_kernel", "achieved": round(achieved, 1), "peak": peak,
+            "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
+            "algorithmic_bytes_per_launch": round(per_launch_bytes),
+            "avg_launch_ms": round(avg_launch_s * 1e3, 4),
+            "traffic": traffic_from_profile("search_kernel"),
+            "filter_drops": sstats["filter_drops"],
+        },
+        "cpu_baseline": cpu,
+        "e2e": {"value": round(world * nq * args.steps / e2e_s, 1), "unit": "queries/s",
+                "h2d_bytes_per_step": nq * d, "d2h_bytes_per_step": nq * k * 8,
+                "api": "gann_search (host buffers, pinned)", "ids_match_device_path": e2e_match},
+        "gpu_launches": args.steps,
+        "clocks": clocks,
+        "build": {
+            "points_per_s": round(n / build_s, 1), "seconds": round(build_s, 3),
+            "phases_ms": {kk: round(v, 1) for kk, v in bstats["build_ms"].items()},
+            "mean_degree": round(deg_mean, 3), "replicas_identical": replicas_identical,
+            "search_roofline": {"achieved": round(build_bytes / (build_search_ms / 1e3) / 1e9, 1) if build_search_ms else None,
+                                "unit": "GB/s", "frac": round(build_bytes / (build_search_ms / 1e3) / 1e9 / peak, 4) if build_search_ms else None},
+            "stats": {kk: v for kk, v in bstats.items() if kk != "build_ms"},
+        },
+        "recall_curve": curve,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _tensor_from_ptr(ptr, nbytes):
+    """A torch uint8 view of device memory owned by the index."""
+    import torch
+
+    class _Holder:
+        def __init__(self, p, n):
+            self.__cuda_array_interface__ = {"shape": (n,), "typestr": "|u1", "data": (p, False), "version": 3}
+
+    return torch.as_tensor(_Holder(ptr, nbytes), device="cuda")
+
+
+def cpu_baseline_search(idx, base, q_host, L, k, seconds, out_ids, nq):
+    from oracle.oracle import Oracle, available
+    kind = "reference" if available("ref") else "port"
+    orc = Oracle("ref" if kind == "reference" else "orc")
+    adj, _, start = idx.export_graph()
+    data = base.view(idx.n, idx.d).cpu().numpy()
+    secs, ids, reps = orc.time_search(adj, start, data, q_host, L, L, 0.0, k_out=k, workers=0, reps=1,
+                                      min_seconds=seconds)
+    gpu_ids = out_ids.cpu().numpy().view(np.uint32).reshape(nq, k)
+    cores = os.cpu_count()
+    return {"value": round(nq / secs, 1), "unit": "queries/s", "cores": cores, "kind": kind,
+            "sample": f"all {nq} queries per pass, best of {reps} passes (>= {seconds:.0f} s), beam {{L={L},L,0}} over "
+                      f"the same {idx.n}-point graph, parallel_for over queries on {cores} threads",
+            "ids_identical_to_gpu": float((ids == gpu_ids).all(axis=1).mean())}
+
+
+# ---------------------------------------------------------------------------------
+def run_reference(args):
+    """The reference's own CPU path (oracle/_ref: graphann compiled from its
+    sources) on a bounded sample of the same workload."""
+    rank = int(os.environ.get("RANK", 0))
+    if rank != 0:
+        return
+    from oracle.oracle import Oracle, available
+
+    kind = "reference" if available("ref") else "port"
+    orc = Oracle("ref" if kind == "reference" else "orc")
+    cfg = datagen.CONFIGS[args.config]
+    n = min(args.ref_n, args.n or cfg.n)
+    nq = args.nq or cfg.n_queries
+    cap = int(n * cfg.batch_cap_frac) if cfg.batch_cap_frac else 0
+    data = datagen.host_base(cfg, n)
+    q = datagen.gen_u8_numpy(nq, cfg.d, cfg.clusters, cfg.sigma, cfg.noise_frac, cfg.center_seed, cfg.query_seed)
+    cores = os.cpu_count()
+    t0 = time.perf_counter()
+    adj, start = orc.build(data, cfg.R, cfg.L, cfg.alpha, cap=cap, workers=0)
+    build_s = time.perf_counter() - t0
+    gt_i, gt_d = orc.groundtruth(data, q, GT_DEPTH, workers=0)
+    curve, chosen = [], args.L
+    for L in ([args.L] if args.L else L_CANDIDATES):
+        _, ids, _ = orc.time_search(adj, start, data, q, L, L, 0.0, k_out=cfg.k, workers=0, reps=1)
+        rec = float(evalutil.recall_at_k(gt_i, gt_d, ids, cfg.k).mean())
+        curve.append({"L": L, "recall@10": round(rec, 5)})
+        if not args.L and rec >= args.target_recall:
+            chosen = L
+            break
+    chosen = chosen or L_CANDIDATES[-1]
+    for _ in range(args.warmup):
+        orc.time_search(adj, start, data, q, chosen, chosen, 0.0, k_out=cfg.k, workers=0, reps=1)
+    secs = []
+    for _ in range(args.steps):
+        s, _, _ = orc.time_search(adj, start, data, q, chosen, chosen, 0.0, k_out=cfg.k, workers=0, reps=1)
+        secs.append(s)
+    value = nq * args.steps / sum(secs)
+    sample = (f"graphann beam_search {{L={chosen},L,0}} top-10 over all {nq} queries per step, graph built by "
+              f"graphann on the first {n} points of {cfg.name} (batch cap {cap}), parallel_for on {cores} threads")
+    line = {
+        "impl": "reference",
+        "metric": "search QPS at recall@10>=0.95 (Alg.1 beam {L,L,0}, top-10) over a B200-built Vamana graph",
+        "value": round(value, 1), "unit": "queries/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(1e3 * sum(secs) / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic: seeded Gaussian mixture with BASELINE config shapes (datagen.py), host numpy restatement",
+        "config": {"workload": f"BASELINE configs[1]: {cfg.name} (bounded CPU sample: first {n} points)",
+                   "n": n, "d": cfg.d, "R": cfg.R, "L_build": cfg.L, "alpha": cfg.alpha, "max_batch": cap,
+                   "queries": nq, "k": cfg.k, "L_search": chosen, "recall@10": curve[-1]["recall@10"]},
+        "cpu_baseline": {"value": round(value, 1), "unit": "queries/s", "cores": cores, "kind": kind, "sample": sample},
+        "e2e": {"value": round(value, 1), "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "build": {"points_per_s": round(n / build_s, 1), "seconds": round(build_s, 3), "n": n, "cores": cores},
+        "recall_curve": curve,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

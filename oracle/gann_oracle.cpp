@@ -16,6 +16,7 @@
 // it.
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -582,6 +583,35 @@ int orc_groundtruth(const void* data, uint32_t n, const void* queries, uint32_t 
         dists[qi * k + t] = all[t].dist;
       }
     });
+  });
+}
+
+// measure_qps (src/eval.cpp:57-101) restated: threads over queries, best of reps.
+int orc_time_search(const uint32_t* adj, uint32_t n, uint32_t R, uint32_t start, const void* data,
+                    uint32_t d, int elem, int metric, const void* queries, uint32_t nq, uint32_t L,
+                    uint32_t k, float eps, uint32_t k_out, int workers, uint32_t reps,
+                    double min_seconds, uint32_t* ids, double* best_seconds, uint32_t* reps_done) {
+  return guarded([&] {
+    Graph g{const_cast<uint32_t*>(adj), n, R};
+    Data ds{static_cast<const uint8_t*>(data), n, d, elem, metric, d * esize(elem)};
+    const uint8_t* qb = static_cast<const uint8_t*>(queries);
+    double best = 1e300, total = 0.0;
+    uint32_t r = 0;
+    for (; r < reps || total < min_seconds; r++) {
+      auto t0 = std::chrono::steady_clock::now();
+      run_parallel(nq, workers, [&](size_t qi) {
+        SearchOut res = beam_search(g, ds, qb + qi * ds.stride, L, k, eps, 0, start);
+        if (r == 0 && ids)
+          for (uint32_t t = 0; t < k_out; t++)
+            ids[qi * k_out + t] = t < res.neighbors.size() ? res.neighbors[t].id : kSent;
+      });
+      double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      best = std::min(best, s);
+      total += s;
+      if (r >= 1000) break;
+    }
+    *best_seconds = best;
+    if (reps_done) *reps_done = r;
   });
 }
 

@@ -81,6 +81,8 @@ class Oracle:
         f("apply_back_edges").argtypes = [vp, u32, u32, vp, u32, i32, i32, vp, vp, u64, f32, i32, i32]
         f("build").argtypes = [vp, u32, u32, i32, i32, u32, u32, f32, i32, u64, u32, i32, vp, vp]
         f("groundtruth").argtypes = [vp, u32, vp, u32, u32, i32, i32, u32, vp, vp, i32]
+        f("time_search").argtypes = [vp, u32, u32, u32, vp, u32, i32, i32, vp, u32, u32, u32, f32, u32, i32,
+                                     u32, C.c_double, vp, vp, vp]
         f("recall").restype = C.c_double
         f("recall").argtypes = [vp, vp, u32, vp, u32, u32]
         self._f = f
@@ -201,6 +203,23 @@ class Oracle:
         self._check(self._f("groundtruth")(_p(data), data.shape[0], _p(queries), nq, data.shape[1],
                                            ELEM[data.dtype], METRIC[metric], k, _p(ids), _p(dists), workers))
         return ids, dists
+
+    def time_search(self, adj, start, data, queries, L, k, eps=0.0, k_out=10, metric="l2", workers=0,
+                    reps=3, min_seconds=0.0):
+        """Best-of-reps wall seconds for one pass over the queries (measure_qps),
+        plus the first pass's top-k_out ids."""
+        adj = np.ascontiguousarray(adj, dtype=np.uint32)
+        data = np.ascontiguousarray(data)
+        queries = np.ascontiguousarray(queries, dtype=data.dtype)
+        n, R = adj.shape
+        nq = queries.shape[0]
+        ids = np.empty((nq, k_out), np.uint32)
+        best = np.zeros(1, np.float64)
+        done = np.zeros(1, np.uint32)
+        self._check(self._f("time_search")(_p(adj), n, R, start, _p(data), data.shape[1], ELEM[data.dtype],
+                                           METRIC[metric], _p(queries), nq, L, k, eps, k_out, workers, reps,
+                                           min_seconds, _p(ids), _p(best), _p(done)))
+        return float(best[0]), ids, int(done[0])
 
     def recall(self, truth_ids, truth_dists, result, k):
         ti = np.ascontiguousarray(truth_ids, dtype=np.uint32)

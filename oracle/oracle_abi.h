@@ -56,6 +56,11 @@
   int P##groundtruth(const void* data, uint32_t n, const void* queries, uint32_t nq,          \
                      uint32_t d, int elem, int metric, uint32_t k, uint32_t* ids,             \
                      float* dists, int workers);                                              \
+  int P##time_search(const uint32_t* adj, uint32_t n, uint32_t R, uint32_t start,              \
+                     const void* data, uint32_t d, int elem, int metric, const void* queries,  \
+                     uint32_t nq, uint32_t L, uint32_t k, float eps, uint32_t k_out,           \
+                     int workers, uint32_t reps, double min_seconds, uint32_t* ids,            \
+                     double* best_seconds, uint32_t* reps_done);                               \
   double P##recall(const uint32_t* truth_ids, const float* truth_dists, uint32_t depth,       \
                    const uint32_t* result, uint32_t n_result, uint32_t k);
 

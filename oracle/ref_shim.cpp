@@ -18,6 +18,7 @@
 //                        public API
 //   ref_groundtruth      graphann::compute_groundtruth (src/dataset.cpp:172)
 //   ref_recall           graphann::recall_k_at_n      (src/eval.cpp:14)
+#include <chrono>
 #include <cstring>
 #include <limits>
 #include <span>
@@ -289,6 +290,39 @@ int ref_groundtruth(const void* data, uint32_t n, const void* queries, uint32_t 
         compute_groundtruth(ds, qs, k, met(metric), static_cast<size_t>(workers < 0 ? 0 : workers));
     std::copy(gt.ids.begin(), gt.ids.end(), ids);
     std::copy(gt.dists.begin(), gt.dists.end(), dists);
+  });
+}
+
+// measure_qps (src/eval.cpp:57-101): parallel_for over the queries, best of
+// `reps` passes (at least `reps`, continuing until min_seconds of work).
+int ref_time_search(const uint32_t* adj, uint32_t n, uint32_t R, uint32_t start, const void* data,
+                    uint32_t d, int elem, int metric, const void* queries, uint32_t nq, uint32_t L,
+                    uint32_t k, float eps, uint32_t k_out, int workers, uint32_t reps,
+                    double min_seconds, uint32_t* ids, double* best_seconds, uint32_t* reps_done) {
+  return guarded([&] {
+    VectorDataset ds = make_ds(data, n, d, elem);
+    NeighborGraph g = make_graph(adj, n, R, start);
+    const size_t stride = ds.stride();
+    const std::byte* qb = static_cast<const std::byte*>(queries);
+    SearchParams sp{L, k, eps};
+    double best = 1e300, total = 0.0;
+    uint32_t r = 0;
+    for (; r < reps || total < min_seconds; r++) {
+      auto t0 = std::chrono::steady_clock::now();
+      parallel_for(nq, static_cast<size_t>(workers < 0 ? 0 : workers), [&](size_t qi, size_t) {
+        VectorView q{qb + qi * stride, d, kind(elem)};
+        SearchResult res = beam_search(g, ds, met(metric), q, sp);
+        if (r == 0 && ids)
+          for (uint32_t t = 0; t < k_out; t++)
+            ids[qi * k_out + t] = t < res.neighbors.size() ? res.neighbors[t].id : kSent;
+      });
+      double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      best = std::min(best, s);
+      total += s;
+      if (r >= 1000) break;
+    }
+    *best_seconds = best;
+    if (reps_done) *reps_done = r;
   });
 }
 

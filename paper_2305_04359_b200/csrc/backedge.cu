@@ -286,6 +286,96 @@ __global__ void __launch_bounds__(NT)
   }
 }
 
+// Hubs of the batch form (more sources than the small path handles, so the
+// merged list certainly exceeds R): the list goes to alpha_prune, which sorts
+// it by (dist, id), so pair order is irrelevant and no ordinal sort is needed.
+// Sources are distinct per target in the batch form (each inserted point
+// contributes at most one pair per target), so only the row check remains.
+template <int E, int M, int LPR, int CPL, int NT>
+__global__ void __launch_bounds__(NT)
+    be_merge_hub_kernel(const BackEdgeArgs a, const uint32_t nbig) {
+  using Op = DistOp<E, M>;
+  constexpr int GROUPS = NT / LPR;
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ uint32_t sh_deg, sh_kept;
+  uint32_t* row = reinterpret_cast<uint32_t*>(smem);
+  const int tid = threadIdx.x;
+  const uint32_t R = a.R;
+  const uint32_t nch = static_cast<uint32_t>(a.stride >> 4);
+  for (uint32_t gi = blockIdx.x; gi < nbig; gi += gridDim.x) {
+    const uint32_t g = a.big_groups[gi];
+    const uint32_t c = a.gcnt[g];
+    const uint32_t t = a.gtarget[g];
+    const uint64_t go = a.goff[g];
+    uint32_t* trow = a.adj + uint64_t(t) * R;
+    if (tid == 0) {
+      sh_deg = 0;
+      sh_kept = 0;
+    }
+    __syncthreads();
+    for (uint32_t i = tid; i < R; i += NT) {
+      const uint32_t v = trow[i];
+      row[i] = v;
+      if (v != kNone) atomicAdd(&sh_deg, 1u);
+    }
+    __syncthreads();
+    const uint32_t deg = sh_deg;
+    uint32_t* pid = a.pid + a.poff[g];
+    for (uint32_t i = tid; i < deg; i += NT) pid[i] = row[i];
+    for (uint32_t i = tid; i < c; i += NT) {
+      const uint32_t s = pair_source(a, a.gsrc[go + i]);
+      bool keep = true;
+      for (uint32_t j = 0; j < deg && keep; j++) keep = row[j] != s;
+      if (keep) pid[deg + atomicAdd(&sh_kept, 1u)] = s;
+    }
+    __syncthreads();
+    const uint32_t nm = deg + sh_kept;
+    const int sub = tid & (LPR - 1), grp = tid / LPR;
+    uint4 tr[CPL];
+    const uint8_t* tp = a.data + uint64_t(t) * a.stride;
+#pragma unroll
+    for (int cc = 0; cc < CPL; cc++) {
+      const uint32_t ch = sub + cc * LPR;
+      tr[cc] = ch < nch ? __ldg(reinterpret_cast<const uint4*>(tp) + ch) : make_uint4(0, 0, 0, 0);
+    }
+    float* pd = a.pdist + a.poff[g];
+    constexpr int U = 4;
+    for (uint32_t b0 = 0; b0 < nm; b0 += GROUPS * U) {
+      uint4 x[U][CPL];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const uint32_t r = b0 + u * GROUPS + grp;
+        const uint32_t id = r < nm ? pid[r] : 0u;
+        const uint8_t* rp = a.data + uint64_t(id) * a.stride;
+#pragma unroll
+        for (int cc = 0; cc < CPL; cc++) {
+          const uint32_t ch = sub + cc * LPR;
+          x[u][cc] = (r < nm && ch < nch) ? __ldg(reinterpret_cast<const uint4*>(rp) + ch)
+                                         : make_uint4(0, 0, 0, 0);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        typename Op::acc_t acc = Op::zero();
+#pragma unroll
+        for (int cc = 0; cc < CPL; cc++) acc = Op::chunk(tr[cc], x[u][cc], acc);
+        acc = group_sum<LPR>(acc);
+        const uint32_t r = b0 + u * GROUPS + grp;
+        if (sub == 0 && r < nm) pd[r] = Op::finish(acc);
+      }
+    }
+    if (tid == 0) {
+      a.plen[g] = nm;
+      atomicMax(a.counters + kCntMaxMerged, static_cast<unsigned long long>(nm));
+      if (nm <= R) atomicAdd(a.counters + kCntTooBig, 1ull);  // cannot happen (c > R); flagged
+      const uint32_t i = static_cast<uint32_t>(atomicAdd(a.counters + kCntPruneBig, 1ull));
+      a.plist_big[i] = g;
+      a.tcount[t] = 0;
+    }
+    __syncthreads();
+  }
+}
+
 template <int E, int M, int LPR, int CPL, int MODE>
 cudaError_t merge_launch(const BackEdgeArgs& a, uint32_t ng, uint32_t nbig, uint32_t* ok,
                          uint32_t* ov, cudaStream_t s) {
@@ -297,7 +387,14 @@ cudaError_t merge_launch(const BackEdgeArgs& a, uint32_t ng, uint32_t nbig, uint
     k<<<ng, 32, smem, s>>>(a, ng, nullptr, a.small_group_cap, ok, ov);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
-  if (nbig > 0) {
+  if (nbig > 0 && MODE == 0 && a.sources_distinct) {
+    auto k = be_merge_hub_kernel<E, M, LPR, CPL, 512>;
+    const size_t smem = size_t(a.R) * 4;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    k<<<nbig, 512, smem, s>>>(a, nbig);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  } else if (nbig > 0) {
     auto k = be_merge_kernel<E, M, LPR, CPL, 512, MODE>;
     const size_t smem = backedge_merge_smem(a.big_group_cap, a.R);
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));

@@ -258,10 +258,15 @@ void run_search(gann_index* idx, SearchArgs a, cudaStream_t s) {
   cu(launch_search(a, idx->elem, idx->metric, idx->geom, s), "search kernel");
 }
 
+// Lists up to kPruneSmallCap are pruned by one warp; longer ones by the
+// chunked CTA kernel (any length). Back-edge groups up to kSmallGroupCap
+// sources are merged by one warp with an in-order sort; bigger (hub) groups of
+// the batch form need no order (they always re-prune). kSortedGroupCap bounds
+// the order-preserving path for explicit pairs (group_by_key,
+// apply_back_edges with possibly repeated pairs).
 constexpr uint32_t kPruneSmallCap = 512;
-constexpr uint32_t kPruneBigCap = 16384;
 constexpr uint32_t kSmallGroupCap = 256;
-constexpr uint32_t kBigGroupCap = 32768;
+constexpr uint32_t kSortedGroupCap = 32768;
 
 PruneArgs base_prune_args(gann_index* idx, float alpha, int rule) {
   PruneArgs p{};
@@ -304,7 +309,7 @@ struct Timer {
 void insert_batch(gann_index* idx, const uint32_t* d_ids, uint32_t B, uint32_t L, float alpha,
                   int rule, bool timed) {
   if (B == 0) return;
-  const uint32_t vcap = std::max<uint32_t>(64, 3 * L);
+  const uint32_t vcap = std::max<uint32_t>(1, env_u32("GANN_VCAP", std::max<uint32_t>(64, 3 * L)));
   idx->vis_ids.ensure(size_t(B) * vcap * 4);
   idx->vis_d.ensure(size_t(B) * vcap * 4);
   idx->nvis.ensure(size_t(B) * 4);
@@ -334,9 +339,49 @@ void insert_batch(gann_index* idx, const uint32_t* d_ids, uint32_t B, uint32_t L
   uint32_t fl[2];
   cu(cudaMemcpyAsync(fl, idx->flags, 8, cudaMemcpyDeviceToHost, idx->stream), "read flags");
   sync(idx);
-  if (fl[0] || fl[1])
-    fail(GANN_ECUDA, "visited list exceeded its capacity (" + std::to_string(vcap) + ") in " +
-                         std::to_string(fl[0]) + " insert searches");
+  if (fl[0] == 0) return;
+  // Rare long walks (|V| > vcap): their lists were skipped by the prune. Re-run
+  // exactly those searches with room for the whole visited list — the graph
+  // they read is unchanged (batch points are unreachable until phase 2), so
+  // the walk is the same — and prune them with the any-length kernel.
+  std::vector<uint32_t> nv(B), ids(B);
+  cu(cudaMemcpyAsync(nv.data(), idx->nvis.p, size_t(B) * 4, cudaMemcpyDeviceToHost, idx->stream), "read |V|");
+  cu(cudaMemcpyAsync(ids.data(), d_ids, size_t(B) * 4, cudaMemcpyDeviceToHost, idx->stream), "read ids");
+  sync(idx);
+  std::vector<uint32_t> redo;
+  uint32_t vmax = 0;
+  for (uint32_t b = 0; b < B; b++)
+    if (nv[b] > vcap) {
+      redo.push_back(ids[b]);
+      vmax = std::max(vmax, nv[b]);
+    }
+  const uint32_t nr = static_cast<uint32_t>(redo.size());
+  const uint32_t vcap2 = vmax;
+  idx->pt.ensure(size_t(nr) * 4);
+  cu(cudaMemcpyAsync(idx->pt.p, redo.data(), size_t(nr) * 4, cudaMemcpyHostToDevice, idx->stream), "upload");
+  idx->vis_ids.ensure(size_t(nr) * vcap2 * 4);
+  idx->vis_d.ensure(size_t(nr) * vcap2 * 4);
+  cu(cudaMemsetAsync(idx->flags, 0, 8, idx->stream), "memset flags");
+  SearchArgs a2 = a;
+  a2.query_rows = idx->pt.as<uint32_t>();
+  a2.nq = nr;
+  a2.vis_ids = idx->vis_ids.as<uint32_t>();
+  a2.vis_dists = idx->vis_d.as<float>();
+  a2.vcap = vcap2;
+  a2.stats = nullptr;  // counted once already
+  run_search(idx, a2, idx->stream);
+  PruneArgs p2 = p;
+  p2.count = nr;
+  p2.points = idx->pt.as<uint32_t>();
+  p2.fixed_stride = vcap2;
+  p2.cand_ids = a2.vis_ids;
+  p2.cand_dists = a2.vis_dists;
+  p2.mcap = vcap2;
+  cu(launch_prune(p2, idx->elem, idx->metric, idx->geom, vcap2 <= kPruneSmallCap ? 32 : 256, idx->stream),
+     "prune kernel (long walks)");
+  cu(cudaMemcpyAsync(fl, idx->flags, 8, cudaMemcpyDeviceToHost, idx->stream), "read flags");
+  sync(idx);
+  if (fl[0] || fl[1]) fail(GANN_ECUDA, "long-walk re-run overflowed its visited buffer");
 }
 
 // Phase 2: group reverse pairs by target and merge (apply_back_edges).
@@ -366,7 +411,8 @@ void apply_back(gann_index* idx, const uint32_t* bsrc, uint32_t B, const uint32_
   b.tgroup = idx->tgroup;
   b.counters = idx->counters;
   b.small_group_cap = kSmallGroupCap;
-  b.big_group_cap = kBigGroupCap;
+  b.big_group_cap = kSortedGroupCap;
+  if (idx->R > kSmallGroupCap) fail(GANN_EINVAL, "degree bound above 256 is not supported by the back-edge merge");
   b.prune_small_cap = kPruneSmallCap;
   b.key_of_target = key_of_target;
   cu(cudaMemsetAsync(idx->counters, 0, sizeof(unsigned long long) * kCntNum, idx->stream), "memset");
@@ -405,10 +451,9 @@ void apply_back(gann_index* idx, const uint32_t* bsrc, uint32_t B, const uint32_
   cu(cudaMemcpyAsync(cnt, idx->counters, sizeof(cnt), cudaMemcpyDeviceToHost, idx->stream), "read");
   sync(idx);
   const uint32_t nbig = static_cast<uint32_t>(cnt[kCntBig]);
-  if (cnt[kCntMaxGroup] > kBigGroupCap)
-    fail(GANN_ECUDA, "a back-edge group of " + std::to_string(cnt[kCntMaxGroup]) +
-                         " sources exceeds the device cap " + std::to_string(kBigGroupCap) +
-                         "; cap the batch size (max_batch)");
+  if ((out_keys || !b.sources_distinct) && cnt[kCntMaxGroup] > kSortedGroupCap)
+    fail(GANN_EINVAL, "a group of " + std::to_string(cnt[kCntMaxGroup]) + " pairs exceeds the ordered-group cap " +
+                          std::to_string(kSortedGroupCap));
   if (timed) idx->build_ms[3] += tg.stop(); else tg.stop();
   if (out_keys) {  // group_by_key mode
     cu(backedge_write_groups(b, ng, nbig, out_keys, out_vals, idx->stream), "group write");
@@ -424,9 +469,6 @@ void apply_back(gann_index* idx, const uint32_t* bsrc, uint32_t B, const uint32_
   if (cnt[kCntTooBig]) fail(GANN_ECUDA, "back-edge group exceeded the merge capacity");
   const uint32_t nps = static_cast<uint32_t>(cnt[kCntPruneSmall]);
   const uint32_t npb = static_cast<uint32_t>(cnt[kCntPruneBig]);
-  if (cnt[kCntMaxMerged] > kPruneBigCap)
-    fail(GANN_ECUDA, "a merged list of " + std::to_string(cnt[kCntMaxMerged]) +
-                         " candidates exceeds the device prune cap " + std::to_string(kPruneBigCap));
   idx->back_pairs += npairs;
   idx->back_groups += ng;
   idx->back_pruned += nps + npb;
@@ -447,7 +489,7 @@ void apply_back(gann_index* idx, const uint32_t* bsrc, uint32_t B, const uint32_
   if (npb) {
     p.count = npb;
     p.list_index = b.plist_big;
-    p.mcap = kPruneBigCap;
+    p.mcap = 0xFFFFFFFFu;
     cu(launch_prune(p, idx->elem, idx->metric, idx->geom, 256, idx->stream), "reprune big");
   }
   sync(idx);
@@ -826,7 +868,7 @@ int gann_alpha_prune(gann_index* idx, const uint32_t* p, const uint64_t* offsets
       if (offsets[i + 1] < offsets[i]) fail(GANN_EINVAL, "offsets must be non-decreasing");
       beg[i] = offsets[i];
       const uint64_t m = offsets[i + 1] - offsets[i];
-      if (m > kPruneBigCap) fail(GANN_EINVAL, "candidate list longer than " + std::to_string(kPruneBigCap));
+      if (m >= 0xFFFFFFFFull) fail(GANN_EINVAL, "candidate list too long");
       len[i] = static_cast<uint32_t>(m);
       if (p[i] >= idx->n) fail(GANN_EINVAL, "point id out of range");
       (m <= kPruneSmallCap ? small : big).push_back(i);
@@ -874,7 +916,7 @@ int gann_alpha_prune(gann_index* idx, const uint32_t* p, const uint64_t* offsets
     if (!big.empty()) {
       a.count = static_cast<uint32_t>(big.size());
       a.list_index = d_big;
-      a.mcap = kPruneBigCap;
+      a.mcap = 0xFFFFFFFFu;
       cu(launch_prune(a, idx->elem, idx->metric, idx->geom, 256, idx->stream), "prune kernel");
     }
     cu(cudaMemcpyAsync(out, d_out, size_t(count) * idx->R * 4, cudaMemcpyDeviceToHost, idx->stream), "download");

@@ -21,7 +21,7 @@ namespace gann {
 
 size_t prune_smem_bytes(uint32_t mcap, uint32_t R) {
   uint32_t M = 32;
-  while (M < mcap) M <<= 1;
+  while (M < mcap && M < (1u << 16)) M <<= 1;
   size_t b = size_t(M) * 8 + 2 * size_t(M) * 2 + size_t(M) + size_t(R) * 4;
   return (b + 15) & ~size_t(15);
 }
@@ -200,23 +200,264 @@ __global__ void __launch_bounds__(NT) prune_kernel(const PruneArgs a, const uint
   }
 }
 
+// ---- long lists: chunked prune ------------------------------------------------
+// Exact restatement of the same greedy for lists of any length (back-edge
+// hubs). The candidates are consumed in key order, C at a time: a radix select
+// over the (dist, id) keys finds the C smallest keys above the previous
+// chunk's last key; those are sorted in shared memory, first culled by every
+// non-zero-distance selection of the earlier chunks (an element is culled iff
+// some earlier selection's test fires on it — the order of the tests does not
+// matter), then walked greedily as above. Most hubs finish inside the first
+// chunk because R selections are reached long before the list ends.
+constexpr uint32_t kChunk = 4096;
+
+size_t prune_chunked_smem(uint32_t R) {
+  size_t b = size_t(kChunk) * 8 + 2 * size_t(kChunk) * 2 + kChunk + size_t(R) * 8 + 256 * 4;
+  return (b + 15) & ~size_t(15);
+}
+
+template <int E, int M, int LPR, int CPL, int NT>
+__global__ void __launch_bounds__(NT) prune_chunked_kernel(const PruneArgs a) {
+  using Op = DistOp<E, M>;
+  constexpr int GROUPS = NT / LPR;
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ uint32_t warp_tot[NT / 32];
+  __shared__ uint32_t sh_cnt;
+  __shared__ uint64_t sh_prefix;
+  __shared__ uint32_t sh_want;
+  __shared__ unsigned long long sh_evals;
+  uint64_t* keys = reinterpret_cast<uint64_t*>(smem);
+  uint16_t* alA = reinterpret_cast<uint16_t*>(keys + kChunk);
+  uint16_t* alB = alA + kChunk;
+  uint8_t* kf = reinterpret_cast<uint8_t*>(alB + kChunk);
+  uint32_t* sel = reinterpret_cast<uint32_t*>(kf + kChunk);
+  float* seld = reinterpret_cast<float*>(sel + a.R);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(seld + a.R);
+  const int tid = threadIdx.x;
+  const int sub = tid & (LPR - 1);
+  const int grp = tid / LPR;
+  const uint32_t nch = static_cast<uint32_t>(a.stride >> 4);
+  const uint32_t R = a.R;
+
+  for (uint32_t li = blockIdx.x; li < a.count; li += gridDim.x) {
+    const uint32_t l = a.list_index ? a.list_index[li] : li;
+    const uint32_t p = a.points[l];
+    const uint64_t beg = a.begins ? a.begins[l] : uint64_t(l) * a.fixed_stride;
+    const uint64_t m = a.lengths[l];
+    uint32_t* orow = a.out_rows ? a.out_rows + uint64_t(l) * R : a.out_adj + uint64_t(p) * R;
+    auto key_at = [&](uint64_t i) -> uint64_t {
+      const uint32_t id = a.cand_ids[beg + i];
+      return id == p ? kMaxKey : make_key(a.cand_dists[beg + i], id);
+    };
+    uint64_t lo_key = 0;        // keys <= lo_key are done
+    bool first = true;
+    uint32_t nsel = 0;
+    uint64_t evals = 0;
+    if (tid == 0) sh_evals = 0;
+    while (nsel < R) {
+      // how many keys remain above lo_key?
+      if (tid == 0) sh_cnt = 0;
+      __syncthreads();
+      uint32_t local = 0;
+      for (uint64_t i = tid; i < m; i += NT) {
+        const uint64_t k = key_at(i);
+        local += (k != kMaxKey && (first || k > lo_key)) ? 1u : 0u;
+      }
+      atomicAdd(&sh_cnt, local);
+      __syncthreads();
+      const uint32_t rem = sh_cnt;
+      if (rem == 0) break;
+      uint64_t hi_key = kMaxKey - 1;
+      if (rem > kChunk) {  // radix select of the kChunk-th smallest key above lo_key
+        if (tid == 0) {
+          sh_prefix = 0;
+          sh_want = kChunk;
+        }
+        for (int shift = 56; shift >= 0; shift -= 8) {
+          for (int b = tid; b < 256; b += NT) hist[b] = 0;
+          __syncthreads();
+          const uint64_t prefix = sh_prefix;
+          const uint64_t hmask = shift == 56 ? 0ull : (~0ull << (shift + 8));
+          for (uint64_t i = tid; i < m; i += NT) {
+            const uint64_t k = key_at(i);
+            if (k != kMaxKey && (first || k > lo_key) && (k & hmask) == prefix)
+              atomicAdd(&hist[(k >> shift) & 0xFF], 1u);
+          }
+          __syncthreads();
+          if (tid == 0) {
+            uint32_t want = sh_want, acc = 0;
+            int b = 0;
+            for (; b < 256; b++) {
+              if (acc + hist[b] >= want) break;
+              acc += hist[b];
+            }
+            sh_want = want - acc;
+            sh_prefix = prefix | (uint64_t(b) << shift);
+          }
+          __syncthreads();
+        }
+        hi_key = sh_prefix;
+      }
+      // gather the chunk (lo_key, hi_key] and sort it
+      if (tid == 0) sh_cnt = 0;
+      __syncthreads();
+      for (uint64_t i = tid; i < m; i += NT) {
+        const uint64_t k = key_at(i);
+        if (k != kMaxKey && (first || k > lo_key) && k <= hi_key) {
+          const uint32_t pos = atomicAdd(&sh_cnt, 1u);
+          if (pos < kChunk) keys[pos] = k;  // only exact duplicate keys can overflow
+        }
+      }
+      __syncthreads();
+      const uint32_t c = min(sh_cnt, kChunk);
+      uint32_t Mp = 32;
+      while (Mp < c) Mp <<= 1;
+      for (uint32_t i = c + tid; i < Mp; i += NT) keys[i] = kMaxKey;
+      __syncthreads();
+      for (uint32_t k = 2; k <= Mp; k <<= 1) {
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+          for (uint32_t i = tid; i < Mp; i += NT) {
+            const uint32_t ixj = i ^ j;
+            if (ixj > i) {
+              const uint64_t x = keys[i], y = keys[ixj];
+              if ((x > y) == ((i & k) == 0)) {
+                keys[i] = y;
+                keys[ixj] = x;
+              }
+            }
+          }
+          __syncthreads();
+        }
+      }
+      // cull the chunk by the earlier chunks' selections
+      for (uint32_t b0 = 0; b0 < c; b0 += GROUPS) {
+        const uint32_t t = b0 + grp;
+        bool culled = false;
+        if (nsel > 0) {
+          uint4 x[CPL];
+          const uint32_t id = t < c ? key_id(keys[t]) : 0u;
+          const float dj = t < c ? key_dist(keys[t]) : 0.0f;
+          const uint8_t* rp = a.data + uint64_t(id) * a.stride;
+#pragma unroll
+          for (int cc = 0; cc < CPL; cc++) {
+            const uint32_t ch = sub + cc * LPR;
+            x[cc] = (t < c && ch < nch) ? __ldg(reinterpret_cast<const uint4*>(rp) + ch) : make_uint4(0, 0, 0, 0);
+          }
+          for (uint32_t s2 = 0; s2 < nsel; s2++) {  // warp-uniform trip count (shuffles inside)
+            if (__all_sync(0xFFFFFFFFu, culled)) break;
+            const float sd = seld[s2];
+            if (sd == 0.0f) continue;
+            const uint8_t* sp = a.data + uint64_t(sel[s2]) * a.stride;
+            typename Op::acc_t acc = Op::zero();
+#pragma unroll
+            for (int cc = 0; cc < CPL; cc++) {
+              const uint32_t ch = sub + cc * LPR;
+              const uint4 y = ch < nch ? __ldg(reinterpret_cast<const uint4*>(sp) + ch) : make_uint4(0, 0, 0, 0);
+              acc = Op::chunk(y, x[cc], acc);
+            }
+            acc = group_sum<LPR>(acc);
+            const float via = Op::finish(acc);
+            if (!culled && sub == 0 && t < c) atomicAdd(&sh_evals, 1ull);
+            culled = culled || (a.rule == 0 ? (__fmul_rn(a.alpha, via) <= dj) : (via < __fmul_rn(a.alpha, sd)));
+          }
+        }
+        if (sub == 0 && t < c) {
+          kf[t] = culled ? 0 : 1;
+          alB[t] = static_cast<uint16_t>(t);
+        }
+      }
+      __syncthreads();
+      uint32_t nalive = cta_compact<NT>(alB, kf, c, alA, warp_tot);
+      __syncthreads();
+      uint16_t* alive = alA;
+      while (nsel < R && nalive > 0) {
+        const uint64_t sk = keys[alive[0]];
+        if (tid == 0) {
+          sel[nsel] = key_id(sk);
+          seld[nsel] = key_dist(sk);
+        }
+        nsel++;
+        if (nsel == R) break;
+        if (key_dist(sk) == 0.0f) {
+          alive++;
+          nalive--;
+          continue;
+        }
+        const uint32_t sid = key_id(sk);
+        const float sdist = key_dist(sk);
+        uint4 sr[CPL];
+        const uint8_t* srow = a.data + uint64_t(sid) * a.stride;
+#pragma unroll
+        for (int cc = 0; cc < CPL; cc++) {
+          const uint32_t ch = sub + cc * LPR;
+          sr[cc] = ch < nch ? __ldg(reinterpret_cast<const uint4*>(srow) + ch) : make_uint4(0, 0, 0, 0);
+        }
+        const uint32_t rest = nalive - 1;
+        evals += rest;
+        for (uint32_t b0 = 0; b0 < rest; b0 += GROUPS) {
+          const uint32_t t = b0 + grp;
+          const uint32_t ix = t < rest ? alive[1 + t] : 0u;
+          const uint32_t id = t < rest ? key_id(keys[ix]) : 0u;
+          const uint8_t* rp = a.data + uint64_t(id) * a.stride;
+          typename Op::acc_t acc = Op::zero();
+#pragma unroll
+          for (int cc = 0; cc < CPL; cc++) {
+            const uint32_t ch = sub + cc * LPR;
+            const uint4 x = (t < rest && ch < nch) ? __ldg(reinterpret_cast<const uint4*>(rp) + ch)
+                                                   : make_uint4(0, 0, 0, 0);
+            acc = Op::chunk(sr[cc], x, acc);
+          }
+          acc = group_sum<LPR>(acc);
+          if (sub == 0 && t < rest) {
+            const float via = Op::finish(acc);
+            const float dj = key_dist(keys[ix]);
+            const bool drop = a.rule == 0 ? (__fmul_rn(a.alpha, via) <= dj) : (via < __fmul_rn(a.alpha, sdist));
+            kf[t] = drop ? 0 : 1;
+          }
+        }
+        __syncthreads();
+        uint16_t* dst = (alive >= alA && alive < alA + kChunk) ? alB : alA;
+        nalive = cta_compact<NT>(alive + 1, kf, rest, dst, warp_tot);
+        alive = dst;
+        __syncthreads();
+      }
+      __syncthreads();
+      if (rem <= kChunk) break;  // that was the last chunk
+      lo_key = hi_key;
+      first = false;
+    }
+    __syncthreads();
+    for (uint32_t i = tid; i < R; i += NT) orow[i] = i < nsel ? sel[i] : kNone;
+    if (tid == 0) {
+      if (a.n_out) a.n_out[l] = nsel;
+      if (a.stats) {
+        atomicAdd(a.stats + kStPruneLists, 1ull);
+        atomicAdd(a.stats + kStPruneCands, static_cast<unsigned long long>(m));
+        atomicAdd(a.stats + kStPruneEvals, static_cast<unsigned long long>(evals) + sh_evals);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 namespace {
 template <int E, int M, int LPR, int CPL>
 cudaError_t launch_nt(const PruneArgs& a, int threads, cudaStream_t s) {
-  uint32_t Mcap = 32;
-  while (Mcap < a.mcap) Mcap <<= 1;
-  const size_t smem = prune_smem_bytes(a.mcap, a.R);
   if (a.count == 0) return cudaSuccess;
   if (threads <= 32) {
+    uint32_t Mcap = 32;
+    while (Mcap < a.mcap && Mcap < (1u << 16)) Mcap <<= 1;
+    const size_t smem = prune_smem_bytes(Mcap, a.R);
     auto k = prune_kernel<E, M, LPR, CPL, 32>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     k<<<a.count, 32, smem, s>>>(a, Mcap);
-  } else {
-    auto k = prune_kernel<E, M, LPR, CPL, 256>;
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  } else {  // any length
+    auto k = prune_chunked_kernel<E, M, LPR, CPL, 256>;
+    const size_t cs = prune_chunked_smem(a.R);
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(cs));
     if (e != cudaSuccess) return e;
-    k<<<a.count, 256, smem, s>>>(a, Mcap);
+    k<<<a.count, 256, cs, s>>>(a);
   }
   return cudaGetLastError();
 }

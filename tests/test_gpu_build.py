@@ -81,24 +81,25 @@ def test_prune_parity_on_reference_visited_lists(oracle, dtype, rule, alpha):
         assert list(got[i]) == list(want), f"list {i}"
 
 
-def test_prune_parity_long_lists(oracle):
-    """Hub-sized lists (the 256-thread path) are bit-exact too."""
+@pytest.mark.parametrize("alpha,R", [(1.2, 64), (0.5, 64), (0.8, 16), (2.0, 8)])
+def test_prune_parity_long_lists(oracle, alpha, R):
+    """Hub-sized lists (the chunked path, several 4096-key chunks when the
+    selections run out) are bit-exact too."""
     g = _g()
-    data = mixture(4, 20000, 16, clusters=4)
+    data = mixture(4, 30000, 16, clusters=4)
     rng = np.random.default_rng(0)
-    R = 64
     idx = g.Index(data, "l2", R)
     ps, lists, dl = [], [], []
-    for m in (600, 2000, 9000):
+    for m in (513, 600, 2000, 9000, 25000):
         p = int(rng.integers(0, len(data)))
         ids = rng.choice(len(data), m, replace=False).astype(np.uint32)
         ps.append(p)
         lists.append(ids)
         dl.append(np.array(l2_cands(data, p, ids), np.float32))
-    got = idx.alpha_prune_many(ps, lists, dl, g.PruneParams(R, 1.2))
+    got = idx.alpha_prune_many(ps, lists, dl, g.PruneParams(R, alpha))
     for i in range(len(ps)):
-        want, _ = oracle.alpha_prune(ps[i], lists[i], dl[i], data, R, 1.2)
-        assert list(got[i]) == list(want)
+        want, _ = oracle.alpha_prune(ps[i], lists[i], dl[i], data, R, alpha)
+        assert list(got[i]) == list(want), f"list {i} (m={len(lists[i])})"
 
 
 def _check_grouping(keys, vals, got):
@@ -223,6 +224,18 @@ def test_build_bit_identical(oracle, dtype, cap):
     assert s == ws
     assert (deg == degrees(want)).all()
     assert (got == want).all()
+
+
+def test_build_long_walk_rerun(oracle, monkeypatch):
+    """Inserts whose visited list outgrows the buffer are re-searched exactly
+    (forced here with a tiny buffer): the graph stays bit-identical."""
+    g = _g()
+    data = mixture(23, 3000, 32, clusters=10)
+    want, ws = oracle.build(data, 16, 32, 1.2, workers=8)
+    monkeypatch.setenv("GANN_VCAP", "8")
+    idx = g.build_diskann(data, "l2", g.DiskannParams(16, 32, 1.2))
+    got, _, s = idx.export_graph()
+    assert s == ws and (got == want).all()
 
 
 def test_build_bit_identical_ip_and_selected_rule(oracle):
