@@ -66,12 +66,15 @@ int guarded(F&& f) {
 struct DevBuf {
   void* p = nullptr;
   size_t cap = 0;
+  // Grows geometrically: cudaFree synchronises the device and large cudaMallocs
+  // are slow, so a build must not reallocate on every slightly larger batch.
   void ensure(size_t bytes) {
     if (bytes <= cap) return;
     if (p) cudaFree(p);
     p = nullptr;
+    size_t want = std::max<size_t>({bytes, cap + cap / 2, size_t(1) << 16});
+    want = (want + 4095) & ~size_t(4095);
     cap = 0;
-    size_t want = std::max<size_t>(bytes, 256);
     cu(cudaMalloc(&p, want), "cudaMalloc scratch");
     cap = want;
   }
@@ -91,14 +94,14 @@ uint32_t env_u32(const char* name, uint32_t dflt) {
   return v && *v ? static_cast<uint32_t>(std::strtoul(v, nullptr, 10)) : dflt;
 }
 
-// Shared-memory visited table size of the fast search mode. Distinct
-// evaluations per query run ~500-2000 at L = 10..200 (SURVEY.md §A probe 1).
+// Shared-memory visited table size of the fast search mode (direct mapped,
+// overwrite on collision): a pure performance knob — it trades re-evaluated
+// rows against per-warp shared memory, i.e. resident warps.
 uint32_t hash_log2_for(uint32_t L) {
   const uint32_t forced = env_u32("GANN_HASH_LOG2", 0);
   if (forced) return std::min<uint32_t>(std::max<uint32_t>(forced, 5), 15);
-  if (L <= 64) return 10;
-  if (L <= 256) return 11;
-  return 12;
+  if (L <= 256) return 10;
+  return 11;
 }
 
 }  // namespace
@@ -304,6 +307,34 @@ struct Timer {
   }
 };
 
+// alpha_prune over lists of length <= maxlen, each by the smallest kernel that
+// fits: integer rows on the tensor-core kernel in 128/256/512 bins, f32 rows
+// on the warp kernel; anything longer on the chunked kernel.
+void prune_binned(gann_index* idx, PruneArgs p, uint32_t maxlen) {
+  p.skip_long = 1;
+  uint32_t done = 0;
+  if (prune_uses_mma(idx->elem, std::min<uint32_t>(maxlen, 512), idx->stride, idx->R) &&
+      !std::getenv("GANN_NO_MMA")) {
+    for (uint32_t hi : {128u, 256u, 512u}) {
+      if (done >= maxlen) break;
+      p.mmin = done + 1;
+      p.mcap = hi;
+      cu(launch_prune(p, idx->elem, idx->metric, idx->geom, 32, idx->stream), "prune kernel (tensor cores)");
+      done = hi;
+    }
+  } else {
+    p.mmin = 0;
+    p.mcap = kPruneSmallCap;
+    cu(launch_prune(p, idx->elem, idx->metric, idx->geom, 32, idx->stream), "prune kernel");
+    done = kPruneSmallCap;
+  }
+  if (maxlen > done) {
+    p.mmin = done + 1;
+    p.mcap = 0xFFFFFFFFu;
+    cu(launch_prune(p, idx->elem, idx->metric, idx->geom, 256, idx->stream), "prune kernel (chunked)");
+  }
+}
+
 // Insert points order[lo..hi) (device ids) against the current graph:
 // search {L, L, 0} + alpha_prune of each visited list into its row.
 void insert_batch(gann_index* idx, const uint32_t* d_ids, uint32_t B, uint32_t L, float alpha,
@@ -334,7 +365,7 @@ void insert_batch(gann_index* idx, const uint32_t* d_ids, uint32_t B, uint32_t L
   p.out_adj = idx->adj;
   p.mcap = vcap;
   Timer tp(idx->stream);
-  cu(launch_prune(p, idx->elem, idx->metric, idx->geom, 32, idx->stream), "prune kernel");
+  prune_binned(idx, p, vcap);
   if (timed) idx->build_ms[2] += tp.stop(); else tp.stop();
   uint32_t fl[2];
   cu(cudaMemcpyAsync(fl, idx->flags, 8, cudaMemcpyDeviceToHost, idx->stream), "read flags");
@@ -376,9 +407,7 @@ void insert_batch(gann_index* idx, const uint32_t* d_ids, uint32_t B, uint32_t L
   p2.fixed_stride = vcap2;
   p2.cand_ids = a2.vis_ids;
   p2.cand_dists = a2.vis_dists;
-  p2.mcap = vcap2;
-  cu(launch_prune(p2, idx->elem, idx->metric, idx->geom, vcap2 <= kPruneSmallCap ? 32 : 256, idx->stream),
-     "prune kernel (long walks)");
+  prune_binned(idx, p2, vcap2);
   cu(cudaMemcpyAsync(fl, idx->flags, 8, cudaMemcpyDeviceToHost, idx->stream), "read flags");
   sync(idx);
   if (fl[0] || fl[1]) fail(GANN_ECUDA, "long-walk re-run overflowed its visited buffer");
@@ -483,12 +512,12 @@ void apply_back(gann_index* idx, const uint32_t* bsrc, uint32_t B, const uint32_
   if (nps) {
     p.count = nps;
     p.list_index = b.plist_small;
-    p.mcap = kPruneSmallCap;
-    cu(launch_prune(p, idx->elem, idx->metric, idx->geom, 32, idx->stream), "reprune small");
+    prune_binned(idx, p, kPruneSmallCap);
   }
   if (npb) {
     p.count = npb;
     p.list_index = b.plist_big;
+    p.mmin = 0;
     p.mcap = 0xFFFFFFFFu;
     cu(launch_prune(p, idx->elem, idx->metric, idx->geom, 256, idx->stream), "reprune big");
   }
@@ -649,10 +678,20 @@ int gann_build(gann_index* idx, uint32_t L, float alpha, int rule, uint64_t seed
        "upload order");
     idx->build_ms[0] += t0.stop();
     const uint32_t* d_order = idx->order.as<uint32_t>();
+    const bool trace = env_u32("GANN_TRACE", 0) != 0;
     for (auto [lo, hi] : batch_ranges(n, max_batch)) {
       const uint32_t B = hi - lo;
+      double before[6];
+      std::copy(idx->build_ms, idx->build_ms + 6, before);
+      auto t0 = std::chrono::steady_clock::now();
       insert_batch(idx, d_order + lo, B, L, alpha, rule, true);
       apply_back(idx, d_order + lo, B, nullptr, nullptr, uint64_t(B) * idx->R, alpha, rule, true);
+      if (trace) {
+        const double wall = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        std::fprintf(stderr, "batch [%u,%u) wall %.2f ms: search %.2f prune %.2f group %.2f merge %.2f reprune %.2f\n",
+                     lo, hi, wall, idx->build_ms[1] - before[1], idx->build_ms[2] - before[2],
+                     idx->build_ms[3] - before[3], idx->build_ms[4] - before[4], idx->build_ms[5] - before[5]);
+      }
     }
     sync(idx);
   });
@@ -910,12 +949,12 @@ int gann_alpha_prune(gann_index* idx, const uint32_t* p, const uint64_t* offsets
     if (!small.empty()) {
       a.count = static_cast<uint32_t>(small.size());
       a.list_index = d_small;
-      a.mcap = kPruneSmallCap;
-      cu(launch_prune(a, idx->elem, idx->metric, idx->geom, 32, idx->stream), "prune kernel");
+      prune_binned(idx, a, kPruneSmallCap);
     }
     if (!big.empty()) {
       a.count = static_cast<uint32_t>(big.size());
       a.list_index = d_big;
+      a.mmin = 0;
       a.mcap = 0xFFFFFFFFu;
       cu(launch_prune(a, idx->elem, idx->metric, idx->geom, 256, idx->stream), "prune kernel");
     }

@@ -69,13 +69,17 @@ struct PruneArgs {
   uint32_t* out_rows;          // or to out_rows[l * R]
   uint32_t* n_out;             // nullable, per list l
   uint32_t mcap;               // max list length this launch supports
-  uint32_t* too_long;          // lists longer than mcap are counted here
+  uint32_t mmin;               // lists shorter than this are left to another launch
+  int skip_long;               // lists longer than mcap: skip silently (binned launches)
+  uint32_t* too_long;          // ... or count them here
   unsigned long long* stats;
 };
 // threads = 32 for short lists, larger for hubs; smem from prune_smem_bytes.
 size_t prune_smem_bytes(uint32_t mcap, uint32_t R);
 cudaError_t launch_prune(const PruneArgs& a, int elem, int metric, const Geometry& g, int threads,
                          cudaStream_t s);
+// Integer lists up to 512 candidates run on the tensor cores (IMMA tiles).
+bool prune_uses_mma(int elem, uint32_t mcap, uint64_t stride, uint32_t R);
 
 // ---- back-edge grouping (phase 2) -----------------------------------------
 // Pairs (target, source) come either from the out-rows of the batch's points

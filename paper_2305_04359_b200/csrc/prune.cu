@@ -14,6 +14,8 @@
 // multiply (__fmul_rn) so the comparison is bit-identical to the reference;
 // integer distances are exact. 32-thread CTAs serve the insert-time lists
 // (|V| ~ L); 256-thread CTAs with up to 16k candidates serve back-edge hubs.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -86,8 +88,9 @@ __global__ void __launch_bounds__(NT) prune_kernel(const PruneArgs a, const uint
     beg = a.begins ? a.begins[l] : uint64_t(l) * a.fixed_stride;
     m = a.lengths[l];
     uint32_t* orow = a.out_rows ? a.out_rows + uint64_t(l) * R : a.out_adj + uint64_t(p) * R;
+    if (m < a.mmin) continue;  // another launch's bin
     if (m > a.mcap) {  // caller routes long lists elsewhere; never truncate silently
-      if (tid == 0) atomicAdd(a.too_long, 1u);
+      if (tid == 0 && !a.skip_long) atomicAdd(a.too_long, 1u);
       continue;
     }
     uint32_t Mp = 32;
@@ -200,6 +203,255 @@ __global__ void __launch_bounds__(NT) prune_kernel(const PruneArgs a, const uint
   }
 }
 
+// ---- integer lists on the tensor cores ---------------------------------------
+// For u8/i8 rows every distance the greedy needs is an exact int32:
+// d(i, j) = |x_i|^2 + |x_j|^2 - 2 x_i.x_j (L2) or -x_i.x_j (IP), identical to
+// the reference's sequential int32 sum. The candidates' rows are gathered
+// once into shared memory (sorted order, rows padded to 32-byte k-steps,
+// stride Kp+16 so ldmatrix is bank-conflict free) and the Gram entries come
+// from int8 MMA (mma.sync m16n8k32 s32 += u8/s8 x u8/s8, fragments loaded with
+// ldmatrix). The distance rows are produced lazily, one 16-row block at a time
+// as the greedy walk enters it (columns right of the block only), so shared
+// memory holds 16 x mc distances instead of mc x mc, and the walk itself
+// reads distances instead of gathering rows.
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(a));
+}
+
+template <bool SIGNED>
+__device__ __forceinline__ void mma_i8(int (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  if (SIGNED)
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+  else
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+struct MmaLayout {
+  uint32_t mc;   // max candidates (multiple of 32)
+  uint32_t kc;   // key slots (power of two >= mc, for the bitonic sort)
+  uint32_t kp;   // row bytes rounded up to 32
+  uint32_t xs;   // smem row stride (kp + 16)
+  uint32_t w;    // 32-bit words per cull mask (mc / 32)
+  size_t off_x, off_norm, off_cm, off_sel, total;
+};
+__host__ __device__ inline MmaLayout mma_layout(uint32_t mc, uint32_t stride, uint32_t R) {
+  MmaLayout l;
+  l.mc = (mc + 31) & ~31u;
+  l.kp = (stride + 31) & ~31u;
+  l.xs = l.kp + 16;
+  l.w = l.mc / 32;
+  l.kc = 32;
+  while (l.kc < l.mc) l.kc <<= 1;
+  size_t o = size_t(l.kc) * 8;  // keys
+  l.off_x = o;
+  o += size_t(l.mc) * l.xs;
+  l.off_norm = o;
+  o += size_t(l.mc) * 4;
+  l.off_cm = o;
+  o += size_t(l.mc) * l.w * 4;
+  l.off_sel = o;
+  o += size_t(R) * 4;
+  l.total = (o + 15) & ~size_t(15);
+  return l;
+}
+
+constexpr int kMmaThreads = 128;
+
+// The greedy of prune.cpp:25-43 needs, for a selected i, the test
+// "i culls j" only for later j; the outcome of that test does not depend on
+// which candidates are still alive. So all tests are evaluated at once — the
+// upper triangle of the Gram matrix on the tensor cores, the alpha test per
+// element, one bit per (i, j) in cull masks — and the walk itself is a serial
+// bit loop in one warp: i is selected iff no earlier selection culled it, and
+// a selection with a non-zero distance ORs its mask into the culled set.
+template <int E, int M>
+__global__ void __launch_bounds__(kMmaThreads) prune_mma_kernel(const PruneArgs a, const MmaLayout ly) {
+  constexpr int NT = kMmaThreads;
+  constexpr bool SIGNED = E == kI8;
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint64_t* keys = reinterpret_cast<uint64_t*>(smem);
+  uint8_t* X = smem + ly.off_x;
+  int* norm = reinterpret_cast<int*>(smem + ly.off_norm);
+  uint32_t* cm = reinterpret_cast<uint32_t*>(smem + ly.off_cm);
+  uint32_t* sel = reinterpret_cast<uint32_t*>(smem + ly.off_sel);
+  __shared__ uint32_t sh_nsel;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t R = a.R, mc = ly.mc, xs = ly.xs, kp = ly.kp, W = ly.w;
+  const uint32_t nch = static_cast<uint32_t>(a.stride >> 4);
+  const uint32_t kch = kp >> 4;  // 16-byte chunks per padded smem row
+  const uint32_t FULL = 0xFFFFFFFFu;
+
+  for (uint32_t li = blockIdx.x; li < a.count; li += gridDim.x) {
+    const uint32_t l = a.list_index ? a.list_index[li] : li;
+    const uint32_t p = a.points[l];
+    const uint64_t beg = a.begins ? a.begins[l] : uint64_t(l) * a.fixed_stride;
+    const uint64_t m = a.lengths[l];
+    uint32_t* orow = a.out_rows ? a.out_rows + uint64_t(l) * R : a.out_adj + uint64_t(p) * R;
+    if (m < a.mmin) continue;
+    if (m > mc) {
+      if (tid == 0 && !a.skip_long) atomicAdd(a.too_long, 1u);
+      continue;
+    }
+    uint32_t Mp = 32;
+    while (Mp < m) Mp <<= 1;
+    for (uint32_t i = tid; i < Mp; i += NT) {
+      uint64_t k = kMaxKey;
+      if (i < m) {
+        const uint32_t id = a.cand_ids[beg + i];
+        if (id != p) k = make_key(a.cand_dists[beg + i], id);  // prune.cpp:18-20 drops p
+      }
+      keys[i] = k;
+    }
+    __syncthreads();
+    for (uint32_t k = 2; k <= Mp; k <<= 1) {  // sort by (dist, id) — prune.cpp:21
+      for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+        for (uint32_t i = tid; i < Mp; i += NT) {
+          const uint32_t ixj = i ^ j;
+          if (ixj > i) {
+            const uint64_t x = keys[i], y = keys[ixj];
+            if ((x > y) == ((i & k) == 0)) {
+              keys[i] = y;
+              keys[ixj] = x;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    const uint32_t m2 = lower_bound_u64(keys, Mp, kMaxKey);
+    const uint32_t mpad = (m2 + 15) & ~15u;
+    const uint32_t mw = (m2 + 31) >> 5;  // mask words in use
+    // gather the rows in sorted order (zero padding to kp bytes and mpad rows)
+    for (uint32_t t = tid; t < mpad * kch; t += NT) {
+      const uint32_t r = t / kch, c = t - r * kch;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (r < m2 && c < nch)
+        v = __ldg(reinterpret_cast<const uint4*>(a.data + uint64_t(key_id(keys[r])) * a.stride) + c);
+      *reinterpret_cast<uint4*>(X + size_t(r) * xs + c * 16) = v;
+    }
+    for (uint32_t t = tid; t < m2 * W; t += NT) cm[t] = 0u;
+    __syncthreads();
+    for (uint32_t r = tid; r < mpad; r += NT) {
+      const uint32_t* w = reinterpret_cast<const uint32_t*>(X + size_t(r) * xs);
+      int acc = 0;
+      for (uint32_t i = 0; i < (kp >> 2); i++) {
+        if (SIGNED) acc = __dp4a(static_cast<int>(w[i]), static_cast<int>(w[i]), acc);
+        else acc = static_cast<int>(__dp4a(w[i], w[i], static_cast<uint32_t>(acc)));
+      }
+      norm[r] = acc;
+    }
+    __syncthreads();
+    // all cull tests of the upper triangle, 16x16 tiles spread over the warps
+    {
+      const uint32_t mt = mpad >> 4;
+      const uint32_t items = mt * (mt + 1) / 2;
+      const int g = lane >> 2, tg = lane & 3;
+      for (uint32_t it = warp; it < items; it += NT / 32) {
+        uint32_t rb = 0, rem = it;  // item -> (row block rb, col block cbk >= rb)
+        while (rem >= mt - rb) {
+          rem -= mt - rb;
+          rb++;
+        }
+        const uint32_t cbk = rb + rem;
+        const uint32_t r0 = rb * 16, n0 = cbk * 16;
+        int acc0[4] = {0, 0, 0, 0}, acc1[4] = {0, 0, 0, 0};
+        for (uint32_t kc = 0; kc < (kp >> 5); kc++) {
+          uint32_t af[4], bf[4];
+          ldsm_x4(af, X + size_t(r0 + (lane & 7) + ((lane >> 3) & 1) * 8) * xs + kc * 32 + (lane >> 4) * 16);
+          ldsm_x4(bf, X + size_t(n0 + (lane & 7) + (lane >> 4) * 8) * xs + kc * 32 + ((lane >> 3) & 1) * 16);
+          mma_i8<SIGNED>(acc0, af, bf[0], bf[1]);
+          mma_i8<SIGNED>(acc1, af, bf[2], bf[3]);
+        }
+        // bits for rows r0+g and r0+g+8, 16 columns n0.. (two per lane per 8-col tile)
+        uint32_t bits_lo = 0, bits_hi = 0;
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+#pragma unroll
+          for (int e = 0; e < 4; e++) {
+            const uint32_t row = r0 + g + (e >> 1) * 8;
+            const uint32_t ccol = h * 8 + tg * 2 + (e & 1);
+            const uint32_t col = n0 + ccol;
+            const int gram = h ? acc1[e] : acc0[e];
+            bool cull = false;
+            if (col > row && col < m2 && row < m2) {
+              const float di = key_dist(keys[row]);
+              if (di != 0.0f) {  // prune.cpp:32: a zero-distance pick culls nothing
+                const float via = M == kL2 ? __int2float_rn(norm[row] + norm[col] - 2 * gram)
+                                           : -__int2float_rn(gram);
+                const float dj = key_dist(keys[col]);
+                // prune.cpp:37-39, one IEEE multiply, never contracted
+                cull = a.rule == 0 ? (__fmul_rn(a.alpha, via) <= dj) : (via < __fmul_rn(a.alpha, di));
+              }
+            }
+            if (cull) {
+              if (e >> 1) bits_hi |= 1u << ccol;
+              else bits_lo |= 1u << ccol;
+            }
+          }
+        }
+        // OR the four lanes of a row group, then one lane per row writes 16 bits
+        bits_lo |= __shfl_xor_sync(FULL, bits_lo, 1);
+        bits_lo |= __shfl_xor_sync(FULL, bits_lo, 2);
+        bits_hi |= __shfl_xor_sync(FULL, bits_hi, 1);
+        bits_hi |= __shfl_xor_sync(FULL, bits_hi, 2);
+        if (tg == 0) {
+          const uint32_t sh = n0 & 31;
+          if (bits_lo && r0 + g < m2) atomicOr(&cm[(r0 + g) * W + (n0 >> 5)], bits_lo << sh);
+          if (bits_hi && r0 + g + 8 < m2) atomicOr(&cm[(r0 + g + 8) * W + (n0 >> 5)], bits_hi << sh);
+        }
+      }
+    }
+    __syncthreads();
+    // the greedy walk (prune.cpp:25-43) as a bit loop in warp 0
+    if (warp == 0) {
+      uint32_t culled = 0;  // lane w holds culled word w
+      uint32_t nsel = 0;
+      uint64_t evals = 0;
+      for (uint32_t i = 0; i < m2; i++) {
+        const uint32_t cw = __shfl_sync(FULL, culled, i >> 5);
+        if ((cw >> (i & 31)) & 1u) continue;
+        if (lane == 0) sel[nsel] = key_id(keys[i]);
+        nsel++;
+        if (nsel == R) break;
+        if (key_dist(keys[i]) == 0.0f) continue;
+        if (a.stats) {  // reference dist_comps: the alive candidates after i
+          uint32_t w = lane < mw ? ~culled : 0u;
+          const uint32_t lo = i + 1;
+          if (lane < (lo >> 5)) w = 0u;
+          else if (lane == (lo >> 5)) w &= ~((1u << (lo & 31)) - 1u);
+          if (lane == mw - 1 && (m2 & 31)) w &= (1u << (m2 & 31)) - 1u;
+          evals += __reduce_add_sync(FULL, __popc(w));
+        }
+        if (lane < mw) culled |= cm[i * W + lane];
+      }
+      if (lane == 0) {
+        sh_nsel = nsel;
+        if (a.stats) {
+          atomicAdd(a.stats + kStPruneLists, 1ull);
+          atomicAdd(a.stats + kStPruneCands, static_cast<unsigned long long>(m));
+          atomicAdd(a.stats + kStPruneEvals, static_cast<unsigned long long>(evals));
+        }
+      }
+    }
+    __syncthreads();
+    const uint32_t nsel = sh_nsel;
+    for (uint32_t i = tid; i < R; i += NT) orow[i] = i < nsel ? sel[i] : kNone;
+    if (tid == 0 && a.n_out) a.n_out[l] = nsel;
+    __syncthreads();
+  }
+}
+
 // ---- long lists: chunked prune ------------------------------------------------
 // Exact restatement of the same greedy for lists of any length (back-edge
 // hubs). The candidates are consumed in key order, C at a time: a radix select
@@ -245,6 +497,7 @@ __global__ void __launch_bounds__(NT) prune_chunked_kernel(const PruneArgs a) {
     const uint64_t beg = a.begins ? a.begins[l] : uint64_t(l) * a.fixed_stride;
     const uint64_t m = a.lengths[l];
     uint32_t* orow = a.out_rows ? a.out_rows + uint64_t(l) * R : a.out_adj + uint64_t(p) * R;
+    if (m < a.mmin) continue;
     auto key_at = [&](uint64_t i) -> uint64_t {
       const uint32_t id = a.cand_ids[beg + i];
       return id == p ? kMaxKey : make_key(a.cand_dists[beg + i], id);
@@ -477,8 +730,28 @@ cudaError_t dispatch(const PruneArgs& a, const Geometry& g, int threads, cudaStr
 }
 }  // namespace
 
+template <int E, int M>
+cudaError_t launch_mma(const PruneArgs& a, cudaStream_t s) {
+  if (a.count == 0) return cudaSuccess;
+  const MmaLayout ly = mma_layout(a.mcap, static_cast<uint32_t>(a.stride), a.R);
+  auto k = prune_mma_kernel<E, M>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ly.total));
+  if (e != cudaSuccess) return e;
+  k<<<a.count, kMmaThreads, ly.total, s>>>(a, ly);
+  return cudaGetLastError();
+}
+
+bool prune_uses_mma(int elem, uint32_t mcap, uint64_t stride, uint32_t R) {
+  if (elem == kF32 || mcap > 512 || mcap == 0) return false;
+  return mma_layout(mcap, static_cast<uint32_t>(stride), R).total <= 200 * 1024;
+}
+
 cudaError_t launch_prune(const PruneArgs& a, int elem, int metric, const Geometry& g, int threads,
                          cudaStream_t s) {
+  if (threads <= 32 && prune_uses_mma(elem, a.mcap, a.stride, a.R) && !std::getenv("GANN_NO_MMA")) {
+    if (metric == kL2) return elem == kU8 ? launch_mma<kU8, kL2>(a, s) : launch_mma<kI8, kL2>(a, s);
+    return elem == kU8 ? launch_mma<kU8, kIP>(a, s) : launch_mma<kI8, kIP>(a, s);
+  }
   if (metric == kL2) {
     if (elem == kU8) return dispatch<kU8, kL2>(a, g, threads, s);
     if (elem == kI8) return dispatch<kI8, kL2>(a, g, threads, s);

@@ -3,7 +3,8 @@
 // Behaviour contract: graphann::beam_search (src/search.cpp:62-131), restated
 // in SURVEY.md §B.1. Per warp:
 //   * the beam (<= L keys, sorted) and its expanded flags live in shared
-//     memory, double-buffered so a merge is one parallel scatter;
+//     memory; a merge moves only the tail behind the first insertion point,
+//     in place, last 32-entry chunk first (targets only move right);
 //   * exactly one vertex is expanded per step (the first unexpanded key,
 //     src/search.cpp:96-103), gated by the k-th best key with epsilon slack
 //     (:105-107) — the only order the reference's visit sequence allows;
@@ -14,10 +15,12 @@
 //   * the new keys are merged into the beam as top-L of the union with exact
 //     (dist, id) duplicates dropped — equal to the reference's sequential
 //     push (:83-90) because the L-th key only ever decreases.
-// Visited filter. FAST: an open-addressing hash in shared memory with a
-// bounded probe; an id that does not fit is simply not remembered, so the
-// filter never reports a false positive and ids / |V| / visit order are the
-// reference's. REF: the reference's own ApproxVisitedSet
+// Visited filter. FAST: a direct-mapped table in shared memory that
+// overwrites on collision (one load + one store per neighbour; it keeps the
+// most recent ids, which is what graph locality re-encounters). An evicted id
+// may be evaluated again, but the table never reports a false positive, so
+// ids / |V| / visit order are the reference's; re-evaluated
+// keys that are still in the beam are dropped as exact duplicates. REF: the reference's own ApproxVisitedSet
 // (L*L slots, mix64(id ^ seed) % L^2, include/graphann/search.hpp:24-38,
 // seed from src/search.cpp:52-58) in global memory, applied per expansion
 // with the order-exact warp rule of SURVEY.md §0.4 (first lane of a slot
@@ -32,14 +35,39 @@ namespace gann {
 namespace {
 
 constexpr int kWarpsPerBlock = 4;
-constexpr int kProbes = 4;
 
+// Rows in flight per lane group per pass: U <= LPR so the transposed
+// reduction can hand every lane of the group (at most) one finished row.
 template <int LPR, int CPL>
 struct Unroll {
-  static constexpr int RPP = 32 / LPR;
-  static constexpr int raw = (32 / RPP) > 8 ? 8 : (32 / RPP);
+  static constexpr int raw = LPR > 8 ? 8 : LPR;
   static constexpr int U = (raw / CPL) < 1 ? 1 : (raw / CPL);
 };
+
+// Sum U per-lane partials over the LPR lanes of a row group so that lane
+// (sub mod U) ends up holding the total of row `sub mod U` (U <= LPR, both
+// powers of two): plain butterflies for the lane bits above U, then a
+// transposed butterfly that halves the live values each step — LPR=U=8 costs
+// 4+2+1 shuffles for 8 rows instead of 3 per row.
+template <int LPR, int U, typename T>
+__device__ __forceinline__ T transpose_reduce(T (&v)[U], int sub) {
+#pragma unroll
+  for (int o = LPR / 2; o >= U; o >>= 1) {
+#pragma unroll
+    for (int u = 0; u < U; u++) v[u] += __shfl_xor_sync(0xFFFFFFFFu, v[u], o);
+  }
+#pragma unroll
+  for (int w = U / 2; w >= 1; w >>= 1) {
+    const bool hi = (sub & w) != 0;
+#pragma unroll
+    for (int i = 0; i < w; i++) {
+      const T send = hi ? v[i] : v[i + w];
+      const T keep = hi ? v[i + w] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xFFFFFFFFu, send, w);
+    }
+  }
+  return v[0];
+}
 
 // Distances from the lane's query chunks qr to rows ids[0..m) -> keys out[].
 template <class Op, int LPR, int CPL>
@@ -52,62 +80,55 @@ __device__ __forceinline__ void eval_rows(const uint8_t* __restrict__ data, uint
   const int grp = lane / LPR;
   for (uint32_t base = 0; base < m; base += RPP * U) {
     uint4 x[U][CPL];
-    uint32_t id[U];
 #pragma unroll
     for (int u = 0; u < U; u++) {
       const uint32_t r = base + u * RPP + grp;
-      id[u] = r < m ? ids[r] : kNone;
-      const uint8_t* rp = data + static_cast<uint64_t>(id[u] == kNone ? 0u : id[u]) * stride;
+      const uint32_t id = r < m ? ids[r] : 0u;
+      const uint8_t* rp = data + static_cast<uint64_t>(id) * stride;
 #pragma unroll
       for (int c = 0; c < CPL; c++) {
         const uint32_t ch = sub + c * LPR;
-        x[u][c] = (id[u] != kNone && ch < nch) ? __ldg(reinterpret_cast<const uint4*>(rp) + ch)
-                                               : make_uint4(0, 0, 0, 0);
+        x[u][c] = (r < m && ch < nch) ? __ldg(reinterpret_cast<const uint4*>(rp) + ch)
+                                      : make_uint4(0, 0, 0, 0);
       }
     }
+    typename Op::acc_t acc[U];
 #pragma unroll
     for (int u = 0; u < U; u++) {
-      typename Op::acc_t acc = Op::zero();
+      acc[u] = Op::zero();
 #pragma unroll
-      for (int c = 0; c < CPL; c++) acc = Op::chunk(qr[c], x[u][c], acc);
-      acc = group_sum<LPR>(acc);
-      const uint32_t r = base + u * RPP + grp;
-      if (sub == 0 && r < m) out[r] = make_key(Op::finish(acc), id[u]);
+      for (int c = 0; c < CPL; c++) acc[u] = Op::chunk(qr[c], x[u][c], acc[u]);
     }
+    const typename Op::acc_t tot = transpose_reduce<LPR, U>(acc, sub);
+    const uint32_t r = base + (sub & (U - 1)) * RPP + grp;
+    if (sub < U && r < m) out[r] = make_key(Op::finish(tot), ids[r]);
   }
-}
-
-__device__ __forceinline__ bool hash_insert(volatile uint32_t* hash, uint32_t log2, uint32_t id,
-                                            uint32_t& drops) {
-  const uint32_t mask = (1u << log2) - 1u;
-  const uint32_t h = (id * 0x9E3779B1u) >> (32 - log2);
-#pragma unroll 1
-  for (int p = 0; p < kProbes; p++) {
-    const uint32_t s = (h + p) & mask;
-    const uint32_t v = hash[s];
-    if (v == id) return false;
-    if (v == kNone) {
-      const uint32_t old = atomicCAS(const_cast<uint32_t*>(hash + s), kNone, id);
-      if (old == kNone) return true;
-      if (old == id) return false;
-    }
-  }
-  drops++;
-  return true;  // not remembered: may be evaluated again later, never wrongly skipped
 }
 
 __device__ __forceinline__ uint32_t lanemask_lt(int lane) { return (1u << lane) - 1u; }
 
+// Number of keys in sorted a[0..n) below k (n is small: linear below 8).
+__device__ __forceinline__ uint32_t count_less(const uint64_t* a, uint32_t n, uint64_t k) {
+  if (n <= 8) {
+    uint32_t c = 0;
+    for (uint32_t i = 0; i < n; i++) c += a[i] < k ? 1u : 0u;
+    return c;
+  }
+  return lower_bound_u64(a, n, k);
+}
+
 }  // namespace
 
+// Per-warp shared memory: beam keys + flags (single buffer, merged in place),
+// candidate scratch, and the direct-mapped visited table.
 size_t search_smem_per_warp(uint32_t L, uint32_t R, uint32_t hash_log2) {
   const size_t Lp = (L + 31) & ~31u, Rp = (R + 31) & ~31u;
-  size_t b = 2 * Lp * 8 + 3 * Rp * 8 + 2 * Rp * 4 + (size_t(1) << hash_log2) * 4 + 2 * Lp;
+  size_t b = Lp * 8 + 3 * Rp * 8 + 2 * Rp * 4 + (size_t(1) << hash_log2) * 4 + Lp;
   return (b + 15) & ~size_t(15);
 }
 
 template <int E, int M, int LPR, int CPL>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, 7)
     search_kernel(const SearchArgs a, const uint32_t per_warp) {
   using Op = DistOp<E, M>;
   extern __shared__ __align__(16) uint8_t smem[];
@@ -115,19 +136,18 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
   const int wib = threadIdx.x >> 5;
   const uint32_t L = a.L, R = a.R;
   const uint32_t Lp = (L + 31) & ~31u, Rp = (R + 31) & ~31u;
-  const uint32_t H = 1u << a.hash_log2;
+  const uint32_t hlog2 = a.hash_log2;
+  const uint32_t H = 1u << hlog2;
   const uint32_t nch = static_cast<uint32_t>(a.stride >> 4);
   uint8_t* base = smem + wib * per_warp;
-  uint64_t* beamA = reinterpret_cast<uint64_t*>(base);
-  uint64_t* beamB = beamA + Lp;
-  uint64_t* ck = beamB + Lp;
+  uint64_t* beam = reinterpret_cast<uint64_t*>(base);
+  uint64_t* ck = beam + Lp;
   uint64_t* srt = ck + Rp;
   uint64_t* tmpk = srt + Rp;
   uint32_t* cid = reinterpret_cast<uint32_t*>(tmpk + Rp);
   uint32_t* posb = cid + Rp;
   uint32_t* hash = posb + Rp;
-  uint8_t* flA = reinterpret_cast<uint8_t*>(hash + H);
-  uint8_t* flB = flA + Lp;
+  uint8_t* fl = reinterpret_cast<uint8_t*>(hash + H);
   const uint32_t FULL = 0xFFFFFFFFu;
 
   const uint32_t nw = gridDim.x * (blockDim.x >> 5);
@@ -159,32 +179,34 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     if (lane == 0) cid[0] = start;
     __syncwarp();
     eval_rows<Op, LPR, CPL>(a.data, a.stride, nch, cid, 1, ck, qr, lane);
-    uint32_t drops = 0;
     __syncwarp();
     if (lane == 0) {
-      beamA[0] = ck[0];
-      flA[0] = 0;
+      beam[0] = ck[0];
+      fl[0] = 0;
       if (a.visited_mode == 1)
         table[mix64(static_cast<uint64_t>(start) ^ seed) % LL] = start;
       else
-        hash_insert(hash, a.hash_log2, start, drops);
+        hash[(start * 0x9E3779B1u) >> (32 - hlog2)] = start;
     }
-    uint64_t* beam = beamA;
-    uint64_t* nbeam = beamB;
-    uint8_t* fl = flA;
-    uint8_t* nfl = flB;
-    uint32_t size = 1, nvis = 0;
+    uint32_t size = 1, nvis = 0, hint = 0, evict = 0;
     uint64_t evals = 1, adjsum = 0;
+    // speculative register prefetch of the next expansion's adjacency row
+    // (R <= 64: two ids per lane); used when the guess turns out right
+    const bool pf_ok = R <= 64;
+    uint32_t pf_id = kNone, pf0 = kNone, pf1 = kNone;
     __syncwarp();
 
     while (true) {
-      __syncwarp();
+      // first unexpanded key at or after `hint` (everything before is expanded)
       int fu = -1;
-      for (uint32_t b0 = 0; b0 < size; b0 += 32) {
+      uint32_t fbal = 0, fb0 = 0;
+      for (uint32_t b0 = hint & ~31u; b0 < size; b0 += 32) {
         const uint32_t i = b0 + lane;
-        const uint32_t bal = __ballot_sync(FULL, i < size && fl[i] == 0);
+        const uint32_t bal = __ballot_sync(FULL, i >= hint && i < size && fl[i] == 0);
         if (bal) {
           fu = static_cast<int>(b0 + __ffs(bal) - 1);
+          fbal = bal;
+          fb0 = b0;
           break;
         }
       }
@@ -196,6 +218,32 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
         if (key_dist(fk) > lim) break;
       }
       const uint32_t cur = key_id(fk);
+      hint = fu + 1;
+      const uint32_t* row = a.adj + static_cast<uint64_t>(cur) * R;
+      uint32_t nb0 = kNone, nb1 = kNone;
+      if (pf_ok) {
+        if (pf_id == cur) {
+          nb0 = pf0;
+          nb1 = pf1;
+        } else {
+          nb0 = lane < R ? __ldg(row + lane) : kNone;
+          nb1 = lane + 32 < R ? __ldg(row + 32 + lane) : kNone;
+        }
+        // guess the next expansion: the next unexpanded key after fu
+        const uint32_t above = fbal & ~((2u << (fu - fb0)) - 1u);
+        int gi = above ? static_cast<int>(fb0 + __ffs(above) - 1) : -1;
+        if (gi < 0 && fb0 + 32 < size) {
+          const uint32_t i = fb0 + 32 + lane;
+          const uint32_t bal = __ballot_sync(FULL, i < size && fl[i] == 0);
+          if (bal) gi = static_cast<int>(fb0 + 32 + __ffs(bal) - 1);
+        }
+        pf_id = gi >= 0 ? key_id(beam[gi]) : kNone;
+        if (pf_id != kNone) {
+          const uint32_t* prow = a.adj + static_cast<uint64_t>(pf_id) * R;
+          pf0 = lane < R ? __ldg(prow + lane) : kNone;
+          pf1 = lane + 32 < R ? __ldg(prow + 32 + lane) : kNone;
+        }
+      }
       __syncwarp();
       if (lane == 0) {
         fl[fu] = 1;
@@ -208,10 +256,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 
       // ---- neighbours through the visited filter (adjacency order kept) ----
       uint32_t m = 0;
-      const uint32_t* row = a.adj + static_cast<uint64_t>(cur) * R;
       for (uint32_t t0 = 0; t0 < R; t0 += 32) {
         const uint32_t t = t0 + lane;
-        const uint32_t nb = t < R ? __ldg(row + t) : kNone;
+        const uint32_t nb = pf_ok ? (t0 == 0 ? nb0 : nb1) : (t < R ? __ldg(row + t) : kNone);
         const bool valid = nb != kNone;
         adjsum += __popc(__ballot_sync(FULL, valid));
         bool fresh;
@@ -228,7 +275,15 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
           __syncwarp();
           fresh = valid && !seen;
         } else {
-          fresh = valid && hash_insert(hash, a.hash_log2, nb, drops);
+          // direct-mapped, overwrite on collision: never a false positive
+          const uint32_t slot = (nb * 0x9E3779B1u) >> (32 - hlog2);
+          const uint32_t old = valid ? hash[slot] : kNone;
+          fresh = valid && old != nb;
+          __syncwarp();
+          if (fresh) {
+            hash[slot] = nb;
+            evict += old != kNone ? 1u : 0u;
+          }
         }
         const uint32_t bal = __ballot_sync(FULL, fresh);
         if (fresh) cid[m + __popc(bal & lanemask_lt(lane))] = nb;
@@ -262,6 +317,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
       }
       if (s == 0) continue;
       __syncwarp();
+      uint32_t p0 = 0xFFFFFFFFu;
       for (uint32_t j0 = 0; j0 < s; j0 += 32) {
         const uint32_t j = j0 + lane;
         if (j < s) {
@@ -269,28 +325,46 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
           uint32_t r = 0;
           for (uint32_t t = 0; t < s; t++) r += tmpk[t] < k ? 1u : 0u;
           srt[r] = k;
-          const uint32_t fin = posb[j] + r;
-          if (fin < L) {
-            nbeam[fin] = k;
-            nfl[fin] = 0;
-          }
+          p0 = min(p0, posb[j]);
         }
       }
+      p0 = __reduce_min_sync(FULL, p0);
       __syncwarp();
-      for (uint32_t i0 = 0; i0 < size; i0 += 32) {
-        const uint32_t i = i0 + lane;
-        if (i < size) {
-          const uint64_t k = beam[i];
-          const uint32_t fin = i + lower_bound_u64(srt, s, k);
+      // move the tail [p0, size) right, last chunk first (targets only grow)
+      for (int b0 = static_cast<int>((size - 1) & ~31u); b0 >= 0 && static_cast<uint32_t>(b0) + 31 >= p0; b0 -= 32) {
+        const uint32_t i = b0 + lane;
+        const bool mv = i >= p0 && i < size;
+        uint64_t k = 0;
+        uint8_t f = 0;
+        uint32_t ni = 0;
+        if (mv) {
+          k = beam[i];
+          f = fl[i];
+          ni = i + count_less(srt, s, k);
+        }
+        __syncwarp();
+        if (mv && ni < L) {
+          beam[ni] = k;
+          fl[ni] = f;
+        }
+        __syncwarp();
+      }
+      for (uint32_t j0 = 0; j0 < s; j0 += 32) {
+        const uint32_t j = j0 + lane;
+        if (j < s) {
+          const uint64_t k = tmpk[j];
+          uint32_t r = 0;
+          for (uint32_t t = 0; t < s; t++) r += srt[t] < k ? 1u : 0u;
+          const uint32_t fin = posb[j] + r;
           if (fin < L) {
-            nbeam[fin] = k;
-            nfl[fin] = fl[i];
+            beam[fin] = k;
+            fl[fin] = 0;
           }
         }
       }
       size = min(L, size + s);
-      uint64_t* tb = beam; beam = nbeam; nbeam = tb;
-      uint8_t* tf = fl; fl = nfl; nfl = tf;
+      hint = min(hint, p0);
+      __syncwarp();
     }
 
     __syncwarp();
@@ -304,6 +378,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
             have ? key_dist(beam[i]) : __int_as_float(0x7f800000);
       }
     }
+    evict = __reduce_add_sync(FULL, evict);
     if (lane == 0) {
       if (a.n_visited) a.n_visited[q] = nvis;
       if (a.dist_comps) a.dist_comps[q] = evals;
@@ -312,7 +387,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
         atomicAdd(a.stats + kStQueries, 1ull);
         atomicAdd(a.stats + kStExpansions, static_cast<unsigned long long>(nvis));
         atomicAdd(a.stats + kStEvals, static_cast<unsigned long long>(evals));
-        atomicAdd(a.stats + kStDrops, static_cast<unsigned long long>(drops));
+        atomicAdd(a.stats + kStDrops, static_cast<unsigned long long>(evict));
         atomicAdd(a.stats + kStAdj, static_cast<unsigned long long>(adjsum));
       }
     }

@@ -226,6 +226,18 @@ def test_build_bit_identical(oracle, dtype, cap):
     assert (got == want).all()
 
 
+@pytest.mark.parametrize("d,dtype,metric", [(128, np.uint8, "l2"), (256, np.uint8, "l2"), (48, np.int8, "l2"),
+                                            (128, np.uint8, "ip")])
+def test_build_bit_identical_widths(oracle, d, dtype, metric):
+    """Wider rows (the tensor-core prune's 4 and 8 k-steps, a 16-byte tail at d=48)."""
+    g = _g()
+    data = mixture(29, 4000, d, clusters=12, dtype=dtype)
+    want, ws = oracle.build(data, 32, 64, 1.2, metric=metric, workers=8)
+    idx = g.build_diskann(data, metric, g.DiskannParams(32, 64, 1.2))
+    got, _, s = idx.export_graph()
+    assert s == ws and (got == want).all()
+
+
 def test_build_long_walk_rerun(oracle, monkeypatch):
     """Inserts whose visited list outgrows the buffer are re-searched exactly
     (forced here with a tiny buffer): the graph stays bit-identical."""

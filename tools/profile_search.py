@@ -1,0 +1,55 @@
+"""Build an index on the GPU and run the search kernel a few times (for ncu).
+
+  python tools/profile_search.py --n 2000000 --L 128 --reps 3
+"""
+import argparse
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+import torch
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+import paper_2305_04359_b200 as g  # noqa: E402
+from paper_2305_04359_b200 import datagen  # noqa: E402
+from paper_2305_04359_b200._lib import check, lib  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="c1")
+ap.add_argument("--n", type=int, default=2_000_000)
+ap.add_argument("--nq", type=int, default=10_000)
+ap.add_argument("--L", type=int, default=128)
+ap.add_argument("--reps", type=int, default=3)
+args = ap.parse_args()
+cfg = datagen.CONFIGS[args.config].scaled(args.n)
+torch.cuda.set_stream(torch.cuda.Stream())
+base = torch.empty(cfg.n * cfg.d, dtype=torch.uint8, device="cuda")
+check(lib().gann_generate_u8(base.data_ptr(), cfg.n, cfg.d, cfg.clusters, cfg.sigma, cfg.noise_frac,
+                             cfg.center_seed, cfg.base_seed, 0, 0))
+q = torch.empty(args.nq * cfg.d, dtype=torch.uint8, device="cuda")
+check(lib().gann_generate_u8(q.data_ptr(), args.nq, cfg.d, cfg.clusters, cfg.sigma, cfg.noise_frac,
+                             cfg.center_seed, cfg.query_seed, 0, 0))
+idx = g.Index.from_device(base.data_ptr(), cfg.n, cfg.d, np.uint8, "l2", cfg.R)
+t0 = time.time()
+idx.build(g.DiskannParams(cfg.R, cfg.L, cfg.alpha, max_batch=cfg.max_batch))
+torch.cuda.synchronize()
+print(f"build {time.time() - t0:.2f}s", idx.stats()["build_ms"], flush=True)
+idx.stage_queries(q.data_ptr(), args.nq)
+ids = torch.empty(args.nq * 10, dtype=torch.int32, device="cuda")
+ds = torch.empty(args.nq * 10, dtype=torch.float32, device="cuda")
+s = torch.cuda.current_stream()
+torch.cuda.synchronize()
+torch.cuda.profiler.start()  # ncu --profile-from-start off captures only these launches
+for r in range(args.reps):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    idx.search_staged(g.SearchParams(args.L, args.L, 0.0), 10, ids.data_ptr(), ds.data_ptr(), s.cuda_stream)
+    e1.record()
+    torch.cuda.synchronize()
+    print(f"search L={args.L}: {e0.elapsed_time(e1):.3f} ms", flush=True)
+torch.cuda.profiler.stop()
+st = idx.stats()
+print("stats", {k: st[k] for k in ("queries", "expansions", "evaluations", "filter_drops", "adj_entries")})
