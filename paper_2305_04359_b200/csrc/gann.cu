@@ -318,15 +318,15 @@ void prune_binned(gann_index* idx, PruneArgs p, uint32_t maxlen) {
     for (uint32_t hi : {128u, 256u, 512u}) {
       if (done >= maxlen) break;
       p.mmin = done + 1;
-      p.mcap = hi;
+      p.mcap = std::min(hi, maxlen);  // never past the lists' own capacity
       cu(launch_prune(p, idx->elem, idx->metric, idx->geom, 32, idx->stream), "prune kernel (tensor cores)");
-      done = hi;
+      done = p.mcap;
     }
   } else {
     p.mmin = 0;
-    p.mcap = kPruneSmallCap;
+    p.mcap = std::min(kPruneSmallCap, maxlen);
     cu(launch_prune(p, idx->elem, idx->metric, idx->geom, 32, idx->stream), "prune kernel");
-    done = kPruneSmallCap;
+    done = p.mcap;
   }
   if (maxlen > done) {
     p.mmin = done + 1;

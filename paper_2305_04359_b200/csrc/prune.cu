@@ -250,9 +250,9 @@ __host__ __device__ inline MmaLayout mma_layout(uint32_t mc, uint32_t stride, ui
   l.mc = (mc + 31) & ~31u;
   l.kp = (stride + 31) & ~31u;
   l.xs = l.kp + 16;
-  l.w = l.mc / 32;
-  l.kc = 32;
-  while (l.kc < l.mc) l.kc <<= 1;
+  l.w = l.mc <= 128 ? 4 : (l.mc <= 256 ? 8 : 16);
+  l.mc = l.w * 32;
+  l.kc = l.mc;
   size_t o = size_t(l.kc) * 8;  // keys
   l.off_x = o;
   o += size_t(l.mc) * l.xs;
@@ -275,63 +275,57 @@ constexpr int kMmaThreads = 128;
 // element, one bit per (i, j) in cull masks — and the walk itself is a serial
 // bit loop in one warp: i is selected iff no earlier selection culled it, and
 // a selection with a non-zero distance ORs its mask into the culled set.
-template <int E, int M>
+template <int E, int M, int W>
 __global__ void __launch_bounds__(kMmaThreads) prune_mma_kernel(const PruneArgs a, const MmaLayout ly) {
   constexpr int NT = kMmaThreads;
   constexpr bool SIGNED = E == kI8;
   extern __shared__ __align__(16) uint8_t smem[];
-  uint64_t* keys = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* keys = reinterpret_cast<uint64_t*>(smem);   // unsorted input, then sorted
   uint8_t* X = smem + ly.off_x;
   int* norm = reinterpret_cast<int*>(smem + ly.off_norm);
   uint32_t* cm = reinterpret_cast<uint32_t*>(smem + ly.off_cm);
   uint32_t* sel = reinterpret_cast<uint32_t*>(smem + ly.off_sel);
-  __shared__ uint32_t sh_nsel;
+  __shared__ uint32_t sh_nsel, sh_m2;
+  __shared__ uint32_t zmask[W];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t R = a.R, mc = ly.mc, xs = ly.xs, kp = ly.kp, W = ly.w;
+  const uint32_t R = a.R, mc = ly.mc, xs = ly.xs, kp = ly.kp;
   const uint32_t nch = static_cast<uint32_t>(a.stride >> 4);
   const uint32_t kch = kp >> 4;  // 16-byte chunks per padded smem row
   const uint32_t FULL = 0xFFFFFFFFu;
+  uint64_t* tmp = reinterpret_cast<uint64_t*>(X);  // unsorted keys live in X until the gather
 
   for (uint32_t li = blockIdx.x; li < a.count; li += gridDim.x) {
     const uint32_t l = a.list_index ? a.list_index[li] : li;
     const uint32_t p = a.points[l];
     const uint64_t beg = a.begins ? a.begins[l] : uint64_t(l) * a.fixed_stride;
-    const uint64_t m = a.lengths[l];
+    const uint32_t m = a.lengths[l];
     uint32_t* orow = a.out_rows ? a.out_rows + uint64_t(l) * R : a.out_adj + uint64_t(p) * R;
     if (m < a.mmin) continue;
-    if (m > mc) {
+    if (m > a.mcap) {  // a.mcap <= mc: the lists' own capacity, not the tile's
       if (tid == 0 && !a.skip_long) atomicAdd(a.too_long, 1u);
       continue;
     }
-    uint32_t Mp = 32;
-    while (Mp < m) Mp <<= 1;
-    for (uint32_t i = tid; i < Mp; i += NT) {
-      uint64_t k = kMaxKey;
-      if (i < m) {
-        const uint32_t id = a.cand_ids[beg + i];
-        if (id != p) k = make_key(a.cand_dists[beg + i], id);  // prune.cpp:18-20 drops p
-      }
-      keys[i] = k;
+    if (tid == 0) sh_m2 = 0;
+    for (uint32_t i = tid; i < W; i += NT) zmask[i] = 0u;
+    __syncthreads();
+    for (uint32_t i = tid; i < m; i += NT) {
+      const uint32_t id = a.cand_ids[beg + i];
+      const uint64_t k = id != p ? make_key(a.cand_dists[beg + i], id) : kMaxKey;  // prune.cpp:18-20
+      tmp[i] = k;
+      if (k != kMaxKey) atomicAdd(&sh_m2, 1u);
     }
     __syncthreads();
-    for (uint32_t k = 2; k <= Mp; k <<= 1) {  // sort by (dist, id) — prune.cpp:21
-      for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-        for (uint32_t i = tid; i < Mp; i += NT) {
-          const uint32_t ixj = i ^ j;
-          if (ixj > i) {
-            const uint64_t x = keys[i], y = keys[ixj];
-            if ((x > y) == ((i & k) == 0)) {
-              keys[i] = y;
-              keys[ixj] = x;
-            }
-          }
-        }
-        __syncthreads();
-      }
+    // sort by (dist, id) — prune.cpp:21 — by rank: keys are distinct
+    for (uint32_t i = tid; i < m; i += NT) {
+      const uint64_t k = tmp[i];
+      if (k == kMaxKey) continue;
+      uint32_t r = 0;
+      for (uint32_t j = 0; j < m; j++) r += tmp[j] < k ? 1u : 0u;
+      keys[r] = k;
     }
-    const uint32_t m2 = lower_bound_u64(keys, Mp, kMaxKey);
+    __syncthreads();
+    const uint32_t m2 = sh_m2;
     const uint32_t mpad = (m2 + 15) & ~15u;
-    const uint32_t mw = (m2 + 31) >> 5;  // mask words in use
     // gather the rows in sorted order (zero padding to kp bytes and mpad rows)
     for (uint32_t t = tid; t < mpad * kch; t += NT) {
       const uint32_t r = t / kch, c = t - r * kch;
@@ -341,6 +335,8 @@ __global__ void __launch_bounds__(kMmaThreads) prune_mma_kernel(const PruneArgs 
       *reinterpret_cast<uint4*>(X + size_t(r) * xs + c * 16) = v;
     }
     for (uint32_t t = tid; t < m2 * W; t += NT) cm[t] = 0u;
+    for (uint32_t i = tid; i < m2; i += NT)
+      if (key_dist(keys[i]) == 0.0f) atomicOr(&zmask[i >> 5], 1u << (i & 31));
     __syncthreads();
     for (uint32_t r = tid; r < mpad; r += NT) {
       const uint32_t* w = reinterpret_cast<const uint32_t*>(X + size_t(r) * xs);
@@ -373,7 +369,6 @@ __global__ void __launch_bounds__(kMmaThreads) prune_mma_kernel(const PruneArgs 
           mma_i8<SIGNED>(acc0, af, bf[0], bf[1]);
           mma_i8<SIGNED>(acc1, af, bf[2], bf[3]);
         }
-        // bits for rows r0+g and r0+g+8, 16 columns n0.. (two per lane per 8-col tile)
         uint32_t bits_lo = 0, bits_hi = 0;
 #pragma unroll
         for (int h = 0; h < 2; h++) {
@@ -384,7 +379,7 @@ __global__ void __launch_bounds__(kMmaThreads) prune_mma_kernel(const PruneArgs 
             const uint32_t col = n0 + ccol;
             const int gram = h ? acc1[e] : acc0[e];
             bool cull = false;
-            if (col > row && col < m2 && row < m2) {
+            if (col > row && col < m2) {
               const float di = key_dist(keys[row]);
               if (di != 0.0f) {  // prune.cpp:32: a zero-distance pick culls nothing
                 const float via = M == kL2 ? __int2float_rn(norm[row] + norm[col] - 2 * gram)
@@ -400,47 +395,66 @@ __global__ void __launch_bounds__(kMmaThreads) prune_mma_kernel(const PruneArgs 
             }
           }
         }
-        // OR the four lanes of a row group, then one lane per row writes 16 bits
         bits_lo |= __shfl_xor_sync(FULL, bits_lo, 1);
         bits_lo |= __shfl_xor_sync(FULL, bits_lo, 2);
         bits_hi |= __shfl_xor_sync(FULL, bits_hi, 1);
         bits_hi |= __shfl_xor_sync(FULL, bits_hi, 2);
         if (tg == 0) {
           const uint32_t sh = n0 & 31;
-          if (bits_lo && r0 + g < m2) atomicOr(&cm[(r0 + g) * W + (n0 >> 5)], bits_lo << sh);
-          if (bits_hi && r0 + g + 8 < m2) atomicOr(&cm[(r0 + g + 8) * W + (n0 >> 5)], bits_hi << sh);
+          if (bits_lo) atomicOr(&cm[(r0 + g) * W + (n0 >> 5)], bits_lo << sh);
+          if (bits_hi) atomicOr(&cm[(r0 + g + 8) * W + (n0 >> 5)], bits_hi << sh);
         }
       }
     }
     __syncthreads();
-    // the greedy walk (prune.cpp:25-43) as a bit loop in warp 0
+    // the greedy walk (prune.cpp:25-43): every lane of warp 0 carries the whole
+    // culled set in registers; the next candidate's mask row is loaded before
+    // the current decision so the chain per candidate is a bit test and an OR
     if (warp == 0) {
-      uint32_t culled = 0;  // lane w holds culled word w
+      uint32_t culled[W], zm[W];
+#pragma unroll
+      for (int w = 0; w < W; w++) {
+        culled[w] = 0u;
+        zm[w] = zmask[w];
+      }
       uint32_t nsel = 0;
-      uint64_t evals = 0;
-      for (uint32_t i = 0; i < m2; i++) {
-        const uint32_t cw = __shfl_sync(FULL, culled, i >> 5);
-        if ((cw >> (i & 31)) & 1u) continue;
-        if (lane == 0) sel[nsel] = key_id(keys[i]);
-        nsel++;
-        if (nsel == R) break;
-        if (key_dist(keys[i]) == 0.0f) continue;
-        if (a.stats) {  // reference dist_comps: the alive candidates after i
-          uint32_t w = lane < mw ? ~culled : 0u;
-          const uint32_t lo = i + 1;
-          if (lane < (lo >> 5)) w = 0u;
-          else if (lane == (lo >> 5)) w &= ~((1u << (lo & 31)) - 1u);
-          if (lane == mw - 1 && (m2 & 31)) w &= (1u << (m2 & 31)) - 1u;
-          evals += __reduce_add_sync(FULL, __popc(w));
+      uint4 nxt[W / 4];
+#pragma unroll
+      for (int q = 0; q < W / 4; q++) nxt[q] = reinterpret_cast<const uint4*>(cm)[q];
+#pragma unroll
+      for (int w = 0; w < W; w++) {
+        if (32u * w >= m2 || nsel == R) break;
+        for (uint32_t b = 0; b < 32; b++) {
+          const uint32_t i = 32u * w + b;
+          if (i >= m2) break;
+          uint4 cur[W / 4];
+#pragma unroll
+          for (int q = 0; q < W / 4; q++) cur[q] = nxt[q];
+          if (i + 1 < m2) {
+#pragma unroll
+            for (int q = 0; q < W / 4; q++) nxt[q] = reinterpret_cast<const uint4*>(cm + (i + 1) * W)[q];
+          }
+          if ((culled[w] >> b) & 1u) continue;
+          if (lane == 0) sel[nsel] = key_id(keys[i]);
+          nsel++;
+          if (nsel == R) break;
+          if ((zm[w] >> b) & 1u) continue;
+#pragma unroll
+          for (int q = 0; q < W / 4; q++) {
+            culled[4 * q + 0] |= cur[q].x;
+            culled[4 * q + 1] |= cur[q].y;
+            culled[4 * q + 2] |= cur[q].z;
+            culled[4 * q + 3] |= cur[q].w;
+          }
         }
-        if (lane < mw) culled |= cm[i * W + lane];
       }
       if (lane == 0) {
         sh_nsel = nsel;
         if (a.stats) {
           atomicAdd(a.stats + kStPruneLists, 1ull);
           atomicAdd(a.stats + kStPruneCands, static_cast<unsigned long long>(m));
-          atomicAdd(a.stats + kStPruneEvals, static_cast<unsigned long long>(evals));
+          // pair tests evaluated on the tensor cores
+          atomicAdd(a.stats + kStPruneEvals, static_cast<unsigned long long>(m2) * (m2 - (m2 > 0)) / 2);
         }
       }
     }
@@ -734,7 +748,7 @@ template <int E, int M>
 cudaError_t launch_mma(const PruneArgs& a, cudaStream_t s) {
   if (a.count == 0) return cudaSuccess;
   const MmaLayout ly = mma_layout(a.mcap, static_cast<uint32_t>(a.stride), a.R);
-  auto k = prune_mma_kernel<E, M>;
+  auto k = ly.w == 4 ? prune_mma_kernel<E, M, 4> : (ly.w == 8 ? prune_mma_kernel<E, M, 8> : prune_mma_kernel<E, M, 16>);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ly.total));
   if (e != cudaSuccess) return e;
   k<<<a.count, kMmaThreads, ly.total, s>>>(a, ly);
