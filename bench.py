@@ -49,6 +49,7 @@ def load_module(name, rel):
 # (which loads libgann_b200.so) so the reference arm never touches our library.
 datagen = load_module("gann_datagen", "paper_2305_04359_b200/datagen.py")
 evalutil = load_module("gann_evalutil", "paper_2305_04359_b200/evalutil.py")
+distutil = load_module("gann_distutil", "paper_2305_04359_b200/distutil.py")
 
 
 def parse():
@@ -170,19 +171,16 @@ def run_ours(args):
         torch.cuda.synchronize()
 
     def allreduce(x, op="max"):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
-        return float(t.item())
+        return distutil.reduce_scalar(x, op, dist if world > 1 else None, "cuda")
 
     # ---- data: generated straight into HBM ------------------------------------------
     base = torch.empty(n * d, dtype=torch.uint8, device="cuda")
     check(lib().gann_generate_u8(base.data_ptr(), n, d, cfg.clusters, cfg.sigma, cfg.noise_frac,
                                  cfg.center_seed, cfg.base_seed, 0, dev))
     qdev = torch.empty(nq * d, dtype=torch.uint8, device="cuda")
+    row0, _ = distutil.query_rows(rank, nq)  # each rank searches its own query shard
     check(lib().gann_generate_u8(qdev.data_ptr(), nq, d, cfg.clusters, cfg.sigma, cfg.noise_frac,
-                                 cfg.center_seed, cfg.query_seed, rank * nq, dev))
+                                 cfg.center_seed, cfg.query_seed, row0, dev))
     idx = g.Index.from_device(base.data_ptr(), n, d, np.uint8, cfg.metric, cfg.R, dev)
 
     # ---- build (timed once) ---------------------------------------------------------------
@@ -196,11 +194,7 @@ def run_ours(args):
     bstats = idx.stats()
     adj_t = _tensor_from_ptr(idx.device_ptrs()[2], n * cfg.R * 4).view(torch.int32)  # a view, no copy
     checksum = int(adj_t.to(torch.int64).mul_(1 + torch.arange(n * cfg.R, device="cuda") % 7919).sum().item())
-    replicas_identical = True
-    if world > 1:
-        sums = [None] * world
-        dist.all_gather_object(sums, checksum)
-        replicas_identical = len(set(sums)) == 1
+    replicas_identical = distutil.replicas_identical(checksum, dist if world > 1 else None)
     deg_mean = float((adj_t != -1).sum().item()) / n
     del adj_t
 
@@ -226,7 +220,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         res = out_ids.cpu().numpy().view(np.uint32).reshape(nq, k)
         rec = float(evalutil.recall_at_k(gt_ids_h, gt_d_h, res, k).mean())
-        rec = allreduce(rec, "sum") / world
+        rec = allreduce(rec, "mean")
         curve.append({"L": L, "recall@10": round(rec, 5)})
         if not args.L and rec >= args.target_recall:
             chosen = L
