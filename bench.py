@@ -33,7 +33,8 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-L_CANDIDATES = [10, 12, 14, 16, 20, 24, 28, 32, 40, 48, 56, 64, 80, 96, 128, 160, 200]
+# BASELINE.json: "beam L swept 10..200"; --L-max widens it
+L_CANDIDATES = [10, 12, 14, 16, 20, 24, 28, 32, 40, 48, 56, 64, 80, 96, 128, 160, 200, 256, 320, 400, 512]
 GT_DEPTH = 16
 
 
@@ -63,6 +64,7 @@ def parse():
     ap.add_argument("--nq", type=int, default=0, help="queries per GPU (default: the config's)")
     ap.add_argument("--target-recall", type=float, default=0.95)
     ap.add_argument("--L", type=int, default=0, help="force the search beam")
+    ap.add_argument("--L-max", type=int, default=200, help="largest beam of the sweep (BASELINE: 10..200)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="CPU baseline sample length")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ref-n", type=int, default=100_000, help="reference arm: points in its CPU build sample")
@@ -124,11 +126,11 @@ def peaks():
 
 
 def search_bytes(stats: dict, row_bytes: int, nq: int, k: int) -> float:
-    """Algorithmic bytes of the search: every distinct evaluated
-    row once (evaluations - filter drops, a lower bound on the distinct count),
-    every expanded adjacency row (deg + 1 words), the queries and the results."""
-    distinct = stats["evaluations"] - stats["filter_drops"]
-    return (distinct * row_bytes + 4.0 * (stats["expansions"] + stats["adj_entries"])
+    """Algorithmic bytes of a search launch:
+    B = sum_q [U_q*d*s + sum_{v in V_q} 4*(1 + deg v) + d*s + 8k], with the
+    distinct-evaluation count U from an EXACT visited-mode run of the same
+    queries (stats["evaluations"] there), |V| and sum deg from the same run."""
+    return (stats["evaluations"] * row_bytes + 4.0 * (stats["expansions"] + stats["adj_entries"])
             + nq * row_bytes + 8.0 * k * nq)
 
 
@@ -215,7 +217,7 @@ def run_ours(args):
 
     curve = []
     chosen = args.L
-    for L in ([args.L] if args.L else L_CANDIDATES):
+    for L in ([args.L] if args.L else [x for x in L_CANDIDATES if x <= args.L_max]):
         search_L(L)
         torch.cuda.synchronize()
         res = out_ids.cpu().numpy().view(np.uint32).reshape(nq, k)
@@ -225,8 +227,9 @@ def run_ours(args):
         if not args.L and rec >= args.target_recall:
             chosen = L
             break
-    if not chosen:
-        chosen = L_CANDIDATES[-1]
+    target_reached = bool(chosen) or args.L > 0
+    if not chosen:  # not reached inside the sweep: report the sweep's largest beam
+        chosen = curve[-1]["L"]
     recall = curve[-1]["recall@10"]
     sp = g.SearchParams(chosen, chosen, 0.0)
 
@@ -242,6 +245,8 @@ def run_ours(args):
     sampler = ClockSampler(dev)
     sampler.start()
     barrier()
+    if os.environ.get("GANN_PROFILE_RANGE"):
+        torch.cuda.profiler.start()  # ncu --profile-from-start off: only the timed launches
     for e0, e1 in evs:
         if flush:
             flush_buf.fill_(1)
@@ -249,12 +254,20 @@ def run_ours(args):
         idx.search_staged(sp, k, out_ids.data_ptr(), out_d.data_ptr(), stream)
         e1.record()
     barrier()
+    if os.environ.get("GANN_PROFILE_RANGE"):
+        torch.cuda.profiler.stop()
     clocks = sampler.stop()
     step_ms = [e0.elapsed_time(e1) for e0, e1 in evs]
     total_ms = allreduce(sum(step_ms))
     sstats = idx.stats()
     qps = world * nq * args.steps / (total_ms / 1e3)
-    per_launch_bytes = search_bytes(sstats, d, nq * args.steps, k) / args.steps
+    # the algorithmic bytes of one launch: the same queries once more in EXACT mode
+    idx.reset_stats()
+    idx.search_device(qdev.data_ptr(), nq, sp, k, out_ids.data_ptr(), out_d.data_ptr(), stream=stream,
+                      visited_mode="exact")
+    torch.cuda.synchronize()
+    xstats = idx.stats()
+    per_launch_bytes = search_bytes(xstats, d, nq, k)
     avg_launch_s = statistics.mean(step_ms) / 1e3
     peak, peak_src = peaks()
     achieved = per_launch_bytes / avg_launch_s / 1e9
@@ -306,6 +319,7 @@ def run_ours(args):
             "n": n, "d": d, "R": cfg.R, "L_build": cfg.L, "alpha": cfg.alpha,
             "max_batch": cfg.max_batch, "queries_per_gpu": nq, "k": k,
             "L_search": chosen, "recall@10": recall, "target_recall": args.target_recall,
+            "target_reached_in_sweep": target_reached,
             "l2": "flushed between steps" if flush else f"inputs larger than L2 ({index_bytes / 1e9:.2f} GB index)",
         },
         "roofline": {
@@ -314,7 +328,9 @@ def run_ours(args):
             "algorithmic_bytes_per_launch": round(per_launch_bytes),
             "avg_launch_ms": round(avg_launch_s * 1e3, 4),
             "traffic": traffic_from_profile("search_kernel"),
-            "filter_drops": sstats["filter_drops"],
+            "distinct_evals_per_query": round(xstats["evaluations"] / nq, 1),
+            "evals_per_query_fast_filter": round(sstats["evaluations"] / (nq * args.steps), 1),
+            "expansions_per_query": round(xstats["expansions"] / nq, 1),
         },
         "cpu_baseline": cpu,
         "e2e": {"value": round(world * nq * args.steps / e2e_s, 1), "unit": "queries/s",
@@ -388,14 +404,14 @@ def run_reference(args):
     build_s = time.perf_counter() - t0
     gt_i, gt_d = orc.groundtruth(data, q, GT_DEPTH, workers=0)
     curve, chosen = [], args.L
-    for L in ([args.L] if args.L else L_CANDIDATES):
+    for L in ([args.L] if args.L else [x for x in L_CANDIDATES if x <= args.L_max]):
         _, ids, _ = orc.time_search(adj, start, data, q, L, L, 0.0, k_out=cfg.k, workers=0, reps=1)
         rec = float(evalutil.recall_at_k(gt_i, gt_d, ids, cfg.k).mean())
         curve.append({"L": L, "recall@10": round(rec, 5)})
         if not args.L and rec >= args.target_recall:
             chosen = L
             break
-    chosen = chosen or L_CANDIDATES[-1]
+    chosen = chosen or curve[-1]["L"]
     for _ in range(args.warmup):
         orc.time_search(adj, start, data, q, chosen, chosen, 0.0, k_out=cfg.k, workers=0, reps=1)
     secs = []

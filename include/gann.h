@@ -45,7 +45,9 @@ enum { GANN_SCALE_CANDIDATE = 0, GANN_SCALE_SELECTED = 1 };
  * reference; dist_comps counts this kernel's own evaluations). REF: the
  * reference's L*L-slot ApproxVisitedSet (include/graphann/search.hpp:24-38)
  * held in global memory, so dist_comps matches the reference too. */
-enum { GANN_VISITED_FAST = 0, GANN_VISITED_REF = 1 };
+/* EXACT: an exact seen-set per query in global memory (never forgets), so
+ * dist_comps counts distinct evaluated ids — the U of SURVEY.md §8d. */
+enum { GANN_VISITED_FAST = 0, GANN_VISITED_REF = 1, GANN_VISITED_EXACT = 2 };
 enum { GANN_OK = 0, GANN_EINVAL = 1, GANN_EIO = 2, GANN_ECUDA = 3 };
 
 typedef struct gann_index gann_index;

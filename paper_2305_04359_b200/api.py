@@ -23,7 +23,7 @@ ELEM = {np.dtype(np.uint8): 0, np.dtype(np.int8): 1, np.dtype(np.float32): 2}
 ELEM_DTYPE = {0: np.uint8, 1: np.int8, 2: np.float32}
 METRIC = {"l2": 0, "ip": 1}
 RULE = {"scale_candidate": 0, "scale_selected": 1}
-VISITED = {"fast": 0, "ref": 1}
+VISITED = {"fast": 0, "ref": 1, "exact": 2}
 
 
 def _p(a) -> Optional[int]:
@@ -187,9 +187,10 @@ class Index:
         return SearchResult(ids, dists, nvis, dc, vi, vd)
 
     def search_device(self, q_ptr: int, nq: int, params: SearchParams, k_out: int, ids_ptr: int,
-                      dists_ptr: int, nvis_ptr: int = 0, dc_ptr: int = 0, stream: int = 0) -> None:
+                      dists_ptr: int, nvis_ptr: int = 0, dc_ptr: int = 0, stream: int = 0,
+                      visited_mode: str = "fast") -> None:
         check(lib().gann_search_device(self._h, C.c_void_p(q_ptr), nq, k_out, params.beam, params.k,
-                                       params.epsilon, 0, C.c_void_p(ids_ptr), C.c_void_p(dists_ptr),
+                                       params.epsilon, VISITED[visited_mode], C.c_void_p(ids_ptr), C.c_void_p(dists_ptr),
                                        C.c_void_p(nvis_ptr or None), C.c_void_p(dc_ptr or None),
                                        C.c_void_p(stream or None)))
 

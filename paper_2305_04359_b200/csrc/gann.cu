@@ -209,7 +209,8 @@ void validate_search(const gann_index* idx, uint32_t k_out, uint32_t L, uint32_t
     fail(GANN_EINVAL, "k=" + std::to_string(k_gate) + " exceeds beam=" + std::to_string(L));
   if (!(eps >= 0.0f && eps <= 0.25f)) fail(GANN_EINVAL, "epsilon must lie in [0, 0.25]");
   if (k_out > k_gate) fail(GANN_EINVAL, "k_out must not exceed k (the expansion gate)");
-  if (mode != GANN_VISITED_FAST && mode != GANN_VISITED_REF) fail(GANN_EINVAL, "unknown visited mode");
+  if (mode != GANN_VISITED_FAST && mode != GANN_VISITED_REF && mode != GANN_VISITED_EXACT)
+    fail(GANN_EINVAL, "unknown visited mode");
   if (idx->n > 0 && idx->start >= idx->n) fail(GANN_EINVAL, "start vertex out of range");
 }
 
@@ -238,8 +239,13 @@ SearchArgs base_search_args(gann_index* idx, uint32_t L, uint32_t k_gate, uint32
 // Launch the search over nq queries, chunking in REF mode so the L*L tables
 // stay under ~1 GiB.
 void run_search(gann_index* idx, SearchArgs a, cudaStream_t s) {
-  if (a.visited_mode == GANN_VISITED_REF) {
-    const uint64_t per = uint64_t(a.L) * a.L * 4;
+  if (a.visited_mode == GANN_VISITED_EXACT) {
+    uint32_t ts = 4096;
+    while (ts < 512u * a.L) ts <<= 1;
+    a.exact_slots = ts;
+  }
+  if (a.visited_mode == GANN_VISITED_REF || a.visited_mode == GANN_VISITED_EXACT) {
+    const uint64_t per = (a.visited_mode == GANN_VISITED_REF ? uint64_t(a.L) * a.L : a.exact_slots) * 4;
     const uint32_t chunk = static_cast<uint32_t>(std::max<uint64_t>(1, (1ull << 30) / per));
     idx->table.ensure(std::min<uint64_t>(chunk, std::max<uint32_t>(a.nq, 1)) * per);
     const uint32_t nq = a.nq;

@@ -32,9 +32,10 @@ struct SearchArgs {
   uint32_t nq;
   uint32_t L, k_gate, k_out;
   float eps;
-  int visited_mode;          // 0 fast (shared hash), 1 reference L*L table
+  int visited_mode;          // 0 fast (shared table), 1 reference L*L table, 2 exact set
+  uint32_t exact_slots;      // mode 2: slots per query (power of two)
   uint32_t hash_log2;        // fast mode table size
-  uint32_t* ref_table;       // mode 1: nq * L * L words, filled by the kernel
+  uint32_t* ref_table;       // modes 1/2: per-query tables, initialised by the kernel
   uint32_t dim;              // real dimension (search_seed)
   uint32_t row_bytes;        // real bytes per row (search_seed)
   uint32_t* out_ids;         // nq * k_out (nullable)

@@ -24,7 +24,10 @@
 // (L*L slots, mix64(id ^ seed) % L^2, include/graphann/search.hpp:24-38,
 // seed from src/search.cpp:52-58) in global memory, applied per expansion
 // with the order-exact warp rule of SURVEY.md §0.4 (first lane of a slot
-// tests, last lane writes), so dist_comps matches the reference too.
+// tests, last lane writes), so dist_comps matches the reference too. EXACT:
+// an open-addressing set per query in global memory that never forgets, so
+// dist_comps is the number of distinct ids evaluated (U in SURVEY.md §8d);
+// used to account the algorithmic bytes of a launch.
 #include <cstdio>
 
 #include "common.cuh"
@@ -165,7 +168,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 7)
     uint32_t* table = nullptr;
     uint64_t seed = 0;
     const uint32_t LL = L * L;
-    if (a.visited_mode == 1) {
+    const uint32_t TS = a.exact_slots;  // mode 2: exact open-addressing set, global memory
+    if (a.visited_mode == 2) {
+      table = a.ref_table + static_cast<uint64_t>(q) * TS;
+      for (uint32_t i = lane; i < TS; i += 32) table[i] = kNone;
+    } else if (a.visited_mode == 1) {
       table = a.ref_table + static_cast<uint64_t>(q) * LL;
       for (uint32_t i = lane; i < LL; i += 32) table[i] = kNone;
       // search_seed — src/search.cpp:52-58 (rows are zero padded to >= 16 bytes,
@@ -183,7 +190,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 7)
     if (lane == 0) {
       beam[0] = ck[0];
       fl[0] = 0;
-      if (a.visited_mode == 1)
+      if (a.visited_mode == 2)
+        table[(start * 0x9E3779B1u) & (TS - 1)] = start;
+      else if (a.visited_mode == 1)
         table[mix64(static_cast<uint64_t>(start) ^ seed) % LL] = start;
       else
         hash[(start * 0x9E3779B1u) >> (32 - hlog2)] = start;
@@ -262,7 +271,18 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 7)
         const bool valid = nb != kNone;
         adjsum += __popc(__ballot_sync(FULL, valid));
         bool fresh;
-        if (a.visited_mode == 1) {
+        if (a.visited_mode == 2) {
+          fresh = false;
+          if (valid) {
+            uint32_t slot = (nb * 0x9E3779B1u) & (TS - 1);
+            while (true) {
+              const uint32_t old = atomicCAS(table + slot, kNone, nb);
+              if (old == kNone) { fresh = true; break; }
+              if (old == nb) break;
+              slot = (slot + 1) & (TS - 1);
+            }
+          }
+        } else if (a.visited_mode == 1) {
           const uint32_t slot =
               valid ? static_cast<uint32_t>(mix64(static_cast<uint64_t>(nb) ^ seed) % LL) : kNone;
           const uint32_t peers = __match_any_sync(FULL, slot);

@@ -322,3 +322,15 @@ def test_generator_matches_numpy_restatement():
         check(lib().gann_generate_u8(buf.data_ptr(), n, d, cl, sig, nf, 1, 2, 500, 0))
         want = datagen.gen_u8_numpy(n, d, cl, sig, nf, 1, 2, row0=500)
         assert (buf.cpu().numpy().reshape(n, d) == want).all()
+
+
+def test_cpp_dropin_runs():
+    """The reference's hand instances through include/gann.hpp (C++)."""
+    import subprocess
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    subprocess.run(["make", "-s", "-C", str(root / "tests" / "cpp")], check=True)
+    r = subprocess.run([str(root / "tests" / "cpp" / "_build" / "test_gann_cpp")], capture_output=True, text=True,
+                       timeout=120)
+    assert r.returncode == 0, r.stderr
+    assert "ok" in r.stdout

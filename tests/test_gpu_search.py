@@ -151,6 +151,22 @@ def test_search_parity_integer(oracle, dtype, L, k, eps):
             assert (got.dist_comps == want["dist_comps"]).all()
 
 
+@pytest.mark.parametrize("L,k", [(10, 10), (64, 64), (128, 10)])
+def test_exact_mode_counts_distinct_evaluations(oracle, orc, L, k):
+    """EXACT visited mode: same ids/|V|, and dist_comps equals the restatement's
+    exact seen-set count (the distinct-evaluation U of SURVEY.md §8d)."""
+    g = _g()
+    data, qs = mixture(13, 4000, 32, clusters=16, nq=200)
+    adj, start = oracle.build(data, 24, 48, 1.2, workers=4)
+    idx = idx_with_graph(data, adj, start)
+    want = orc.beam_search(adj, start, data, qs, L, k, 0.0, visited_mode=0)
+    got = idx.search(qs, g.SearchParams(L, k, 0.0), visited_mode="exact")
+    assert (got.ids == want["ids"]).all() and (got.n_visited == want["n_visited"]).all()
+    assert (got.dist_comps == want["dist_comps"]).all()
+    fast = idx.search(qs, g.SearchParams(L, k, 0.0), visited_mode="fast")
+    assert (fast.ids == want["ids"]).all() and (fast.dist_comps >= want["dist_comps"]).all()
+
+
 @pytest.mark.parametrize("d", [16, 128, 256])
 def test_search_parity_u8_widths(oracle, d):
     """Row widths exercise the 2/8/16-lanes-per-row gathers."""

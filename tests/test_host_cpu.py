@@ -105,3 +105,13 @@ def test_recall_matches_reference(orc):
     mine = recall_at_k(ti, td, res, 10)
     theirs = [orc.recall(ti[i], td[i], res[i], 10) for i in range(50)]
     assert np.allclose(mine, theirs)
+
+
+def test_cpp_dropin_header_builds_and_links():
+    """include/gann.hpp (the C++ mirror of graphann's API) compiles and links."""
+    import subprocess
+    subprocess.run(["make", "-s", "-C", str(ROOT / "tests" / "cpp")], check=True)
+    exe = ROOT / "tests" / "cpp" / "_build" / "test_gann_cpp"
+    assert exe.exists()
+    out = subprocess.run(["nm", "-D", "--undefined-only", str(exe)], capture_output=True, text=True).stdout
+    assert "gann_build" in out and "gann_search" in out
