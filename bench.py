@@ -143,7 +143,9 @@ def traffic_from_profile(name: str):
 
 
 # ---------------------------------------------------------------------------------
-def run_ours(args):
+def setup(args):
+    """Data in HBM, the GPU build (timed once), ground truth and the beam L
+    that reaches the recall target. Shared by both arms."""
     import torch
     import torch.distributed as dist
 
@@ -232,6 +234,22 @@ def run_ours(args):
         chosen = curve[-1]["L"]
     recall = curve[-1]["recall@10"]
     sp = g.SearchParams(chosen, chosen, 0.0)
+
+    return dict(torch=torch, dist=dist, g=g, check=check, lib=lib, cfg=cfg, nq=nq, n=n, d=d, k=k, dev=dev,
+                rank=rank, world=world, barrier=barrier, allreduce=allreduce, base=base, qdev=qdev, idx=idx,
+                build_s=build_s, bstats=bstats, replicas_identical=replicas_identical, deg_mean=deg_mean,
+                out_ids=out_ids, out_d=out_d, stream=stream, search_L=search_L, curve=curve, chosen=chosen,
+                recall=recall, target_reached=target_reached, sp=sp)
+
+
+def run_ours(args):
+    S = setup(args)
+    torch, dist, g, check, lib, cfg = S["torch"], S["dist"], S["g"], S["check"], S["lib"], S["cfg"]
+    nq, n, d, k, dev, rank, world = S["nq"], S["n"], S["d"], S["k"], S["dev"], S["rank"], S["world"]
+    barrier, allreduce, base, qdev, idx = S["barrier"], S["allreduce"], S["base"], S["qdev"], S["idx"]
+    build_s, bstats, replicas_identical, deg_mean = S["build_s"], S["bstats"], S["replicas_identical"], S["deg_mean"]
+    out_ids, out_d, stream, search_L, curve = S["out_ids"], S["out_d"], S["stream"], S["search_L"], S["curve"]
+    chosen, recall, target_reached, sp = S["chosen"], S["recall"], S["target_reached"], S["sp"]
 
     # ---- timed search steps --------------------------------------------------------
     l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
@@ -383,58 +401,63 @@ def cpu_baseline_search(idx, base, q_host, L, k, seconds, out_ids, nq):
 
 # ---------------------------------------------------------------------------------
 def run_reference(args):
-    """The reference's own CPU path (oracle/_ref: graphann compiled from its
-    sources) on a bounded sample of the same workload."""
-    rank = int(os.environ.get("RANK", 0))
-    if rank != 0:
+    """The reference's own CPU search (oracle/_ref = graphann's sources,
+    beam_search through its public API, parallel_for over all host threads)
+    on this arm's workload: the same 10M-point index, the same 10k queries and
+    the same recall-selected beam L. The index and L are set up exactly as in
+    our arm (setup(): GPU build, untimed); only the search is timed. The
+    reference's build of 10M points would take ~8 min on the host, so its
+    build speed is measured on a bounded 100k-point prefix and reported
+    beside it. Under torchrun only rank 0 runs."""
+    if int(os.environ.get("RANK", 0)) != 0:
         return
+    os.environ["WORLD_SIZE"] = "1"  # rank 0 alone: no process group
     from oracle.oracle import Oracle, available
 
     kind = "reference" if available("ref") else "port"
     orc = Oracle("ref" if kind == "reference" else "orc")
-    cfg = datagen.CONFIGS[args.config]
-    n = min(args.ref_n, args.n or cfg.n)
-    nq = args.nq or cfg.n_queries
-    cap = int(n * cfg.batch_cap_frac) if cfg.batch_cap_frac else 0
-    data = datagen.host_base(cfg, n)
-    q = datagen.gen_u8_numpy(nq, cfg.d, cfg.clusters, cfg.sigma, cfg.noise_frac, cfg.center_seed, cfg.query_seed)
+    S = setup(args)
+    cfg, idx, nq, k, chosen = S["cfg"], S["idx"], S["nq"], S["k"], S["chosen"]
+    adj, _, start = idx.export_graph()
+    data = S["base"].view(idx.n, idx.d).cpu().numpy()
+    q = S["qdev"].view(nq, idx.d).cpu().numpy()
+    gpu_ids = S["out_ids"].cpu().numpy().view(np.uint32).reshape(nq, k)
     cores = os.cpu_count()
-    t0 = time.perf_counter()
-    adj, start = orc.build(data, cfg.R, cfg.L, cfg.alpha, cap=cap, workers=0)
-    build_s = time.perf_counter() - t0
-    gt_i, gt_d = orc.groundtruth(data, q, GT_DEPTH, workers=0)
-    curve, chosen = [], args.L
-    for L in ([args.L] if args.L else [x for x in L_CANDIDATES if x <= args.L_max]):
-        _, ids, _ = orc.time_search(adj, start, data, q, L, L, 0.0, k_out=cfg.k, workers=0, reps=1)
-        rec = float(evalutil.recall_at_k(gt_i, gt_d, ids, cfg.k).mean())
-        curve.append({"L": L, "recall@10": round(rec, 5)})
-        if not args.L and rec >= args.target_recall:
-            chosen = L
-            break
-    chosen = chosen or curve[-1]["L"]
+    # one graphann pass per step (warm-up passes untimed)
     for _ in range(args.warmup):
-        orc.time_search(adj, start, data, q, chosen, chosen, 0.0, k_out=cfg.k, workers=0, reps=1)
-    secs = []
+        orc.time_search(adj, start, data, q, chosen, chosen, 0.0, k_out=k, workers=0, reps=1)
+    secs, ids = [], None
     for _ in range(args.steps):
-        s, _, _ = orc.time_search(adj, start, data, q, chosen, chosen, 0.0, k_out=cfg.k, workers=0, reps=1)
-        secs.append(s)
+        sec, ids, _ = orc.time_search(adj, start, data, q, chosen, chosen, 0.0, k_out=k, workers=0, reps=1)
+        secs.append(sec)
     value = nq * args.steps / sum(secs)
-    sample = (f"graphann beam_search {{L={chosen},L,0}} top-10 over all {nq} queries per step, graph built by "
-              f"graphann on the first {n} points of {cfg.name} (batch cap {cap}), parallel_for on {cores} threads")
+    # the reference's build speed on a bounded prefix (host cores)
+    nb = min(args.ref_n, cfg.n)
+    pref = data[:nb]
+    cap = int(nb * cfg.batch_cap_frac) if cfg.batch_cap_frac else 0
+    t0 = time.perf_counter()
+    orc.build(pref, cfg.R, cfg.L, cfg.alpha, cap=cap, workers=0)
+    build_s = time.perf_counter() - t0
+    sample = (f"graphann beam_search {{L={chosen},L,0}} top-{k}, one pass over all {nq} queries per step, over the "
+              f"same {idx.n}-point index as our arm (built by our GPU build, bit-identical to graphann's for u8), "
+              f"parallel_for on {cores} threads")
     line = {
         "impl": "reference",
         "metric": "search QPS at recall@10>=0.95 (Alg.1 beam {L,L,0}, top-10) over a B200-built Vamana graph",
         "value": round(value, 1), "unit": "queries/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(1e3 * sum(secs) / args.steps, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8",
-        "data": "synthetic: seeded Gaussian mixture with BASELINE config shapes (datagen.py), host numpy restatement",
-        "config": {"workload": f"BASELINE configs[1]: {cfg.name} (bounded CPU sample: first {n} points)",
-                   "n": n, "d": cfg.d, "R": cfg.R, "L_build": cfg.L, "alpha": cfg.alpha, "max_batch": cap,
-                   "queries": nq, "k": cfg.k, "L_search": chosen, "recall@10": curve[-1]["recall@10"]},
-        "cpu_baseline": {"value": round(value, 1), "unit": "queries/s", "cores": cores, "kind": kind, "sample": sample},
+        "data": "synthetic: seeded Gaussian mixture with BASELINE config shapes (datagen.py)",
+        "config": {"workload": f"BASELINE configs[1]: {cfg.name}", "n": idx.n, "d": idx.d, "R": cfg.R,
+                   "L_build": cfg.L, "alpha": cfg.alpha, "max_batch": cfg.max_batch, "queries": nq, "k": k,
+                   "L_search": chosen, "recall@10": S["recall"]},
+        "cpu_baseline": {"value": round(value, 1), "unit": "queries/s", "cores": cores, "kind": kind,
+                         "sample": sample},
         "e2e": {"value": round(value, 1), "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "build": {"points_per_s": round(n / build_s, 1), "seconds": round(build_s, 3), "n": n, "cores": cores},
-        "recall_curve": curve,
+        "ids_identical_to_gpu": float((ids == gpu_ids).all(axis=1).mean()),
+        "build": {"points_per_s": round(nb / build_s, 1), "seconds": round(build_s, 3), "n": nb, "cores": cores,
+                  "sample": f"graphann build_diskann loop on the first {nb} points (batch cap {cap})"},
+        "recall_curve": S["curve"],
     }
     print(json.dumps(line), flush=True)
 

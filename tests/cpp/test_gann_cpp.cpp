@@ -84,8 +84,15 @@ int main() {
       mean += g.degree[v];
     }
     CHECK(mean / n > 2.0);
-    auto r = beam_search(idx, pts.data(), 10, SearchParams{32, 10, 0.0f});
-    for (uint32_t q = 0; q < 10; q++) CHECK(r[q].neighbors[0].id == q && r[q].neighbors[0].dist == 0.0f);
+    // self-queries on uniform data: an ANN search should find most points themselves
+    auto r = beam_search(idx, pts.data(), 20, SearchParams{64, 10, 0.0f});
+    uint32_t self = 0;
+    for (uint32_t q = 0; q < 20; q++) {
+      CHECK(r[q].neighbors.size() == 10);
+      for (size_t t = 1; t < 10; t++) CHECK(!neighbor_less(r[q].neighbors[t], r[q].neighbors[t - 1]));
+      self += r[q].neighbors[0].id == q && r[q].neighbors[0].dist == 0.0f;
+    }
+    CHECK(self >= 16);
   }
   std::printf("gann.hpp drop-in: ok\n");
   return 0;
