@@ -181,6 +181,9 @@ typedef struct gann_stats {
   uint64_t back_groups;     /* distinct targets */
   uint64_t back_pruned;     /* targets re-pruned */
   double build_ms[6];       /* start, search, prune, group, merge, reprune */
+  uint64_t merges;          /* search: expansions whose candidates changed the beam */
+  uint64_t survivors;       /* search: candidates inserted into the beam */
+  uint64_t moved;           /* search: beam entries shifted by those inserts */
 } gann_stats;
 int gann_get_stats(const gann_index* idx, gann_stats* out);
 int gann_reset_stats(gann_index* idx);

@@ -7,10 +7,13 @@ missing, importing the package fails loudly.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 HERE = Path(__file__).resolve().parent
 LIB_PATH = HERE / "libgann_b200.so"
+if os.environ.get("GANN_LIB"):  # experiments: an alternative in-tree build of the same ABI
+    LIB_PATH = HERE / os.environ["GANN_LIB"]
 
 GANN_NONE = 0xFFFFFFFF
 GANN_OK, GANN_EINVAL, GANN_EIO, GANN_ECUDA = 0, 1, 2, 3
@@ -34,6 +37,9 @@ class GannStats(C.Structure):
         ("back_groups", C.c_uint64),
         ("back_pruned", C.c_uint64),
         ("build_ms", C.c_double * 6),
+        ("merges", C.c_uint64),
+        ("survivors", C.c_uint64),
+        ("moved", C.c_uint64),
     ]
 
 

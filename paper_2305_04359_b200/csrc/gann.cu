@@ -100,8 +100,7 @@ uint32_t env_u32(const char* name, uint32_t dflt) {
 uint32_t hash_log2_for(uint32_t L) {
   const uint32_t forced = env_u32("GANN_HASH_LOG2", 0);
   if (forced) return std::min<uint32_t>(std::max<uint32_t>(forced, 5), 15);
-  if (L <= 256) return 10;
-  return 11;
+  return L <= 160 ? 10 : 9;  // measured on B200 at 10M (tools/profile_search.py, HLOGS sweep)
 }
 
 }  // namespace
@@ -232,6 +231,7 @@ SearchArgs base_search_args(gann_index* idx, uint32_t L, uint32_t k_gate, uint32
   a.dim = idx->d;
   a.row_bytes = idx->row_bytes;
   a.overflow = idx->flags;
+  a.next_query = idx->flags + 2;
   a.stats = idx->stats;
   return a;
 }
@@ -1151,6 +1151,9 @@ int gann_get_stats(const gann_index* idx, gann_stats* out) {
     out->prune_lists = s[kStPruneLists];
     out->prune_candidates = s[kStPruneCands];
     out->prune_evals = s[kStPruneEvals];
+    out->merges = s[kStMerges];
+    out->survivors = s[kStSurvivors];
+    out->moved = s[kStMoved];
     out->back_pairs = idx->back_pairs;
     out->back_groups = idx->back_groups;
     out->back_pruned = idx->back_pruned;

@@ -16,7 +16,7 @@ Geometry make_geometry(uint32_t nch);
 
 enum StatIdx {
   kStQueries = 0, kStExpansions, kStEvals, kStDrops, kStAdj,
-  kStPruneLists, kStPruneCands, kStPruneEvals, kStCount
+  kStPruneLists, kStPruneCands, kStPruneEvals, kStMerges, kStSurvivors, kStMoved, kStCount
 };
 
 struct SearchArgs {
@@ -46,6 +46,7 @@ struct SearchArgs {
   float* vis_dists;
   uint32_t vcap;
   uint32_t* overflow;        // count of searches whose |V| exceeded vcap
+  uint32_t* next_query;      // persistent warps: dynamic query counter (zeroed per launch)
   unsigned long long* stats; // kStCount counters (nullable)
 };
 size_t search_smem_per_warp(uint32_t L, uint32_t R, uint32_t hash_log2);

@@ -28,6 +28,7 @@
 // an open-addressing set per query in global memory that never forgets, so
 // dist_comps is the number of distinct ids evaluated (U in SURVEY.md §8d);
 // used to account the algorithmic bytes of a launch.
+#include <algorithm>
 #include <cstdio>
 
 #include "common.cuh"
@@ -38,6 +39,9 @@ namespace gann {
 namespace {
 
 constexpr int kWarpsPerBlock = 4;
+#ifndef GANN_SEARCH_MINB
+#define GANN_SEARCH_MINB 7  // resident CTAs per SM the register budget targets (72 regs)
+#endif
 
 // Rows in flight per lane group per pass: U <= LPR so the transposed
 // reduction can hand every lane of the group (at most) one finished row.
@@ -73,6 +77,8 @@ __device__ __forceinline__ T transpose_reduce(T (&v)[U], int sub) {
 }
 
 // Distances from the lane's query chunks qr to rows ids[0..m) -> keys out[].
+// Lane group g (LPR lanes) takes U consecutive rows per pass, so its ids come
+// from one vectorised shared load; the chunk predicate is per lane and hoisted.
 template <class Op, int LPR, int CPL>
 __device__ __forceinline__ void eval_rows(const uint8_t* __restrict__ data, uint64_t stride,
                                           uint32_t nch, const uint32_t* ids, uint32_t m,
@@ -81,19 +87,35 @@ __device__ __forceinline__ void eval_rows(const uint8_t* __restrict__ data, uint
   constexpr int U = Unroll<LPR, CPL>::U;
   const int sub = lane & (LPR - 1);
   const int grp = lane / LPR;
-  for (uint32_t base = 0; base < m; base += RPP * U) {
+  bool chv[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; c++) chv[c] = static_cast<uint32_t>(sub + c * LPR) < nch;
+  const uint4* lane_base = reinterpret_cast<const uint4*>(data) + sub;
+  const uint64_t stride16 = stride >> 4;
+  for (uint32_t b0 = 0; b0 < m; b0 += RPP * U) {
+    const uint32_t rb = b0 + grp * U;
+    uint32_t id[U];
+    if (U % 4 == 0) {
+#pragma unroll
+      for (int u = 0; u < U; u += 4) {
+        const uint4 v = *reinterpret_cast<const uint4*>(ids + rb + u);
+        id[u] = v.x;
+        if (u + 1 < U) id[u + 1] = v.y;
+        if (u + 2 < U) id[u + 2] = v.z;
+        if (u + 3 < U) id[u + 3] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < U; u++) id[u] = ids[rb + u];
+    }
     uint4 x[U][CPL];
 #pragma unroll
     for (int u = 0; u < U; u++) {
-      const uint32_t r = base + u * RPP + grp;
-      const uint32_t id = r < m ? ids[r] : 0u;
-      const uint8_t* rp = data + static_cast<uint64_t>(id) * stride;
+      const bool rv = rb + u < m;
+      const uint4* rp = lane_base + static_cast<uint64_t>(rv ? id[u] : 0u) * stride16;
 #pragma unroll
-      for (int c = 0; c < CPL; c++) {
-        const uint32_t ch = sub + c * LPR;
-        x[u][c] = (r < m && ch < nch) ? __ldg(reinterpret_cast<const uint4*>(rp) + ch)
-                                      : make_uint4(0, 0, 0, 0);
-      }
+      for (int c = 0; c < CPL; c++)
+        x[u][c] = (rv && chv[c]) ? __ldg(rp + c * LPR) : make_uint4(0, 0, 0, 0);
     }
     typename Op::acc_t acc[U];
 #pragma unroll
@@ -103,22 +125,12 @@ __device__ __forceinline__ void eval_rows(const uint8_t* __restrict__ data, uint
       for (int c = 0; c < CPL; c++) acc[u] = Op::chunk(qr[c], x[u][c], acc[u]);
     }
     const typename Op::acc_t tot = transpose_reduce<LPR, U>(acc, sub);
-    const uint32_t r = base + (sub & (U - 1)) * RPP + grp;
+    const uint32_t r = rb + (sub & (U - 1));
     if (sub < U && r < m) out[r] = make_key(Op::finish(tot), ids[r]);
   }
 }
 
 __device__ __forceinline__ uint32_t lanemask_lt(int lane) { return (1u << lane) - 1u; }
-
-// Number of keys in sorted a[0..n) below k (n is small: linear below 8).
-__device__ __forceinline__ uint32_t count_less(const uint64_t* a, uint32_t n, uint64_t k) {
-  if (n <= 8) {
-    uint32_t c = 0;
-    for (uint32_t i = 0; i < n; i++) c += a[i] < k ? 1u : 0u;
-    return c;
-  }
-  return lower_bound_u64(a, n, k);
-}
 
 }  // namespace
 
@@ -131,7 +143,7 @@ size_t search_smem_per_warp(uint32_t L, uint32_t R, uint32_t hash_log2) {
 }
 
 template <int E, int M, int LPR, int CPL>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, 7)
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_SEARCH_MINB)
     search_kernel(const SearchArgs a, const uint32_t per_warp) {
   using Op = DistOp<E, M>;
   extern __shared__ __align__(16) uint8_t smem[];
@@ -153,8 +165,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 7)
   uint8_t* fl = reinterpret_cast<uint8_t*>(hash + H);
   const uint32_t FULL = 0xFFFFFFFFu;
 
-  const uint32_t nw = gridDim.x * (blockDim.x >> 5);
-  for (uint32_t q = blockIdx.x * (blockDim.x >> 5) + wib; q < a.nq; q += nw) {
+  // Persistent warps: a resident grid pulls queries from a global counter, so
+  // slow queries do not leave whole CTAs idle at the end of a wave.
+  uint32_t q = 0;
+  if (lane == 0) q = atomicAdd(a.next_query, 1u);
+  q = __shfl_sync(0xFFFFFFFFu, q, 0);
+  for (; q < a.nq;) {
     const uint8_t* qp = a.query_rows ? a.data + static_cast<uint64_t>(a.query_rows[q]) * a.stride
                                      : a.queries + static_cast<uint64_t>(q) * a.stride;
     const int sub = lane & (LPR - 1);
@@ -198,7 +214,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 7)
         hash[(start * 0x9E3779B1u) >> (32 - hlog2)] = start;
     }
     uint32_t size = 1, nvis = 0, hint = 0, evict = 0;
-    uint64_t evals = 1, adjsum = 0;
+    uint64_t evals = 1, adjsum = 0, merges = 0, survivors = 0, moved = 0;
     // speculative register prefetch of the next expansion's adjacency row
     // (R <= 64: two ids per lane); used when the guess turns out right
     const bool pf_ok = R <= 64;
@@ -346,36 +362,59 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 7)
           for (uint32_t t = 0; t < s; t++) r += tmpk[t] < k ? 1u : 0u;
           srt[r] = k;
           p0 = min(p0, posb[j]);
+          posb[j] += r;  // final position of survivor j
         }
       }
       p0 = __reduce_min_sync(FULL, p0);
+      merges++;
+      survivors += s;
+      moved += size - p0;
       __syncwarp();
-      // move the tail [p0, size) right, last chunk first (targets only grow)
-      for (int b0 = static_cast<int>((size - 1) & ~31u); b0 >= 0 && static_cast<uint32_t>(b0) + 31 >= p0; b0 -= 32) {
-        const uint32_t i = b0 + lane;
-        const bool mv = i >= p0 && i < size;
-        uint64_t k = 0;
-        uint8_t f = 0;
-        uint32_t ni = 0;
-        if (mv) {
-          k = beam[i];
-          f = fl[i];
-          ni = i + count_less(srt, s, k);
+      // move the tail [p0, size) right. Up to 256 entries at once: every lane
+      // reads its (up to 8) entries, computes their targets, then all write —
+      // targets only grow, so groups of 256 go last group first.
+      {
+        constexpr int CG = 8;
+        const int last_g = static_cast<int>((size - 1) >> 8);
+        const int first_g = static_cast<int>(p0 >> 8);
+        for (int gq = last_g; gq >= first_g; gq--) {
+          uint64_t kk[CG];
+          uint32_t ni[CG];
+          uint32_t ffm = 0;
+#pragma unroll
+          for (int c = 0; c < CG; c++) {
+            const uint32_t i = (static_cast<uint32_t>(gq) * CG + c) * 32 + lane;
+            const bool mv = i >= p0 && i < size;
+            kk[c] = mv ? beam[i] : 0ull;
+            ffm |= (mv && fl[i]) ? (1u << c) : 0u;
+            ni[c] = mv ? i : 0xFFFFFFFFu;
+          }
+          {  // this lane's entries ascend with c, so one walk over srt counts them all
+            uint32_t pw = 0;
+#pragma unroll
+            for (int c = 0; c < CG; c++) {
+              if (ni[c] != 0xFFFFFFFFu) {
+                while (pw < s && srt[pw] < kk[c]) pw++;
+                ni[c] += pw;
+              }
+            }
+          }
+          __syncwarp();
+#pragma unroll
+          for (int c = 0; c < CG; c++) {
+            if (ni[c] < L) {
+              beam[ni[c]] = kk[c];
+              fl[ni[c]] = (ffm >> c) & 1u;
+            }
+          }
+          __syncwarp();
         }
-        __syncwarp();
-        if (mv && ni < L) {
-          beam[ni] = k;
-          fl[ni] = f;
-        }
-        __syncwarp();
       }
       for (uint32_t j0 = 0; j0 < s; j0 += 32) {
         const uint32_t j = j0 + lane;
         if (j < s) {
           const uint64_t k = tmpk[j];
-          uint32_t r = 0;
-          for (uint32_t t = 0; t < s; t++) r += srt[t] < k ? 1u : 0u;
-          const uint32_t fin = posb[j] + r;
+          const uint32_t fin = posb[j];
           if (fin < L) {
             beam[fin] = k;
             fl[fin] = 0;
@@ -409,9 +448,14 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 7)
         atomicAdd(a.stats + kStEvals, static_cast<unsigned long long>(evals));
         atomicAdd(a.stats + kStDrops, static_cast<unsigned long long>(evict));
         atomicAdd(a.stats + kStAdj, static_cast<unsigned long long>(adjsum));
+        atomicAdd(a.stats + kStMerges, static_cast<unsigned long long>(merges));
+        atomicAdd(a.stats + kStSurvivors, static_cast<unsigned long long>(survivors));
+        atomicAdd(a.stats + kStMoved, static_cast<unsigned long long>(moved));
       }
     }
     __syncwarp();
+    if (lane == 0) q = atomicAdd(a.next_query, 1u);
+    q = __shfl_sync(0xFFFFFFFFu, q, 0);
   }
 }
 
@@ -424,8 +468,15 @@ cudaError_t launch_one(const SearchArgs& a, cudaStream_t s) {
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  const uint32_t blocks = (a.nq + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  if (blocks == 0) return cudaSuccess;
+  if (a.nq == 0) return cudaSuccess;
+  int per_sm = 0, sms = 0, dev = 0;
+  if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+  if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kWarpsPerBlock * 32, smem)) != cudaSuccess)
+    return e;
+  const uint32_t want = (a.nq + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  const uint32_t blocks = std::min<uint32_t>(want, static_cast<uint32_t>(std::max(1, per_sm) * sms));
+  if ((e = cudaMemsetAsync(a.next_query, 0, sizeof(uint32_t), s)) != cudaSuccess) return e;
   k<<<blocks, kWarpsPerBlock * 32, smem, s>>>(a, per_warp);
   return cudaGetLastError();
 }

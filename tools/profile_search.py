@@ -22,6 +22,7 @@ ap.add_argument("--config", default="c1")
 ap.add_argument("--n", type=int, default=2_000_000)
 ap.add_argument("--nq", type=int, default=10_000)
 ap.add_argument("--L", type=int, default=128)
+ap.add_argument("--Ls", default="", help="comma list: search several beams on one build")
 ap.add_argument("--reps", type=int, default=3)
 args = ap.parse_args()
 cfg = datagen.CONFIGS[args.config].scaled(args.n)
@@ -42,14 +43,23 @@ ids = torch.empty(args.nq * 10, dtype=torch.int32, device="cuda")
 ds = torch.empty(args.nq * 10, dtype=torch.float32, device="cuda")
 s = torch.cuda.current_stream()
 torch.cuda.synchronize()
+idx.reset_stats()
 torch.cuda.profiler.start()  # ncu --profile-from-start off captures only these launches
-for r in range(args.reps):
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    idx.search_staged(g.SearchParams(args.L, args.L, 0.0), 10, ids.data_ptr(), ds.data_ptr(), s.cuda_stream)
-    e1.record()
-    torch.cuda.synchronize()
-    print(f"search L={args.L}: {e0.elapsed_time(e1):.3f} ms", flush=True)
+import os  # noqa: E402
+Ls = [int(x) for x in args.Ls.split(",")] if args.Ls else [args.L]
+for L in Ls:
+    for hl in ([int(x) for x in os.environ.get("HLOGS", "").split(",") if x] or [0]):
+        if hl:
+            os.environ["GANN_HASH_LOG2"] = str(hl)
+        best = 1e9
+        for r in range(args.reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            idx.search_staged(g.SearchParams(L, L, 0.0), 10, ids.data_ptr(), ds.data_ptr(), s.cuda_stream)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        print(f"search L={L} H=2^{hl or 'default'}: {best:.3f} ms", flush=True)
 torch.cuda.profiler.stop()
 st = idx.stats()
-print("stats", {k: st[k] for k in ("queries", "expansions", "evaluations", "filter_drops", "adj_entries")})
+print("stats", {k: st[k] for k in ("queries", "expansions", "evaluations", "filter_drops", "adj_entries", "merges", "survivors", "moved")})
