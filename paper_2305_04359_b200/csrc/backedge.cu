@@ -234,6 +234,14 @@ __global__ void __launch_bounds__(NT)
     cta_sync<NT>();
     if (nm <= R) {  // builder_common.cpp:129-131
       for (uint32_t i = tid; i < R; i += NT) trow[i] = i < nm ? pid[i] : kNone;
+    } else if (nm <= a.prune_small_cap && !a.small_dists) {
+      // the tensor-core prune gathers these rows anyway and computes d(t, .) itself
+      if (tid == 0) {
+        a.plen[g] = nm;
+        atomicMax(a.counters + kCntMaxMerged, static_cast<unsigned long long>(nm));
+        const uint32_t i = static_cast<uint32_t>(atomicAdd(a.counters + kCntPruneSmall, 1ull));
+        a.plist_small[i] = g;
+      }
     } else {  // stage for alpha_prune with fresh distances (:133-138)
       const int sub = tid & (LPR - 1), grp = tid / LPR;
       uint4 tr[CPL];

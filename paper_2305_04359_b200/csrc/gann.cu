@@ -129,7 +129,7 @@ struct gann_index {
   DevBuf q, qids, qdists, qnvis, qdc, qvids, qvd, qstart, table;
   DevBuf order, vis_ids, vis_d, nvis;
   DevBuf gtarget, gcnt, goff, gcursor, gsrc, poff, plen, pid, pdist, bigg, pls, plb;
-  DevBuf pt, ps, ok, ov, misc, gt;
+  DevBuf pt, ps, ok, ov, misc, gt, bins;
   uint32_t staged_nq = 0;
 };
 
@@ -317,27 +317,43 @@ struct Timer {
 // fits: integer rows on the tensor-core kernel in 128/256/512 bins, f32 rows
 // on the warp kernel; anything longer on the chunked kernel.
 void prune_binned(gann_index* idx, PruneArgs p, uint32_t maxlen) {
-  p.skip_long = 1;
-  uint32_t done = 0;
-  if (prune_uses_mma(idx->elem, std::min<uint32_t>(maxlen, 512), idx->stride, idx->R) &&
-      !std::getenv("GANN_NO_MMA")) {
-    for (uint32_t hi : {128u, 256u, 512u}) {
-      if (done >= maxlen) break;
-      p.mmin = done + 1;
-      p.mcap = std::min(hi, maxlen);  // never past the lists' own capacity
-      cu(launch_prune(p, idx->elem, idx->metric, idx->geom, 32, idx->stream), "prune kernel (tensor cores)");
-      done = p.mcap;
+  if (p.count == 0) return;
+  const bool mma = prune_uses_mma(idx->elem, std::min<uint32_t>(maxlen, 512), idx->stride, idx->R) &&
+                   !std::getenv("GANN_NO_MMA");
+  // bins: (0,128] (128,256] (256,512] on the tensor cores, or (0,512] on the
+  // warp kernel for f32; then anything longer on the chunked kernel
+  std::vector<uint32_t> bounds = mma ? std::vector<uint32_t>{128, 256, 512} : std::vector<uint32_t>{kPruneSmallCap};
+  const int nb = static_cast<int>(bounds.size());
+  idx->bins.ensure(size_t(p.count) * (nb + 1) * 4 + 64 + 16 * 4);
+  uint32_t* d_counts = idx->bins.as<uint32_t>();
+  uint32_t* d_bounds = d_counts + 8;
+  uint32_t* d_lists = d_counts + 16;
+  cu(cudaMemcpyAsync(d_bounds, bounds.data(), bounds.size() * 4, cudaMemcpyHostToDevice, idx->stream), "bins");
+  cu(launch_bin_lists(p, d_bounds, nb, d_counts, d_lists, idx->stream), "bin lists");
+  uint32_t counts[8] = {};
+  cu(cudaMemcpyAsync(counts, d_counts, nb * 4, cudaMemcpyDeviceToHost, idx->stream), "bin counts");
+  sync(idx);
+  uint32_t lo = 0, total = 0;
+  for (int b = 0; b < nb; b++) {
+    total += counts[b];
+    if (counts[b]) {
+      PruneArgs q = p;
+      q.list_index = d_lists + size_t(b) * p.count;
+      q.count = counts[b];
+      q.mmin = lo + 1;
+      q.mcap = std::min(bounds[b], maxlen);
+      q.skip_long = 0;
+      cu(launch_prune(q, idx->elem, idx->metric, idx->geom, 32, idx->stream),
+         mma ? "prune kernel (tensor cores)" : "prune kernel");
     }
-  } else {
-    p.mmin = 0;
-    p.mcap = std::min(kPruneSmallCap, maxlen);
-    cu(launch_prune(p, idx->elem, idx->metric, idx->geom, 32, idx->stream), "prune kernel");
-    done = p.mcap;
+    lo = bounds[b];
   }
-  if (maxlen > done) {
-    p.mmin = done + 1;
-    p.mcap = 0xFFFFFFFFu;
-    cu(launch_prune(p, idx->elem, idx->metric, idx->geom, 256, idx->stream), "prune kernel (chunked)");
+  if (total < p.count) {  // the rest is longer than the last bound
+    PruneArgs q = p;
+    q.mmin = lo + 1;
+    q.mcap = 0xFFFFFFFFu;
+    q.skip_long = 1;
+    cu(launch_prune(q, idx->elem, idx->metric, idx->geom, 256, idx->stream), "prune kernel (chunked)");
   }
 }
 
@@ -449,6 +465,7 @@ void apply_back(gann_index* idx, const uint32_t* bsrc, uint32_t B, const uint32_
   b.big_group_cap = kSortedGroupCap;
   if (idx->R > kSmallGroupCap) fail(GANN_EINVAL, "degree bound above 256 is not supported by the back-edge merge");
   b.prune_small_cap = kPruneSmallCap;
+  b.small_dists = !prune_uses_mma(idx->elem, kPruneSmallCap, idx->stride, R) || std::getenv("GANN_NO_MMA");
   b.key_of_target = key_of_target;
   cu(cudaMemsetAsync(idx->counters, 0, sizeof(unsigned long long) * kCntNum, idx->stream), "memset");
   const uint64_t gmax = npairs;  // groups <= pairs
@@ -518,7 +535,9 @@ void apply_back(gann_index* idx, const uint32_t* bsrc, uint32_t B, const uint32_
   if (nps) {
     p.count = nps;
     p.list_index = b.plist_small;
+    p.cand_dists = b.small_dists ? b.pdist : nullptr;  // nullptr: the prune computes d(t, .)
     prune_binned(idx, p, kPruneSmallCap);
+    p.cand_dists = b.pdist;
   }
   if (npb) {
     p.count = npb;
@@ -638,7 +657,7 @@ void gann_index_free(gann_index* idx) {
                     &idx->qvd, &idx->qstart, &idx->table, &idx->order, &idx->vis_ids, &idx->vis_d,
                     &idx->nvis, &idx->gtarget, &idx->gcnt, &idx->goff, &idx->gcursor, &idx->gsrc,
                     &idx->poff, &idx->plen, &idx->pid, &idx->pdist, &idx->bigg, &idx->pls,
-                    &idx->plb, &idx->pt, &idx->ps, &idx->ok, &idx->ov, &idx->misc, &idx->gt})
+                    &idx->plb, &idx->pt, &idx->ps, &idx->ok, &idx->ov, &idx->misc, &idx->gt, &idx->bins})
     b->release();
   if (idx->stream) cudaStreamDestroy(idx->stream);
   delete idx;
@@ -684,6 +703,27 @@ int gann_build(gann_index* idx, uint32_t L, float alpha, int rule, uint64_t seed
        "upload order");
     idx->build_ms[0] += t0.stop();
     const uint32_t* d_order = idx->order.as<uint32_t>();
+    // size the per-batch scratch once, from the largest batch: a cudaFree /
+    // cudaMalloc inside the loop stalls the device for tens of milliseconds
+    {
+      uint32_t bmax = 0;
+      for (auto [lo, hi] : batch_ranges(n, max_batch)) bmax = std::max(bmax, hi - lo);
+      const uint32_t vcap = std::max<uint32_t>(64, 3 * L);
+      const uint64_t pairs = uint64_t(bmax) * idx->R;
+      const uint64_t groups = std::min<uint64_t>(pairs, n);
+      idx->vis_ids.ensure(size_t(bmax) * vcap * 4);
+      idx->vis_d.ensure(size_t(bmax) * vcap * 4);
+      idx->nvis.ensure(size_t(bmax) * 4);
+      idx->gtarget.ensure(pairs * 4);
+      idx->gsrc.ensure(pairs * 4);
+      for (DevBuf* b : {&idx->gcnt, &idx->gcursor, &idx->plen, &idx->bigg, &idx->pls, &idx->plb})
+        b->ensure(groups * 4);
+      idx->goff.ensure(groups * 8);
+      idx->poff.ensure(groups * 8);
+      const uint64_t ptotal = groups * idx->R + pairs;
+      idx->pid.ensure(ptotal * 4);
+      idx->pdist.ensure(ptotal * 4);
+    }
     const bool trace = env_u32("GANN_TRACE", 0) != 0;
     for (auto [lo, hi] : batch_ranges(n, max_batch)) {
       const uint32_t B = hi - lo;

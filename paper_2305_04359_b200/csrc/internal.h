@@ -80,6 +80,9 @@ struct PruneArgs {
 size_t prune_smem_bytes(uint32_t mcap, uint32_t R);
 cudaError_t launch_prune(const PruneArgs& a, int elem, int metric, const Geometry& g, int threads,
                          cudaStream_t s);
+// Length bins: lists[b * count + i] for i < counts[b], b over bounds (last bin: longer).
+cudaError_t launch_bin_lists(const PruneArgs& a, const uint32_t* d_bounds, int nb, uint32_t* d_counts,
+                             uint32_t* d_lists, cudaStream_t s);
 // Integer lists up to 512 candidates run on the tensor cores (IMMA tiles).
 bool prune_uses_mma(int elem, uint32_t mcap, uint64_t stride, uint32_t R);
 
@@ -117,6 +120,7 @@ struct BackEdgeArgs {
   uint32_t small_group_cap;
   uint32_t big_group_cap;
   uint32_t prune_small_cap;
+  int small_dists;          // stage d(t, .) for small lists too (else the prune computes them)
 };
 enum { kCntGroups = 0, kCntPairsCursor, kCntPruneCursor, kCntBig, kCntMaxGroup,
        kCntPruneSmall, kCntPruneBig, kCntMaxMerged, kCntTooBig, kCntNum };

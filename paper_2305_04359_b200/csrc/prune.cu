@@ -14,6 +14,7 @@
 // multiply (__fmul_rn) so the comparison is bit-identical to the reference;
 // integer distances are exact. 32-thread CTAs serve the insert-time lists
 // (|V| ~ L); 256-thread CTAs with up to 16k candidates serve back-edge hubs.
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -238,107 +239,144 @@ __device__ __forceinline__ void mma_i8(int (&c)[4], const uint32_t (&a)[4], uint
 }
 
 struct MmaLayout {
-  uint32_t mc;   // max candidates (multiple of 32)
-  uint32_t kc;   // key slots (power of two >= mc, for the bitonic sort)
+  uint32_t mc;   // max candidates (32 * W)
   uint32_t kp;   // row bytes rounded up to 32
-  uint32_t xs;   // smem row stride (kp + 16)
-  uint32_t w;    // 32-bit words per cull mask (mc / 32)
-  size_t off_x, off_norm, off_cm, off_sel, total;
+  uint32_t xs;   // smem row stride (kp + 16, ldmatrix bank-conflict free)
+  uint32_t w;    // 32-bit words per cull mask
+  uint32_t stride;  // words per list in the global hand-off region
+  size_t off_sk, off_perm, off_x, off_xp, off_norm, off_dk, off_ns, off_cm, total;
 };
-__host__ __device__ inline MmaLayout mma_layout(uint32_t mc, uint32_t stride, uint32_t R) {
+__host__ __device__ inline MmaLayout mma_layout(uint32_t mcap, uint32_t stride, uint32_t /*R*/) {
   MmaLayout l;
-  l.mc = (mc + 31) & ~31u;
+  l.w = mcap <= 128 ? 4 : (mcap <= 256 ? 8 : 16);
+  l.mc = l.w * 32;
   l.kp = (stride + 31) & ~31u;
   l.xs = l.kp + 16;
-  l.w = l.mc <= 128 ? 4 : (l.mc <= 256 ? 8 : 16);
-  l.mc = l.w * 32;
-  l.kc = l.mc;
-  size_t o = size_t(l.kc) * 8;  // keys
+  l.stride = 4 + l.mc + l.w + l.mc * l.w;  // [m2, pad x3][ids mc][zero mask W][cull rows mc*W]
+  size_t o = size_t(l.mc) * 8;              // input-order keys
+  l.off_sk = o;
+  o += size_t(l.mc) * 8;                    // sorted keys
+  l.off_perm = o;
+  o += size_t(l.mc) * 2;
+  o = (o + 15) & ~size_t(15);
   l.off_x = o;
-  o += size_t(l.mc) * l.xs;
+  o += size_t(l.mc + 1) * l.xs;             // + one zero row for padding tiles
+  l.off_xp = o;
+  o += l.xs;
   l.off_norm = o;
-  o += size_t(l.mc) * 4;
+  o += size_t(l.mc + 1) * 4;
+  l.off_dk = o;                              // sorted distances to p (float)
+  o += size_t(l.mc + 16) * 4;
+  l.off_ns = o;                              // sorted norms
+  o += size_t(l.mc + 16) * 4;
+  o = (o + 15) & ~size_t(15);
   l.off_cm = o;
-  o += size_t(l.mc) * l.w * 4;
-  l.off_sel = o;
-  o += size_t(R) * 4;
+  o += size_t(l.mc) * l.w * 4 + size_t(l.w) * 4;
   l.total = (o + 15) & ~size_t(15);
   return l;
 }
 
 constexpr int kMmaThreads = 128;
 
-// The greedy of prune.cpp:25-43 needs, for a selected i, the test
-// "i culls j" only for later j; the outcome of that test does not depend on
-// which candidates are still alive. So all tests are evaluated at once — the
-// upper triangle of the Gram matrix on the tensor cores, the alpha test per
-// element, one bit per (i, j) in cull masks — and the walk itself is a serial
-// bit loop in one warp: i is selected iff no earlier selection culled it, and
-// a selection with a non-zero distance ORs its mask into the culled set.
+// Stage-1 -> stage-2 hand-off buffer (grows; one per process and device).
+uint32_t* prune_handoff(uint64_t bytes, cudaStream_t s) {
+  static uint32_t* buf[16] = {};
+  static uint64_t cap[16] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 16) return nullptr;
+  if (bytes > cap[dev]) {
+    cudaStreamSynchronize(s);
+    if (buf[dev]) cudaFree(buf[dev]);
+    buf[dev] = nullptr;
+    cap[dev] = 0;
+    if (cudaMalloc(&buf[dev], bytes) != cudaSuccess) return nullptr;
+    cap[dev] = bytes;
+  }
+  return buf[dev];
+}
+
+// Stage 1 of the integer prune (one CTA per list, no serial part): gather the
+// candidates' rows once into shared memory; when the caller has no distances
+// (back-edge re-prunes) compute d(p, .) from the same rows; rank-sort the
+// (dist, id) keys; evaluate every cull test of the upper triangle from IMMA
+// Gram tiles (rows addressed through the sort permutation); hand the sorted
+// ids and the cull bitmasks to stage 2 through global memory.
+//
+// The greedy of prune.cpp:25-43 needs, for a selected i, the test "i culls j"
+// only for later j, and its outcome does not depend on which candidates are
+// still alive — so evaluating all of them up front is exact.
 template <int E, int M, int W>
-__global__ void __launch_bounds__(kMmaThreads) prune_mma_kernel(const PruneArgs a, const MmaLayout ly) {
+__global__ void __launch_bounds__(kMmaThreads)
+    prune_prep_kernel(const PruneArgs a, const MmaLayout ly, uint32_t* hand, uint32_t l0, uint32_t lcount) {
+  using Op = DistOp<E, M>;
   constexpr int NT = kMmaThreads;
   constexpr bool SIGNED = E == kI8;
   extern __shared__ __align__(16) uint8_t smem[];
-  uint64_t* keys = reinterpret_cast<uint64_t*>(smem);   // unsorted input, then sorted
+  uint64_t* tk = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* sk = reinterpret_cast<uint64_t*>(smem + ly.off_sk);
+  uint16_t* perm = reinterpret_cast<uint16_t*>(smem + ly.off_perm);
   uint8_t* X = smem + ly.off_x;
+  uint8_t* Xp = smem + ly.off_xp;
   int* norm = reinterpret_cast<int*>(smem + ly.off_norm);
   uint32_t* cm = reinterpret_cast<uint32_t*>(smem + ly.off_cm);
-  uint32_t* sel = reinterpret_cast<uint32_t*>(smem + ly.off_sel);
-  __shared__ uint32_t sh_nsel, sh_m2;
-  __shared__ uint32_t zmask[W];
+  uint32_t* zmask = cm + ly.mc * W;
+  float* dk = reinterpret_cast<float*>(smem + ly.off_dk);
+  int* ns = reinterpret_cast<int*>(smem + ly.off_ns);
+  __shared__ uint32_t sh_m2;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t R = a.R, mc = ly.mc, xs = ly.xs, kp = ly.kp;
+  const uint32_t mc = ly.mc, xs = ly.xs, kp = ly.kp;
   const uint32_t nch = static_cast<uint32_t>(a.stride >> 4);
-  const uint32_t kch = kp >> 4;  // 16-byte chunks per padded smem row
+  const uint32_t kch = kp >> 4;
   const uint32_t FULL = 0xFFFFFFFFu;
-  uint64_t* tmp = reinterpret_cast<uint64_t*>(X);  // unsorted keys live in X until the gather
+  // the zero row that pads partial tiles (written once)
+  for (uint32_t c = tid; c < kch; c += NT) *reinterpret_cast<uint4*>(X + size_t(mc) * xs + c * 16) = make_uint4(0, 0, 0, 0);
+  if (tid == 0) norm[mc] = 0;
 
-  for (uint32_t li = blockIdx.x; li < a.count; li += gridDim.x) {
+  for (uint32_t rel = blockIdx.x; rel < lcount; rel += gridDim.x) {
+    const uint32_t li = l0 + rel;
     const uint32_t l = a.list_index ? a.list_index[li] : li;
+    const uint32_t m = a.lengths[l];
+    if (m < a.mmin || m > a.mcap) continue;  // another launch's bin (the walk skips it too)
     const uint32_t p = a.points[l];
     const uint64_t beg = a.begins ? a.begins[l] : uint64_t(l) * a.fixed_stride;
-    const uint32_t m = a.lengths[l];
-    uint32_t* orow = a.out_rows ? a.out_rows + uint64_t(l) * R : a.out_adj + uint64_t(p) * R;
-    if (m < a.mmin) continue;
-    if (m > a.mcap) {  // a.mcap <= mc: the lists' own capacity, not the tile's
-      if (tid == 0 && !a.skip_long) atomicAdd(a.too_long, 1u);
-      continue;
-    }
+    uint32_t* out = hand + size_t(rel) * ly.stride;
+    __syncthreads();
     if (tid == 0) sh_m2 = 0;
     for (uint32_t i = tid; i < W; i += NT) zmask[i] = 0u;
+    // gather rows in input order (+ p's row when distances must be computed)
+    const bool own_d = a.cand_dists == nullptr;
+    for (uint32_t t = tid; t < (m + (own_d ? 1u : 0u)) * kch; t += NT) {
+      const uint32_t r = t / kch, c = t - r * kch;
+      const uint32_t id = r < m ? a.cand_ids[beg + r] : p;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (c < nch) v = __ldg(reinterpret_cast<const uint4*>(a.data + uint64_t(id) * a.stride) + c);
+      uint8_t* dst = r < m ? X + size_t(r) * xs : Xp;
+      *reinterpret_cast<uint4*>(dst + c * 16) = v;
+    }
+    for (uint32_t t = tid; t < m * W; t += NT) cm[t] = 0u;
     __syncthreads();
+    // keys (distances from the caller, or d(p, .) — src/builder_common.cpp:136)
     for (uint32_t i = tid; i < m; i += NT) {
       const uint32_t id = a.cand_ids[beg + i];
-      const uint64_t k = id != p ? make_key(a.cand_dists[beg + i], id) : kMaxKey;  // prune.cpp:18-20
-      tmp[i] = k;
-      if (k != kMaxKey) atomicAdd(&sh_m2, 1u);
+      uint64_t k = kMaxKey;
+      if (id != p) {  // prune.cpp:18-20 drops p
+        float dist;
+        if (own_d) {
+          typename Op::acc_t acc = Op::zero();
+          for (uint32_t c = 0; c < nch; c++)
+            acc = Op::chunk(*reinterpret_cast<const uint4*>(Xp + c * 16),
+                            *reinterpret_cast<const uint4*>(X + size_t(i) * xs + c * 16), acc);
+          dist = Op::finish(acc);
+        } else {
+          dist = a.cand_dists[beg + i];
+        }
+        k = make_key(dist, id);
+        atomicAdd(&sh_m2, 1u);
+      }
+      tk[i] = k;
     }
-    __syncthreads();
-    // sort by (dist, id) — prune.cpp:21 — by rank: keys are distinct
-    for (uint32_t i = tid; i < m; i += NT) {
-      const uint64_t k = tmp[i];
-      if (k == kMaxKey) continue;
-      uint32_t r = 0;
-      for (uint32_t j = 0; j < m; j++) r += tmp[j] < k ? 1u : 0u;
-      keys[r] = k;
-    }
-    __syncthreads();
-    const uint32_t m2 = sh_m2;
-    const uint32_t mpad = (m2 + 15) & ~15u;
-    // gather the rows in sorted order (zero padding to kp bytes and mpad rows)
-    for (uint32_t t = tid; t < mpad * kch; t += NT) {
-      const uint32_t r = t / kch, c = t - r * kch;
-      uint4 v = make_uint4(0, 0, 0, 0);
-      if (r < m2 && c < nch)
-        v = __ldg(reinterpret_cast<const uint4*>(a.data + uint64_t(key_id(keys[r])) * a.stride) + c);
-      *reinterpret_cast<uint4*>(X + size_t(r) * xs + c * 16) = v;
-    }
-    for (uint32_t t = tid; t < m2 * W; t += NT) cm[t] = 0u;
-    for (uint32_t i = tid; i < m2; i += NT)
-      if (key_dist(keys[i]) == 0.0f) atomicOr(&zmask[i >> 5], 1u << (i & 31));
-    __syncthreads();
-    for (uint32_t r = tid; r < mpad; r += NT) {
+    // norms of the gathered rows (input order)
+    for (uint32_t r = tid; r < m; r += NT) {
       const uint32_t* w = reinterpret_cast<const uint32_t*>(X + size_t(r) * xs);
       int acc = 0;
       for (uint32_t i = 0; i < (kp >> 2); i++) {
@@ -348,50 +386,84 @@ __global__ void __launch_bounds__(kMmaThreads) prune_mma_kernel(const PruneArgs 
       norm[r] = acc;
     }
     __syncthreads();
-    // all cull tests of the upper triangle, 16x16 tiles spread over the warps
+    // rank sort by (dist, id) — prune.cpp:21 (keys are distinct)
+    for (uint32_t i = tid; i < m; i += NT) {
+      const uint64_t k = tk[i];
+      if (k == kMaxKey) continue;
+      uint32_t r = 0;
+      for (uint32_t j = 0; j < m; j++) r += tk[j] < k ? 1u : 0u;
+      sk[r] = k;
+      perm[r] = static_cast<uint16_t>(i);
+    }
+    __syncthreads();
+    const uint32_t m2 = sh_m2;
+    const uint32_t mpad = (m2 + 15) & ~15u;
+    const uint32_t mw = (m2 + 31) >> 5;
+    // per sorted position: distance to p and norm (padding positions: +inf, 0)
+    for (uint32_t i = tid; i < mpad; i += NT) {
+      const float dd = i < m2 ? key_dist(sk[i]) : __int_as_float(0x7f800000);
+      dk[i] = dd;
+      ns[i] = i < m2 ? norm[perm[i]] : 0;
+      if (i < m2 && dd == 0.0f) atomicOr(&zmask[i >> 5], 1u << (i & 31));
+    }
+    __syncthreads();
+    // all cull tests of the upper triangle (sorted positions), 16x16 tiles per warp
     {
       const uint32_t mt = mpad >> 4;
       const uint32_t items = mt * (mt + 1) / 2;
       const int g = lane >> 2, tg = lane & 3;
+      const float alpha = a.alpha;
       for (uint32_t it = warp; it < items; it += NT / 32) {
-        uint32_t rb = 0, rem = it;  // item -> (row block rb, col block cbk >= rb)
+        uint32_t rb = 0, rem = it;
         while (rem >= mt - rb) {
           rem -= mt - rb;
           rb++;
         }
-        const uint32_t cbk = rb + rem;
-        const uint32_t r0 = rb * 16, n0 = cbk * 16;
+        const uint32_t r0 = rb * 16, n0 = (rb + rem) * 16;
+        const uint32_t ar = r0 + (lane & 7) + ((lane >> 3) & 1) * 8;
+        const uint32_t br = n0 + (lane & 7) + (lane >> 4) * 8;
+        const uint8_t* arow = X + size_t(ar < m2 ? perm[ar] : mc) * xs + (lane >> 4) * 16;
+        const uint8_t* brow = X + size_t(br < m2 ? perm[br] : mc) * xs + ((lane >> 3) & 1) * 16;
         int acc0[4] = {0, 0, 0, 0}, acc1[4] = {0, 0, 0, 0};
         for (uint32_t kc = 0; kc < (kp >> 5); kc++) {
           uint32_t af[4], bf[4];
-          ldsm_x4(af, X + size_t(r0 + (lane & 7) + ((lane >> 3) & 1) * 8) * xs + kc * 32 + (lane >> 4) * 16);
-          ldsm_x4(bf, X + size_t(n0 + (lane & 7) + (lane >> 4) * 8) * xs + kc * 32 + ((lane >> 3) & 1) * 16);
+          ldsm_x4(af, arow + kc * 32);
+          ldsm_x4(bf, brow + kc * 32);
           mma_i8<SIGNED>(acc0, af, bf[0], bf[1]);
           mma_i8<SIGNED>(acc1, af, bf[2], bf[3]);
+        }
+        // this lane's two rows and four columns of the tile
+        float rd[2], rlim[2];
+        int rn[2];
+        uint32_t rowi[2];
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          rowi[h] = r0 + g + h * 8;
+          rd[h] = dk[rowi[h]];
+          rn[h] = ns[rowi[h]];
+          rlim[h] = __fmul_rn(alpha, rd[h]);
         }
         uint32_t bits_lo = 0, bits_hi = 0;
 #pragma unroll
         for (int h = 0; h < 2; h++) {
 #pragma unroll
-          for (int e = 0; e < 4; e++) {
-            const uint32_t row = r0 + g + (e >> 1) * 8;
-            const uint32_t ccol = h * 8 + tg * 2 + (e & 1);
+          for (int e2 = 0; e2 < 2; e2++) {
+            const uint32_t ccol = h * 8 + tg * 2 + e2;
             const uint32_t col = n0 + ccol;
-            const int gram = h ? acc1[e] : acc0[e];
-            bool cull = false;
-            if (col > row && col < m2) {
-              const float di = key_dist(keys[row]);
-              if (di != 0.0f) {  // prune.cpp:32: a zero-distance pick culls nothing
-                const float via = M == kL2 ? __int2float_rn(norm[row] + norm[col] - 2 * gram)
-                                           : -__int2float_rn(gram);
-                const float dj = key_dist(keys[col]);
-                // prune.cpp:37-39, one IEEE multiply, never contracted
-                cull = a.rule == 0 ? (__fmul_rn(a.alpha, via) <= dj) : (via < __fmul_rn(a.alpha, di));
+            const float cd = dk[col];
+            const int cn = ns[col];
+#pragma unroll
+            for (int rr = 0; rr < 2; rr++) {
+              const int gram = h ? acc1[rr * 2 + e2] : acc0[rr * 2 + e2];
+              const float via = M == kL2 ? __int2float_rn(rn[rr] + cn - 2 * gram) : -__int2float_rn(gram);
+              // prune.cpp:32 (zero-distance picks cull nothing) and :37-39, one
+              // IEEE multiply, never contracted; padding columns carry +inf
+              const bool cull = col > rowi[rr] && col < m2 && rd[rr] != 0.0f &&
+                                (a.rule == 0 ? (__fmul_rn(alpha, via) <= cd) : (via < rlim[rr]));
+              if (cull) {
+                if (rr) bits_hi |= 1u << ccol;
+                else bits_lo |= 1u << ccol;
               }
-            }
-            if (cull) {
-              if (e >> 1) bits_hi |= 1u << ccol;
-              else bits_lo |= 1u << ccol;
             }
           }
         }
@@ -407,63 +479,124 @@ __global__ void __launch_bounds__(kMmaThreads) prune_mma_kernel(const PruneArgs 
       }
     }
     __syncthreads();
-    // the greedy walk (prune.cpp:25-43): every lane of warp 0 carries the whole
-    // culled set in registers; the next candidate's mask row is loaded before
-    // the current decision so the chain per candidate is a bit test and an OR
-    if (warp == 0) {
-      uint32_t culled[W], zm[W];
+    // hand off: [m2][sorted ids][zero mask][cull rows]
+    if (tid == 0) out[0] = m2;
+    for (uint32_t i = tid; i < m2; i += NT) out[4 + i] = key_id(sk[i]);
+    for (uint32_t i = tid; i < W; i += NT) out[4 + mc + i] = i < mw ? zmask[i] : 0u;
+    uint4* dst = reinterpret_cast<uint4*>(out + 4 + mc + W);
+    const uint4* srcm = reinterpret_cast<const uint4*>(cm);
+    for (uint32_t i = tid; i < m2 * (W / 4); i += NT) dst[i] = srcm[i];
+    if (tid == 0 && a.stats) {
+      atomicAdd(a.stats + kStPruneLists, 1ull);
+      atomicAdd(a.stats + kStPruneCands, static_cast<unsigned long long>(m));
+      // pair tests evaluated on the tensor cores
+      atomicAdd(a.stats + kStPruneEvals, static_cast<unsigned long long>(m2) * (m2 - (m2 > 0)) / 2);
+    }
+  }
+}
+
+// Stage 2: the greedy walk, one warp per list. The list's cull rows are staged
+// in shared memory with coalesced loads; every lane carries the whole culled
+// set in W registers and the next row is read before the current decision, so
+// the chain per candidate is a bit test and an OR (prune.cpp:25-43).
+constexpr int kWalkWarps = 4;
+template <int W>
+__global__ void __launch_bounds__(kWalkWarps * 32)
+    prune_walk_kernel(const PruneArgs a, const MmaLayout ly, const uint32_t* hand, uint32_t l0, uint32_t lcount) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  uint4* srows = reinterpret_cast<uint4*>(smem) + size_t(wib) * ly.mc * (W / 4);
+  const uint32_t rel = blockIdx.x * kWalkWarps + wib;
+  if (rel >= lcount) return;
+  const uint32_t li = l0 + rel;
+  const uint32_t l = a.list_index ? a.list_index[li] : li;
+  const uint32_t m = a.lengths[l];
+  if (m < a.mmin || m > a.mcap) return;
+  const uint32_t p = a.points[l];
+  const uint32_t R = a.R;
+  uint32_t* orow = a.out_rows ? a.out_rows + uint64_t(l) * R : a.out_adj + uint64_t(p) * R;
+  const uint32_t* in = hand + size_t(rel) * ly.stride;
+  const uint32_t m2 = in[0];
+  const uint32_t* ids = in + 4;
+  const uint32_t* zm = ids + ly.mc;
+  const uint4* rows = reinterpret_cast<const uint4*>(zm + W);
+  for (uint32_t i = lane; i < m2 * (W / 4); i += 32) srows[i] = rows[i];
+  uint32_t culled[W], z[W];
 #pragma unroll
-      for (int w = 0; w < W; w++) {
-        culled[w] = 0u;
-        zm[w] = zmask[w];
+  for (int w = 0; w < W; w++) {
+    culled[w] = 0u;
+    z[w] = zm[w];
+  }
+  __syncwarp();
+  uint32_t nsel = 0;
+  uint4 nxt[W / 4];
+#pragma unroll
+  for (int q = 0; q < W / 4; q++) nxt[q] = srows[q];
+#pragma unroll
+  for (int w = 0; w < W; w++) {
+    if (32u * w >= m2 || nsel == R) break;
+    for (uint32_t b = 0; b < 32; b++) {
+      const uint32_t i = 32u * w + b;
+      if (i >= m2) break;
+      uint4 cur[W / 4];
+#pragma unroll
+      for (int q = 0; q < W / 4; q++) cur[q] = nxt[q];
+      if (i + 1 < m2) {
+#pragma unroll
+        for (int q = 0; q < W / 4; q++) nxt[q] = srows[size_t(i + 1) * (W / 4) + q];
       }
-      uint32_t nsel = 0;
-      uint4 nxt[W / 4];
+      if ((culled[w] >> b) & 1u) continue;
+      if (lane == 0) orow[nsel] = ids[i];
+      nsel++;
+      if (nsel == R) break;
+      if ((z[w] >> b) & 1u) continue;
 #pragma unroll
-      for (int q = 0; q < W / 4; q++) nxt[q] = reinterpret_cast<const uint4*>(cm)[q];
-#pragma unroll
-      for (int w = 0; w < W; w++) {
-        if (32u * w >= m2 || nsel == R) break;
-        for (uint32_t b = 0; b < 32; b++) {
-          const uint32_t i = 32u * w + b;
-          if (i >= m2) break;
-          uint4 cur[W / 4];
-#pragma unroll
-          for (int q = 0; q < W / 4; q++) cur[q] = nxt[q];
-          if (i + 1 < m2) {
-#pragma unroll
-            for (int q = 0; q < W / 4; q++) nxt[q] = reinterpret_cast<const uint4*>(cm + (i + 1) * W)[q];
-          }
-          if ((culled[w] >> b) & 1u) continue;
-          if (lane == 0) sel[nsel] = key_id(keys[i]);
-          nsel++;
-          if (nsel == R) break;
-          if ((zm[w] >> b) & 1u) continue;
-#pragma unroll
-          for (int q = 0; q < W / 4; q++) {
-            culled[4 * q + 0] |= cur[q].x;
-            culled[4 * q + 1] |= cur[q].y;
-            culled[4 * q + 2] |= cur[q].z;
-            culled[4 * q + 3] |= cur[q].w;
-          }
-        }
-      }
-      if (lane == 0) {
-        sh_nsel = nsel;
-        if (a.stats) {
-          atomicAdd(a.stats + kStPruneLists, 1ull);
-          atomicAdd(a.stats + kStPruneCands, static_cast<unsigned long long>(m));
-          // pair tests evaluated on the tensor cores
-          atomicAdd(a.stats + kStPruneEvals, static_cast<unsigned long long>(m2) * (m2 - (m2 > 0)) / 2);
-        }
+      for (int q = 0; q < W / 4; q++) {
+        culled[4 * q + 0] |= cur[q].x;
+        culled[4 * q + 1] |= cur[q].y;
+        culled[4 * q + 2] |= cur[q].z;
+        culled[4 * q + 3] |= cur[q].w;
       }
     }
-    __syncthreads();
-    const uint32_t nsel = sh_nsel;
-    for (uint32_t i = tid; i < R; i += NT) orow[i] = i < nsel ? sel[i] : kNone;
-    if (tid == 0 && a.n_out) a.n_out[l] = nsel;
-    __syncthreads();
   }
+  for (uint32_t i = nsel + lane; i < R; i += 32) orow[i] = kNone;
+  if (lane == 0 && a.n_out) a.n_out[l] = nsel;
+}
+
+// ---- length binning --------------------------------------------------------
+// Splits the lists of a launch into kBins length bins (bounds[b-1], bounds[b]]
+// so each bin's prune launch covers only its own lists.
+__global__ void bin_lists_kernel(const PruneArgs a, const uint32_t* bounds, int nb, uint32_t* counts,
+                                 uint32_t* lists, uint32_t cap) {
+  const uint32_t li = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = li < a.count;
+  const uint32_t l = valid ? (a.list_index ? a.list_index[li] : li) : 0u;
+  const uint32_t m = valid ? a.lengths[l] : 0u;
+  int b = nb;
+  if (valid)
+    for (int i = 0; i < nb; i++)
+      if (m <= bounds[i]) {
+        b = i;
+        break;
+      }
+  for (int i = 0; i < nb; i++) {  // warp-aggregated append per bin
+    const uint32_t mask = __ballot_sync(0xFFFFFFFFu, b == i);
+    if (!mask) continue;
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(mask) - 1;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(counts + i, __popc(mask));
+    base = __shfl_sync(0xFFFFFFFFu, base, leader);
+    if (b == i) lists[size_t(i) * cap + base + __popc(mask & ((1u << lane) - 1u))] = l;
+  }
+}
+
+cudaError_t launch_bin_lists(const PruneArgs& a, const uint32_t* d_bounds, int nb, uint32_t* d_counts,
+                             uint32_t* d_lists, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(d_counts, 0, sizeof(uint32_t) * nb, s);
+  if (e != cudaSuccess || a.count == 0) return e;
+  bin_lists_kernel<<<(a.count + 255) / 256, 256, 0, s>>>(a, d_bounds, nb, d_counts, d_lists, a.count);
+  return cudaGetLastError();
 }
 
 // ---- long lists: chunked prune ------------------------------------------------
@@ -744,15 +877,37 @@ cudaError_t dispatch(const PruneArgs& a, const Geometry& g, int threads, cudaStr
 }
 }  // namespace
 
+template <int E, int M, int W>
+cudaError_t launch_mma_w(const PruneArgs& a, const MmaLayout& ly, cudaStream_t s) {
+  auto kp = prune_prep_kernel<E, M, W>;
+  cudaError_t e = cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ly.total));
+  if (e != cudaSuccess) return e;
+  // the hand-off region is reused chunk by chunk (~1 GiB)
+  const uint64_t per = uint64_t(ly.stride) * 4;
+  const uint32_t chunk = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(a.count, (1ull << 30) / per)));
+  uint32_t* hand = prune_handoff(uint64_t(chunk) * per, s);
+  if (!hand) return cudaErrorMemoryAllocation;
+  const size_t walk_smem = size_t(kWalkWarps) * ly.mc * W * 4;
+  if ((e = cudaFuncSetAttribute(prune_walk_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(walk_smem))) !=
+      cudaSuccess)
+    return e;
+  for (uint32_t l0 = 0; l0 < a.count; l0 += chunk) {
+    const uint32_t n = std::min(chunk, a.count - l0);
+    kp<<<n, kMmaThreads, ly.total, s>>>(a, ly, hand, l0, n);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    prune_walk_kernel<W><<<(n + kWalkWarps - 1) / kWalkWarps, kWalkWarps * 32, walk_smem, s>>>(a, ly, hand, l0, n);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 template <int E, int M>
 cudaError_t launch_mma(const PruneArgs& a, cudaStream_t s) {
   if (a.count == 0) return cudaSuccess;
   const MmaLayout ly = mma_layout(a.mcap, static_cast<uint32_t>(a.stride), a.R);
-  auto k = ly.w == 4 ? prune_mma_kernel<E, M, 4> : (ly.w == 8 ? prune_mma_kernel<E, M, 8> : prune_mma_kernel<E, M, 16>);
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ly.total));
-  if (e != cudaSuccess) return e;
-  k<<<a.count, kMmaThreads, ly.total, s>>>(a, ly);
-  return cudaGetLastError();
+  if (ly.w == 4) return launch_mma_w<E, M, 4>(a, ly, s);
+  if (ly.w == 8) return launch_mma_w<E, M, 8>(a, ly, s);
+  return launch_mma_w<E, M, 16>(a, ly, s);
 }
 
 bool prune_uses_mma(int elem, uint32_t mcap, uint64_t stride, uint32_t R) {

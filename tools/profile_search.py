@@ -55,7 +55,11 @@ for L in Ls:
         for r in range(args.reps):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            idx.search_staged(g.SearchParams(L, L, 0.0), 10, ids.data_ptr(), ds.data_ptr(), s.cuda_stream)
+            if os.environ.get("MODE", "fast") == "fast":
+                idx.search_staged(g.SearchParams(L, L, 0.0), 10, ids.data_ptr(), ds.data_ptr(), s.cuda_stream)
+            else:
+                idx.search_device(q.data_ptr(), args.nq, g.SearchParams(L, L, 0.0), 10, ids.data_ptr(), ds.data_ptr(),
+                                  stream=s.cuda_stream, visited_mode=os.environ["MODE"])
             e1.record()
             torch.cuda.synchronize()
             best = min(best, e0.elapsed_time(e1))
