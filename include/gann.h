@@ -152,6 +152,28 @@ uint32_t gann_batch_ranges(uint64_t n, uint32_t max_batch, uint32_t* lo, uint32_
 /* The seed build_diskann derives for shuffled_order: mix64(seed, "insert"). */
 uint64_t gann_insert_seed(uint64_t seed);
 
+/* ---- files in the reference's formats ----------------
+ * Graph: graphann's ANNG layout (src/graph.cpp:96-178): "ANNG", u32 version 1,
+ * u32 n, u32 capacity, u32 start, u32 degrees[n], then the live ids in vertex
+ * order. load validates like graphann::load_graph (magic, version, start,
+ * degree <= capacity, ids, self loops, duplicates, trailing bytes) and returns
+ * GANN_EIO on a malformed file; the file's capacity must not exceed R.
+ * Vectors: graphann::load_vectors (src/dataset.cpp:71-122): .u8bin/.i8bin/.fbin
+ * ("bin": u32 n, u32 d, payload) and .bvecs/.fvecs ("vecs": per-vector u32 d
+ * prefix); the element kind comes from the extension. */
+int gann_save_graph(const gann_index* idx, const char* path);
+int gann_load_graph(gann_index* idx, const char* path);
+int gann_index_create_from_file(const char* path, int metric, uint32_t R, int device,
+                                gann_index** out);
+
+/* ---- range search --------------------------------------
+ * graphann::range_search (src/search.cpp:133-149): the drained beam {L, L, eps}
+ * then every visited vertex with dist <= r^2 (L2) or <= r (IP), ascending
+ * (dist, id). Query q's results go to ids/dists[q*cap ..]; counts[q] is the
+ * full count (it may exceed cap). */
+int gann_range_search(gann_index* idx, const void* queries, uint32_t nq, float radius, uint32_t L,
+                      float eps, uint32_t cap, uint32_t* counts, uint32_t* ids, float* dists);
+
 /* ---- next-row helpers --------------------------------------
  * Exact top-k by (dist, id): graphann::compute_groundtruth (src/dataset.cpp:172-217). */
 int gann_groundtruth(gann_index* idx, const void* queries, uint32_t nq, uint32_t k,

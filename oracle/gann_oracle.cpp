@@ -20,6 +20,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <fstream>
 #include <limits>
 #include <random>
 #include <stdexcept>
@@ -612,6 +613,71 @@ int orc_time_search(const uint32_t* adj, uint32_t n, uint32_t R, uint32_t start,
     }
     *best_seconds = best;
     if (reps_done) *reps_done = r;
+  });
+}
+
+// range_search — src/search.cpp:133-149: drain {L, L, eps}, keep visited with
+// dist <= internal_radius (src/dataset.cpp:248-250), sorted by (dist, id).
+int orc_range_search(const uint32_t* adj, uint32_t n, uint32_t R, uint32_t start, const void* data,
+                     uint32_t d, int elem, int metric, const void* queries, uint32_t nq, float radius,
+                     uint32_t L, float eps, uint32_t cap, uint32_t* counts, uint32_t* ids, float* dists) {
+  return guarded([&] {
+    if (!(radius > 0)) throw std::invalid_argument("range radius must be positive");
+    Graph g{const_cast<uint32_t*>(adj), n, R};
+    Data ds{static_cast<const uint8_t*>(data), n, d, elem, metric, d * esize(elem)};
+    const float rr = metric == 0 ? radius * radius : radius;
+    const uint8_t* qb = static_cast<const uint8_t*>(queries);
+    for (uint32_t qi = 0; qi < nq; qi++) {
+      SearchOut r = beam_search(g, ds, qb + qi * ds.stride, L, L, eps, 0, start);
+      std::vector<Nb> in;
+      for (const auto& v : r.visited)
+        if (v.dist <= rr) in.push_back(v);
+      std::sort(in.begin(), in.end(), nb_less);
+      counts[qi] = static_cast<uint32_t>(in.size());
+      for (uint32_t t = 0; t < cap; t++) {
+        const bool have = t < in.size();
+        ids[size_t(qi) * cap + t] = have ? in[t].id : kSent;
+        dists[size_t(qi) * cap + t] = have ? in[t].dist : kInf;
+      }
+    }
+  });
+}
+
+// ANNG layout — src/graph.cpp:101-178
+int orc_save_graph(const uint32_t* adj, uint32_t n, uint32_t R, uint32_t start, const char* path) {
+  return guarded([&] {
+    std::ofstream out(path, std::ios::binary | std::ios::trunc);
+    if (!out) throw std::runtime_error("cannot open for writing");
+    Graph g{const_cast<uint32_t*>(adj), n, R};
+    out.write("ANNG", 4);
+    const uint32_t h[4] = {1u, n, R, start};
+    out.write(reinterpret_cast<const char*>(h), sizeof(h));
+    std::vector<uint32_t> deg(n);
+    for (uint32_t v = 0; v < n; v++) deg[v] = g.degree(v);
+    out.write(reinterpret_cast<const char*>(deg.data()), std::streamsize(n) * 4);
+    for (uint32_t v = 0; v < n; v++) out.write(reinterpret_cast<const char*>(g.row(v)), std::streamsize(deg[v]) * 4);
+  });
+}
+
+int orc_load_graph(const char* path, uint32_t* n, uint32_t* cap, uint32_t* start, uint32_t* adj,
+                   uint64_t adj_words) {
+  return guarded([&] {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw std::runtime_error("cannot open for reading");
+    char magic[4];
+    uint32_t h[4];
+    in.read(magic, 4);
+    in.read(reinterpret_cast<char*>(h), sizeof(h));
+    if (!in || std::memcmp(magic, "ANNG", 4) != 0 || h[0] != 1u) throw std::runtime_error("not a graph file");
+    *n = h[1];
+    *cap = h[2];
+    *start = h[3];
+    if (!adj || adj_words < uint64_t(h[1]) * h[2]) return;
+    std::vector<uint32_t> deg(h[1]);
+    in.read(reinterpret_cast<char*>(deg.data()), std::streamsize(h[1]) * 4);
+    std::fill(adj, adj + uint64_t(h[1]) * h[2], kSent);
+    for (uint32_t v = 0; v < h[1]; v++) in.read(reinterpret_cast<char*>(adj + uint64_t(v) * h[2]), std::streamsize(deg[v]) * 4);
+    if (!in) throw std::runtime_error("truncated graph data");
   });
 }
 

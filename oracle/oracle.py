@@ -83,6 +83,11 @@ class Oracle:
         f("groundtruth").argtypes = [vp, u32, vp, u32, u32, i32, i32, u32, vp, vp, i32]
         f("time_search").argtypes = [vp, u32, u32, u32, vp, u32, i32, i32, vp, u32, u32, u32, f32, u32, i32,
                                      u32, C.c_double, vp, vp, vp]
+        f("range_search").argtypes = [vp, u32, u32, u32, vp, u32, i32, i32, vp, u32, f32, u32, f32, u32, vp, vp, vp]
+        f("save_graph").argtypes = [vp, u32, u32, u32, C.c_char_p]
+        f("load_graph").argtypes = [C.c_char_p, vp, vp, vp, vp, u64]
+        if prefix == "ref":
+            L.ref_write_vectors.argtypes = [vp, u32, u32, i32, C.c_char_p, i32]
         f("recall").restype = C.c_double
         f("recall").argtypes = [vp, vp, u32, vp, u32, u32]
         self._f = f
@@ -220,6 +225,37 @@ class Oracle:
                                            METRIC[metric], _p(queries), nq, L, k, eps, k_out, workers, reps,
                                            min_seconds, _p(ids), _p(best), _p(done)))
         return float(best[0]), ids, int(done[0])
+
+    def range_search(self, adj, start, data, queries, radius, L, eps=0.0, metric="l2", cap=256):
+        adj = np.ascontiguousarray(adj, dtype=np.uint32)
+        data = np.ascontiguousarray(data)
+        queries = np.ascontiguousarray(queries, dtype=data.dtype)
+        n, R = adj.shape
+        nq = len(queries)
+        counts = np.empty(nq, np.uint32)
+        ids = np.empty((nq, cap), np.uint32)
+        dists = np.empty((nq, cap), np.float32)
+        self._check(self._f("range_search")(_p(adj), n, R, start, _p(data), data.shape[1], ELEM[data.dtype],
+                                            METRIC[metric], _p(queries), nq, radius, L, eps, cap, _p(counts),
+                                            _p(ids), _p(dists)))
+        return [(ids[i, : min(counts[i], cap)].copy(), dists[i, : min(counts[i], cap)].copy())
+                for i in range(nq)], counts
+
+    def save_graph(self, adj, start, path):
+        adj = np.ascontiguousarray(adj, dtype=np.uint32)
+        self._check(self._f("save_graph")(_p(adj), adj.shape[0], adj.shape[1], start, str(path).encode()))
+
+    def load_graph(self, path):
+        n, cap, s = np.zeros(1, np.uint32), np.zeros(1, np.uint32), np.zeros(1, np.uint32)
+        self._check(self._f("load_graph")(str(path).encode(), _p(n), _p(cap), _p(s), None, 0))
+        adj = np.empty((int(n[0]), int(cap[0])), np.uint32)
+        self._check(self._f("load_graph")(str(path).encode(), _p(n), _p(cap), _p(s), _p(adj), adj.size))
+        return adj, int(s[0])
+
+    def write_vectors(self, data, path, fmt="bin"):
+        data = np.ascontiguousarray(data)
+        self._check(self.lib.ref_write_vectors(_p(data), data.shape[0], data.shape[1], ELEM[data.dtype],
+                                               str(path).encode(), 0 if fmt == "bin" else 1))
 
     def recall(self, truth_ids, truth_dists, result, k):
         ti = np.ascontiguousarray(truth_ids, dtype=np.uint32)

@@ -61,6 +61,14 @@
                      uint32_t nq, uint32_t L, uint32_t k, float eps, uint32_t k_out,           \
                      int workers, uint32_t reps, double min_seconds, uint32_t* ids,            \
                      double* best_seconds, uint32_t* reps_done);                               \
+  int P##range_search(const uint32_t* adj, uint32_t n, uint32_t R, uint32_t start,             \
+                      const void* data, uint32_t d, int elem, int metric, const void* queries, \
+                      uint32_t nq, float radius, uint32_t L, float eps, uint32_t cap,          \
+                      uint32_t* counts, uint32_t* ids, float* dists);                          \
+  int P##save_graph(const uint32_t* adj, uint32_t n, uint32_t R, uint32_t start,               \
+                    const char* path);                                                         \
+  int P##load_graph(const char* path, uint32_t* n, uint32_t* cap, uint32_t* start,             \
+                    uint32_t* adj, uint64_t adj_words);                                        \
   double P##recall(const uint32_t* truth_ids, const float* truth_dists, uint32_t depth,       \
                    const uint32_t* result, uint32_t n_result, uint32_t k);
 
@@ -69,6 +77,8 @@ extern "C" {
 #endif
 ORACLE_DECLS(orc_)
 ORACLE_DECLS(ref_)
+/* reference only: graphann::write_vectors (src/dataset.cpp:124-140); format 0 = bin, 1 = vecs */
+int ref_write_vectors(const void* data, uint32_t n, uint32_t d, int elem, const char* path, int format);
 #ifdef __cplusplus
 }
 #endif

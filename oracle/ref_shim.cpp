@@ -326,6 +326,49 @@ int ref_time_search(const uint32_t* adj, uint32_t n, uint32_t R, uint32_t start,
   });
 }
 
+// graphann::range_search (src/search.cpp:133-149)
+int ref_range_search(const uint32_t* adj, uint32_t n, uint32_t R, uint32_t start, const void* data,
+                     uint32_t d, int elem, int metric, const void* queries, uint32_t nq, float radius,
+                     uint32_t L, float eps, uint32_t cap, uint32_t* counts, uint32_t* ids, float* dists) {
+  return guarded([&] {
+    VectorDataset ds = make_ds(data, n, d, elem);
+    NeighborGraph g = make_graph(adj, n, R, start);
+    const std::byte* qb = static_cast<const std::byte*>(queries);
+    for (uint32_t qi = 0; qi < nq; qi++) {
+      VectorView q{qb + size_t(qi) * ds.stride(), d, kind(elem)};
+      RangeResult r = range_search(g, ds, met(metric), q, radius, SearchParams{L, 1, eps});
+      counts[qi] = static_cast<uint32_t>(r.in_range.size());
+      for (uint32_t t = 0; t < cap; t++) {
+        const bool have = t < r.in_range.size();
+        ids[size_t(qi) * cap + t] = have ? r.in_range[t].id : kSent;
+        dists[size_t(qi) * cap + t] = have ? r.in_range[t].dist : std::numeric_limits<float>::infinity();
+      }
+    }
+  });
+}
+
+// graphann::save_graph / load_graph (src/graph.cpp:101-178)
+int ref_save_graph(const uint32_t* adj, uint32_t n, uint32_t R, uint32_t start, const char* path) {
+  return guarded([&] { save_graph(make_graph(adj, n, R, start), std::string(path)); });
+}
+
+int ref_load_graph(const char* path, uint32_t* n, uint32_t* cap, uint32_t* start, uint32_t* adj,
+                   uint64_t adj_words) {
+  return guarded([&] {
+    NeighborGraph g = load_graph(std::string(path));
+    *n = g.size();
+    *cap = g.capacity();
+    *start = g.start();
+    if (adj && adj_words >= uint64_t(g.size()) * g.capacity()) export_graph(g, adj);
+  });
+}
+
+int ref_write_vectors(const void* data, uint32_t n, uint32_t d, int elem, const char* path, int format) {
+  return guarded([&] {
+    write_vectors(make_ds(data, n, d, elem), std::string(path), format == 0 ? FileFormat::bin : FileFormat::vecs);
+  });
+}
+
 double ref_recall(const uint32_t* truth_ids, const float* truth_dists, uint32_t depth,
                   const uint32_t* result, uint32_t n_result, uint32_t k) {
   try {

@@ -160,6 +160,40 @@ class Index:
         check(lib().gann_export_graph(self._h, _p(adj), _p(deg), C.byref(s)))
         return adj, deg, s.value
 
+    @classmethod
+    def from_file(cls, path: str, metric: str = "l2", degree_bound: int = 64, device: int = 0) -> "Index":
+        """graphann::load_vectors (src/dataset.cpp:71-122): .u8bin/.i8bin/.fbin/.bvecs/.fvecs."""
+        self = cls.__new__(cls)
+        h = C.c_void_p()
+        check(lib().gann_index_create_from_file(str(path).encode(), METRIC[metric], degree_bound, device,
+                                                C.byref(h)))
+        self._init(h, metric, device)
+        return self
+
+    def save_graph(self, path: str) -> None:
+        """graphann::save_graph (ANNG, src/graph.cpp:101-121)."""
+        check(lib().gann_save_graph(self._h, str(path).encode()))
+
+    def load_graph(self, path: str) -> None:
+        """graphann::load_graph (src/graph.cpp:136-178) into this index."""
+        check(lib().gann_load_graph(self._h, str(path).encode()))
+
+    def range_search(self, queries: np.ndarray, radius: float, params: SearchParams, cap: int = 256):
+        """graphann::range_search (src/search.cpp:133-149), batched: returns a list
+        of (ids, dists) per query, ascending (dist, id)."""
+        queries = np.ascontiguousarray(queries)
+        if queries.ndim != 2 or queries.shape[1] != self.d or queries.dtype != self.dtype:
+            raise ValueError("query does not match dataset dimension/element kind")
+        nq = queries.shape[0]
+        counts = np.empty(nq, np.uint32)
+        ids = np.empty((nq, cap), np.uint32)
+        dists = np.empty((nq, cap), np.float32)
+        check(lib().gann_range_search(self._h, _p(queries), nq, radius, params.beam, params.epsilon, cap,
+                                      _p(counts), _p(ids), _p(dists)))
+        if (counts > cap).any():
+            return self.range_search(queries, radius, params, int(counts.max()))
+        return [(ids[i, : counts[i]].copy(), dists[i, : counts[i]].copy()) for i in range(nq)]
+
     # -- search -----------------------------------------------------------------
     def search(self, queries: np.ndarray, params: SearchParams = SearchParams(), k_out: Optional[int] = None,
                visited_mode: str = "fast", start_override=None, vcap: int = 0) -> SearchResult:

@@ -20,6 +20,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <fstream>
 #include <random>
 #include <stdexcept>
 #include <string>
@@ -1176,6 +1177,184 @@ uint32_t gann_batch_ranges(uint64_t n, uint32_t max_batch, uint32_t* lo, uint32_
 }
 
 uint64_t gann_insert_seed(uint64_t seed) { return mix64(seed, 0x696e73657274ULL); }
+
+namespace {
+
+[[noreturn]] void fmt_fail(const std::string& msg) { fail(GANN_EIO, msg); }
+
+void read_exact(std::ifstream& in, void* dst, size_t bytes, const std::string& what) {
+  in.read(static_cast<char*>(dst), static_cast<std::streamsize>(bytes));
+  if (static_cast<size_t>(in.gcount()) != bytes) fmt_fail("truncated " + what);
+}
+
+bool ends_with(const std::string& s, const char* suf) {
+  const size_t n = std::strlen(suf);
+  return s.size() >= n && s.compare(s.size() - n, n, suf) == 0;
+}
+
+}  // namespace
+
+int gann_save_graph(const gann_index* cidx, const char* path) {
+  return guarded([&] {
+    gann_index* idx = const_cast<gann_index*>(cidx);
+    if (!idx || !path) fail(GANN_EINVAL, "NULL argument");
+    set_device(idx);
+    std::ofstream out(path, std::ios::binary | std::ios::trunc);
+    if (!out) fail(GANN_EIO, std::string("cannot open for writing: ") + path);
+    const uint64_t n = idx->n;
+    const uint32_t R = idx->R;
+    out.write("ANNG", 4);
+    const uint32_t header[4] = {1u, static_cast<uint32_t>(n), R, idx->start};
+    out.write(reinterpret_cast<const char*>(header), sizeof(header));
+    // degrees then ids, streamed from the device in slabs
+    const uint64_t slab = 1u << 20;
+    std::vector<uint32_t> rows(std::min<uint64_t>(n, slab) * R);
+    std::vector<uint32_t> deg(n);
+    for (int pass = 0; pass < 2; pass++) {
+      for (uint64_t v0 = 0; v0 < n; v0 += slab) {
+        const uint64_t cnt = std::min<uint64_t>(slab, n - v0);
+        cu(cudaMemcpyAsync(rows.data(), idx->adj + v0 * R, cnt * R * 4, cudaMemcpyDeviceToHost, idx->stream),
+           "download graph");
+        sync(idx);
+        for (uint64_t i = 0; i < cnt; i++) {
+          const uint32_t* r = rows.data() + i * R;
+          uint32_t k = 0;
+          while (k < R && r[k] != GANN_NONE) k++;
+          if (pass == 0) deg[v0 + i] = k;
+          else out.write(reinterpret_cast<const char*>(r), static_cast<std::streamsize>(k) * 4);
+        }
+      }
+      if (pass == 0) out.write(reinterpret_cast<const char*>(deg.data()), static_cast<std::streamsize>(n) * 4);
+    }
+    if (!out) fail(GANN_EIO, std::string("write failed: ") + path);
+  });
+}
+
+int gann_load_graph(gann_index* idx, const char* path) {
+  return guarded([&] {
+    if (!idx || !path) fail(GANN_EINVAL, "NULL argument");
+    const std::string ctx(path);
+    std::ifstream in(path, std::ios::binary);
+    if (!in) fail(GANN_EIO, "cannot open for reading: " + ctx);
+    char magic[4];
+    read_exact(in, magic, 4, "graph data: " + ctx);
+    if (std::memcmp(magic, "ANNG", 4) != 0) fmt_fail("not a graph file: " + ctx);
+    uint32_t header[4];
+    read_exact(in, header, sizeof(header), "graph data: " + ctx);
+    if (header[0] != 1u) fmt_fail("unsupported graph version " + std::to_string(header[0]) + ": " + ctx);
+    const uint32_t n = header[1], cap = header[2], start = header[3];
+    if (n > 0 && start >= n) fmt_fail("start vertex out of range: " + ctx);
+    if (n != idx->n) fail(GANN_EINVAL, "graph has " + std::to_string(n) + " vertices, index " + std::to_string(idx->n));
+    if (cap > idx->R) fail(GANN_EINVAL, "graph capacity " + std::to_string(cap) + " exceeds the index's R");
+    std::vector<uint32_t> deg(n);
+    read_exact(in, deg.data(), size_t(n) * 4, "graph data: " + ctx);
+    std::vector<uint32_t> adj(size_t(n) * idx->R, GANN_NONE), tmp;
+    for (uint32_t v = 0; v < n; v++) {
+      if (deg[v] > cap) fmt_fail("degree exceeds capacity at vertex " + std::to_string(v) + ": " + ctx);
+      uint32_t* r = adj.data() + size_t(v) * idx->R;
+      read_exact(in, r, size_t(deg[v]) * 4, "graph data: " + ctx);
+      tmp.assign(r, r + deg[v]);
+      std::sort(tmp.begin(), tmp.end());
+      for (uint32_t t = 0; t < deg[v]; t++) {  // set_neighbors + check_graph_invariants
+        if (tmp[t] >= n) fmt_fail("neighbor id out of range at vertex " + std::to_string(v) + ": " + ctx);
+        if (tmp[t] == v) fmt_fail("self loop at vertex " + std::to_string(v) + ": " + ctx);
+        if (t > 0 && tmp[t] == tmp[t - 1]) fmt_fail("duplicate neighbor at vertex " + std::to_string(v) + ": " + ctx);
+      }
+    }
+    in.peek();
+    if (!in.eof()) fmt_fail("trailing bytes: " + ctx);
+    set_device(idx);
+    if (n) cu(cudaMemcpyAsync(idx->adj, adj.data(), adj.size() * 4, cudaMemcpyHostToDevice, idx->stream), "upload graph");
+    idx->start = start;
+    sync(idx);
+  });
+}
+
+int gann_index_create_from_file(const char* path, int metric, uint32_t R, int device, gann_index** out) {
+  int rc = GANN_OK;
+  std::vector<uint8_t> payload;
+  uint32_t n = 0, d = 0;
+  int elem = GANN_F32;
+  rc = guarded([&] {
+    if (!path || !out) fail(GANN_EINVAL, "NULL argument");
+    const std::string p(path);
+    // graphann::elem_from_path / format_from_path (src/dataset.cpp:56-66)
+    if (ends_with(p, ".fvecs") || ends_with(p, ".fbin")) elem = GANN_F32;
+    else if (ends_with(p, ".bvecs") || ends_with(p, ".u8bin")) elem = GANN_U8;
+    else if (ends_with(p, ".i8bin")) elem = GANN_I8;
+    const size_t esz = elem == GANN_F32 ? 4 : 1;
+    const bool vecs = ends_with(p, "vecs");
+    std::ifstream in(path, std::ios::binary | std::ios::ate);
+    if (!in) fail(GANN_EIO, "cannot open for reading: " + p);
+    const uint64_t fsize = static_cast<uint64_t>(in.tellg());
+    in.seekg(0);
+    if (!vecs) {
+      uint32_t h[2];
+      read_exact(in, h, 8, "vector data: " + p);
+      n = h[0];
+      d = h[1];
+      if (n == 0 || d == 0) fmt_fail("empty dataset (n or d is zero): " + p);
+      if (fsize != uint64_t(n) * d * esz + 8) fmt_fail("size mismatch (header says " + std::to_string(n) + "x" + std::to_string(d) + "): " + p);
+      payload.resize(size_t(n) * d * esz);
+      read_exact(in, payload.data(), payload.size(), "vector data: " + p);
+    } else {
+      read_exact(in, &d, 4, "vector data: " + p);
+      if (d == 0) fmt_fail("zero dimension prefix: " + p);
+      const uint64_t rec = 4 + uint64_t(d) * esz;
+      if (fsize % rec != 0) fmt_fail("truncated or misaligned vecs file: " + p);
+      n = static_cast<uint32_t>(fsize / rec);
+      payload.resize(size_t(n) * d * esz);
+      read_exact(in, payload.data(), d * esz, "vector data: " + p);
+      for (uint32_t i = 1; i < n; i++) {
+        uint32_t di = 0;
+        read_exact(in, &di, 4, "vector data: " + p);
+        if (di != d) fmt_fail("inconsistent dimension prefix at vector " + std::to_string(i) + ": " + p);
+        read_exact(in, payload.data() + size_t(i) * d * esz, d * esz, "vector data: " + p);
+      }
+    }
+  });
+  if (rc != GANN_OK) return rc;
+  return gann_index_create(payload.data(), n, d, elem, metric, R, device, out);
+}
+
+int gann_range_search(gann_index* idx, const void* queries, uint32_t nq, float radius, uint32_t L,
+                      float eps, uint32_t cap, uint32_t* counts, uint32_t* ids, float* dists) {
+  return guarded([&] {
+    if (!idx) fail(GANN_EINVAL, "index is NULL");
+    if (!(radius > 0)) fail(GANN_EINVAL, "range radius must be positive");  // search.cpp:136
+    validate_search(idx, 0, L, L, eps, GANN_VISITED_FAST);
+    if (nq == 0) return;
+    // internal_radius (src/dataset.cpp:248-250): squared under l2, as is under ip
+    const float rr = idx->metric == GANN_L2 ? radius * radius : radius;
+    uint32_t vcap = 4 * L + 64;
+    std::vector<uint32_t> vi, nv(nq);
+    std::vector<float> vd;
+    for (int attempt = 0; attempt < 4; attempt++) {
+      vi.assign(size_t(nq) * vcap, GANN_NONE);
+      vd.assign(size_t(nq) * vcap, 0.0f);
+      const int rc = gann_search(idx, queries, nq, 0, L, L, eps, GANN_VISITED_FAST, nullptr, nullptr, nullptr,
+                                 nv.data(), nullptr, vi.data(), vd.data(), vcap);
+      if (rc != GANN_OK) fail(rc, g_err);
+      const uint32_t vmax = *std::max_element(nv.begin(), nv.end());
+      if (vmax <= vcap) break;
+      vcap = vmax;  // a long walk: run again with room for every visited vertex
+    }
+    for (uint32_t q = 0; q < nq; q++) {
+      std::vector<std::pair<float, uint32_t>> in;
+      for (uint32_t t = 0; t < nv[q]; t++) {
+        const float dv = vd[size_t(q) * vcap + t];
+        if (dv <= rr) in.emplace_back(dv, vi[size_t(q) * vcap + t]);
+      }
+      std::sort(in.begin(), in.end());  // (dist, id): neighbor_less
+      counts[q] = static_cast<uint32_t>(in.size());
+      for (uint32_t t = 0; t < cap; t++) {
+        const bool have = t < in.size();
+        if (ids) ids[size_t(q) * cap + t] = have ? in[t].second : GANN_NONE;
+        if (dists) dists[size_t(q) * cap + t] = have ? in[t].first : __builtin_inff();
+      }
+    }
+  });
+}
 
 int gann_get_stats(const gann_index* idx, gann_stats* out) {
   return guarded([&] {
