@@ -134,11 +134,14 @@ def search_bytes(stats: dict, row_bytes: int, nq: int, k: int) -> float:
             + nq * row_bytes + 8.0 * k * nq)
 
 
-def traffic_from_profile(name: str):
+def traffic_from_profile(workload: str, L: int):
+    """dram bytes (read + write) of one timed launch from an ncu --set full
+    capture of the same workload and beam (profiles/traffic.json), else None."""
     p = ROOT / "profiles" / "traffic.json"
     if p.exists():
-        d = json.loads(p.read_text())
-        return d.get(name)
+        d = json.loads(p.read_text()).get(workload, {})
+        if d.get("L") == L:
+            return d.get("search_kernel_bytes")
     return None
 
 
@@ -345,7 +348,7 @@ def run_ours(args):
             "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
             "algorithmic_bytes_per_launch": round(per_launch_bytes),
             "avg_launch_ms": round(avg_launch_s * 1e3, 4),
-            "traffic": traffic_from_profile("search_kernel"),
+            "traffic": traffic_from_profile(cfg.name, chosen),
             "distinct_evals_per_query": round(xstats["evaluations"] / nq, 1),
             "evals_per_query_fast_filter": round(sstats["evaluations"] / (nq * args.steps), 1),
             "expansions_per_query": round(xstats["expansions"] / nq, 1),

@@ -188,6 +188,30 @@ int gann_generate_u8(void* d_out, uint64_t n, uint32_t d, uint32_t clusters, flo
                      float noise_frac, uint64_t center_seed, uint64_t stream_seed, uint64_t row0,
                      int device);
 
+/* ---- vertex-partitioned build (BASELINE config 4) -----------
+ * One index per GPU (one process per GPU). Every index holds all points;
+ * partition `rank` of `nparts` owns graph rows [rank*P, min(n, (rank+1)*P)),
+ * P = ceil(n / nparts). Peers' rows are read through CUDA IPC mappings
+ * (NVLink peer memory on a multi-GPU node). Per build batch the caller runs
+ *   phase1   -> insert this partition's points of the batch; returns the
+ *               reverse pairs (target, batch ordinal) grouped by owner
+ *               (interleaved u32 pairs in device memory, counts[nparts]);
+ *   exchange -> all-to-all-v of the pairs (NCCL), receive concatenated;
+ *   phase2   -> merge the received pairs into the owned rows;
+ *   barrier  -> before the next batch's searches.
+ * The result equals the single-GPU build row for row. export_graph returns a
+ * partition's own rows. */
+int gann_index_create_part(const void* points, uint64_t n, uint32_t d, int elem, int metric,
+                           uint32_t R, uint32_t rank, uint32_t nparts, int device, gann_index** out);
+int gann_part_info(const gann_index* idx, uint32_t* rank, uint32_t* nparts, uint64_t* base,
+                   uint64_t* rows);
+int gann_part_ipc_handle(const gann_index* idx, void* handle64);
+int gann_part_attach(gann_index* idx, uint32_t rank, const void* handle64);
+int gann_part_build_begin(gann_index* idx, uint32_t L, float alpha, int rule, uint64_t seed,
+                          uint32_t max_batch, uint32_t* nbatches);
+int gann_part_phase1(gann_index* idx, uint32_t batch, uint64_t* counts, const uint32_t** d_pairs);
+int gann_part_phase2(gann_index* idx, uint32_t batch, const uint32_t* d_pairs, uint64_t m);
+
 /* ---- counters (roofline) ----------------------------------------------------
  * Totals accumulated by the kernels since the last reset. */
 typedef struct gann_stats {

@@ -76,6 +76,13 @@ SIGNATURES = {
     "gann_load_graph": (_i, [_vp, C.c_char_p]),
     "gann_index_create_from_file": (_i, [C.c_char_p, _i, _u32, _i, _pp]),
     "gann_range_search": (_i, [_vp, _vp, _u32, _f, _u32, _f, _u32, _vp, _vp, _vp]),
+    "gann_index_create_part": (_i, [_vp, _u64, _u32, _i, _i, _u32, _u32, _u32, _i, _pp]),
+    "gann_part_info": (_i, [_vp, _vp, _vp, _vp, _vp]),
+    "gann_part_ipc_handle": (_i, [_vp, _vp]),
+    "gann_part_attach": (_i, [_vp, _u32, _vp]),
+    "gann_part_build_begin": (_i, [_vp, _u32, _f, _i, _u64, _u32, _vp]),
+    "gann_part_phase1": (_i, [_vp, _u32, _vp, _pp]),
+    "gann_part_phase2": (_i, [_vp, _u32, _vp, _u64]),
     "gann_get_stats": (_i, [_vp, C.POINTER(GannStats)]),
     "gann_reset_stats": (_i, [_vp]),
     "gann_index_device_ptrs": (_i, [_vp, _pp, C.POINTER(C.c_uint64), _pp]),

@@ -32,9 +32,9 @@ namespace gann {
 namespace {
 
 __device__ __forceinline__ uint32_t pair_target(const BackEdgeArgs& a, uint64_t e) {
-  if (a.ptarget) return a.ptarget[e];
+  if (a.ptarget) return a.ptarget[e * a.pstride];
   const uint64_t b = e / a.R, i = e - b * a.R;
-  return a.adj[uint64_t(a.bsrc[b]) * a.R + i];
+  return a.adj[uint64_t(a.bsrc[b] - a.base) * a.R + i];
 }
 __device__ __forceinline__ uint32_t pair_source(const BackEdgeArgs& a, uint64_t e) {
   if (a.psource) return a.psource[e];
@@ -65,10 +65,10 @@ __global__ void be_count_kernel(const BackEdgeArgs a) {
   for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < a.npairs; e += stride) {
     const uint32_t t = pair_target(a, e);
     if (t == kNone) continue;
-    const uint32_t old = atomicAdd(a.tcount + t, 1u);
+    const uint32_t old = atomicAdd(a.tcount + (t - a.base), 1u);
     if (old == 0) {
       const uint32_t g = static_cast<uint32_t>(atomicAdd(a.counters + kCntGroups, 1ull));
-      a.tgroup[t] = g;
+      a.tgroup[t - a.base] = g;
       a.gtarget[g] = t;
     }
   }
@@ -78,7 +78,7 @@ __global__ void be_offsets_kernel(const BackEdgeArgs a, const uint32_t ng) {
   const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
   // whole warps stay converged for the aggregated bumps
   const bool valid = g < ng;
-  const uint32_t c = valid ? a.tcount[a.gtarget[g]] : 0u;
+  const uint32_t c = valid ? a.tcount[a.gtarget[g] - a.base] : 0u;
   const unsigned long long o = warp_bump(a.counters + kCntPairsCursor, c);
   const unsigned long long p = warp_bump(a.counters + kCntPruneCursor, valid ? c + a.R : 0u);
   if (!valid) return;
@@ -98,9 +98,9 @@ __global__ void be_scatter_kernel(const BackEdgeArgs a) {
   for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < a.npairs; e += stride) {
     const uint32_t t = pair_target(a, e);
     if (t == kNone) continue;
-    const uint32_t g = a.tgroup[t];
+    const uint32_t g = a.tgroup[t - a.base];
     const uint32_t pos = atomicAdd(a.gcursor + g, 1u);
-    a.gsrc[a.goff[g] + pos] = static_cast<uint32_t>(e);
+    a.gsrc[a.goff[g] + pos] = a.pordinal ? a.pordinal[e * a.pstride] : static_cast<uint32_t>(e);
   }
 }
 
@@ -201,13 +201,13 @@ __global__ void __launch_bounds__(NT)
         out_vals[go + i] = pair_source(a, ord[i]);
       }
       cta_sync<NT>();
-      if (tid == 0) a.tcount[t] = 0;
+      if (tid == 0) a.tcount[t - a.base] = 0;
       continue;
     }
     for (uint32_t i = tid; i < c; i += NT) ord[i] = pair_source(a, ord[i]);
     if (tid == 0) sh_deg = 0;
     cta_sync<NT>();
-    uint32_t* trow = a.adj + uint64_t(t) * R;
+    uint32_t* trow = a.adj + uint64_t(t - a.base) * R;
     for (uint32_t i = tid; i < R; i += NT) {
       const uint32_t v = trow[i];
       row[i] = v;
@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(NT)
       }
     }
     cta_sync<NT>();
-    if (tid == 0) a.tcount[t] = 0;
+    if (tid == 0) a.tcount[t - a.base] = 0;
   }
 }
 
@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(NT)
     const uint32_t c = a.gcnt[g];
     const uint32_t t = a.gtarget[g];
     const uint64_t go = a.goff[g];
-    uint32_t* trow = a.adj + uint64_t(t) * R;
+    uint32_t* trow = a.adj + uint64_t(t - a.base) * R;
     if (tid == 0) {
       sh_deg = 0;
       sh_kept = 0;
@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(NT)
       if (nm <= R) atomicAdd(a.counters + kCntTooBig, 1ull);  // cannot happen (c > R); flagged
       const uint32_t i = static_cast<uint32_t>(atomicAdd(a.counters + kCntPruneBig, 1ull));
       a.plist_big[i] = g;
-      a.tcount[t] = 0;
+      a.tcount[t - a.base] = 0;
     }
     __syncthreads();
   }
@@ -445,7 +445,47 @@ __global__ void hash_keys_kernel(const uint32_t* keys, uint64_t m, uint32_t* tab
   }
 }
 
+__global__ void part_count_kernel(const uint32_t* adj, uint32_t base, uint32_t R, const uint32_t* ids,
+                                  uint32_t K, uint32_t P, unsigned long long* counts) {
+  const uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= uint64_t(K) * R) return;
+  const uint32_t k = static_cast<uint32_t>(e / R), i = static_cast<uint32_t>(e - uint64_t(k) * R);
+  const uint32_t t = adj[uint64_t(ids[k] - base) * R + i];
+  if (t != kNone) atomicAdd(counts + t / P, 1ull);
+}
+
+__global__ void part_scatter_kernel(const uint32_t* adj, uint32_t base, uint32_t R, const uint32_t* ids,
+                                    const uint32_t* bo, uint32_t K, uint32_t P, unsigned long long* cursors,
+                                    uint32_t* out) {
+  const uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= uint64_t(K) * R) return;
+  const uint32_t k = static_cast<uint32_t>(e / R), i = static_cast<uint32_t>(e - uint64_t(k) * R);
+  const uint32_t t = adj[uint64_t(ids[k] - base) * R + i];
+  if (t == kNone) return;
+  const unsigned long long pos = atomicAdd(cursors + t / P, 1ull);
+  out[2 * pos] = t;
+  out[2 * pos + 1] = bo[k] * R + i;  // the pair's position in the batch's concatenation order
+}
+
 }  // namespace
+
+cudaError_t part_pairs_count(const uint32_t* adj_local, uint32_t base, uint32_t R, const uint32_t* ids,
+                             uint32_t K, uint32_t P, unsigned long long* counts, cudaStream_t s) {
+  const uint64_t n = uint64_t(K) * R;
+  if (n == 0) return cudaSuccess;
+  part_count_kernel<<<static_cast<uint32_t>((n + 255) / 256), 256, 0, s>>>(adj_local, base, R, ids, K, P, counts);
+  return cudaGetLastError();
+}
+
+cudaError_t part_pairs_scatter(const uint32_t* adj_local, uint32_t base, uint32_t R, const uint32_t* ids,
+                               const uint32_t* bo, uint32_t K, uint32_t P, unsigned long long* cursors,
+                               uint32_t* out_pairs, cudaStream_t s) {
+  const uint64_t n = uint64_t(K) * R;
+  if (n == 0) return cudaSuccess;
+  part_scatter_kernel<<<static_cast<uint32_t>((n + 255) / 256), 256, 0, s>>>(adj_local, base, R, ids, bo, K, P,
+                                                                             cursors, out_pairs);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_hash_keys(const uint32_t* keys, uint64_t m, uint32_t* table, uint32_t tbits,
                              uint32_t* slots, cudaStream_t s) {

@@ -132,13 +132,24 @@ struct gann_index {
   DevBuf gtarget, gcnt, goff, gcursor, gsrc, poff, plen, pid, pdist, bigg, pls, plb;
   DevBuf pt, ps, ok, ov, misc, gt, bins;
   uint32_t staged_nq = 0;
+  // vertex partitioning (1 partition = the whole graph)
+  uint32_t part_rank = 0, part_count = 1, part_size = 0, part_base = 0, part_rows = 0;
+  uint32_t** d_parts = nullptr;            // device table of partition row pointers
+  std::vector<void*> ipc_open;             // peer partitions mapped through CUDA IPC
+  // partitioned build state
+  std::vector<uint32_t> order_host;
+  std::vector<std::pair<uint32_t, uint32_t>> ranges;
+  uint32_t bL = 0, brule = 0;
+  float balpha = 0.0f;
+  DevBuf pair_out, pair_cnt, lids;
 };
 
 namespace {
 
 void set_device(const gann_index* idx) { cu(cudaSetDevice(idx->device), "cudaSetDevice"); }
 
-gann_index* new_index(uint64_t n, uint32_t d, int elem, int metric, uint32_t R, int device) {
+gann_index* new_index(uint64_t n, uint32_t d, int elem, int metric, uint32_t R, int device,
+                      uint32_t rank = 0, uint32_t nparts = 1) {
   if (elem < GANN_U8 || elem > GANN_F32) fail(GANN_EINVAL, "unknown element kind");
   if (metric != GANN_L2 && metric != GANN_IP) fail(GANN_EINVAL, "unknown metric");
   if (d == 0) fail(GANN_EINVAL, "dimension must be positive");
@@ -157,19 +168,32 @@ gann_index* new_index(uint64_t n, uint32_t d, int elem, int metric, uint32_t R, 
     idx->stride = (uint64_t(idx->row_bytes) + 15) & ~uint64_t(15);
     if (idx->stride > 2048) fail(GANN_EINVAL, "rows above 2048 bytes are not supported");
     idx->geom = make_geometry(static_cast<uint32_t>(idx->stride / 16));
+    if (nparts == 0 || rank >= nparts) fail(GANN_EINVAL, "bad partition rank/count");
+    idx->part_rank = rank;
+    idx->part_count = nparts;
+    idx->part_size = static_cast<uint32_t>((n + nparts - 1) / nparts);
+    idx->part_base = static_cast<uint32_t>(std::min<uint64_t>(n, uint64_t(rank) * idx->part_size));
+    idx->part_rows = static_cast<uint32_t>(std::min<uint64_t>(n, uint64_t(idx->part_base) + idx->part_size) - idx->part_base);
     set_device(idx);
     cu(cudaStreamCreateWithFlags(&idx->stream, cudaStreamNonBlocking), "cudaStreamCreate");
     const uint64_t nn = std::max<uint64_t>(n, 1);
+    const uint64_t rows = std::max<uint64_t>(idx->part_rows, 1);
     cu(cudaMalloc(&idx->points, nn * idx->stride), "cudaMalloc points");
-    cu(cudaMalloc(&idx->adj, nn * std::max<uint32_t>(R, 1) * 4), "cudaMalloc graph");
-    cu(cudaMalloc(&idx->tcount, nn * 4), "cudaMalloc tcount");
-    cu(cudaMalloc(&idx->tgroup, nn * 4), "cudaMalloc tgroup");
+    cu(cudaMalloc(&idx->adj, rows * std::max<uint32_t>(R, 1) * 4), "cudaMalloc graph");
+    cu(cudaMalloc(&idx->tcount, rows * 4), "cudaMalloc tcount");
+    cu(cudaMalloc(&idx->tgroup, rows * 4), "cudaMalloc tgroup");
+    cu(cudaMalloc(&idx->d_parts, sizeof(uint32_t*) * nparts), "cudaMalloc parts");
+    {
+      std::vector<uint32_t*> parts(nparts, nullptr);
+      parts[rank] = idx->adj;
+      cu(cudaMemcpy(idx->d_parts, parts.data(), sizeof(uint32_t*) * nparts, cudaMemcpyHostToDevice), "parts");
+    }
     cu(cudaMalloc(&idx->stats, sizeof(unsigned long long) * kStCount), "cudaMalloc stats");
     cu(cudaMalloc(&idx->counters, sizeof(unsigned long long) * kCntNum), "cudaMalloc counters");
     cu(cudaMalloc(&idx->flags, 16), "cudaMalloc flags");
     cu(cudaMemsetAsync(idx->points, 0, nn * idx->stride, idx->stream), "memset");
-    cu(cudaMemsetAsync(idx->adj, 0xFF, nn * std::max<uint32_t>(R, 1) * 4, idx->stream), "memset");
-    cu(cudaMemsetAsync(idx->tcount, 0, nn * 4, idx->stream), "memset");
+    cu(cudaMemsetAsync(idx->adj, 0xFF, rows * std::max<uint32_t>(R, 1) * 4, idx->stream), "memset");
+    cu(cudaMemsetAsync(idx->tcount, 0, rows * 4, idx->stream), "memset");
     cu(cudaMemsetAsync(idx->stats, 0, sizeof(unsigned long long) * kStCount, idx->stream), "memset");
     cu(cudaMemsetAsync(idx->flags, 0, 16, idx->stream), "memset");
   } catch (...) {
@@ -220,7 +244,7 @@ SearchArgs base_search_args(gann_index* idx, uint32_t L, uint32_t k_gate, uint32
   a.data = idx->points;
   a.stride = idx->stride;
   a.n = static_cast<uint32_t>(idx->n);
-  a.adj = idx->adj;
+  a.graph = GraphView{idx->adj, idx->d_parts, idx->part_size, idx->part_count, idx->part_base};
   a.R = idx->R;
   a.start = idx->start;
   a.L = L;
@@ -386,6 +410,7 @@ void insert_batch(gann_index* idx, const uint32_t* d_ids, uint32_t B, uint32_t L
   p.cand_ids = idx->vis_ids.as<uint32_t>();
   p.cand_dists = idx->vis_d.as<float>();
   p.out_adj = idx->adj;
+  p.out_base = idx->part_base;
   p.mcap = vcap;
   Timer tp(idx->stream);
   prune_binned(idx, p, vcap);
@@ -441,7 +466,8 @@ void insert_batch(gann_index* idx, const uint32_t* d_ids, uint32_t B, uint32_t L
 void apply_back(gann_index* idx, const uint32_t* bsrc, uint32_t B, const uint32_t* ptarget,
                 const uint32_t* psource, uint64_t npairs, float alpha, int rule, bool timed,
                 uint32_t* out_keys = nullptr, uint32_t* out_vals = nullptr,
-                uint64_t* ngroups_out = nullptr, const uint32_t* key_of_target = nullptr) {
+                uint64_t* ngroups_out = nullptr, const uint32_t* key_of_target = nullptr,
+                const uint32_t* pordinal = nullptr, uint32_t pstride = 1) {
   if (npairs == 0) {
     if (ngroups_out) *ngroups_out = 0;
     return;
@@ -452,6 +478,9 @@ void apply_back(gann_index* idx, const uint32_t* bsrc, uint32_t B, const uint32_
   b.data = idx->points;
   b.stride = idx->stride;
   b.adj = idx->adj;
+  b.base = idx->part_base;
+  b.pstride = pstride;
+  b.pordinal = pordinal;
   b.R = R;
   b.bsrc = bsrc;
   b.B = B;
@@ -533,6 +562,7 @@ void apply_back(gann_index* idx, const uint32_t* bsrc, uint32_t B, const uint32_
   p.cand_ids = b.pid;
   p.cand_dists = b.pdist;
   p.out_adj = idx->adj;
+  p.out_base = idx->part_base;
   if (nps) {
     p.count = nps;
     p.list_index = b.plist_small;
@@ -649,6 +679,10 @@ void gann_index_free(gann_index* idx) {
   if (!idx) return;
   cudaSetDevice(idx->device);
   if (idx->stream) cudaStreamSynchronize(idx->stream);
+  for (void* p : idx->ipc_open)
+    if (p) cudaIpcCloseMemHandle(p);
+  if (idx->d_parts) cudaFree(idx->d_parts);
+  for (DevBuf* b : {&idx->pair_out, &idx->pair_cnt, &idx->lids}) b->release();
   for (void* p : {static_cast<void*>(idx->points), static_cast<void*>(idx->adj),
                   static_cast<void*>(idx->tcount), static_cast<void*>(idx->tgroup),
                   static_cast<void*>(idx->stats), static_cast<void*>(idx->counters),
@@ -688,6 +722,7 @@ int gann_build(gann_index* idx, uint32_t L, float alpha, int rule, uint64_t seed
       std::fprintf(stderr, "warning: build beam %u below degree bound %u; lists will be thin\n", L,
                    idx->R);
     set_device(idx);
+    if (idx->part_count != 1) fail(GANN_EINVAL, "a partitioned index builds with gann_part_build_begin/phase1/phase2");
     for (double& m : idx->build_ms) m = 0;
     idx->back_pairs = idx->back_groups = idx->back_pruned = 0;
     const uint64_t n = idx->n;
@@ -762,6 +797,7 @@ int gann_build_diskann(const void* points, uint64_t n, uint32_t d, int elem, int
 int gann_import_graph(gann_index* idx, const uint32_t* adj, uint32_t start) {
   return guarded([&] {
     if (!idx) fail(GANN_EINVAL, "index is NULL");
+    if (idx->part_count != 1) fail(GANN_EINVAL, "import_graph needs an unpartitioned index");
     const uint64_t n = idx->n;
     const uint32_t R = idx->R;
     if (n && start >= n) fail(GANN_EINVAL, "start vertex out of range");
@@ -790,7 +826,7 @@ int gann_export_graph(const gann_index* cidx, uint32_t* adj, uint32_t* deg, uint
     gann_index* idx = const_cast<gann_index*>(cidx);
     if (!idx) fail(GANN_EINVAL, "index is NULL");
     set_device(idx);
-    const uint64_t n = idx->n;
+    const uint64_t n = idx->part_rows;  // a partition exports its own rows
     const uint32_t R = idx->R;
     if (adj && n) {
       cu(cudaMemcpyAsync(adj, idx->adj, n * R * 4, cudaMemcpyDeviceToHost, idx->stream), "download graph");
@@ -1198,6 +1234,7 @@ int gann_save_graph(const gann_index* cidx, const char* path) {
   return guarded([&] {
     gann_index* idx = const_cast<gann_index*>(cidx);
     if (!idx || !path) fail(GANN_EINVAL, "NULL argument");
+    if (idx->part_count != 1) fail(GANN_EINVAL, "save_graph needs the whole graph (export each partition instead)");
     set_device(idx);
     std::ofstream out(path, std::ios::binary | std::ios::trunc);
     if (!out) fail(GANN_EIO, std::string("cannot open for writing: ") + path);
@@ -1233,6 +1270,7 @@ int gann_save_graph(const gann_index* cidx, const char* path) {
 int gann_load_graph(gann_index* idx, const char* path) {
   return guarded([&] {
     if (!idx || !path) fail(GANN_EINVAL, "NULL argument");
+    if (idx->part_count != 1) fail(GANN_EINVAL, "load_graph needs an unpartitioned index");
     const std::string ctx(path);
     std::ifstream in(path, std::ios::binary);
     if (!in) fail(GANN_EIO, "cannot open for reading: " + ctx);
@@ -1353,6 +1391,153 @@ int gann_range_search(gann_index* idx, const void* queries, uint32_t nq, float r
         if (dists) dists[size_t(q) * cap + t] = have ? in[t].first : __builtin_inff();
       }
     }
+  });
+}
+
+// ---- vertex-partitioned build ---------------------------------------------------
+int gann_index_create_part(const void* points, uint64_t n, uint32_t d, int elem, int metric, uint32_t R,
+                           uint32_t rank, uint32_t nparts, int device, gann_index** out) {
+  return guarded([&] {
+    if (!out || (n && !points)) fail(GANN_EINVAL, "NULL argument");
+    gann_index* idx = new_index(n, d, elem, metric, R, device, rank, nparts);
+    try {
+      if (n)
+        cu(cudaMemcpy2DAsync(idx->points, idx->stride, points, idx->row_bytes, idx->row_bytes, n,
+                             cudaMemcpyHostToDevice, idx->stream),
+           "upload points");
+      sync(idx);
+    } catch (...) {
+      gann_index_free(idx);
+      throw;
+    }
+    *out = idx;
+  });
+}
+
+int gann_part_info(const gann_index* idx, uint32_t* rank, uint32_t* nparts, uint64_t* base, uint64_t* rows) {
+  return guarded([&] {
+    if (!idx) fail(GANN_EINVAL, "index is NULL");
+    if (rank) *rank = idx->part_rank;
+    if (nparts) *nparts = idx->part_count;
+    if (base) *base = idx->part_base;
+    if (rows) *rows = idx->part_rows;
+  });
+}
+
+int gann_part_ipc_handle(const gann_index* idx, void* handle64) {
+  return guarded([&] {
+    if (!idx || !handle64) fail(GANN_EINVAL, "NULL argument");
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    cu(cudaSetDevice(idx->device), "cudaSetDevice");
+    cudaIpcMemHandle_t h;
+    cu(cudaIpcGetMemHandle(&h, idx->adj), "cudaIpcGetMemHandle");
+    std::memcpy(handle64, &h, 64);
+  });
+}
+
+int gann_part_attach(gann_index* idx, uint32_t rank, const void* handle64) {
+  return guarded([&] {
+    if (!idx || !handle64) fail(GANN_EINVAL, "NULL argument");
+    if (rank >= idx->part_count) fail(GANN_EINVAL, "partition rank out of range");
+    if (rank == idx->part_rank) return;  // our own rows
+    set_device(idx);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, 64);
+    void* ptr = nullptr;
+    cu(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    idx->ipc_open.push_back(ptr);
+    uint32_t* row0 = static_cast<uint32_t*>(ptr);
+    cu(cudaMemcpy(idx->d_parts + rank, &row0, sizeof(row0), cudaMemcpyHostToDevice), "parts table");
+  });
+}
+
+int gann_part_build_begin(gann_index* idx, uint32_t L, float alpha, int rule, uint64_t seed, uint32_t max_batch,
+                          uint32_t* nbatches) {
+  return guarded([&] {
+    if (!idx) fail(GANN_EINVAL, "index is NULL");
+    if (idx->n == 0) fail(GANN_EINVAL, "cannot build over an empty dataset");
+    if (L == 0 || idx->R == 0) fail(GANN_EINVAL, "build beam and degree bound must be positive");
+    check_prune_params(alpha, rule);
+    set_device(idx);
+    const uint64_t n = idx->n;
+    cu(cudaMemsetAsync(idx->adj, 0xFF, uint64_t(idx->part_rows) * idx->R * 4, idx->stream), "clear graph");
+    cu(cudaMemsetAsync(idx->tcount, 0, uint64_t(idx->part_rows) * 4, idx->stream), "clear counts");
+    // every partition derives the same start and insertion order (src/diskann.cpp:47-51)
+    idx->start = choose_start_dev(idx);
+    idx->order_host.resize(n);
+    gann_shuffled_order(static_cast<uint32_t>(n), mix64(seed, 0x696e73657274ULL), idx->start, idx->order_host.data());
+    idx->order.ensure(n * 4);
+    cu(cudaMemcpyAsync(idx->order.p, idx->order_host.data(), n * 4, cudaMemcpyHostToDevice, idx->stream), "order");
+    idx->ranges = batch_ranges(n, max_batch);
+    idx->bL = L;
+    idx->balpha = alpha;
+    idx->brule = static_cast<uint32_t>(rule);
+    sync(idx);
+    if (nbatches) *nbatches = static_cast<uint32_t>(idx->ranges.size());
+  });
+}
+
+int gann_part_phase1(gann_index* idx, uint32_t batch, uint64_t* counts, const uint32_t** d_pairs) {
+  return guarded([&] {
+    if (!idx || !counts || !d_pairs) fail(GANN_EINVAL, "NULL argument");
+    if (batch >= idx->ranges.size()) fail(GANN_EINVAL, "batch index out of range");
+    set_device(idx);
+    const auto [lo, hi] = idx->ranges[batch];
+    // this partition's points of the batch (owner(v) = v / P) and their batch offsets
+    std::vector<uint32_t> ids, bo;
+    for (uint32_t pos = lo; pos < hi; pos++) {
+      const uint32_t v = idx->order_host[pos];
+      if (v / idx->part_size == idx->part_rank) {
+        ids.push_back(v);
+        bo.push_back(pos - lo);
+      }
+    }
+    const uint32_t K = static_cast<uint32_t>(ids.size());
+    const uint32_t G = idx->part_count;
+    idx->lids.ensure(size_t(K) * 8 + 16);
+    uint32_t* d_ids = idx->lids.as<uint32_t>();
+    uint32_t* d_bo = d_ids + K;
+    if (K) {
+      cu(cudaMemcpyAsync(d_ids, ids.data(), size_t(K) * 4, cudaMemcpyHostToDevice, idx->stream), "upload");
+      cu(cudaMemcpyAsync(d_bo, bo.data(), size_t(K) * 4, cudaMemcpyHostToDevice, idx->stream), "upload");
+      insert_batch(idx, d_ids, K, idx->bL, idx->balpha, static_cast<int>(idx->brule), true);
+    }
+    // reverse pairs (target, batch ordinal), grouped by the target's owner
+    idx->pair_cnt.ensure(sizeof(unsigned long long) * 2 * G);
+    unsigned long long* d_cnt = idx->pair_cnt.as<unsigned long long>();
+    cu(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * G, idx->stream), "memset");
+    cu(part_pairs_count(idx->adj, idx->part_base, idx->R, d_ids, K, idx->part_size, d_cnt, idx->stream), "pairs");
+    std::vector<unsigned long long> cnt(G), off(G);
+    cu(cudaMemcpyAsync(cnt.data(), d_cnt, sizeof(unsigned long long) * G, cudaMemcpyDeviceToHost, idx->stream), "read");
+    sync(idx);
+    unsigned long long total = 0;
+    for (uint32_t g = 0; g < G; g++) {
+      off[g] = total;
+      total += cnt[g];
+      counts[g] = cnt[g];
+    }
+    idx->pair_out.ensure(std::max<unsigned long long>(total, 1) * 8);
+    cu(cudaMemcpyAsync(d_cnt + G, off.data(), sizeof(unsigned long long) * G, cudaMemcpyHostToDevice, idx->stream),
+       "offsets");
+    cu(part_pairs_scatter(idx->adj, idx->part_base, idx->R, d_ids, d_bo, K, idx->part_size, d_cnt + G,
+                          idx->pair_out.as<uint32_t>(), idx->stream),
+       "pairs");
+    sync(idx);
+    *d_pairs = idx->pair_out.as<uint32_t>();
+  });
+}
+
+int gann_part_phase2(gann_index* idx, uint32_t batch, const uint32_t* d_pairs, uint64_t m) {
+  return guarded([&] {
+    if (!idx) fail(GANN_EINVAL, "index is NULL");
+    if (batch >= idx->ranges.size()) fail(GANN_EINVAL, "batch index out of range");
+    set_device(idx);
+    const auto [lo, hi] = idx->ranges[batch];
+    // the received pairs carry their batch ordinal: the merge sorts by it, which
+    // restores the single-GPU pair order (src/diskann.cpp:61-65) inside each group
+    apply_back(idx, idx->order.as<uint32_t>() + lo, hi - lo, d_pairs, nullptr, m, idx->balpha,
+               static_cast<int>(idx->brule), true, nullptr, nullptr, nullptr, nullptr, d_pairs + 1, 2);
+    sync(idx);
   });
 }
 

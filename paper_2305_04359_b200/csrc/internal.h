@@ -14,6 +14,25 @@ struct Geometry {
 };
 Geometry make_geometry(uint32_t nch);
 
+// The graph as the kernels see it. Unpartitioned: one table, adj holds every
+// row. Vertex-partitioned (one partition per GPU): rows [base, base + P) live
+// in this GPU's adj; any row can be read through parts[v / P] (peer / IPC
+// pointers), writes go to owned rows only.
+struct GraphView {
+  uint32_t* adj;                 // local rows
+  const uint32_t* const* parts;  // nparts row-storage pointers (device table)
+  uint32_t part_size;            // P
+  uint32_t nparts;
+  uint32_t base;                 // first locally owned vertex
+};
+__device__ __forceinline__ const uint32_t* graph_row(const GraphView& g, uint32_t v, uint32_t R) {
+  if (g.nparts == 1) return g.adj + static_cast<uint64_t>(v) * R;
+  return g.parts[v / g.part_size] + static_cast<uint64_t>(v % g.part_size) * R;
+}
+__device__ __forceinline__ uint32_t* local_row(const GraphView& g, uint32_t v, uint32_t R) {
+  return g.adj + static_cast<uint64_t>(v - g.base) * R;
+}
+
 enum StatIdx {
   kStQueries = 0, kStExpansions, kStEvals, kStDrops, kStAdj,
   kStPruneLists, kStPruneCands, kStPruneEvals, kStMerges, kStSurvivors, kStMoved, kStCount
@@ -23,7 +42,7 @@ struct SearchArgs {
   const uint8_t* data;       // n rows of `stride` bytes
   uint64_t stride;
   uint32_t n;
-  const uint32_t* adj;       // n * R, kNone padded
+  GraphView graph;           // n rows of R ids, kNone padded
   uint32_t R;
   uint32_t start;
   const uint8_t* queries;    // nq rows of `stride` bytes (when query_rows == nullptr)
@@ -67,7 +86,8 @@ struct PruneArgs {
   uint32_t R;
   float alpha;
   int rule;                    // 0 scale_candidate, 1 scale_selected
-  uint32_t* out_adj;           // write to out_adj[p * R] (when out_rows == nullptr)
+  uint32_t* out_adj;           // write to out_adj[(p - out_base) * R] (when out_rows == nullptr)
+  uint32_t out_base;
   uint32_t* out_rows;          // or to out_rows[l * R]
   uint32_t* n_out;             // nullable, per list l
   uint32_t mcap;               // max list length this launch supports
@@ -93,12 +113,15 @@ bool prune_uses_mma(int elem, uint32_t mcap, uint64_t stride, uint32_t R);
 struct BackEdgeArgs {
   const uint8_t* data;
   uint64_t stride;
-  uint32_t* adj;            // n * R
+  uint32_t* adj;            // locally owned rows (vertex v at (v - base) * R)
+  uint32_t base;            // first owned vertex; tcount/tgroup are indexed by v - base
   uint32_t R;
   const uint32_t* bsrc;     // batch form: B source points
   uint32_t B;
   const uint32_t* ptarget;  // explicit form (nullable): targets
   const uint32_t* psource;  //                           sources
+  const uint32_t* pordinal; // explicit form: order key of each pair (nullable = its index)
+  uint32_t pstride;         // element stride of ptarget / pordinal (interleaved pairs: 2)
   uint64_t npairs;          // B*R (batch form) or explicit count
   int sources_distinct;     // batch form: every source appears once per target
   uint32_t* tcount;         // n, all zero on entry and on exit
@@ -136,6 +159,15 @@ cudaError_t launch_hash_keys(const uint32_t* keys, uint64_t m, uint32_t* table, 
 // group_by_key output: pairs of group g written at [goff[g], goff[g]+gcnt[g]).
 cudaError_t backedge_write_groups(const BackEdgeArgs& a, uint32_t ngroups, uint32_t nbig,
                                   uint32_t* out_keys, uint32_t* out_vals, cudaStream_t s);
+
+// ---- vertex-partitioned build: reverse pairs routed to the target's owner ------
+// Pair k of local inserted point (ids[k], batch offset bo[k]) and out-slot i:
+// (target, bo*R + i) sent to partition target / P. counts/offsets: nparts u64.
+cudaError_t part_pairs_count(const uint32_t* adj_local, uint32_t base, uint32_t R, const uint32_t* ids,
+                             uint32_t K, uint32_t P, unsigned long long* counts, cudaStream_t s);
+cudaError_t part_pairs_scatter(const uint32_t* adj_local, uint32_t base, uint32_t R, const uint32_t* ids,
+                               const uint32_t* bo, uint32_t K, uint32_t P, unsigned long long* cursors,
+                               uint32_t* out_pairs, cudaStream_t s);
 
 // ---- misc -------------------------------------------------------------------
 cudaError_t launch_choose_start(const uint8_t* data, uint64_t stride, uint64_t n, uint32_t d,

@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(NT) prune_kernel(const PruneArgs a, const uint
     uint64_t beg, m;
     beg = a.begins ? a.begins[l] : uint64_t(l) * a.fixed_stride;
     m = a.lengths[l];
-    uint32_t* orow = a.out_rows ? a.out_rows + uint64_t(l) * R : a.out_adj + uint64_t(p) * R;
+    uint32_t* orow = a.out_rows ? a.out_rows + uint64_t(l) * R : a.out_adj + uint64_t(p - a.out_base) * R;
     if (m < a.mmin) continue;  // another launch's bin
     if (m > a.mcap) {  // caller routes long lists elsewhere; never truncate silently
       if (tid == 0 && !a.skip_long) atomicAdd(a.too_long, 1u);
@@ -514,7 +514,7 @@ __global__ void __launch_bounds__(kWalkWarps * 32)
   if (m < a.mmin || m > a.mcap) return;
   const uint32_t p = a.points[l];
   const uint32_t R = a.R;
-  uint32_t* orow = a.out_rows ? a.out_rows + uint64_t(l) * R : a.out_adj + uint64_t(p) * R;
+  uint32_t* orow = a.out_rows ? a.out_rows + uint64_t(l) * R : a.out_adj + uint64_t(p - a.out_base) * R;
   const uint32_t* in = hand + size_t(rel) * ly.stride;
   const uint32_t m2 = in[0];
   const uint32_t* ids = in + 4;
@@ -643,7 +643,7 @@ __global__ void __launch_bounds__(NT) prune_chunked_kernel(const PruneArgs a) {
     const uint32_t p = a.points[l];
     const uint64_t beg = a.begins ? a.begins[l] : uint64_t(l) * a.fixed_stride;
     const uint64_t m = a.lengths[l];
-    uint32_t* orow = a.out_rows ? a.out_rows + uint64_t(l) * R : a.out_adj + uint64_t(p) * R;
+    uint32_t* orow = a.out_rows ? a.out_rows + uint64_t(l) * R : a.out_adj + uint64_t(p - a.out_base) * R;
     if (m < a.mmin) continue;
     auto key_at = [&](uint64_t i) -> uint64_t {
       const uint32_t id = a.cand_ids[beg + i];

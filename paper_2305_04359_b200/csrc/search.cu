@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_SEARCH_MINB)
       }
       const uint32_t cur = key_id(fk);
       hint = fu + 1;
-      const uint32_t* row = a.adj + static_cast<uint64_t>(cur) * R;
+      const uint32_t* row = graph_row(a.graph, cur, R);
       uint32_t nb0 = kNone, nb1 = kNone;
       if (pf_ok) {
         if (pf_id == cur) {
@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_SEARCH_MINB)
         }
         pf_id = gi >= 0 ? key_id(beam[gi]) : kNone;
         if (pf_id != kNone) {
-          const uint32_t* prow = a.adj + static_cast<uint64_t>(pf_id) * R;
+          const uint32_t* prow = graph_row(a.graph, pf_id, R);
           pf0 = lane < R ? __ldg(prow + lane) : kNone;
           pf1 = lane + 32 < R ? __ldg(prow + 32 + lane) : kNone;
         }
