@@ -19,6 +19,7 @@ synchronize on both sides, max over ranks.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import importlib.util
 import json
 import os
@@ -68,6 +69,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="CPU baseline sample length")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ref-n", type=int, default=100_000, help="reference arm: points in its CPU build sample")
+    ap.add_argument("--replicated-build", action="store_true",
+                    help="N>1: every rank builds the whole graph (default: one vertex-partitioned build)")
     return ap.parse_args()
 
 
@@ -193,12 +196,40 @@ def setup(args):
     # ---- build (timed once) ---------------------------------------------------------------
     params = g.DiskannParams(cfg.R, cfg.L, cfg.alpha, seed=42, max_batch=cfg.max_batch)
     idx.reset_stats()
-    barrier()
-    t0 = time.perf_counter()
-    idx.build(params)
-    torch.cuda.synchronize()
-    build_s = allreduce(time.perf_counter() - t0)
-    bstats = idx.stats()
+    build_mode = "single-gpu"
+    if world > 1 and not args.replicated_build:
+        # one vertex-partitioned build over the N GPUs (peer rows over NVLink,
+        # NCCL all-to-all-v of the reverse pairs), then every rank gathers the
+        # full graph for its replica
+        from paper_2305_04359_b200.partition import PartitionedIndex
+        pidx = PartitionedIndex(base.data_ptr(), cfg.metric, cfg.R, dist, device=dev, shape=(n, d), dtype=np.uint8)
+        if pidx.peers_ok:
+            barrier()
+            t0 = time.perf_counter()
+            pidx.build(params, nccl=True)
+            torch.cuda.synchronize()
+            build_s = allreduce(time.perf_counter() - t0)
+            P = -(-n // world)
+            rows = torch.full((P * cfg.R,), -1, dtype=torch.int32, device="cuda")
+            rows[: pidx.rows * cfg.R] = pidx.device_rows()
+            full = torch.empty((world * P * cfg.R,), dtype=torch.int32, device="cuda")
+            dist.all_gather_into_tensor(full, rows)
+            check(lib().gann_import_graph_device(idx._h, ctypes.c_void_p(full.data_ptr()), pidx.start()))
+            bstats = pidx.stats()  # this rank's share of the build
+            del full, rows
+            pidx.close()
+            build_mode = f"vertex-partitioned over {world} GPUs (NCCL all-to-all-v)"
+        else:
+            pidx.close()
+    if build_mode == "single-gpu":
+        barrier()
+        t0 = time.perf_counter()
+        idx.build(params)
+        torch.cuda.synchronize()
+        build_s = allreduce(time.perf_counter() - t0)
+        if world > 1:
+            build_mode = "replicated: every rank builds the whole graph"
+        bstats = idx.stats()
     adj_t = _tensor_from_ptr(idx.device_ptrs()[2], n * cfg.R * 4).view(torch.int32)  # a view, no copy
     checksum = int(adj_t.to(torch.int64).mul_(1 + torch.arange(n * cfg.R, device="cuda") % 7919).sum().item())
     replicas_identical = distutil.replicas_identical(checksum, dist if world > 1 else None)
@@ -241,6 +272,7 @@ def setup(args):
     return dict(torch=torch, dist=dist, g=g, check=check, lib=lib, cfg=cfg, nq=nq, n=n, d=d, k=k, dev=dev,
                 rank=rank, world=world, barrier=barrier, allreduce=allreduce, base=base, qdev=qdev, idx=idx,
                 build_s=build_s, bstats=bstats, replicas_identical=replicas_identical, deg_mean=deg_mean,
+                build_mode=build_mode,
                 out_ids=out_ids, out_d=out_d, stream=stream, search_L=search_L, curve=curve, chosen=chosen,
                 recall=recall, target_reached=target_reached, sp=sp)
 
@@ -251,6 +283,7 @@ def run_ours(args):
     nq, n, d, k, dev, rank, world = S["nq"], S["n"], S["d"], S["k"], S["dev"], S["rank"], S["world"]
     barrier, allreduce, base, qdev, idx = S["barrier"], S["allreduce"], S["base"], S["qdev"], S["idx"]
     build_s, bstats, replicas_identical, deg_mean = S["build_s"], S["bstats"], S["replicas_identical"], S["deg_mean"]
+    build_mode = S["build_mode"]
     out_ids, out_d, stream, search_L, curve = S["out_ids"], S["out_d"], S["stream"], S["search_L"], S["curve"]
     chosen, recall, target_reached, sp = S["chosen"], S["recall"], S["target_reached"], S["sp"]
 
@@ -360,7 +393,7 @@ def run_ours(args):
         "gpu_launches": args.steps,
         "clocks": clocks,
         "build": {
-            "points_per_s": round(n / build_s, 1), "seconds": round(build_s, 3),
+            "points_per_s": round(n / build_s, 1), "seconds": round(build_s, 3), "mode": build_mode,
             "phases_ms": {kk: round(v, 1) for kk, v in bstats["build_ms"].items()},
             "mean_degree": round(deg_mean, 3), "replicas_identical": replicas_identical,
             "search_roofline": {"achieved": round(build_bytes / (build_search_ms / 1e3) / 1e9, 1) if build_search_ms else None,

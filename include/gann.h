@@ -88,6 +88,9 @@ int gann_build_diskann(const void* points, uint64_t n, uint32_t d, int elem, int
  * import validates ids (< n, no self loops) like set_neighbors
  * (src/graph.cpp:42-59). deg may be NULL on export. */
 int gann_import_graph(gann_index* idx, const uint32_t* adj, uint32_t start);
+/* Device-resident rows (n*R, GANN_NONE padded), copied as is (trusted: no
+ * validation) — e.g. the rows all-gathered from a partitioned build. */
+int gann_import_graph_device(gann_index* idx, const uint32_t* d_adj, uint32_t start);
 int gann_export_graph(const gann_index* idx, uint32_t* adj, uint32_t* deg, uint32_t* start);
 
 /* ---- search ---------------------------------------------------------------
@@ -203,6 +206,9 @@ int gann_generate_u8(void* d_out, uint64_t n, uint32_t d, uint32_t clusters, flo
  * partition's own rows. */
 int gann_index_create_part(const void* points, uint64_t n, uint32_t d, int elem, int metric,
                            uint32_t R, uint32_t rank, uint32_t nparts, int device, gann_index** out);
+int gann_index_create_part_device(const void* d_points, uint64_t n, uint32_t d, int elem, int metric,
+                                  uint32_t R, uint32_t rank, uint32_t nparts, int device,
+                                  gann_index** out);
 int gann_part_info(const gann_index* idx, uint32_t* rank, uint32_t* nparts, uint64_t* base,
                    uint64_t* rows);
 int gann_part_ipc_handle(const gann_index* idx, void* handle64);

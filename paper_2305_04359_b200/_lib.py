@@ -77,6 +77,8 @@ SIGNATURES = {
     "gann_index_create_from_file": (_i, [C.c_char_p, _i, _u32, _i, _pp]),
     "gann_range_search": (_i, [_vp, _vp, _u32, _f, _u32, _f, _u32, _vp, _vp, _vp]),
     "gann_index_create_part": (_i, [_vp, _u64, _u32, _i, _i, _u32, _u32, _u32, _i, _pp]),
+    "gann_index_create_part_device": (_i, [_vp, _u64, _u32, _i, _i, _u32, _u32, _u32, _i, _pp]),
+    "gann_import_graph_device": (_i, [_vp, _vp, _u32]),
     "gann_part_info": (_i, [_vp, _vp, _vp, _vp, _vp]),
     "gann_part_ipc_handle": (_i, [_vp, _vp]),
     "gann_part_attach": (_i, [_vp, _u32, _vp]),

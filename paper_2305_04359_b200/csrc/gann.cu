@@ -821,6 +821,19 @@ int gann_import_graph(gann_index* idx, const uint32_t* adj, uint32_t start) {
   });
 }
 
+int gann_import_graph_device(gann_index* idx, const uint32_t* d_adj, uint32_t start) {
+  return guarded([&] {
+    if (!idx || (idx->n && !d_adj)) fail(GANN_EINVAL, "NULL argument");
+    if (idx->part_count != 1) fail(GANN_EINVAL, "import_graph needs an unpartitioned index");
+    if (idx->n && start >= idx->n) fail(GANN_EINVAL, "start vertex out of range");
+    set_device(idx);
+    if (idx->n)
+      cu(cudaMemcpyAsync(idx->adj, d_adj, idx->n * idx->R * 4, cudaMemcpyDeviceToDevice, idx->stream), "copy graph");
+    idx->start = start;
+    sync(idx);
+  });
+}
+
 int gann_export_graph(const gann_index* cidx, uint32_t* adj, uint32_t* deg, uint32_t* start) {
   return guarded([&] {
     gann_index* idx = const_cast<gann_index*>(cidx);
@@ -1405,6 +1418,25 @@ int gann_index_create_part(const void* points, uint64_t n, uint32_t d, int elem,
         cu(cudaMemcpy2DAsync(idx->points, idx->stride, points, idx->row_bytes, idx->row_bytes, n,
                              cudaMemcpyHostToDevice, idx->stream),
            "upload points");
+      sync(idx);
+    } catch (...) {
+      gann_index_free(idx);
+      throw;
+    }
+    *out = idx;
+  });
+}
+
+int gann_index_create_part_device(const void* d_points, uint64_t n, uint32_t d, int elem, int metric, uint32_t R,
+                                  uint32_t rank, uint32_t nparts, int device, gann_index** out) {
+  return guarded([&] {
+    if (!out || (n && !d_points)) fail(GANN_EINVAL, "NULL argument");
+    gann_index* idx = new_index(n, d, elem, metric, R, device, rank, nparts);
+    try {
+      if (n)
+        cu(cudaMemcpy2DAsync(idx->points, idx->stride, d_points, idx->row_bytes, idx->row_bytes, n,
+                             cudaMemcpyDeviceToDevice, idx->stream),
+           "copy points");
       sync(idx);
     } catch (...) {
       gann_index_free(idx);

@@ -30,17 +30,24 @@ from .api import ELEM, METRIC, RULE, DiskannParams, _p
 class PartitionedIndex:
     """This rank's partition of a vertex-partitioned index."""
 
-    def __init__(self, points: np.ndarray, metric: str, degree_bound: int, dist, device: int = 0):
-        points = np.ascontiguousarray(points)
+    def __init__(self, points, metric: str, degree_bound: int, dist, device: int = 0, shape=None, dtype=None):
+        """points: a host array (n, d), or a device pointer with shape=(n, d) and dtype."""
         self.dist = dist
         self.rank = dist.get_rank()
         self.world = dist.get_world_size()
         self.device = device
         self.R = degree_bound
-        self.n, self.d = points.shape
         h = C.c_void_p()
-        check(lib().gann_index_create_part(_p(points), self.n, self.d, ELEM[points.dtype], METRIC[metric],
-                                           degree_bound, self.rank, self.world, device, C.byref(h)))
+        if shape is None:
+            points = np.ascontiguousarray(points)
+            self.n, self.d = points.shape
+            check(lib().gann_index_create_part(_p(points), self.n, self.d, ELEM[points.dtype], METRIC[metric],
+                                               degree_bound, self.rank, self.world, device, C.byref(h)))
+        else:
+            self.n, self.d = shape
+            check(lib().gann_index_create_part_device(C.c_void_p(points), self.n, self.d, ELEM[np.dtype(dtype)],
+                                                      METRIC[metric], degree_bound, self.rank, self.world, device,
+                                                      C.byref(h)))
         self._h = h
         base, rows = C.c_uint64(), C.c_uint64()
         check(lib().gann_part_info(h, None, None, C.byref(base), C.byref(rows)))
@@ -48,15 +55,23 @@ class PartitionedIndex:
         self._attach_peers()
 
     def _attach_peers(self):
+        """Open every peer's rows. A failure on any rank is seen by all ranks
+        (``peers_ok``) instead of leaving the others waiting in a collective."""
         handle = (C.c_uint8 * 64)()
         check(lib().gann_part_ipc_handle(self._h, handle))
         handles = [None] * self.world
         self.dist.all_gather_object(handles, bytes(handle))
-        for r, hb in enumerate(handles):
-            if r != self.rank:
-                buf = (C.c_uint8 * 64).from_buffer_copy(hb)
-                check(lib().gann_part_attach(self._h, r, buf))
-        self.dist.barrier()
+        ok, self.attach_error = 1, None
+        try:
+            for r, hb in enumerate(handles):
+                if r != self.rank:
+                    buf = (C.c_uint8 * 64).from_buffer_copy(hb)
+                    check(lib().gann_part_attach(self._h, r, buf))
+        except Exception as e:  # noqa: BLE001 — reported through peers_ok
+            ok, self.attach_error = 0, str(e)
+        oks = [None] * self.world
+        self.dist.all_gather_object(oks, ok)
+        self.peers_ok = all(oks)
 
     def close(self):
         if getattr(self, "_h", None):
@@ -71,6 +86,8 @@ class PartitionedIndex:
 
     def build(self, params: DiskannParams, nccl: bool = False) -> dict:
         import torch
+        if not self.peers_ok:
+            raise RuntimeError(f"peer rows not mapped on every rank ({self.attach_error})")
         nb = C.c_uint32()
         check(lib().gann_part_build_begin(self._h, params.build_beam, params.alpha, RULE[params.rule], params.seed,
                                           params.max_batch, C.byref(nb)))
@@ -103,6 +120,23 @@ class PartitionedIndex:
             exchanged += total
             self.dist.barrier()  # every rank's rows are final before the next batch searches
         return {"batches": nb.value, "pairs_sent": exchanged}
+
+    def stats(self) -> dict:
+        """This rank's share of the build counters and phase times."""
+        from .api import Index
+        return Index.stats(self)
+
+    def start(self) -> int:
+        s = C.c_uint32()
+        check(lib().gann_index_info(self._h, None, None, None, None, None, C.byref(s)))
+        return s.value
+
+    def device_rows(self):
+        """A torch view (rows * R int32) of this partition's rows on the device."""
+        pts, stride, adj = C.c_void_p(), C.c_uint64(), C.c_void_p()
+        check(lib().gann_index_device_ptrs(self._h, C.byref(pts), C.byref(stride), C.byref(adj)))
+        import torch
+        return _device_view(adj.value, self.rows * self.R * 4).view(torch.int32)
 
     def export_rows(self):
         """This partition's rows (rows x R) and the start vertex."""

@@ -38,6 +38,66 @@ def _rank_main(rank, world, port, data, params, q):
     dist.destroy_process_group()
 
 
+def _rank_main_device(rank, world, port, data, params, q):
+    """bench.py's N>1 path: points from device memory, partitioned build, rows
+    gathered into every rank's full replica (gann_import_graph_device)."""
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2305_04359_b200 as g
+    from paper_2305_04359_b200._lib import check, lib
+    from paper_2305_04359_b200.partition import PartitionedIndex
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    base = torch.from_numpy(data).cuda()
+    n, d = data.shape
+    pidx = PartitionedIndex(base.data_ptr(), "l2", params["R"], dist, device=0, shape=(n, d), dtype=np.uint8)
+    assert pidx.peers_ok
+    pidx.build(g.DiskannParams(params["R"], params["L"], params["alpha"], max_batch=params["cap"]))
+    P = -(-n // world)
+    rows = torch.full((P * params["R"],), -1, dtype=torch.int32, device="cuda")
+    rows[: pidx.rows * params["R"]] = pidx.device_rows()
+    parts = [torch.empty(P * params["R"], dtype=torch.int32) for _ in range(world)]
+    dist.all_gather(parts, rows.cpu())  # gloo: host staging; NCCL gathers on the device
+    full = torch.cat(parts).cuda()
+    idx = g.Index.from_device(base.data_ptr(), n, d, np.uint8, "l2", params["R"], 0)
+    check(lib().gann_import_graph_device(idx._h, ctypes.c_void_p(full.data_ptr()), pidx.start()))
+    adj, _, start = idx.export_graph()
+    q.put((rank, adj, start))
+    dist.barrier()
+    idx.close()
+    pidx.close()
+    dist.destroy_process_group()
+
+
+def _spawn(target, world, data, params):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=target, args=(r, world, port, data, params, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    return sorted(out, key=lambda x: x[0])
+
+
+def test_partitioned_build_gathered_replicas():
+    import paper_2305_04359_b200 as g
+    data = mixture(62, 3000, 32, clusters=10)
+    params = {"R": 20, "L": 40, "alpha": 1.2, "cap": 120}
+    want = g.build_diskann(data, "l2", g.DiskannParams(20, 40, 1.2, max_batch=120))
+    wadj, _, wstart = want.export_graph()
+    want.close()
+    for rank, adj, start in _spawn(_rank_main_device, 2, data, params):
+        assert start == wstart and (adj == wadj).all(), rank
+
+
 @pytest.mark.parametrize("world,cap", [(2, 0), (3, 150)])
 def test_partitioned_build_equals_single_gpu(world, cap):
     import torch.multiprocessing as mp
