@@ -40,6 +40,7 @@ class GannStats(C.Structure):
         ("merges", C.c_uint64),
         ("survivors", C.c_uint64),
         ("moved", C.c_uint64),
+        ("duplicates", C.c_uint64),
     ]
 
 

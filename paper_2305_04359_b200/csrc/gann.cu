@@ -1590,6 +1590,7 @@ int gann_get_stats(const gann_index* idx, gann_stats* out) {
     out->merges = s[kStMerges];
     out->survivors = s[kStSurvivors];
     out->moved = s[kStMoved];
+    out->duplicates = s[kStDups];
     out->back_pairs = idx->back_pairs;
     out->back_groups = idx->back_groups;
     out->back_pruned = idx->back_pruned;

@@ -138,7 +138,7 @@ __device__ __forceinline__ uint32_t lanemask_lt(int lane) { return (1u << lane) 
 // candidate scratch, and the direct-mapped visited table.
 size_t search_smem_per_warp(uint32_t L, uint32_t R, uint32_t hash_log2) {
   const size_t Lp = (L + 31) & ~31u, Rp = (R + 31) & ~31u;
-  size_t b = Lp * 8 + 3 * Rp * 8 + 2 * Rp * 4 + (size_t(1) << hash_log2) * 4 + Lp;
+  size_t b = Lp * 8 + 3 * Rp * 8 + 2 * Rp * 4 + (size_t(1) << hash_log2) * 4 + Lp / 8 + Lp;
   return (b + 15) & ~size_t(15);
 }
 
@@ -162,7 +162,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_SEARCH_MINB)
   uint32_t* cid = reinterpret_cast<uint32_t*>(tmpk + Rp);
   uint32_t* posb = cid + Rp;
   uint32_t* hash = posb + Rp;
-  uint8_t* fl = reinterpret_cast<uint8_t*>(hash + H);
+  uint32_t* bm = hash + H;  // Lp bits: final positions of a merge's survivors (zero between merges)
+  uint8_t* fl = reinterpret_cast<uint8_t*>(bm + Lp / 32);
   const uint32_t FULL = 0xFFFFFFFFu;
 
   // Persistent warps: a resident grid pulls queries from a global counter, so
@@ -199,6 +200,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_SEARCH_MINB)
     } else {
       for (uint32_t i = lane; i < H; i += 32) hash[i] = kNone;
     }
+    for (uint32_t i = lane; i < Lp / 32; i += 32) bm[i] = 0;
     if (lane == 0) cid[0] = start;
     __syncwarp();
     eval_rows<Op, LPR, CPL>(a.data, a.stride, nch, cid, 1, ck, qr, lane);
@@ -214,7 +216,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_SEARCH_MINB)
         hash[(start * 0x9E3779B1u) >> (32 - hlog2)] = start;
     }
     uint32_t size = 1, nvis = 0, hint = 0, evict = 0;
-    uint64_t evals = 1, adjsum = 0, merges = 0, survivors = 0, moved = 0;
+    uint64_t evals = 1, adjsum = 0, merges = 0, survivors = 0, moved = 0, dups = 0;
     // speculative register prefetch of the next expansion's adjacency row
     // (R <= 64: two ids per lane); used when the guess turns out right
     const bool pf_ok = R <= 64;
@@ -332,93 +334,96 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_SEARCH_MINB)
       __syncwarp();
 
       // ---- merge: top-L of beam U new, exact duplicates dropped ----
+      // pass 1: keys below the L-th beam key (ck -> tmpk, order kept)
       const uint64_t worst = size == L ? beam[L - 1] : kMaxKey;
-      uint32_t s = 0;
+      uint32_t c1 = 0;
       for (uint32_t i0 = 0; i0 < m; i0 += 32) {
         const uint32_t i = i0 + lane;
         const uint64_t k = i < m ? ck[i] : kMaxKey;
-        bool keep = k < worst;
+        const bool keep = k < worst;
+        const uint32_t bal = __ballot_sync(FULL, keep);
+        if (keep) tmpk[c1 + __popc(bal & lanemask_lt(lane))] = k;
+        c1 += __popc(bal);
+      }
+      if (c1 == 0) continue;
+      __syncwarp();
+      // pass 2: insertion points; exact (dist, id) duplicates of beam keys drop
+      uint32_t s = 0;
+      for (uint32_t j0 = 0; j0 < c1; j0 += 32) {
+        const uint32_t j = j0 + lane;
+        bool keep = j < c1;
+        const uint64_t k = keep ? tmpk[j] : kMaxKey;
         uint32_t pb = 0;
         if (keep) {
           pb = lower_bound_u64(beam, size, k);
-          if (pb < size && beam[pb] == k) keep = false;
+          if (pb < size && beam[pb] == k) {
+            keep = false;
+            dups++;
+          }
         }
         const uint32_t bal = __ballot_sync(FULL, keep);
         if (keep) {
           const uint32_t o = s + __popc(bal & lanemask_lt(lane));
-          tmpk[o] = k;
+          ck[o] = k;
           posb[o] = pb;
         }
         s += __popc(bal);
       }
       if (s == 0) continue;
       __syncwarp();
-      uint32_t p0 = 0xFFFFFFFFu;
+      // survivors sorted (srt), final positions fin = insertion point + rank
+      // marked in a bitmap of beam positions (only fin < L is kept)
+      uint32_t p0 = 0xFFFFFFFFu, kept = 0;
       for (uint32_t j0 = 0; j0 < s; j0 += 32) {
         const uint32_t j = j0 + lane;
+        bool in = false;
         if (j < s) {
-          const uint64_t k = tmpk[j];
+          const uint64_t k = ck[j];
           uint32_t r = 0;
-          for (uint32_t t = 0; t < s; t++) r += tmpk[t] < k ? 1u : 0u;
+          for (uint32_t t = 0; t < s; t++) r += ck[t] < k ? 1u : 0u;
           srt[r] = k;
           p0 = min(p0, posb[j]);
-          posb[j] += r;  // final position of survivor j
+          const uint32_t fin = posb[j] + r;
+          in = fin < L;
+          if (in) atomicOr(bm + (fin >> 5), 1u << (fin & 31));
         }
+        kept += __popc(__ballot_sync(FULL, in));
       }
       p0 = __reduce_min_sync(FULL, p0);
       merges++;
       survivors += s;
       moved += size - p0;
       __syncwarp();
-      // move the tail [p0, size) right. Up to 256 entries at once: every lane
-      // reads its (up to 8) entries, computes their targets, then all write —
-      // targets only grow, so groups of 256 go last group first.
+      // rebuild positions [p0, new size) chunk by chunk, last chunk first:
+      // position t holds survivor #before(t) if its bit is set, else the old
+      // entry t - before(t); sources never lie above t, so descending chunks
+      // read only entries not yet overwritten
       {
-        constexpr int CG = 8;
-        const int last_g = static_cast<int>((size - 1) >> 8);
-        const int first_g = static_cast<int>(p0 >> 8);
-        for (int gq = last_g; gq >= first_g; gq--) {
-          uint64_t kk[CG];
-          uint32_t ni[CG];
-          uint32_t ffm = 0;
-#pragma unroll
-          for (int c = 0; c < CG; c++) {
-            const uint32_t i = (static_cast<uint32_t>(gq) * CG + c) * 32 + lane;
-            const bool mv = i >= p0 && i < size;
-            kk[c] = mv ? beam[i] : 0ull;
-            ffm |= (mv && fl[i]) ? (1u << c) : 0u;
-            ni[c] = mv ? i : 0xFFFFFFFFu;
-          }
-          {  // this lane's entries ascend with c, so one walk over srt counts them all
-            uint32_t pw = 0;
-#pragma unroll
-            for (int c = 0; c < CG; c++) {
-              if (ni[c] != 0xFFFFFFFFu) {
-                while (pw < s && srt[pw] < kk[c]) pw++;
-                ni[c] += pw;
-              }
+        const uint32_t nsz = min(L, size + s);
+        uint32_t running = kept;
+        for (int c = static_cast<int>((nsz - 1) >> 5); c >= static_cast<int>(p0 >> 5); c--) {
+          const uint32_t w = bm[c];
+          running -= __popc(w);
+          const uint32_t t = static_cast<uint32_t>(c) * 32 + lane;
+          const uint32_t before = running + __popc(w & lanemask_lt(lane));
+          const bool act = t >= p0 && t < nsz;
+          uint64_t key = 0;
+          uint8_t f = 0;
+          if (act) {
+            if ((w >> lane) & 1u) {
+              key = srt[before];
+            } else {
+              key = beam[t - before];
+              f = fl[t - before];
             }
           }
           __syncwarp();
-#pragma unroll
-          for (int c = 0; c < CG; c++) {
-            if (ni[c] < L) {
-              beam[ni[c]] = kk[c];
-              fl[ni[c]] = (ffm >> c) & 1u;
-            }
+          if (act) {
+            beam[t] = key;
+            fl[t] = f;
           }
+          if (lane == 0) bm[c] = 0;
           __syncwarp();
-        }
-      }
-      for (uint32_t j0 = 0; j0 < s; j0 += 32) {
-        const uint32_t j = j0 + lane;
-        if (j < s) {
-          const uint64_t k = tmpk[j];
-          const uint32_t fin = posb[j];
-          if (fin < L) {
-            beam[fin] = k;
-            fl[fin] = 0;
-          }
         }
       }
       size = min(L, size + s);
@@ -438,6 +443,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_SEARCH_MINB)
       }
     }
     evict = __reduce_add_sync(FULL, evict);
+    dups = __reduce_add_sync(FULL, static_cast<uint32_t>(dups));
     if (lane == 0) {
       if (a.n_visited) a.n_visited[q] = nvis;
       if (a.dist_comps) a.dist_comps[q] = evals;
@@ -451,6 +457,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_SEARCH_MINB)
         atomicAdd(a.stats + kStMerges, static_cast<unsigned long long>(merges));
         atomicAdd(a.stats + kStSurvivors, static_cast<unsigned long long>(survivors));
         atomicAdd(a.stats + kStMoved, static_cast<unsigned long long>(moved));
+        atomicAdd(a.stats + kStDups, static_cast<unsigned long long>(dups));
       }
     }
     __syncwarp();

@@ -52,6 +52,7 @@ for L in Ls:
         if hl:
             os.environ["GANN_HASH_LOG2"] = str(hl)
         best = 1e9
+        idx.reset_stats()
         for r in range(args.reps):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
@@ -63,7 +64,11 @@ for L in Ls:
             e1.record()
             torch.cuda.synchronize()
             best = min(best, e0.elapsed_time(e1))
-        print(f"search L={L} H=2^{hl or 'default'}: {best:.3f} ms", flush=True)
+        st = idx.stats()
+        nqq = max(1, st["queries"])
+        print(f"search L={L} H=2^{hl or 'default'}: {best:.3f} ms  evals/q {st['evaluations'] / nqq:.1f}  "
+              f"exp/q {st['expansions'] / nqq:.1f}  survivors/q {st['survivors'] / nqq:.1f}  "
+              f"moved/q {st['moved'] / nqq:.1f}  dups/q {st['duplicates'] / nqq:.1f}", flush=True)
 torch.cuda.profiler.stop()
 st = idx.stats()
 print("stats", {k: st[k] for k in ("queries", "expansions", "evaluations", "filter_drops", "adj_entries", "merges", "survivors", "moved")})
