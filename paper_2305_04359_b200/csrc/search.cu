@@ -78,9 +78,14 @@ __device__ __forceinline__ T transpose_reduce(T (&v)[U], int sub) {
 
 // Distances from the lane's query chunks qr to rows ids[0..m) -> keys out[].
 // Lane group g (LPR lanes) takes U consecutive rows per pass, so its ids come
-// from one vectorised shared load; the chunk predicate is per lane and hoisted.
+// from one vectorised shared load. ids[] must be padded with valid vertex ids
+// up to the next multiple of RPP*U (<= 32): every pass then loads whole
+// without per-row predicates, and each row address is one IMAD.WIDE.U32
+// (id * stride + the lane's hoisted chunk base). A chunk index beyond the row
+// (nch not a multiple of LPR) is clamped to the row's last chunk and its
+// contribution predicated off.
 template <class Op, int LPR, int CPL>
-__device__ __forceinline__ void eval_rows(const uint8_t* __restrict__ data, uint64_t stride,
+__device__ __forceinline__ void eval_rows(const uint8_t* __restrict__ data, uint32_t stride,
                                           uint32_t nch, const uint32_t* ids, uint32_t m,
                                           uint64_t* out, const uint4 (&qr)[CPL], int lane) {
   constexpr int RPP = 32 / LPR;
@@ -88,10 +93,13 @@ __device__ __forceinline__ void eval_rows(const uint8_t* __restrict__ data, uint
   const int sub = lane & (LPR - 1);
   const int grp = lane / LPR;
   bool chv[CPL];
+  const uint8_t* cb[CPL];
 #pragma unroll
-  for (int c = 0; c < CPL; c++) chv[c] = static_cast<uint32_t>(sub + c * LPR) < nch;
-  const uint4* lane_base = reinterpret_cast<const uint4*>(data) + sub;
-  const uint64_t stride16 = stride >> 4;
+  for (int c = 0; c < CPL; c++) {
+    const uint32_t ch = static_cast<uint32_t>(sub + c * LPR);
+    chv[c] = ch < nch;
+    cb[c] = data + static_cast<size_t>(chv[c] ? ch : nch - 1) * 16;
+  }
   for (uint32_t b0 = 0; b0 < m; b0 += RPP * U) {
     const uint32_t rb = b0 + grp * U;
     uint32_t id[U];
@@ -111,18 +119,17 @@ __device__ __forceinline__ void eval_rows(const uint8_t* __restrict__ data, uint
     uint4 x[U][CPL];
 #pragma unroll
     for (int u = 0; u < U; u++) {
-      const bool rv = rb + u < m;
-      const uint4* rp = lane_base + static_cast<uint64_t>(rv ? id[u] : 0u) * stride16;
 #pragma unroll
       for (int c = 0; c < CPL; c++)
-        x[u][c] = (rv && chv[c]) ? __ldg(rp + c * LPR) : make_uint4(0, 0, 0, 0);
+        x[u][c] = __ldg(reinterpret_cast<const uint4*>(cb[c] + static_cast<size_t>(id[u]) * stride));
     }
     typename Op::acc_t acc[U];
 #pragma unroll
     for (int u = 0; u < U; u++) {
       acc[u] = Op::zero();
 #pragma unroll
-      for (int c = 0; c < CPL; c++) acc[u] = Op::chunk(qr[c], x[u][c], acc[u]);
+      for (int c = 0; c < CPL; c++)
+        if (chv[c]) acc[u] = Op::chunk(qr[c], x[u][c], acc[u]);
     }
     const typename Op::acc_t tot = transpose_reduce<LPR, U>(acc, sub);
     const uint32_t r = rb + (sub & (U - 1));
@@ -154,6 +161,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_SEARCH_MINB)
   const uint32_t hlog2 = a.hash_log2;
   const uint32_t H = 1u << hlog2;
   const uint32_t nch = static_cast<uint32_t>(a.stride >> 4);
+  const uint32_t stride32 = static_cast<uint32_t>(a.stride);  // host: stride < 2^32
   uint8_t* base = smem + wib * per_warp;
   uint64_t* beam = reinterpret_cast<uint64_t*>(base);
   uint64_t* ck = beam + Lp;
@@ -201,9 +209,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_SEARCH_MINB)
       for (uint32_t i = lane; i < H; i += 32) hash[i] = kNone;
     }
     for (uint32_t i = lane; i < Lp / 32; i += 32) bm[i] = 0;
-    if (lane == 0) cid[0] = start;
+    cid[lane] = start;  // padded: eval_rows loads whole passes
     __syncwarp();
-    eval_rows<Op, LPR, CPL>(a.data, a.stride, nch, cid, 1, ck, qr, lane);
+    eval_rows<Op, LPR, CPL>(a.data, stride32, nch, cid, 1, ck, qr, lane);
     __syncwarp();
     if (lane == 0) {
       beam[0] = ck[0];
@@ -328,9 +336,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_SEARCH_MINB)
         m += __popc(bal);
       }
       if (m == 0) continue;
+      if (m + lane < ((m + 31) & ~31u)) cid[m + lane] = cur;  // pad to a whole pass
       __syncwarp();
       evals += m;
-      eval_rows<Op, LPR, CPL>(a.data, a.stride, nch, cid, m, ck, qr, lane);
+      eval_rows<Op, LPR, CPL>(a.data, stride32, nch, cid, m, ck, qr, lane);
       __syncwarp();
 
       // ---- merge: top-L of beam U new, exact duplicates dropped ----
