@@ -98,10 +98,21 @@ uint32_t env_u32(const char* name, uint32_t dflt) {
 // Shared-memory visited table size of the fast search mode (direct mapped,
 // overwrite on collision): a pure performance knob — it trades re-evaluated
 // rows against per-warp shared memory, i.e. resident warps.
-uint32_t hash_log2_for(uint32_t L) {
-  const uint32_t forced = env_u32("GANN_HASH_LOG2", 0);
-  if (forced) return std::min<uint32_t>(std::max<uint32_t>(forced, 5), 15);
-  return L <= 160 ? 10 : 9;  // measured on B200 at 10M (tools/profile_search.py, HLOGS sweep)
+// With n <= 2^(log2 + 15) a slot stores the 15-bit remainder of a bijective
+// hash of the id (half the bytes of an id slot, so twice the entries for the
+// same shared memory, still no false positives).
+void hash_config(uint32_t L, uint64_t n, uint32_t* log2, uint32_t* bits) {
+  const uint32_t forced = std::min<uint32_t>(env_u32("GANN_HASH_LOG2", 0), 15);
+  const bool narrow = env_u32("GANN_HASH16", 1) != 0;
+  uint32_t l = forced ? std::max<uint32_t>(forced, 5) : 11;
+  if (narrow && n <= (uint64_t(1) << (l + 15))) {
+    *log2 = l;
+    *bits = l + 15;
+    return;
+  }
+  // u32 id slots; measured on B200 at 10M (tools/profile_search.py, HLOGS sweep)
+  *log2 = forced ? std::max<uint32_t>(forced, 5) : (L <= 160 ? 10 : 9);
+  *bits = 0;
 }
 
 }  // namespace
@@ -252,7 +263,7 @@ SearchArgs base_search_args(gann_index* idx, uint32_t L, uint32_t k_gate, uint32
   a.k_out = k_out;
   a.eps = eps;
   a.visited_mode = mode;
-  a.hash_log2 = hash_log2_for(L);
+  hash_config(L, idx->n, &a.hash_log2, &a.hash_bits);
   a.dim = idx->d;
   a.row_bytes = idx->row_bytes;
   a.overflow = idx->flags;

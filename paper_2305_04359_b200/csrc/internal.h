@@ -53,7 +53,9 @@ struct SearchArgs {
   float eps;
   int visited_mode;          // 0 fast (shared table), 1 reference L*L table, 2 exact set
   uint32_t exact_slots;      // mode 2: slots per query (power of two)
-  uint32_t hash_log2;        // fast mode table size
+  uint32_t hash_log2;        // fast mode table size (entries)
+  uint32_t hash_bits;        // fast mode: 0 = u32 id slots; else u16 remainders of a
+                             // bijective hash over hash_bits = hash_log2 + 15 bits
   uint32_t* ref_table;       // modes 1/2: per-query tables, initialised by the kernel
   uint32_t dim;              // real dimension (search_seed)
   uint32_t row_bytes;        // real bytes per row (search_seed)
@@ -68,7 +70,7 @@ struct SearchArgs {
   uint32_t* next_query;      // persistent warps: dynamic query counter (zeroed per launch)
   unsigned long long* stats; // kStCount counters (nullable)
 };
-size_t search_smem_per_warp(uint32_t L, uint32_t R, uint32_t hash_log2);
+size_t search_smem_per_warp(uint32_t L, uint32_t R, uint32_t hash_log2, bool hash16);
 cudaError_t launch_search(const SearchArgs& a, int elem, int metric, const Geometry& g,
                           cudaStream_t s);
 

@@ -45,9 +45,12 @@ constexpr int kWarpsPerBlock = 4;
 
 // Rows in flight per lane group per pass: U <= LPR so the transposed
 // reduction can hand every lane of the group (at most) one finished row.
+#ifndef GANN_SEARCH_U
+#define GANN_SEARCH_U 8  // rows in flight per lane group (registers: U * CPL * 4)
+#endif
 template <int LPR, int CPL>
 struct Unroll {
-  static constexpr int raw = LPR > 8 ? 8 : LPR;
+  static constexpr int raw = LPR > GANN_SEARCH_U ? GANN_SEARCH_U : LPR;
   static constexpr int U = (raw / CPL) < 1 ? 1 : (raw / CPL);
 };
 
@@ -143,9 +146,9 @@ __device__ __forceinline__ uint32_t lanemask_lt(int lane) { return (1u << lane) 
 
 // Per-warp shared memory: beam keys + flags (single buffer, merged in place),
 // candidate scratch, and the direct-mapped visited table.
-size_t search_smem_per_warp(uint32_t L, uint32_t R, uint32_t hash_log2) {
+size_t search_smem_per_warp(uint32_t L, uint32_t R, uint32_t hash_log2, bool hash16) {
   const size_t Lp = (L + 31) & ~31u, Rp = (R + 31) & ~31u;
-  size_t b = Lp * 8 + 3 * Rp * 8 + 2 * Rp * 4 + (size_t(1) << hash_log2) * 4 + Lp / 8 + Lp;
+  size_t b = Lp * 8 + 2 * Rp * 8 + Rp * 4 + (size_t(1) << hash_log2) * (hash16 ? 2 : 4) + Lp / 8 + Lp;
   return (b + 15) & ~size_t(15);
 }
 
@@ -164,13 +167,19 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_SEARCH_MINB)
   const uint32_t stride32 = static_cast<uint32_t>(a.stride);  // host: stride < 2^32
   uint8_t* base = smem + wib * per_warp;
   uint64_t* beam = reinterpret_cast<uint64_t*>(base);
+  // ck: candidate keys; tmpk: keys below the L-th (dead after the duplicate
+  // pass, so it also holds the sorted survivors srt); cid: candidate ids
+  // (dead after the gather, so it also holds the insertion points posb)
   uint64_t* ck = beam + Lp;
-  uint64_t* srt = ck + Rp;
-  uint64_t* tmpk = srt + Rp;
+  uint64_t* tmpk = ck + Rp;
+  uint64_t* srt = tmpk;
   uint32_t* cid = reinterpret_cast<uint32_t*>(tmpk + Rp);
-  uint32_t* posb = cid + Rp;
-  uint32_t* hash = posb + Rp;
-  uint32_t* bm = hash + H;  // Lp bits: final positions of a merge's survivors (zero between merges)
+  uint32_t* posb = cid;
+  uint32_t* hash = cid + Rp;
+  uint16_t* h16 = reinterpret_cast<uint16_t*>(hash);
+  const uint32_t hbits = a.hash_bits;
+  const uint32_t hmask = hbits ? (1u << hbits) - 1u : 0u;
+  uint32_t* bm = hash + (hbits ? H / 2 : H);  // Lp bits: final positions of a merge's survivors
   uint8_t* fl = reinterpret_cast<uint8_t*>(bm + Lp / 32);
   const uint32_t FULL = 0xFFFFFFFFu;
 
@@ -206,7 +215,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_SEARCH_MINB)
       const uint64_t h = mix64(start, a.dim);
       seed = mix64(h ^ q64[0], q64[1]);
     } else {
-      for (uint32_t i = lane; i < H; i += 32) hash[i] = kNone;
+      for (uint32_t i = lane; i < (hbits ? H / 2 : H); i += 32) hash[i] = kNone;  // u16 slots: 0xFFFF
     }
     for (uint32_t i = lane; i < Lp / 32; i += 32) bm[i] = 0;
     cid[lane] = start;  // padded: eval_rows loads whole passes
@@ -220,7 +229,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_SEARCH_MINB)
         table[(start * 0x9E3779B1u) & (TS - 1)] = start;
       else if (a.visited_mode == 1)
         table[mix64(static_cast<uint64_t>(start) ^ seed) % LL] = start;
-      else
+      else if (hbits) {
+        const uint32_t h = (start * 0x9E3779B1u) & hmask;
+        h16[h >> 15] = static_cast<uint16_t>(h & 0x7FFFu);
+      } else
         hash[(start * 0x9E3779B1u) >> (32 - hlog2)] = start;
     }
     uint32_t size = 1, nvis = 0, hint = 0, evict = 0;
@@ -320,6 +332,19 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_SEARCH_MINB)
           if (valid && last) table[slot] = nb;
           __syncwarp();
           fresh = valid && !seen;
+        } else if (hbits) {
+          // direct-mapped u16 slots: slot and remainder of a bijection of the
+          // id over hbits bits (id < 2^hbits), so a match is the same id;
+          // 0xFFFF (no 15-bit remainder) marks an empty slot
+          const uint32_t h = (nb * 0x9E3779B1u) & hmask;
+          const uint32_t slot = h >> 15, rem = h & 0x7FFFu;
+          const uint32_t old = valid ? h16[slot] : 0xFFFFu;
+          fresh = valid && old != rem;
+          __syncwarp();
+          if (fresh) {
+            h16[slot] = static_cast<uint16_t>(rem);
+            evict += old != 0xFFFFu ? 1u : 0u;
+          }
         } else {
           // direct-mapped, overwrite on collision: never a false positive
           const uint32_t slot = (nb * 0x9E3779B1u) >> (32 - hlog2);
@@ -478,7 +503,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_SEARCH_MINB)
 namespace {
 template <int E, int M, int LPR, int CPL>
 cudaError_t launch_one(const SearchArgs& a, cudaStream_t s) {
-  const uint32_t per_warp = static_cast<uint32_t>(search_smem_per_warp(a.L, a.R, a.hash_log2));
+  const uint32_t per_warp = static_cast<uint32_t>(search_smem_per_warp(a.L, a.R, a.hash_log2, a.hash_bits != 0));
   const size_t smem = size_t(per_warp) * kWarpsPerBlock;
   auto k = search_kernel<E, M, LPR, CPL>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
