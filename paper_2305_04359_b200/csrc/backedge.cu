@@ -81,6 +81,10 @@ __global__ void be_offsets_kernel(const BackEdgeArgs a, const uint32_t ng) {
   const uint32_t c = valid ? a.tcount[a.gtarget[g] - a.base] : 0u;
   const unsigned long long o = warp_bump(a.counters + kCntPairsCursor, c);
   const unsigned long long p = warp_bump(a.counters + kCntPruneCursor, valid ? c + a.R : 0u);
+  // one atomic per warp for the largest group (a per-thread atomicMax on one
+  // address serialises ~n_groups operations in L2)
+  const uint32_t wmax = __reduce_max_sync(0xFFFFFFFFu, c);
+  if ((threadIdx.x & 31) == 0 && wmax) atomicMax(a.counters + kCntMaxGroup, static_cast<unsigned long long>(wmax));
   if (!valid) return;
   a.gcnt[g] = c;
   a.goff[g] = o;
@@ -90,7 +94,6 @@ __global__ void be_offsets_kernel(const BackEdgeArgs a, const uint32_t ng) {
     const uint32_t i = static_cast<uint32_t>(atomicAdd(a.counters + kCntBig, 1ull));
     a.big_groups[i] = g;
   }
-  atomicMax(a.counters + kCntMaxGroup, static_cast<unsigned long long>(c));
 }
 
 __global__ void be_scatter_kernel(const BackEdgeArgs a) {

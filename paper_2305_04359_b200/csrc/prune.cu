@@ -265,9 +265,9 @@ __host__ __device__ inline MmaLayout mma_layout(uint32_t mcap, uint32_t stride, 
   o += l.xs;
   l.off_norm = o;
   o += size_t(l.mc + 1) * 4;
-  l.off_dk = o;                              // sorted distances to p (float)
+  l.off_dk = o;                              // sorted norms (int)
   o += size_t(l.mc + 16) * 4;
-  l.off_ns = o;                              // sorted norms
+  l.off_ns = o;                              // sorted cull thresholds (int)
   o += size_t(l.mc + 16) * 4;
   o = (o + 15) & ~size_t(15);
   l.off_cm = o;
@@ -305,7 +305,44 @@ uint32_t* prune_handoff(uint64_t bytes, cudaStream_t s) {
 // The greedy of prune.cpp:25-43 needs, for a selected i, the test "i culls j"
 // only for later j, and its outcome does not depend on which candidates are
 // still alive — so evaluating all of them up front is exact.
-template <int E, int M, int W>
+// Largest integer S with pred(S), pred monotone (true up to a point, then
+// false) over [-2^30, 2^30]; e is an estimate of the answer. Exponential
+// search from e, then bisection: a few evaluations when e is close.
+template <class Pred>
+__device__ __forceinline__ int last_true(Pred pred, float e) {
+  constexpr int kLo = -(1 << 30), kHi = 1 << 30;
+  const int e0 = e != e ? 0 : static_cast<int>(fminf(fmaxf(floorf(e), float(kLo)), float(kHi)));
+  int lo, hi;  // pred(lo) true (or lo = kLo - 1), pred(hi) false (or hi = kHi + 1)
+  if (pred(e0)) {
+    lo = e0;
+    int st = 1;
+    hi = e0;
+    while (true) {
+      const long long c = static_cast<long long>(lo) + st;
+      if (c > kHi) { hi = kHi + 1; break; }
+      if (!pred(static_cast<int>(c))) { hi = static_cast<int>(c); break; }
+      lo = static_cast<int>(c);
+      st <<= 1;
+    }
+  } else {
+    hi = e0;
+    int st = 1;
+    while (true) {
+      const long long c = static_cast<long long>(hi) - st;
+      if (c < kLo) { lo = kLo - 1; break; }
+      if (pred(static_cast<int>(c))) { lo = static_cast<int>(c); break; }
+      hi = static_cast<int>(c);
+      st <<= 1;
+    }
+  }
+  while (hi - lo > 1) {
+    const int mid = lo + (hi - lo) / 2;
+    if (pred(mid)) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+template <int E, int M, int W, int RULE>
 __global__ void __launch_bounds__(kMmaThreads)
     prune_prep_kernel(const PruneArgs a, const MmaLayout ly, uint32_t* hand, uint32_t l0, uint32_t lcount) {
   using Op = DistOp<E, M>;
@@ -320,9 +357,9 @@ __global__ void __launch_bounds__(kMmaThreads)
   int* norm = reinterpret_cast<int*>(smem + ly.off_norm);
   uint32_t* cm = reinterpret_cast<uint32_t*>(smem + ly.off_cm);
   uint32_t* zmask = cm + ly.mc * W;
-  float* dk = reinterpret_cast<float*>(smem + ly.off_dk);
+  int* sn = reinterpret_cast<int*>(smem + ly.off_dk);  // sorted norms
   int* ns = reinterpret_cast<int*>(smem + ly.off_ns);
-  __shared__ uint32_t sh_m2;
+  __shared__ uint32_t sh_m2, sh_pre;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t mc = ly.mc, xs = ly.xs, kp = ly.kp;
   const uint32_t nch = static_cast<uint32_t>(a.stride >> 4);
@@ -341,17 +378,42 @@ __global__ void __launch_bounds__(kMmaThreads)
     const uint64_t beg = a.begins ? a.begins[l] : uint64_t(l) * a.fixed_stride;
     uint32_t* out = hand + size_t(rel) * ly.stride;
     __syncthreads();
-    if (tid == 0) sh_m2 = 0;
+    if (tid == 0) {
+      sh_m2 = 0;
+      sh_pre = m;
+    }
     for (uint32_t i = tid; i < W; i += NT) zmask[i] = 0u;
     // gather rows in input order (+ p's row when distances must be computed)
     const bool own_d = a.cand_dists == nullptr;
-    for (uint32_t t = tid; t < (m + (own_d ? 1u : 0u)) * kch; t += NT) {
-      const uint32_t r = t / kch, c = t - r * kch;
-      const uint32_t id = r < m ? a.cand_ids[beg + r] : p;
-      uint4 v = make_uint4(0, 0, 0, 0);
-      if (c < nch) v = __ldg(reinterpret_cast<const uint4*>(a.data + uint64_t(id) * a.stride) + c);
-      uint8_t* dst = r < m ? X + size_t(r) * xs : Xp;
-      *reinterpret_cast<uint4*>(dst + c * 16) = v;
+    const uint32_t rows_g = m + (own_d ? 1u : 0u);
+    if ((kch & (kch - 1)) == 0 && kch <= NT) {
+      // a thread keeps one chunk column; 4 rows' loads in flight per thread
+      const uint32_t lk = __ffs(kch) - 1, c = tid & (kch - 1), step = NT >> lk;
+      constexpr int GU = 4;
+      for (uint32_t r0 = tid >> lk; r0 < rows_g; r0 += GU * step) {
+        uint4 v[GU];
+#pragma unroll
+        for (int u = 0; u < GU; u++) {
+          const uint32_t r = r0 + u * step;
+          const uint32_t id = r < m ? a.cand_ids[beg + r] : p;
+          v[u] = (r < rows_g && c < nch) ? __ldg(reinterpret_cast<const uint4*>(a.data + uint64_t(id) * a.stride) + c)
+                                         : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < GU; u++) {
+          const uint32_t r = r0 + u * step;
+          if (r < rows_g) *reinterpret_cast<uint4*>((r < m ? X + size_t(r) * xs : Xp) + c * 16) = v[u];
+        }
+      }
+    } else {
+      for (uint32_t t = tid; t < rows_g * kch; t += NT) {
+        const uint32_t r = t / kch, c = t - r * kch;
+        const uint32_t id = r < m ? a.cand_ids[beg + r] : p;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (c < nch) v = __ldg(reinterpret_cast<const uint4*>(a.data + uint64_t(id) * a.stride) + c);
+        uint8_t* dst = r < m ? X + size_t(r) * xs : Xp;
+        *reinterpret_cast<uint4*>(dst + c * 16) = v;
+      }
     }
     for (uint32_t t = tid; t < m * W; t += NT) cm[t] = 0u;
     __syncthreads();
@@ -386,40 +448,81 @@ __global__ void __launch_bounds__(kMmaThreads)
       norm[r] = acc;
     }
     __syncthreads();
-    // rank sort by (dist, id) — prune.cpp:21 (keys are distinct)
-    for (uint32_t i = tid; i < m; i += NT) {
-      const uint64_t k = tk[i];
-      if (k == kMaxKey) continue;
-      uint32_t r = 0;
-      for (uint32_t j = 0; j < m; j++) r += tk[j] < k ? 1u : 0u;
-      sk[r] = k;
-      perm[r] = static_cast<uint16_t>(i);
+    // rank sort by (dist, id) — prune.cpp:21 (keys are distinct; p carries
+    // kMaxKey and is not written). Re-prune lists are a row in ascending
+    // order (a prune's output) with a few sources appended, so: find the
+    // longest ascending prefix P, then a prefix key's rank is its index plus
+    // the suffix keys below it, and a suffix key's rank is a binary search in
+    // the prefix plus the other suffix keys below it (O(m - P) per key).
+    for (uint32_t i = tid; i + 1 < m; i += NT)
+      if (!(tk[i] < tk[i + 1])) atomicMin(&sh_pre, i + 1);
+    __syncthreads();
+    {
+      const uint32_t P = sh_pre;  // keys [0, P) ascend
+      for (uint32_t i = tid; i < m; i += NT) {
+        const uint64_t k = tk[i];
+        if (k == kMaxKey) continue;
+        uint32_t r;
+        if (i < P) {
+          r = i;
+        } else {
+          uint32_t lo = 0, hi = P;
+          while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (tk[mid] < k) lo = mid + 1; else hi = mid;
+          }
+          r = lo;
+        }
+        for (uint32_t j = P; j < m; j++) r += tk[j] < k ? 1u : 0u;
+        sk[r] = k;
+        perm[r] = static_cast<uint16_t>(i);
+      }
     }
     __syncthreads();
     const uint32_t m2 = sh_m2;
     const uint32_t mpad = (m2 + 15) & ~15u;
     const uint32_t mw = (m2 + 31) >> 5;
-    // per sorted position: distance to p and norm (padding positions: +inf, 0)
+    // per sorted position: the cull thresholds. With S(i, j) the exact int
+    // the reference converts (L2: |x_i|^2 + |x_j|^2 - 2 x_i.x_j; IP: -x_i.x_j),
+    // prune.cpp:37-39 culls j from pick i iff
+    //   rule 0: fmul(alpha, float(S)) <= d(p, j)  <=>  S <= T_j
+    //   rule 1: float(S) < fmul(alpha, d(p, i))   <=>  S <= V_i
+    // both monotone in S, so T_j / V_i are exact. Stored folded with the
+    // norms: thr[j] = T_j - |x_j|^2 (rule 0, per column) or V_i - |x_i|^2
+    // (rule 1, per row); padding positions never cull.
     for (uint32_t i = tid; i < mpad; i += NT) {
-      const float dd = i < m2 ? key_dist(sk[i]) : __int_as_float(0x7f800000);
-      dk[i] = dd;
-      ns[i] = i < m2 ? norm[perm[i]] : 0;
-      if (i < m2 && dd == 0.0f) atomicOr(&zmask[i >> 5], 1u << (i & 31));
+      int th = -(1 << 30);
+      int nrm = 0;
+      if (i < m2) {
+        const float dd = key_dist(sk[i]);
+        nrm = M == kL2 ? norm[perm[i]] : 0;
+        const float alpha = a.alpha;
+        if (RULE == 0)
+          th = last_true([&](int S) { return __fmul_rn(alpha, __int2float_rn(S)) <= dd; }, dd / alpha);
+        else {
+          const float lim = __fmul_rn(alpha, dd);
+          th = last_true([&](int S) { return __int2float_rn(S) < lim; }, lim);
+        }
+        th -= nrm;  // |th| <= 2^30 + 2^28: no overflow
+        if (dd == 0.0f) atomicOr(&zmask[i >> 5], 1u << (i & 31));
+      }
+      ns[i] = th;   // folded threshold
+      sn[i] = nrm;  // sorted norm (0 for IP and padding)
     }
     __syncthreads();
     // all cull tests of the upper triangle (sorted positions), 16x16 tiles per warp
     {
       const uint32_t mt = mpad >> 4;
-      const uint32_t items = mt * (mt + 1) / 2;
       const int g = lane >> 2, tg = lane & 3;
-      const float alpha = a.alpha;
-      for (uint32_t it = warp; it < items; it += NT / 32) {
-        uint32_t rb = 0, rem = it;
-        while (rem >= mt - rb) {
-          rem -= mt - rb;
-          rb++;
-        }
-        const uint32_t r0 = rb * 16, n0 = (rb + rem) * 16;
+      // upper-triangle tiles in column-major order (it = cb (cb + 1) / 2 + rb),
+      // warp w takes it = w, w + 4, ...; (cb, rb) advance incrementally
+      uint32_t cb = 0, rb = static_cast<uint32_t>(warp);
+      while (rb > cb) {
+        rb -= cb + 1;
+        cb++;
+      }
+      for (; cb < mt; ) {
+        const uint32_t r0 = rb * 16, n0 = cb * 16;
         const uint32_t ar = r0 + (lane & 7) + ((lane >> 3) & 1) * 8;
         const uint32_t br = n0 + (lane & 7) + (lane >> 4) * 8;
         const uint8_t* arow = X + size_t(ar < m2 ? perm[ar] : mc) * xs + (lane >> 4) * 16;
@@ -433,39 +536,45 @@ __global__ void __launch_bounds__(kMmaThreads)
           mma_i8<SIGNED>(acc1, af, bf[2], bf[3]);
         }
         // this lane's two rows and four columns of the tile
-        float rd[2], rlim[2];
-        int rn[2];
-        uint32_t rowi[2];
+        // rule 0: cull iff |x_i|^2 - 2 g <= T_j - |x_j|^2 (column threshold)
+        // rule 1: cull iff |x_j|^2 - 2 g <= V_i - |x_i|^2 (row threshold)
+        // (IP: norms 0, -g in place of -2 g)
+        uint32_t vmask[2];  // columns (bit = tile column) this row may cull
+        int rv[2];          // rule 0: |x_i|^2 ; rule 1: row threshold
 #pragma unroll
         for (int h = 0; h < 2; h++) {
-          rowi[h] = r0 + g + h * 8;
-          rd[h] = dk[rowi[h]];
-          rn[h] = ns[rowi[h]];
-          rlim[h] = __fmul_rn(alpha, rd[h]);
+          const uint32_t row = r0 + g + h * 8;
+          // prune.cpp:32: a zero-distance pick culls nothing; only columns
+          // right of the row and inside the list
+          const bool live = row < m2 && ((zmask[row >> 5] >> (row & 31)) & 1u) == 0;
+          const uint32_t right = row < n0 ? 0xFFFFu : (row - n0 >= 15 ? 0u : (0xFFFFu << (row - n0 + 1)) & 0xFFFFu);
+          const uint32_t inside = m2 >= n0 + 16 ? 0xFFFFu : (m2 <= n0 ? 0u : (1u << (m2 - n0)) - 1u);
+          vmask[h] = live ? (right & inside) : 0u;
+          rv[h] = RULE == 0 ? sn[row] : ns[row];
         }
-        uint32_t bits_lo = 0, bits_hi = 0;
+        uint32_t bits[2] = {0u, 0u};
 #pragma unroll
         for (int h = 0; h < 2; h++) {
 #pragma unroll
           for (int e2 = 0; e2 < 2; e2++) {
             const uint32_t ccol = h * 8 + tg * 2 + e2;
             const uint32_t col = n0 + ccol;
-            const float cd = dk[col];
-            const int cn = ns[col];
+            // rule 0: column threshold; rule 1: column norm
+            const int cv = RULE == 0 ? ns[col] : sn[col];
 #pragma unroll
             for (int rr = 0; rr < 2; rr++) {
               const int gram = h ? acc1[rr * 2 + e2] : acc0[rr * 2 + e2];
-              const float via = M == kL2 ? __int2float_rn(rn[rr] + cn - 2 * gram) : -__int2float_rn(gram);
-              // prune.cpp:32 (zero-distance picks cull nothing) and :37-39, one
-              // IEEE multiply, never contracted; padding columns carry +inf
-              const bool cull = col > rowi[rr] && col < m2 && rd[rr] != 0.0f &&
-                                (a.rule == 0 ? (__fmul_rn(alpha, via) <= cd) : (via < rlim[rr]));
-              if (cull) {
-                if (rr) bits_hi |= 1u << ccol;
-                else bits_lo |= 1u << ccol;
-              }
+              const int gm = M == kL2 ? -2 * gram : -gram;
+              const bool cull = RULE == 0 ? (rv[rr] + gm <= cv) : (cv + gm <= rv[rr]);
+              if (cull) bits[rr] |= 1u << ccol;
             }
           }
+        }
+        uint32_t bits_lo = bits[0] & vmask[0], bits_hi = bits[1] & vmask[1];
+        rb += NT / 32;
+        while (rb > cb) {
+          rb -= cb + 1;
+          cb++;
         }
         bits_lo |= __shfl_xor_sync(FULL, bits_lo, 1);
         bits_lo |= __shfl_xor_sync(FULL, bits_lo, 2);
@@ -879,7 +988,7 @@ cudaError_t dispatch(const PruneArgs& a, const Geometry& g, int threads, cudaStr
 
 template <int E, int M, int W>
 cudaError_t launch_mma_w(const PruneArgs& a, const MmaLayout& ly, cudaStream_t s) {
-  auto kp = prune_prep_kernel<E, M, W>;
+  auto kp = a.rule == 0 ? prune_prep_kernel<E, M, W, 0> : prune_prep_kernel<E, M, W, 1>;
   cudaError_t e = cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ly.total));
   if (e != cudaSuccess) return e;
   // the hand-off region is reused chunk by chunk (~1 GiB)

@@ -1,13 +1,16 @@
 """Per-phase instruction / stall shares of search_kernel from an ncu source dump
-(tools/ncu_summary.sh writes /tmp/_ncu_src.csv). Phases are search.cu line
-ranges given as name=lo-hi arguments; common.cuh lines are reported apart."""
+(tools/ncu_summary.sh writes /tmp/_ncu_src.csv). Phases are line ranges of
+one source file given as name=lo-hi arguments; other files are reported apart.
+
+  python tools/phase_hot.py /tmp/_ncu_src.csv search.cu eval=80-140 ..."""
 import csv
 import sys
 from collections import defaultdict
 
 rows = list(csv.reader(open(sys.argv[1])))
 phases = []
-for a in sys.argv[2:]:
+target = sys.argv[2]
+for a in sys.argv[3:]:
     name, rng = a.split("=")
     lo, hi = map(int, rng.split("-"))
     phases.append((name, lo, hi))
@@ -37,7 +40,7 @@ ts, te = sum(st.values()) or 1, sum(ex.values()) or 1
 agg_s, agg_e = defaultdict(int), defaultdict(int)
 for (f, ln), e in ex.items():
     name = f
-    if f == "search.cu":
+    if f == target:
         for p, lo, hi in phases:
             if lo <= ln <= hi:
                 name = p
