@@ -133,7 +133,10 @@ def search_bytes(stats: dict, row_bytes: int, nq: int, k: int) -> float:
     B = sum_q [U_q*d*s + sum_{v in V_q} 4*(1 + deg v) + d*s + 8k], with the
     distinct-evaluation count U from an EXACT visited-mode run of the same
     queries (stats["evaluations"] there), |V| and sum deg from the same run."""
-    return (stats["evaluations"] * row_bytes + 4.0 * (stats["expansions"] + stats["adj_entries"])
+    # the fast-mode kernel keeps no adjacency counter (diagnostics off): count
+    # the full R-wide row it reads per expansion instead
+    adj = stats["adj_entries"] or stats["expansions"] * stats.get("R", 64)
+    return (stats["evaluations"] * row_bytes + 4.0 * (stats["expansions"] + adj)
             + nq * row_bytes + 8.0 * k * nq)
 
 
@@ -353,7 +356,7 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline_search(idx, base, qh.numpy(), chosen, k, args.cpu_seconds, out_ids, nq)
 
-    build_bytes = search_bytes(bstats, d, bstats["queries"], 0)
+    build_bytes = search_bytes(dict(bstats, R=cfg.R), d, bstats["queries"], 0)
     build_search_ms = bstats["build_ms"]["search"]
     line = {
         "metric": "search QPS at recall@10>=0.95 (Alg.1 beam {L,L,0}, top-10) over a B200-built Vamana graph",

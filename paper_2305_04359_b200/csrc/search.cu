@@ -30,6 +30,7 @@
 // used to account the algorithmic bytes of a launch.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "internal.h"
@@ -152,7 +153,11 @@ size_t search_smem_per_warp(uint32_t L, uint32_t R, uint32_t hash_log2, bool has
   return (b + 15) & ~size_t(15);
 }
 
-template <int E, int M, int LPR, int CPL>
+// F16: the fast mode with u16 slots, compiled without the other modes'
+// branches and without the diagnostic counters (filter drops, adjacency
+// entries, merges, survivors, moved, duplicates); the general instance keeps
+// them (GANN_SEARCH_DIAG=1 selects it for the fast mode too)
+template <int E, int M, int LPR, int CPL, bool F16>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_SEARCH_MINB)
     search_kernel(const SearchArgs a, const uint32_t per_warp) {
   using Op = DistOp<E, M>;
@@ -177,7 +182,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_SEARCH_MINB)
   uint32_t* posb = cid;
   uint32_t* hash = cid + Rp;
   uint16_t* h16 = reinterpret_cast<uint16_t*>(hash);
-  const uint32_t hbits = a.hash_bits;
+  const uint32_t hbits = a.hash_bits;  // F16 implies hbits != 0
+  const int vmode = F16 ? 0 : a.visited_mode;
   const uint32_t hmask = hbits ? (1u << hbits) - 1u : 0u;
   uint32_t* bm = hash + (hbits ? H / 2 : H);  // Lp bits: final positions of a merge's survivors
   uint8_t* fl = reinterpret_cast<uint8_t*>(bm + Lp / 32);
@@ -203,10 +209,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_SEARCH_MINB)
     uint64_t seed = 0;
     const uint32_t LL = L * L;
     const uint32_t TS = a.exact_slots;  // mode 2: exact open-addressing set, global memory
-    if (a.visited_mode == 2) {
+    if (vmode == 2) {
       table = a.ref_table + static_cast<uint64_t>(q) * TS;
       for (uint32_t i = lane; i < TS; i += 32) table[i] = kNone;
-    } else if (a.visited_mode == 1) {
+    } else if (vmode == 1) {
       table = a.ref_table + static_cast<uint64_t>(q) * LL;
       for (uint32_t i = lane; i < LL; i += 32) table[i] = kNone;
       // search_seed — src/search.cpp:52-58 (rows are zero padded to >= 16 bytes,
@@ -225,18 +231,19 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_SEARCH_MINB)
     if (lane == 0) {
       beam[0] = ck[0];
       fl[0] = 0;
-      if (a.visited_mode == 2)
+      if (vmode == 2)
         table[(start * 0x9E3779B1u) & (TS - 1)] = start;
-      else if (a.visited_mode == 1)
+      else if (vmode == 1)
         table[mix64(static_cast<uint64_t>(start) ^ seed) % LL] = start;
-      else if (hbits) {
+      else if (F16 || hbits) {
         const uint32_t h = (start * 0x9E3779B1u) & hmask;
         h16[h >> 15] = static_cast<uint16_t>(h & 0x7FFFu);
       } else
         hash[(start * 0x9E3779B1u) >> (32 - hlog2)] = start;
     }
     uint32_t size = 1, nvis = 0, hint = 0, evict = 0;
-    uint64_t evals = 1, adjsum = 0, merges = 0, survivors = 0, moved = 0, dups = 0;
+    uint64_t evals = 1;
+    uint32_t adjsum = 0, merges = 0, survivors = 0, moved = 0, dups = 0;  // per query: 32 bits suffice
     // speculative register prefetch of the next expansion's adjacency row
     // (R <= 64: two ids per lane); used when the guess turns out right
     const bool pf_ok = R <= 64;
@@ -307,9 +314,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_SEARCH_MINB)
         const uint32_t t = t0 + lane;
         const uint32_t nb = pf_ok ? (t0 == 0 ? nb0 : nb1) : (t < R ? __ldg(row + t) : kNone);
         const bool valid = nb != kNone;
-        adjsum += __popc(__ballot_sync(FULL, valid));
+        if (!F16) adjsum += __popc(__ballot_sync(FULL, valid));
         bool fresh;
-        if (a.visited_mode == 2) {
+        if (vmode == 2) {
           fresh = false;
           if (valid) {
             uint32_t slot = (nb * 0x9E3779B1u) & (TS - 1);
@@ -320,7 +327,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_SEARCH_MINB)
               slot = (slot + 1) & (TS - 1);
             }
           }
-        } else if (a.visited_mode == 1) {
+        } else if (vmode == 1) {
           const uint32_t slot =
               valid ? static_cast<uint32_t>(mix64(static_cast<uint64_t>(nb) ^ seed) % LL) : kNone;
           const uint32_t peers = __match_any_sync(FULL, slot);
@@ -332,7 +339,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_SEARCH_MINB)
           if (valid && last) table[slot] = nb;
           __syncwarp();
           fresh = valid && !seen;
-        } else if (hbits) {
+        } else if (F16 || hbits) {
           // direct-mapped u16 slots: slot and remainder of a bijection of the
           // id over hbits bits (id < 2^hbits), so a match is the same id;
           // 0xFFFF (no 15-bit remainder) marks an empty slot
@@ -343,7 +350,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_SEARCH_MINB)
           __syncwarp();
           if (fresh) {
             h16[slot] = static_cast<uint16_t>(rem);
-            evict += old != 0xFFFFu ? 1u : 0u;
+            if (!F16) evict += old != 0xFFFFu ? 1u : 0u;
           }
         } else {
           // direct-mapped, overwrite on collision: never a false positive
@@ -392,7 +399,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_SEARCH_MINB)
           pb = lower_bound_u64(beam, size, k);
           if (pb < size && beam[pb] == k) {
             keep = false;
-            dups++;
+            if (!F16) dups++;
           }
         }
         const uint32_t bal = __ballot_sync(FULL, keep);
@@ -424,9 +431,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_SEARCH_MINB)
         kept += __popc(__ballot_sync(FULL, in));
       }
       p0 = __reduce_min_sync(FULL, p0);
-      merges++;
-      survivors += s;
-      moved += size - p0;
+      if (!F16) {
+        merges++;
+        survivors += s;
+        moved += size - p0;
+      }
       __syncwarp();
       // rebuild positions [p0, new size) chunk by chunk, last chunk first:
       // position t holds survivor #before(t) if its bit is set, else the old
@@ -477,7 +486,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_SEARCH_MINB)
       }
     }
     evict = __reduce_add_sync(FULL, evict);
-    dups = __reduce_add_sync(FULL, static_cast<uint32_t>(dups));
+    dups = __reduce_add_sync(FULL, dups);
     if (lane == 0) {
       if (a.n_visited) a.n_visited[q] = nvis;
       if (a.dist_comps) a.dist_comps[q] = evals;
@@ -486,12 +495,14 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_SEARCH_MINB)
         atomicAdd(a.stats + kStQueries, 1ull);
         atomicAdd(a.stats + kStExpansions, static_cast<unsigned long long>(nvis));
         atomicAdd(a.stats + kStEvals, static_cast<unsigned long long>(evals));
-        atomicAdd(a.stats + kStDrops, static_cast<unsigned long long>(evict));
-        atomicAdd(a.stats + kStAdj, static_cast<unsigned long long>(adjsum));
-        atomicAdd(a.stats + kStMerges, static_cast<unsigned long long>(merges));
-        atomicAdd(a.stats + kStSurvivors, static_cast<unsigned long long>(survivors));
-        atomicAdd(a.stats + kStMoved, static_cast<unsigned long long>(moved));
-        atomicAdd(a.stats + kStDups, static_cast<unsigned long long>(dups));
+        if (!F16) {
+          atomicAdd(a.stats + kStDrops, static_cast<unsigned long long>(evict));
+          atomicAdd(a.stats + kStAdj, static_cast<unsigned long long>(adjsum));
+          atomicAdd(a.stats + kStMerges, static_cast<unsigned long long>(merges));
+          atomicAdd(a.stats + kStSurvivors, static_cast<unsigned long long>(survivors));
+          atomicAdd(a.stats + kStMoved, static_cast<unsigned long long>(moved));
+          atomicAdd(a.stats + kStDups, static_cast<unsigned long long>(dups));
+        }
       }
     }
     __syncwarp();
@@ -505,7 +516,12 @@ template <int E, int M, int LPR, int CPL>
 cudaError_t launch_one(const SearchArgs& a, cudaStream_t s) {
   const uint32_t per_warp = static_cast<uint32_t>(search_smem_per_warp(a.L, a.R, a.hash_log2, a.hash_bits != 0));
   const size_t smem = size_t(per_warp) * kWarpsPerBlock;
-  auto k = search_kernel<E, M, LPR, CPL>;
+  static const bool diag = [] {
+    const char* v = std::getenv("GANN_SEARCH_DIAG");
+    return v && *v && *v != '0';
+  }();
+  const bool f16 = a.visited_mode == 0 && a.hash_bits != 0 && !diag;
+  auto k = f16 ? search_kernel<E, M, LPR, CPL, true> : search_kernel<E, M, LPR, CPL, false>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;

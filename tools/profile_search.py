@@ -13,6 +13,9 @@ import torch
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 
+import os  # noqa: E402
+
+os.environ.setdefault("GANN_SEARCH_DIAG", "1")  # per-query diagnostic counters (general kernel)
 import paper_2305_04359_b200 as g  # noqa: E402
 from paper_2305_04359_b200 import datagen  # noqa: E402
 from paper_2305_04359_b200._lib import check, lib  # noqa: E402
