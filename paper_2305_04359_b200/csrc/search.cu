@@ -80,14 +80,55 @@ __device__ __forceinline__ T transpose_reduce(T (&v)[U], int sub) {
   return v[0];
 }
 
+// One pass: lane group g (LPR lanes) takes UU consecutive rows from b0 + g*UU,
+// their ids from one vectorised shared load.
+template <class Op, int LPR, int CPL, int UU>
+__device__ __forceinline__ void eval_pass(uint32_t b0, const uint32_t* ids, uint32_t m, uint32_t stride,
+                                          const uint8_t* const (&cb)[CPL], const bool (&chv)[CPL],
+                                          uint64_t* out, const uint4 (&qr)[CPL], int sub, int grp) {
+  const uint32_t rb = b0 + grp * UU;
+  uint32_t id[UU];
+  if (UU % 4 == 0) {
+#pragma unroll
+    for (int u = 0; u < UU; u += 4) {
+      const uint4 v = *reinterpret_cast<const uint4*>(ids + rb + u);
+      id[u] = v.x;
+      if (u + 1 < UU) id[u + 1] = v.y;
+      if (u + 2 < UU) id[u + 2] = v.z;
+      if (u + 3 < UU) id[u + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int u = 0; u < UU; u++) id[u] = ids[rb + u];
+  }
+  uint4 x[UU][CPL];
+#pragma unroll
+  for (int u = 0; u < UU; u++) {
+#pragma unroll
+    for (int c = 0; c < CPL; c++)
+      x[u][c] = __ldg(reinterpret_cast<const uint4*>(cb[c] + static_cast<size_t>(id[u]) * stride));
+  }
+  typename Op::acc_t acc[UU];
+#pragma unroll
+  for (int u = 0; u < UU; u++) {
+    acc[u] = Op::zero();
+#pragma unroll
+    for (int c = 0; c < CPL; c++)
+      if (chv[c]) acc[u] = Op::chunk(qr[c], x[u][c], acc[u]);
+  }
+  const typename Op::acc_t tot = transpose_reduce<LPR, UU>(acc, sub);
+  const uint32_t r = rb + (sub & (UU - 1));
+  if (sub < UU && r < m) out[r] = make_key(Op::finish(tot), ids[r]);
+}
+
 // Distances from the lane's query chunks qr to rows ids[0..m) -> keys out[].
-// Lane group g (LPR lanes) takes U consecutive rows per pass, so its ids come
-// from one vectorised shared load. ids[] must be padded with valid vertex ids
-// up to the next multiple of RPP*U (<= 32): every pass then loads whole
-// without per-row predicates, and each row address is one IMAD.WIDE.U32
-// (id * stride + the lane's hoisted chunk base). A chunk index beyond the row
-// (nch not a multiple of LPR) is clamped to the row's last chunk and its
-// contribution predicated off.
+// Full passes take RPP*U rows; the last, partial pass shrinks to a quarter or
+// half of that when the remaining rows fit (fewer instructions for the same
+// rows). ids[] must be padded with valid vertex ids up to the next multiple of
+// RPP*U (<= 32): passes load whole without per-row predicates, and each row
+// address is one IMAD.WIDE.U32 (id * stride + the lane's hoisted chunk base).
+// A chunk index beyond the row (nch not a multiple of LPR) is clamped to the
+// row's last chunk and its contribution predicated off.
 template <class Op, int LPR, int CPL>
 __device__ __forceinline__ void eval_rows(const uint8_t* __restrict__ data, uint32_t stride,
                                           uint32_t nch, const uint32_t* ids, uint32_t m,
@@ -104,41 +145,16 @@ __device__ __forceinline__ void eval_rows(const uint8_t* __restrict__ data, uint
     chv[c] = ch < nch;
     cb[c] = data + static_cast<size_t>(chv[c] ? ch : nch - 1) * 16;
   }
-  for (uint32_t b0 = 0; b0 < m; b0 += RPP * U) {
-    const uint32_t rb = b0 + grp * U;
-    uint32_t id[U];
-    if (U % 4 == 0) {
-#pragma unroll
-      for (int u = 0; u < U; u += 4) {
-        const uint4 v = *reinterpret_cast<const uint4*>(ids + rb + u);
-        id[u] = v.x;
-        if (u + 1 < U) id[u + 1] = v.y;
-        if (u + 2 < U) id[u + 2] = v.z;
-        if (u + 3 < U) id[u + 3] = v.w;
-      }
-    } else {
-#pragma unroll
-      for (int u = 0; u < U; u++) id[u] = ids[rb + u];
-    }
-    uint4 x[U][CPL];
-#pragma unroll
-    for (int u = 0; u < U; u++) {
-#pragma unroll
-      for (int c = 0; c < CPL; c++)
-        x[u][c] = __ldg(reinterpret_cast<const uint4*>(cb[c] + static_cast<size_t>(id[u]) * stride));
-    }
-    typename Op::acc_t acc[U];
-#pragma unroll
-    for (int u = 0; u < U; u++) {
-      acc[u] = Op::zero();
-#pragma unroll
-      for (int c = 0; c < CPL; c++)
-        if (chv[c]) acc[u] = Op::chunk(qr[c], x[u][c], acc[u]);
-    }
-    const typename Op::acc_t tot = transpose_reduce<LPR, U>(acc, sub);
-    const uint32_t r = rb + (sub & (U - 1));
-    if (sub < U && r < m) out[r] = make_key(Op::finish(tot), ids[r]);
-  }
+  uint32_t b0 = 0;
+  for (; b0 + RPP * U <= m; b0 += RPP * U) eval_pass<Op, LPR, CPL, U>(b0, ids, m, stride, cb, chv, out, qr, sub, grp);
+  const uint32_t rem = m - b0;
+  if (rem == 0) return;
+  if (U >= 8 && rem <= RPP * (U / 4))
+    eval_pass<Op, LPR, CPL, (U >= 8 ? U / 4 : 1)>(b0, ids, m, stride, cb, chv, out, qr, sub, grp);
+  else if (U >= 4 && rem <= RPP * (U / 2))
+    eval_pass<Op, LPR, CPL, (U >= 4 ? U / 2 : 1)>(b0, ids, m, stride, cb, chv, out, qr, sub, grp);
+  else
+    eval_pass<Op, LPR, CPL, U>(b0, ids, m, stride, cb, chv, out, qr, sub, grp);
 }
 
 __device__ __forceinline__ uint32_t lanemask_lt(int lane) { return (1u << lane) - 1u; }
