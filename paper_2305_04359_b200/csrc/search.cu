@@ -85,7 +85,8 @@ __device__ __forceinline__ T transpose_reduce(T (&v)[U], int sub) {
 template <class Op, int LPR, int CPL, int UU>
 __device__ __forceinline__ void eval_pass(uint32_t b0, const uint32_t* ids, uint32_t m, uint32_t stride,
                                           const uint8_t* const (&cb)[CPL], const bool (&chv)[CPL],
-                                          uint64_t* out, const uint4 (&qr)[CPL], int sub, int grp) {
+                                          uint64_t* out, const uint4 (&qr)[CPL], int sub, int grp,
+                                          uint64_t worst, uint32_t& n_out, int lane) {
   const uint32_t rb = b0 + grp * UU;
   uint32_t id[UU];
   if (UU % 4 == 0) {
@@ -118,10 +119,18 @@ __device__ __forceinline__ void eval_pass(uint32_t b0, const uint32_t* ids, uint
   }
   const typename Op::acc_t tot = transpose_reduce<LPR, UU>(acc, sub);
   const uint32_t r = rb + (sub & (UU - 1));
-  if (sub < UU && r < m) out[r] = make_key(Op::finish(tot), ids[r]);
+  // keys below the L-th beam key are appended to out (candidate order is not
+  // needed: the merge ranks them)
+  uint64_t key = kMaxKey;
+  if (sub < UU && r < m) key = make_key(Op::finish(tot), ids[r]);
+  const bool keep = key < worst;
+  const uint32_t bal = __ballot_sync(0xFFFFFFFFu, keep);
+  if (keep) out[n_out + __popc(bal & ((1u << lane) - 1u))] = key;
+  n_out += __popc(bal);
 }
 
-// Distances from the lane's query chunks qr to rows ids[0..m) -> keys out[].
+// Distances from the lane's query chunks qr to rows ids[0..m); the keys below
+// `worst` go to out[0..returned count).
 // Full passes take RPP*U rows; the last, partial pass shrinks to a quarter or
 // half of that when the remaining rows fit (fewer instructions for the same
 // rows). ids[] must be padded with valid vertex ids up to the next multiple of
@@ -130,9 +139,10 @@ __device__ __forceinline__ void eval_pass(uint32_t b0, const uint32_t* ids, uint
 // A chunk index beyond the row (nch not a multiple of LPR) is clamped to the
 // row's last chunk and its contribution predicated off.
 template <class Op, int LPR, int CPL>
-__device__ __forceinline__ void eval_rows(const uint8_t* __restrict__ data, uint32_t stride,
-                                          uint32_t nch, const uint32_t* ids, uint32_t m,
-                                          uint64_t* out, const uint4 (&qr)[CPL], int lane) {
+__device__ __forceinline__ uint32_t eval_rows(const uint8_t* __restrict__ data, uint32_t stride,
+                                              uint32_t nch, const uint32_t* ids, uint32_t m,
+                                              uint64_t* out, const uint4 (&qr)[CPL], int lane,
+                                              uint64_t worst) {
   constexpr int RPP = 32 / LPR;
   constexpr int U = Unroll<LPR, CPL>::U;
   const int sub = lane & (LPR - 1);
@@ -145,16 +155,18 @@ __device__ __forceinline__ void eval_rows(const uint8_t* __restrict__ data, uint
     chv[c] = ch < nch;
     cb[c] = data + static_cast<size_t>(chv[c] ? ch : nch - 1) * 16;
   }
-  uint32_t b0 = 0;
-  for (; b0 + RPP * U <= m; b0 += RPP * U) eval_pass<Op, LPR, CPL, U>(b0, ids, m, stride, cb, chv, out, qr, sub, grp);
+  uint32_t b0 = 0, n_out = 0;
+  for (; b0 + RPP * U <= m; b0 += RPP * U)
+    eval_pass<Op, LPR, CPL, U>(b0, ids, m, stride, cb, chv, out, qr, sub, grp, worst, n_out, lane);
   const uint32_t rem = m - b0;
-  if (rem == 0) return;
+  if (rem == 0) return n_out;
   if (U >= 8 && rem <= RPP * (U / 4))
-    eval_pass<Op, LPR, CPL, (U >= 8 ? U / 4 : 1)>(b0, ids, m, stride, cb, chv, out, qr, sub, grp);
+    eval_pass<Op, LPR, CPL, (U >= 8 ? U / 4 : 1)>(b0, ids, m, stride, cb, chv, out, qr, sub, grp, worst, n_out, lane);
   else if (U >= 4 && rem <= RPP * (U / 2))
-    eval_pass<Op, LPR, CPL, (U >= 4 ? U / 2 : 1)>(b0, ids, m, stride, cb, chv, out, qr, sub, grp);
+    eval_pass<Op, LPR, CPL, (U >= 4 ? U / 2 : 1)>(b0, ids, m, stride, cb, chv, out, qr, sub, grp, worst, n_out, lane);
   else
-    eval_pass<Op, LPR, CPL, U>(b0, ids, m, stride, cb, chv, out, qr, sub, grp);
+    eval_pass<Op, LPR, CPL, U>(b0, ids, m, stride, cb, chv, out, qr, sub, grp, worst, n_out, lane);
+  return n_out;
 }
 
 __device__ __forceinline__ uint32_t lanemask_lt(int lane) { return (1u << lane) - 1u; }
@@ -242,7 +254,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_SEARCH_MINB)
     for (uint32_t i = lane; i < Lp / 32; i += 32) bm[i] = 0;
     cid[lane] = start;  // padded: eval_rows loads whole passes
     __syncwarp();
-    eval_rows<Op, LPR, CPL>(a.data, stride32, nch, cid, 1, ck, qr, lane);
+    eval_rows<Op, LPR, CPL>(a.data, stride32, nch, cid, 1, ck, qr, lane, kMaxKey);
     __syncwarp();
     if (lane == 0) {
       beam[0] = ck[0];
@@ -387,24 +399,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_SEARCH_MINB)
       if (m + lane < ((m + 31) & ~31u)) cid[m + lane] = cur;  // pad to a whole pass
       __syncwarp();
       evals += m;
-      eval_rows<Op, LPR, CPL>(a.data, stride32, nch, cid, m, ck, qr, lane);
-      __syncwarp();
-
-      // ---- merge: top-L of beam U new, exact duplicates dropped ----
-      // pass 1: keys below the L-th beam key (ck -> tmpk, order kept)
+      // distances; keys below the L-th beam key go to tmpk (c1 of them)
       const uint64_t worst = size == L ? beam[L - 1] : kMaxKey;
-      uint32_t c1 = 0;
-      for (uint32_t i0 = 0; i0 < m; i0 += 32) {
-        const uint32_t i = i0 + lane;
-        const uint64_t k = i < m ? ck[i] : kMaxKey;
-        const bool keep = k < worst;
-        const uint32_t bal = __ballot_sync(FULL, keep);
-        if (keep) tmpk[c1 + __popc(bal & lanemask_lt(lane))] = k;
-        c1 += __popc(bal);
-      }
+      const uint32_t c1 = eval_rows<Op, LPR, CPL>(a.data, stride32, nch, cid, m, tmpk, qr, lane, worst);
       if (c1 == 0) continue;
       __syncwarp();
-      // pass 2: insertion points; exact (dist, id) duplicates of beam keys drop
+      // ---- merge: top-L of beam U new, exact duplicates dropped ----
+      // insertion points; exact (dist, id) duplicates of beam keys drop
       uint32_t s = 0;
       for (uint32_t j0 = 0; j0 < c1; j0 += 32) {
         const uint32_t j = j0 + lane;
