@@ -9,12 +9,18 @@ the C ABI with host buffers, and the reference's CPU search timed beside it.
 
 A step is one search launch over one batch of 10,000 queries per GPU (the
 config's query set); the index (1.28 GB vectors + 2.56 GB graph) is larger
-than L2, so no flush is needed between steps (smaller indexes are flushed).
-Multi-GPU: one process per GPU, the index is rebuilt identically on every rank
-(the build is deterministic; a checksum all-gather verifies the replicas) and
-each rank searches its own 10k-query shard — no data-path collective
-("scaling": "weak"). Timing: CUDA events on the launching stream, barrier +
-synchronize on both sides, max over ranks.
+than L2, so no flush is needed between steps (smaller indexes are flushed,
+and then launch serially). Steps alternate over two streams, so one batch's
+tail (its last, longest queries) overlaps the next batch's start, as a
+serving loop would; every step still searches its whole batch. e2e runs the
+same loop through gann_search_async with pinned host buffers (H2D + search +
+D2H per step); the blocking gann_search is reported beside it.
+Multi-GPU: one process per GPU; one vertex-partitioned build over all GPUs
+(NCCL all-to-all-v of reverse pairs), the rows all-gathered into a replica
+per rank (checksum all-gather verifies them); each rank searches its own
+10k-query shard — no data-path collective ("scaling": "weak"). Timing: CUDA
+events on the launching streams, barrier + synchronize on both sides, max
+over ranks.
 """
 from __future__ import annotations
 
@@ -69,6 +75,9 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="CPU baseline sample length")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ref-n", type=int, default=100_000, help="reference arm: points in its CPU build sample")
+    ap.add_argument("--streams", type=int, default=2,
+                    help="timed steps alternate over this many streams, so one step's tail overlaps the next "
+                         "step's start (1 = serial launches; forced to 1 when steps flush L2)")
     ap.add_argument("--replicated-build", action="store_true",
                     help="N>1: every rank builds the whole graph (default: one vertex-partitioned build)")
     return ap.parse_args()
@@ -295,29 +304,47 @@ def run_ours(args):
     index_bytes = n * (d + 4 * cfg.R)
     flush = index_bytes < 2 * l2_bytes
     flush_buf = torch.empty(max(4 * l2_bytes, 1), dtype=torch.uint8, device="cuda") if flush else None
+    nstreams = 1 if flush else max(1, args.streams)
+    streams = [stream] + [torch.cuda.Stream().cuda_stream for _ in range(nstreams - 1)]
+    souts = [(out_ids, out_d)] + [(torch.empty_like(out_ids), torch.empty_like(out_d)) for _ in range(nstreams - 1)]
+    ext = [torch.cuda.ExternalStream(sp_) for sp_ in streams]
     for _ in range(args.warmup):
         search_L(chosen)
     idx.reset_stats()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     sampler = ClockSampler(dev)
     sampler.start()
     barrier()
     if os.environ.get("GANN_PROFILE_RANGE"):
         torch.cuda.profiler.start()  # ncu --profile-from-start off: only the timed launches
-    for e0, e1 in evs:
+    t_start.record(ext[0])
+    for es in ext[1:]:
+        es.wait_event(t_start)
+    for i, (e0, e1) in enumerate(evs):
+        j = i % nstreams
         if flush:
             flush_buf.fill_(1)
-        e0.record()
-        idx.search_staged(sp, k, out_ids.data_ptr(), out_d.data_ptr(), stream)
-        e1.record()
+        e0.record(ext[j])
+        idx.search_staged(sp, k, souts[j][0].data_ptr(), souts[j][1].data_ptr(), streams[j])
+        e1.record(ext[j])
+    for es in ext[1:]:
+        ev = torch.cuda.Event()
+        ev.record(es)
+        ext[0].wait_event(ev)
+    t_end.record(ext[0])
+    torch.cuda.synchronize()
     barrier()
     if os.environ.get("GANN_PROFILE_RANGE"):
         torch.cuda.profiler.stop()
     clocks = sampler.stop()
-    step_ms = [e0.elapsed_time(e1) for e0, e1 in evs]
-    total_ms = allreduce(sum(step_ms))
+    step_ms = [e0.elapsed_time(e1) for e0, e1 in evs]  # each launch on its stream (overlaps its neighbours)
+    # serial launches: the sum of the launches' own spans (excludes the L2
+    # flushes between them); pipelined: the elapsed time of all K launches
+    total_ms = allreduce(sum(step_ms) if nstreams == 1 else t_start.elapsed_time(t_end))
     sstats = idx.stats()
     qps = world * nq * args.steps / (total_ms / 1e3)
+    outs_agree = all(bool((o[0] == out_ids).all().item()) for o in souts[1:])
     # the algorithmic bytes of one launch: the same queries once more in EXACT mode
     idx.reset_stats()
     idx.search_device(qdev.data_ptr(), nq, sp, k, out_ids.data_ptr(), out_d.data_ptr(), stream=stream,
@@ -325,31 +352,59 @@ def run_ours(args):
     torch.cuda.synchronize()
     xstats = idx.stats()
     per_launch_bytes = search_bytes(xstats, d, nq, k)
-    avg_launch_s = statistics.mean(step_ms) / 1e3
+    # sustained time per launch: the K launches' elapsed time / K (with 2
+    # streams a launch's own event span includes its overlap with neighbours)
+    avg_launch_s = total_ms / args.steps / 1e3
     peak, peak_src = peaks()
     achieved = per_launch_bytes / avg_launch_s / 1e9
 
     # ---- end to end through the C ABI with host buffers -------------------------------------
+    # every step: pinned host queries -> HBM, the search, ids + dists -> pinned
+    # host buffers. gann_search_async enqueues a step on a stream with its own
+    # scratch; steps alternate over the same streams as above. The blocking
+    # gann_search is timed too (e2e.blocking).
     import ctypes as C
     qh = torch.empty((nq, d), dtype=torch.uint8).pin_memory()
     qh.copy_(qdev.view(nq, d).cpu())
-    ih = torch.empty((nq, k), dtype=torch.int32).pin_memory()
-    dh = torch.empty((nq, k), dtype=torch.float32).pin_memory()
+    hout = [(torch.empty((nq, k), dtype=torch.int32).pin_memory(), torch.empty((nq, k), dtype=torch.float32).pin_memory())
+            for _ in range(nstreams)]
+    scratch_b = idx.async_scratch_bytes(nq, k)
+    scratch = [torch.empty(scratch_b, dtype=torch.uint8, device="cuda") for _ in range(nstreams)]
     L_ = lib()
 
-    def e2e_step():
+    def e2e_async(i):
+        j = i % nstreams
+        idx.search_async(qh.data_ptr(), nq, sp, k, hout[j][0].data_ptr(), hout[j][1].data_ptr(),
+                         scratch[j].data_ptr(), scratch_b, streams[j])
+
+    for i in range(args.warmup):
+        e2e_async(i)
+    torch.cuda.synchronize()
+    barrier()
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        e2e_async(i)
+    torch.cuda.synchronize()
+    barrier()
+    e2e_s = allreduce(time.perf_counter() - t0)
+    ref_ids = out_ids.cpu().numpy().view(np.uint32).reshape(nq, k)
+    e2e_match = all(bool((h[0].numpy().view(np.uint32) == ref_ids).all()) for h in hout)
+
+    ih = hout[0][0]
+
+    def e2e_blocking():
         check(L_.gann_search(idx.handle, C.c_void_p(qh.data_ptr()), nq, k, chosen, chosen, 0.0, 0, None,
-                             C.c_void_p(ih.data_ptr()), C.c_void_p(dh.data_ptr()), None, None, None, None, 0))
+                             C.c_void_p(ih.data_ptr()), C.c_void_p(hout[0][1].data_ptr()), None, None, None, None, 0))
 
     for _ in range(args.warmup):
-        e2e_step()
+        e2e_blocking()
     barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        e2e_step()
+        e2e_blocking()
     barrier()
-    e2e_s = allreduce(time.perf_counter() - t0)
-    e2e_match = bool((ih.numpy().view(np.uint32) == out_ids.cpu().numpy().view(np.uint32).reshape(nq, k)).all())
+    e2e_block_s = allreduce(time.perf_counter() - t0)
+    e2e_match = e2e_match and bool((ih.numpy().view(np.uint32) == ref_ids).all())
 
     # ---- CPU baseline: the reference's beam_search over the same graph, rank 0 at N=1 ------
     cpu = None
@@ -378,12 +433,20 @@ def run_ours(args):
             "L_search": chosen, "recall@10": recall, "target_recall": args.target_recall,
             "target_reached_in_sweep": target_reached,
             "l2": "flushed between steps" if flush else f"inputs larger than L2 ({index_bytes / 1e9:.2f} GB index)",
+            "streams": nstreams,
+            "step_pipelining": ("steps alternate over 2 streams: a step's tail overlaps the next step's start; every "
+                                "step searches its whole batch; value = K*nq / elapsed of all K" if nstreams > 1
+                                else "serial launches"),
         },
         "roofline": {
             "bound": "hbm", "kernel": "search_kernel", "achieved": round(achieved, 1), "peak": peak,
             "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
             "algorithmic_bytes_per_launch": round(per_launch_bytes),
             "avg_launch_ms": round(avg_launch_s * 1e3, 4),
+            "launch_ms_basis": ("elapsed of the K pipelined launches / K (sustained)" if nstreams > 1
+                                else "mean of the launches' own event spans"),
+            "launch_event_span_ms_mean": round(statistics.mean(step_ms), 4),
+            "outputs_agree_across_streams": outs_agree,
             "traffic": traffic_from_profile(cfg.name, chosen),
             "distinct_evals_per_query": round(xstats["evaluations"] / nq, 1),
             "evals_per_query_fast_filter": round(sstats["evaluations"] / (nq * args.steps), 1),
@@ -392,7 +455,10 @@ def run_ours(args):
         "cpu_baseline": cpu,
         "e2e": {"value": round(world * nq * args.steps / e2e_s, 1), "unit": "queries/s",
                 "h2d_bytes_per_step": nq * d, "d2h_bytes_per_step": nq * k * 8,
-                "api": "gann_search (host buffers, pinned)", "ids_match_device_path": e2e_match},
+                "api": f"gann_search_async on {nstreams} stream(s) (pinned host buffers, H2D + search + D2H per step)",
+                "ids_match_device_path": e2e_match,
+                "blocking": {"value": round(world * nq * args.steps / e2e_block_s, 1),
+                             "api": "gann_search (blocking call, pinned host buffers)"}},
         "gpu_launches": args.steps,
         "clocks": clocks,
         "build": {

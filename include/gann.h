@@ -116,6 +116,18 @@ int gann_search_device(gann_index* idx, const void* d_queries, uint32_t nq, uint
 int gann_stage_queries(gann_index* idx, const void* d_queries, uint32_t nq);
 int gann_search_staged(gann_index* idx, uint32_t k_out, uint32_t L, uint32_t k_gate, float eps,
                        uint32_t* d_ids, float* d_dists, void* stream);
+/* Serving form of gann_search (fast visited mode): everything is enqueued on
+ * `stream` and the call returns at once; results are in h_ids / h_dists
+ * (nq*k_out, pinned host memory for a truly asynchronous copy) when the
+ * stream has reached this point. All per-call device state lives in the
+ * caller's d_scratch (gann_search_async_scratch bytes), so calls on different
+ * streams may run concurrently: a batch's tail overlaps the next batch. The
+ * index itself is only read (synchronise those streams before
+ * gann_index_free). */
+uint64_t gann_search_async_scratch(const gann_index* idx, uint32_t nq, uint32_t k_out);
+int gann_search_async(gann_index* idx, const void* h_queries, uint32_t nq, uint32_t k_out,
+                      uint32_t L, uint32_t k_gate, float eps, uint32_t* h_ids, float* h_dists,
+                      void* d_scratch, uint64_t scratch_bytes, void* stream);
 
 /* ---- the build's internals, individually (parity + reuse) ------------------
  * alpha_prune: graphann::alpha_prune (include/graphann/prune.hpp:31-33,

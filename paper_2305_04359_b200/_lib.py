@@ -62,6 +62,8 @@ SIGNATURES = {
     "gann_search_device": (_i, [_vp, _vp, _u32, _u32, _u32, _u32, _f, _i, _vp, _vp, _vp, _vp, _vp]),
     "gann_stage_queries": (_i, [_vp, _vp, _u32]),
     "gann_search_staged": (_i, [_vp, _u32, _u32, _u32, _f, _vp, _vp, _vp]),
+    "gann_search_async_scratch": (_u64, [_vp, _u32, _u32]),
+    "gann_search_async": (_i, [_vp, _vp, _u32, _u32, _u32, _u32, _f, _vp, _vp, _vp, _u64, _vp]),
     "gann_alpha_prune": (_i, [_vp, _vp, _vp, _u32, _vp, _vp, _f, _i, _vp, _vp]),
     "gann_group_by_key": (_i, [_vp, _vp, _u64, _i, _vp, _vp, _vp, _vp]),
     "gann_choose_start": (_i, [_vp, _vp]),

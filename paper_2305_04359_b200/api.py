@@ -236,6 +236,18 @@ class Index:
         check(lib().gann_search_staged(self._h, k_out, params.beam, params.k, params.epsilon,
                                        C.c_void_p(ids_ptr), C.c_void_p(dists_ptr), C.c_void_p(stream or None)))
 
+    def async_scratch_bytes(self, nq: int, k_out: int) -> int:
+        return int(lib().gann_search_async_scratch(self._h, nq, k_out))
+
+    def search_async(self, h_queries_ptr: int, nq: int, params: SearchParams, k_out: int, h_ids_ptr: int,
+                     h_dists_ptr: int, scratch_ptr: int, scratch_bytes: int, stream: int) -> None:
+        """Enqueue a host-buffer search on `stream` (gann_search_async): the H2D
+        copy, the kernel and the D2H copy; returns at once. Calls on different
+        streams with their own scratch run concurrently."""
+        check(lib().gann_search_async(self._h, C.c_void_p(h_queries_ptr), nq, k_out, params.beam, params.k,
+                                      params.epsilon, C.c_void_p(h_ids_ptr), C.c_void_p(h_dists_ptr),
+                                      C.c_void_p(scratch_ptr), scratch_bytes, C.c_void_p(stream or None)))
+
     # -- build internals ------------------------------------------------------------
     def alpha_prune_many(self, points, candidate_ids, candidate_dists, params: PruneParams):
         """alpha_prune over many lists; returns a list of kept-id arrays."""

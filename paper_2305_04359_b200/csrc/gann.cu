@@ -16,6 +16,7 @@
 //   reprune (alpha_prune of the staged rows)
 // on one stream, with one host read-back per phase-2 step for grid sizes.
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -117,6 +118,8 @@ void hash_config(uint32_t L, uint64_t n, uint32_t* log2, uint32_t* bits) {
 
 }  // namespace
 
+constexpr uint32_t kQueryCounters = 64;  // per-launch query counters per index
+
 struct gann_index {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -135,6 +138,8 @@ struct gann_index {
   unsigned long long* stats = nullptr;  // kStCount
   unsigned long long* counters = nullptr;  // kCntNum
   uint32_t* flags = nullptr;  // [0] overflow, [1] too_long
+  uint32_t* qctr = nullptr;   // kQueryCounters per-launch query counters (round robin)
+  std::atomic<uint32_t> qslot{0};
   double build_ms[6] = {0, 0, 0, 0, 0, 0};
   uint64_t back_pairs = 0, back_groups = 0, back_pruned = 0;
   // scratch
@@ -202,6 +207,7 @@ gann_index* new_index(uint64_t n, uint32_t d, int elem, int metric, uint32_t R, 
     cu(cudaMalloc(&idx->stats, sizeof(unsigned long long) * kStCount), "cudaMalloc stats");
     cu(cudaMalloc(&idx->counters, sizeof(unsigned long long) * kCntNum), "cudaMalloc counters");
     cu(cudaMalloc(&idx->flags, 16), "cudaMalloc flags");
+    cu(cudaMalloc(&idx->qctr, kQueryCounters * 4), "cudaMalloc query counters");
     cu(cudaMemsetAsync(idx->points, 0, nn * idx->stride, idx->stream), "memset");
     cu(cudaMemsetAsync(idx->adj, 0xFF, rows * std::max<uint32_t>(R, 1) * 4, idx->stream), "memset");
     cu(cudaMemsetAsync(idx->tcount, 0, rows * 4, idx->stream), "memset");
@@ -267,7 +273,9 @@ SearchArgs base_search_args(gann_index* idx, uint32_t L, uint32_t k_gate, uint32
   a.dim = idx->d;
   a.row_bytes = idx->row_bytes;
   a.overflow = idx->flags;
-  a.next_query = idx->flags + 2;
+  // each launch pulls queries from its own counter: launches on different
+  // streams may run concurrently (up to kQueryCounters in flight)
+  a.next_query = idx->qctr + (idx->qslot.fetch_add(1) % kQueryCounters);
   a.stats = idx->stats;
   return a;
 }
@@ -697,7 +705,7 @@ void gann_index_free(gann_index* idx) {
   for (void* p : {static_cast<void*>(idx->points), static_cast<void*>(idx->adj),
                   static_cast<void*>(idx->tcount), static_cast<void*>(idx->tgroup),
                   static_cast<void*>(idx->stats), static_cast<void*>(idx->counters),
-                  static_cast<void*>(idx->flags)})
+                  static_cast<void*>(idx->flags), static_cast<void*>(idx->qctr)})
     if (p) cudaFree(p);
   for (DevBuf* b : {&idx->q, &idx->qids, &idx->qdists, &idx->qnvis, &idx->qdc, &idx->qvids,
                     &idx->qvd, &idx->qstart, &idx->table, &idx->order, &idx->vis_ids, &idx->vis_d,
@@ -995,6 +1003,50 @@ int gann_search_staged(gann_index* idx, uint32_t k_out, uint32_t L, uint32_t k_g
     a.out_ids = d_ids;
     a.out_dists = d_dists;
     cu(launch_search(a, idx->elem, idx->metric, idx->geom, s), "search kernel");
+  });
+}
+
+uint64_t gann_search_async_scratch(const gann_index* idx, uint32_t nq, uint32_t k_out) {
+  if (!idx) return 0;
+  // [counter 256 B][queries nq*stride][ids nq*k_out*4][dists nq*k_out*4]
+  return 256 + uint64_t(nq) * idx->stride + uint64_t(nq) * k_out * 8;
+}
+
+int gann_search_async(gann_index* idx, const void* h_queries, uint32_t nq, uint32_t k_out, uint32_t L,
+                      uint32_t k_gate, float eps, uint32_t* h_ids, float* h_dists, void* d_scratch,
+                      uint64_t scratch_bytes, void* stream) {
+  return guarded([&] {
+    if (!idx) fail(GANN_EINVAL, "index is NULL");
+    validate_search(idx, k_out, L, k_gate, eps, GANN_VISITED_FAST);
+    if (nq == 0) return;
+    if (idx->n == 0) fail(GANN_EINVAL, "search over an empty index");
+    if (!h_queries || !d_scratch || (k_out && (!h_ids || !h_dists))) fail(GANN_EINVAL, "NULL argument");
+    if (scratch_bytes < gann_search_async_scratch(idx, nq, k_out)) fail(GANN_EINVAL, "scratch too small");
+    set_device(idx);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : idx->stream;
+    uint8_t* base = static_cast<uint8_t*>(d_scratch);
+    uint8_t* dq = base + 256;
+    uint32_t* dids = reinterpret_cast<uint32_t*>(dq + uint64_t(nq) * idx->stride);
+    float* dd = reinterpret_cast<float*>(dids + uint64_t(nq) * k_out);
+    if (idx->stride == idx->row_bytes) {
+      cu(cudaMemcpyAsync(dq, h_queries, uint64_t(nq) * idx->stride, cudaMemcpyHostToDevice, s), "upload queries");
+    } else {
+      cu(cudaMemsetAsync(dq, 0, uint64_t(nq) * idx->stride, s), "memset");
+      cu(cudaMemcpy2DAsync(dq, idx->stride, h_queries, idx->row_bytes, idx->row_bytes, nq, cudaMemcpyHostToDevice, s),
+         "upload queries");
+    }
+    SearchArgs a = base_search_args(idx, L, k_gate, k_out, eps, GANN_VISITED_FAST);
+    a.next_query = reinterpret_cast<uint32_t*>(base);  // this call's own counter
+    a.stats = nullptr;  // concurrent calls do not touch the index
+    a.queries = dq;
+    a.nq = nq;
+    a.out_ids = k_out ? dids : nullptr;
+    a.out_dists = k_out ? dd : nullptr;
+    cu(launch_search(a, idx->elem, idx->metric, idx->geom, s), "search kernel");
+    if (k_out) {
+      cu(cudaMemcpyAsync(h_ids, dids, uint64_t(nq) * k_out * 4, cudaMemcpyDeviceToHost, s), "download ids");
+      cu(cudaMemcpyAsync(h_dists, dd, uint64_t(nq) * k_out * 4, cudaMemcpyDeviceToHost, s), "download dists");
+    }
   });
 }
 

@@ -246,3 +246,34 @@ def test_device_entry_matches_host_entry(oracle):
                       stream=torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     assert (ids.cpu().numpy().view(np.uint32) == host.ids).all()
+
+
+@pytest.mark.parametrize("dtype", [np.uint8, np.float32])
+def test_search_async_concurrent_streams_equal_sync(dtype):
+    """gann_search_async: batches enqueued on two streams (own scratch each,
+    overlapping kernels) return exactly what the blocking gann_search does."""
+    import torch
+    g = _g()
+    data, qs = mixture(71, 3000, 24, clusters=10, dtype=dtype, nq=700)
+    idx = g.build_diskann(data, "l2", g.DiskannParams(16, 32, 1.2))
+    sp = g.SearchParams(40, 10, 0.0)
+    want = idx.search(qs, sp)
+    qh = torch.from_numpy(np.ascontiguousarray(qs).view(np.uint8)).pin_memory()
+    nq, k = qs.shape[0], 10
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    nbytes = idx.async_scratch_bytes(nq, k)
+    scratch = [torch.empty(nbytes, dtype=torch.uint8, device="cuda") for _ in range(2)]
+    outs = [(torch.empty(nq * k, dtype=torch.int32).pin_memory(), torch.empty(nq * k, dtype=torch.float32).pin_memory())
+            for _ in range(4)]
+    for i, (oi, od) in enumerate(outs):
+        s = streams[i % 2]
+        idx.search_async(qh.data_ptr(), nq, sp, k, oi.data_ptr(), od.data_ptr(), scratch[i % 2].data_ptr(), nbytes,
+                         s.cuda_stream)
+    torch.cuda.synchronize()
+    for oi, od in outs:
+        assert (oi.numpy().view(np.uint32).reshape(nq, k) == want.ids).all()
+        assert (od.numpy().reshape(nq, k) == want.dists).all()
+    with pytest.raises(ValueError):
+        idx.search_async(qh.data_ptr(), nq, sp, k, outs[0][0].data_ptr(), outs[0][1].data_ptr(),
+                         scratch[0].data_ptr(), nbytes - 1, streams[0].cuda_stream)
+    idx.close()
