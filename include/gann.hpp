@@ -151,6 +151,16 @@ class Index {
     return out;
   }
 
+  // Serving form (gann_search_async): enqueue one batch on `stream` (a
+  // cudaStream_t) with caller scratch of search_async_scratch(nq, k) bytes;
+  // h_ids / h_dists (nq*k, pinned) are valid once the stream reaches it.
+  uint64_t search_async_scratch(uint32_t nq, uint32_t k) const { return gann_search_async_scratch(h_.get(), nq, k); }
+  void search_async(const void* h_queries, uint32_t nq, const SearchParams& p, uint32_t* h_ids, float* h_dists,
+                    void* d_scratch, uint64_t scratch_bytes, void* stream) const {
+    check(gann_search_async(h_.get(), h_queries, nq, p.k, p.beam, p.k, p.epsilon, h_ids, h_dists, d_scratch,
+                            scratch_bytes, stream));
+  }
+
   uint32_t choose_start() const {
     uint32_t s = 0;
     check(gann_choose_start(h_.get(), &s));
