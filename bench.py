@@ -43,6 +43,7 @@ sys.path.insert(0, str(ROOT))
 # BASELINE.json: "beam L swept 10..200"; --L-max widens it
 L_CANDIDATES = [10, 12, 14, 16, 20, 24, 28, 32, 40, 48, 56, 64, 80, 96, 128, 160, 200, 256, 320, 400, 512]
 GT_DEPTH = 16
+CFG_INDEX = {"c0": 0, "c1": 1, "c2": 2, "c3": 3, "c4": 4}  # BASELINE.json configs[i]
 
 
 def load_module(name, rel):
@@ -196,14 +197,13 @@ def setup(args):
         return distutil.reduce_scalar(x, op, dist if world > 1 else None, "cuda")
 
     # ---- data: generated straight into HBM ------------------------------------------
-    base = torch.empty(n * d, dtype=torch.uint8, device="cuda")
-    check(lib().gann_generate_u8(base.data_ptr(), n, d, cfg.clusters, cfg.sigma, cfg.noise_frac,
-                                 cfg.center_seed, cfg.base_seed, 0, dev))
-    qdev = torch.empty(nq * d, dtype=torch.uint8, device="cuda")
+    tdt = {"u8": torch.uint8, "i8": torch.int8, "f32": torch.float32}[cfg.dtype]
+    base = torch.empty(n * d, dtype=tdt, device="cuda")
+    check(datagen.generate_device(lib(), cfg, base.data_ptr(), n, queries=False, device=dev))
+    qdev = torch.empty(nq * d, dtype=tdt, device="cuda")
     row0, _ = distutil.query_rows(rank, nq)  # each rank searches its own query shard
-    check(lib().gann_generate_u8(qdev.data_ptr(), nq, d, cfg.clusters, cfg.sigma, cfg.noise_frac,
-                                 cfg.center_seed, cfg.query_seed, row0, dev))
-    idx = g.Index.from_device(base.data_ptr(), n, d, np.uint8, cfg.metric, cfg.R, dev)
+    check(datagen.generate_device(lib(), cfg, qdev.data_ptr(), nq, queries=True, row0=row0, device=dev))
+    idx = g.Index.from_device(base.data_ptr(), n, d, cfg.np_dtype, cfg.metric, cfg.R, dev)
 
     # ---- build (timed once) ---------------------------------------------------------------
     params = g.DiskannParams(cfg.R, cfg.L, cfg.alpha, seed=42, max_batch=cfg.max_batch)
@@ -214,7 +214,7 @@ def setup(args):
         # NCCL all-to-all-v of the reverse pairs), then every rank gathers the
         # full graph for its replica
         from paper_2305_04359_b200.partition import PartitionedIndex
-        pidx = PartitionedIndex(base.data_ptr(), cfg.metric, cfg.R, dist, device=dev, shape=(n, d), dtype=np.uint8)
+        pidx = PartitionedIndex(base.data_ptr(), cfg.metric, cfg.R, dist, device=dev, shape=(n, d), dtype=cfg.np_dtype)
         if pidx.peers_ok:
             barrier()
             t0 = time.perf_counter()
@@ -249,12 +249,15 @@ def setup(args):
     del adj_t
 
     # ---- ground truth (GPU brute force) and the beam giving recall >= target -----------------
-    gt_ids = torch.empty(nq * GT_DEPTH, dtype=torch.int32, device="cuda")
-    gt_d = torch.empty(nq * GT_DEPTH, dtype=torch.float32, device="cuda")
-    idx.groundtruth_device(qdev.data_ptr(), nq, GT_DEPTH, gt_ids.data_ptr(), gt_d.data_ptr())
-    torch.cuda.synchronize()
-    gt_ids_h = gt_ids.cpu().numpy().view(np.uint32).reshape(nq, GT_DEPTH)
-    gt_d_h = gt_d.cpu().numpy().reshape(nq, GT_DEPTH)
+    if d * cfg.elem_bytes <= 256:
+        gt_ids = torch.empty(nq * GT_DEPTH, dtype=torch.int32, device="cuda")
+        gt_d = torch.empty(nq * GT_DEPTH, dtype=torch.float32, device="cuda")
+        idx.groundtruth_device(qdev.data_ptr(), nq, GT_DEPTH, gt_ids.data_ptr(), gt_d.data_ptr())
+        torch.cuda.synchronize()
+        gt_ids_h = gt_ids.cpu().numpy().view(np.uint32).reshape(nq, GT_DEPTH)
+        gt_d_h = gt_d.cpu().numpy().reshape(nq, GT_DEPTH)
+    else:  # wide f32 rows (config 3): gann_groundtruth takes rows up to 256 B
+        gt_ids_h, gt_d_h = groundtruth_wide_f32(torch, base.view(n, d), qdev.view(nq, d), cfg.metric, GT_DEPTH)
     idx.stage_queries(qdev.data_ptr(), nq)
     out_ids = torch.empty(nq * k, dtype=torch.int32, device="cuda")
     out_d = torch.empty(nq * k, dtype=torch.float32, device="cuda")
@@ -301,7 +304,8 @@ def run_ours(args):
 
     # ---- timed search steps --------------------------------------------------------
     l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
-    index_bytes = n * (d + 4 * cfg.R)
+    s_el = cfg.elem_bytes
+    index_bytes = n * (d * s_el + 4 * cfg.R)
     flush = index_bytes < 2 * l2_bytes
     flush_buf = torch.empty(max(4 * l2_bytes, 1), dtype=torch.uint8, device="cuda") if flush else None
     nstreams = 1 if flush else max(1, args.streams)
@@ -351,7 +355,7 @@ def run_ours(args):
                       visited_mode="exact")
     torch.cuda.synchronize()
     xstats = idx.stats()
-    per_launch_bytes = search_bytes(xstats, d, nq, k)
+    per_launch_bytes = search_bytes(xstats, d * s_el, nq, k)
     # sustained time per launch: the K launches' elapsed time / K (with 2
     # streams a launch's own event span includes its overlap with neighbours)
     avg_launch_s = total_ms / args.steps / 1e3
@@ -364,7 +368,7 @@ def run_ours(args):
     # scratch; steps alternate over the same streams as above. The blocking
     # gann_search is timed too (e2e.blocking).
     import ctypes as C
-    qh = torch.empty((nq, d), dtype=torch.uint8).pin_memory()
+    qh = torch.empty((nq, d), dtype=qdev.dtype).pin_memory()
     qh.copy_(qdev.view(nq, d).cpu())
     hout = [(torch.empty((nq, k), dtype=torch.int32).pin_memory(), torch.empty((nq, k), dtype=torch.float32).pin_memory())
             for _ in range(nstreams)]
@@ -409,9 +413,9 @@ def run_ours(args):
     # ---- CPU baseline: the reference's beam_search over the same graph, rank 0 at N=1 ------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline_search(idx, base, qh.numpy(), chosen, k, args.cpu_seconds, out_ids, nq)
+        cpu = cpu_baseline_search(idx, base, qh.numpy(), chosen, k, args.cpu_seconds, out_ids, nq, cfg.metric)
 
-    build_bytes = search_bytes(dict(bstats, R=cfg.R), d, bstats["queries"], 0)
+    build_bytes = search_bytes(dict(bstats, R=cfg.R), d * s_el, bstats["queries"], 0)
     build_search_ms = bstats["build_ms"]["search"]
     line = {
         "metric": "search QPS at recall@10>=0.95 (Alg.1 beam {L,L,0}, top-10) over a B200-built Vamana graph",
@@ -424,11 +428,11 @@ def run_ours(args):
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "u8",
+        "dtype": cfg.dtype,
         "data": "synthetic: seeded Gaussian mixture with BASELINE config shapes (datagen.py), generated in HBM",
         "config": {
-            "workload": f"BASELINE configs[1]: {cfg.name}",
-            "n": n, "d": d, "R": cfg.R, "L_build": cfg.L, "alpha": cfg.alpha,
+            "workload": f"BASELINE configs[{CFG_INDEX.get(args.config, '?')}]: {cfg.name}",
+            "n": n, "d": d, "metric": cfg.metric, "R": cfg.R, "L_build": cfg.L, "alpha": cfg.alpha,
             "max_batch": cfg.max_batch, "queries_per_gpu": nq, "k": k,
             "L_search": chosen, "recall@10": recall, "target_recall": args.target_recall,
             "target_reached_in_sweep": target_reached,
@@ -447,6 +451,8 @@ def run_ours(args):
                                 else "mean of the launches' own event spans"),
             "launch_event_span_ms_mean": round(statistics.mean(step_ms), 4),
             "outputs_agree_across_streams": outs_agree,
+            "note": ("algorithmic bytes count each query's rows; rows shared across queries (hubs) are served "
+                     "from the 126 MB L2, so achieved can exceed the HBM peak" if achieved > peak else None),
             "traffic": traffic_from_profile(cfg.name, chosen),
             "distinct_evals_per_query": round(xstats["evaluations"] / nq, 1),
             "evals_per_query_fast_filter": round(sstats["evaluations"] / (nq * args.steps), 1),
@@ -454,7 +460,7 @@ def run_ours(args):
         },
         "cpu_baseline": cpu,
         "e2e": {"value": round(world * nq * args.steps / e2e_s, 1), "unit": "queries/s",
-                "h2d_bytes_per_step": nq * d, "d2h_bytes_per_step": nq * k * 8,
+                "h2d_bytes_per_step": nq * d * s_el, "d2h_bytes_per_step": nq * k * 8,
                 "api": f"gann_search_async on {nstreams} stream(s) (pinned host buffers, H2D + search + D2H per step)",
                 "ids_match_device_path": e2e_match,
                 "blocking": {"value": round(world * nq * args.steps / e2e_block_s, 1),
@@ -465,8 +471,10 @@ def run_ours(args):
             "points_per_s": round(n / build_s, 1), "seconds": round(build_s, 3), "mode": build_mode,
             "phases_ms": {kk: round(v, 1) for kk, v in bstats["build_ms"].items()},
             "mean_degree": round(deg_mean, 3), "replicas_identical": replicas_identical,
-            "search_roofline": {"achieved": round(build_bytes / (build_search_ms / 1e3) / 1e9, 1) if build_search_ms else None,
-                                "unit": "GB/s", "frac": round(build_bytes / (build_search_ms / 1e3) / 1e9 / peak, 4) if build_search_ms else None},
+            "search_gather_rate": {
+                "value": round(build_bytes / (build_search_ms / 1e3) / 1e9, 1) if build_search_ms else None, "unit": "GB/s",
+                "basis": "fast-mode evaluations x row bytes + adjacency rows, / the build's search time; "
+                         "re-evaluations are partly L2 hits, so this is a gather rate, not DRAM bandwidth"},
             "stats": {kk: v for kk, v in bstats.items() if kk != "build_ms"},
         },
         "recall_curve": curve,
@@ -488,14 +496,48 @@ def _tensor_from_ptr(ptr, nbytes):
     return torch.as_tensor(_Holder(ptr, nbytes), device="cuda")
 
 
-def cpu_baseline_search(idx, base, q_host, L, k, seconds, out_ids, nq):
+def groundtruth_wide_f32(torch, X, Q, metric, depth, pre=64, chunk=200_000):
+    """compute_groundtruth (src/dataset.cpp:172-217) for wide f32 rows, setup
+    only: an fp32 GEMM (TF32 off) keeps the best `pre` candidates per query,
+    then those are re-scored in the reference's order (sequential over the
+    dimensions, each multiply and add rounded separately: src/metric.cpp:38-59)
+    and sorted by (dist, id). A true top-`depth` id would have to lose more
+    than `pre - depth` places to GEMM rounding to be missed."""
+    torch.backends.cuda.matmul.allow_tf32 = False
+    nq, n = Q.shape[0], X.shape[0]
+    best_s = torch.full((nq, pre), float("inf"), device="cuda")
+    best_i = torch.zeros((nq, pre), dtype=torch.int64, device="cuda")
+    qn = (Q * Q).sum(1, keepdim=True)
+    for p0 in range(0, n, chunk):
+        xc = X[p0:p0 + chunk]
+        sc = -(Q @ xc.T) if metric == "ip" else qn + (xc * xc).sum(1)[None, :] - 2.0 * (Q @ xc.T)
+        vals, ids = torch.topk(sc, min(pre, sc.shape[1]), dim=1, largest=False)
+        cat_s = torch.cat([best_s, vals], 1)
+        cat_i = torch.cat([best_i, ids + p0], 1)
+        sel = torch.topk(cat_s, pre, dim=1, largest=False).indices
+        best_s, best_i = torch.gather(cat_s, 1, sel), torch.gather(cat_i, 1, sel)
+    cand = X[best_i]  # (nq, pre, d)
+    acc = torch.zeros((nq, pre), device="cuda")
+    for j in range(Q.shape[1]):  # elementwise ops round separately: mul, then add
+        if metric == "ip":
+            acc = acc + Q[:, j:j + 1] * cand[:, :, j]
+        else:
+            diff = Q[:, j:j + 1] - cand[:, :, j]
+            acc = acc + diff * diff
+    dist_ = -acc if metric == "ip" else acc
+    dh, ih = dist_.cpu().numpy(), best_i.cpu().numpy()
+    order = np.lexsort((ih, dh), axis=1)[:, :depth]
+    return (np.take_along_axis(ih, order, 1).astype(np.uint32), np.take_along_axis(dh, order, 1).astype(np.float32))
+
+
+def cpu_baseline_search(idx, base, q_host, L, k, seconds, out_ids, nq, metric="l2"):
     from oracle.oracle import Oracle, available
     kind = "reference" if available("ref") else "port"
     orc = Oracle("ref" if kind == "reference" else "orc")
     adj, _, start = idx.export_graph()
     data = base.view(idx.n, idx.d).cpu().numpy()
-    secs, ids, reps = orc.time_search(adj, start, data, q_host, L, L, 0.0, k_out=k, workers=0, reps=1,
-                                      min_seconds=seconds)
+    secs, ids, reps = orc.time_search(adj, start, data, q_host, L, L, 0.0, k_out=k, metric=metric, workers=0,
+                                      reps=1, min_seconds=seconds)
     gpu_ids = out_ids.cpu().numpy().view(np.uint32).reshape(nq, k)
     cores = os.cpu_count()
     return {"value": round(nq / secs, 1), "unit": "queries/s", "cores": cores, "kind": kind,
@@ -530,10 +572,11 @@ def run_reference(args):
     cores = os.cpu_count()
     # one graphann pass per step (warm-up passes untimed)
     for _ in range(args.warmup):
-        orc.time_search(adj, start, data, q, chosen, chosen, 0.0, k_out=k, workers=0, reps=1)
+        orc.time_search(adj, start, data, q, chosen, chosen, 0.0, k_out=k, metric=cfg.metric, workers=0, reps=1)
     secs, ids = [], None
     for _ in range(args.steps):
-        sec, ids, _ = orc.time_search(adj, start, data, q, chosen, chosen, 0.0, k_out=k, workers=0, reps=1)
+        sec, ids, _ = orc.time_search(adj, start, data, q, chosen, chosen, 0.0, k_out=k, metric=cfg.metric, workers=0,
+                                      reps=1)
         secs.append(sec)
     value = nq * args.steps / sum(secs)
     # the reference's build speed on a bounded prefix (host cores)
@@ -541,7 +584,7 @@ def run_reference(args):
     pref = data[:nb]
     cap = int(nb * cfg.batch_cap_frac) if cfg.batch_cap_frac else 0
     t0 = time.perf_counter()
-    orc.build(pref, cfg.R, cfg.L, cfg.alpha, cap=cap, workers=0)
+    orc.build(pref, cfg.R, cfg.L, cfg.alpha, metric=cfg.metric, cap=cap, workers=0)
     build_s = time.perf_counter() - t0
     sample = (f"graphann beam_search {{L={chosen},L,0}} top-{k}, one pass over all {nq} queries per step, over the "
               f"same {idx.n}-point index as our arm (built by our GPU build, bit-identical to graphann's for u8), "
@@ -551,9 +594,10 @@ def run_reference(args):
         "metric": "search QPS at recall@10>=0.95 (Alg.1 beam {L,L,0}, top-10) over a B200-built Vamana graph",
         "value": round(value, 1), "unit": "queries/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(1e3 * sum(secs) / args.steps, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "scaling": "weak", "vs_baseline": None, "dtype": cfg.dtype,
         "data": "synthetic: seeded Gaussian mixture with BASELINE config shapes (datagen.py)",
-        "config": {"workload": f"BASELINE configs[1]: {cfg.name}", "n": idx.n, "d": idx.d, "R": cfg.R,
+        "config": {"workload": f"BASELINE configs[{CFG_INDEX.get(args.config, '?')}]: {cfg.name}", "n": idx.n,
+                   "d": idx.d, "metric": cfg.metric, "R": cfg.R,
                    "L_build": cfg.L, "alpha": cfg.alpha, "max_batch": cfg.max_batch, "queries": nq, "k": k,
                    "L_search": chosen, "recall@10": S["recall"]},
         "cpu_baseline": {"value": round(value, 1), "unit": "queries/s", "cores": cores, "kind": kind,

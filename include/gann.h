@@ -202,6 +202,14 @@ int gann_groundtruth_device(gann_index* idx, const void* d_queries, uint32_t nq,
 int gann_generate_u8(void* d_out, uint64_t n, uint32_t d, uint32_t clusters, float sigma,
                      float noise_frac, uint64_t center_seed, uint64_t stream_seed, uint64_t row0,
                      int device);
+/* Seeded synthetic f32 rows (BASELINE config 3, TTI-like): a `clusters`-
+ * component mixture, v = c + sigma z (c, z ~ Irwin-Hall(4) normals), scaled
+ * to norm exp(norm_sigma g) (log-normal per-point norms); shift > 0 moves
+ * every centre by shift * N(0, 1) (the out-of-distribution query set).
+ * Computed in double, rounded to f32 once. */
+int gann_generate_f32(void* d_out, uint64_t n, uint32_t d, uint32_t clusters, float sigma,
+                      float norm_sigma, float shift, uint64_t center_seed, uint64_t stream_seed,
+                      uint64_t row0, int device);
 
 /* ---- vertex-partitioned build (BASELINE config 4) -----------
  * One index per GPU (one process per GPU). Every index holds all points;

@@ -1269,6 +1269,18 @@ int gann_generate_u8(void* d_out, uint64_t n, uint32_t d, uint32_t clusters, flo
   });
 }
 
+int gann_generate_f32(void* d_out, uint64_t n, uint32_t d, uint32_t clusters, float sigma, float norm_sigma,
+                      float shift, uint64_t center_seed, uint64_t stream_seed, uint64_t row0, int device) {
+  return guarded([&] {
+    if (clusters == 0 || d == 0) fail(GANN_EINVAL, "gen: d and clusters must be positive");
+    cu(cudaSetDevice(device), "cudaSetDevice");
+    cu(launch_generate_f32(static_cast<float*>(d_out), n, d, clusters, sigma, norm_sigma, shift, center_seed,
+                           stream_seed, row0, nullptr),
+       "generate");
+    cu(cudaDeviceSynchronize(), "generate sync");
+  });
+}
+
 void gann_shuffled_order(uint32_t n, uint64_t seed, uint32_t front, uint32_t* out) {
   std::vector<uint32_t> order(n);
   for (uint32_t i = 0; i < n; i++) order[i] = i;

@@ -175,6 +175,9 @@ cudaError_t part_pairs_scatter(const uint32_t* adj_local, uint32_t base, uint32_
 cudaError_t launch_choose_start(const uint8_t* data, uint64_t stride, uint64_t n, uint32_t d,
                                 int elem, int metric, double* colsum, float* centroid,
                                 unsigned long long* best, cudaStream_t s);
+cudaError_t launch_generate_f32(float* out, uint64_t n, uint32_t d, uint32_t clusters, float sigma,
+                                float norm_sigma, float shift, uint64_t center_seed, uint64_t stream_seed,
+                                uint64_t row0, cudaStream_t s);
 cudaError_t launch_generate_u8(uint8_t* out, uint64_t out_stride, uint64_t n, uint32_t d,
                                uint32_t clusters, float sigma, float noise_frac,
                                uint64_t center_seed, uint64_t stream_seed, uint64_t row0,

@@ -105,6 +105,43 @@ __global__ void gen_u8_kernel(uint8_t* out, uint64_t out_stride, uint64_t n, uin
   }
 }
 
+// f32 mixture rows (config 3): one warp per row. Normals are Irwin-Hall(4)
+// over 16-bit uniforms (integer exact), the rest is double arithmetic, one
+// rounding to f32 at the end (datagen.gen_f32_numpy restates it).
+constexpr uint64_t kKShift = 0x8CB92BA72F3D8DD7ull;
+constexpr uint64_t kKNorm = 0x3C6EF372FE94F82Bull;
+
+__device__ __forceinline__ double ih_normal(uint64_t h) {
+  const int s = static_cast<int>((h & 0xFFFF) + ((h >> 16) & 0xFFFF) + ((h >> 32) & 0xFFFF) + ((h >> 48) & 0xFFFF)) -
+                131070;
+  return static_cast<double>(s) / 37837.22269;
+}
+
+__global__ void gen_f32_kernel(float* out, uint64_t n, uint32_t d, uint32_t clusters, double sigma,
+                               double norm_sigma, double shift, uint64_t cseed, uint64_t sseed, uint64_t row0) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x >> 5);
+  for (uint64_t i = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {
+    const uint64_t r = row0 + i;
+    const uint64_t c = mix64(sseed ^ kKCluster, r) % clusters;
+    double ss = 0.0;
+    for (uint32_t j = lane; j < d; j += 32) {
+      double v = ih_normal(mix64(cseed ^ kKCenter, c * d + j));
+      if (shift > 0.0) v += shift * ih_normal(mix64(cseed ^ kKShift, c * d + j));
+      v += sigma * ih_normal(mix64(sseed ^ kKNormal, r * d + j));
+      ss += v * v;
+    }
+    for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xFFFFFFFFu, ss, o);
+    const double scale = exp(norm_sigma * ih_normal(mix64(sseed ^ kKNorm, r))) / sqrt(ss);
+    for (uint32_t j = lane; j < d; j += 32) {
+      double v = ih_normal(mix64(cseed ^ kKCenter, c * d + j));
+      if (shift > 0.0) v += shift * ih_normal(mix64(cseed ^ kKShift, c * d + j));
+      v += sigma * ih_normal(mix64(sseed ^ kKNormal, r * d + j));
+      out[i * d + j] = static_cast<float>(v * scale);
+    }
+  }
+}
+
 // ---- brute-force ground truth ---------------------------------------------
 // compute_groundtruth (src/dataset.cpp:172-217): exact top-k by (dist, id).
 // One thread per query (its row in registers), a shared-memory tile of points
@@ -254,6 +291,15 @@ cudaError_t launch_generate_u8(uint8_t* out, uint64_t out_stride, uint64_t n, ui
   const uint32_t thr = static_cast<uint32_t>(static_cast<double>(noise_frac) * 16777216.0);
   gen_u8_kernel<<<148 * 16, 256, 0, s>>>(out, out_stride, n, d, clusters, sigma, thr, center_seed,
                                          stream_seed, row0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_generate_f32(float* out, uint64_t n, uint32_t d, uint32_t clusters, float sigma,
+                                float norm_sigma, float shift, uint64_t center_seed, uint64_t stream_seed,
+                                uint64_t row0, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  gen_f32_kernel<<<148 * 16, 256, 0, s>>>(out, n, d, clusters, sigma, norm_sigma, shift, center_seed, stream_seed,
+                                          row0);
   return cudaGetLastError();
 }
 

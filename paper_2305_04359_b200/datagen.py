@@ -23,6 +23,8 @@ K_CLUSTER = np.uint64(0x2545F4914F6CDD1D)
 K_NOISE_ROW = np.uint64(0x9E3779B97F4A7C15)
 K_UNIFORM = np.uint64(0xD6E8FEB86659FD93)
 K_NORMAL = np.uint64(0xA0761D6478BD642F)
+K_SHIFT = np.uint64(0x8CB92BA72F3D8DD7)
+K_NORM = np.uint64(0x3C6EF372FE94F82B)
 
 
 def mix64(x):
@@ -59,6 +61,29 @@ def gen_u8_numpy(n, d, clusters, sigma, noise_frac, center_seed, stream_seed, ro
     return np.where(noise_row, uni, v)
 
 
+def _ih_normal(h):
+    """Irwin-Hall(4) over the four 16-bit fields of h, unit variance (float64)."""
+    s = ((h & np.uint64(0xFFFF)) + ((h >> np.uint64(16)) & np.uint64(0xFFFF)) +
+         ((h >> np.uint64(32)) & np.uint64(0xFFFF)) + ((h >> np.uint64(48)) & np.uint64(0xFFFF))).astype(np.int64)
+    return (s - 131070).astype(np.float64) / 37837.22269
+
+
+def gen_f32_numpy(n, d, clusters, sigma, norm_sigma, shift, center_seed, stream_seed, row0=0):
+    """Host restatement of ``gen_f32_kernel`` (csrc/misc.cu): double arithmetic,
+    one rounding to f32 (the device's warp-order sum of squares may differ in
+    the last double bit, so compare with a ~1e-6 relative tolerance)."""
+    r = np.arange(row0, row0 + n, dtype=np.uint64)[:, None]
+    j = np.arange(d, dtype=np.uint64)[None, :]
+    c = mix64_2(np.uint64(stream_seed) ^ K_CLUSTER, r) % np.uint64(clusters)
+    v = _ih_normal(mix64_2(np.uint64(center_seed) ^ K_CENTER, c * np.uint64(d) + j))
+    if shift > 0:
+        v = v + float(np.float32(shift)) * _ih_normal(mix64_2(np.uint64(center_seed) ^ K_SHIFT, c * np.uint64(d) + j))
+    v = v + float(np.float32(sigma)) * _ih_normal(mix64_2(np.uint64(stream_seed) ^ K_NORMAL, r * np.uint64(d) + j))
+    g = _ih_normal(mix64_2(np.uint64(stream_seed) ^ K_NORM, r))
+    scale = np.exp(float(np.float32(norm_sigma)) * g) / np.sqrt((v * v).sum(axis=1, keepdims=True))
+    return (v * scale).astype(np.float32)
+
+
 @dataclass(frozen=True)
 class Config:
     """One BASELINE.json config as a synthetic workload."""
@@ -79,6 +104,16 @@ class Config:
     center_seed: int = 1
     base_seed: int = 2
     query_seed: int = 3
+    norm_sigma: float = 0.0   # f32 configs: log-normal sigma of the per-point norms
+    query_shift: float = 0.0  # f32 configs: queries from centres shifted by N(0, shift^2)
+
+    @property
+    def np_dtype(self):
+        return {"u8": np.uint8, "i8": np.int8, "f32": np.float32}[self.dtype]
+
+    @property
+    def elem_bytes(self) -> int:
+        return np.dtype(self.np_dtype).itemsize
 
     @property
     def max_batch(self) -> int:
@@ -96,6 +131,11 @@ CONFIGS = {
     "c1": Config("c1-10M-u8-d128", 10_000_000, 128, "u8", "l2", 1000, 20.0, 0.0, 64, 128, 1.2, 0.02),
     # configs[2]: 10M x 256 u8, 5000 clusters, sigma 12, 10% uniform noise points
     "c2": Config("c2-10M-u8-d256", 10_000_000, 256, "u8", "l2", 5000, 12.0, 0.10, 64, 128, 1.2, 0.02),
+    # configs[3]: 10M x 200 f32, negative inner product, 2000-component mixture,
+    # log-normal(0, 0.3) per-point norms, out-of-distribution queries (centres
+    # shifted by N(0, 0.5)), alpha 1.0 (TTI-like)
+    "c3": Config("c3-10M-f32-d200-ip", 10_000_000, 200, "f32", "ip", 2000, 0.5, 0.0, 64, 128, 1.0, 0.02,
+                 norm_sigma=0.3, query_shift=0.5),
     # configs[4]: 1B x 128 u8 with 100k clusters (multi-GPU build; not runnable on one GPU)
     "c4": Config("c4-1B-u8-d128", 1_000_000_000, 128, "u8", "l2", 100_000, 20.0, 0.0, 64, 128, 1.2, 0.02),
 }
@@ -104,9 +144,26 @@ CONFIGS = {
 def host_base(cfg: Config, n: int | None = None) -> np.ndarray:
     """Base points [0, n) of a config on the host (numpy restatement)."""
     n = cfg.n if n is None else n
+    if cfg.dtype == "f32":
+        return gen_f32_numpy(n, cfg.d, cfg.clusters, cfg.sigma, cfg.norm_sigma, 0.0, cfg.center_seed, cfg.base_seed)
     return gen_u8_numpy(n, cfg.d, cfg.clusters, cfg.sigma, cfg.noise_frac, cfg.center_seed, cfg.base_seed)
 
 
 def host_queries(cfg: Config, nq: int | None = None) -> np.ndarray:
     nq = cfg.n_queries if nq is None else nq
+    if cfg.dtype == "f32":
+        return gen_f32_numpy(nq, cfg.d, cfg.clusters, cfg.sigma, cfg.norm_sigma, cfg.query_shift, cfg.center_seed,
+                             cfg.query_seed)
     return gen_u8_numpy(nq, cfg.d, cfg.clusters, cfg.sigma, cfg.noise_frac, cfg.center_seed, cfg.query_seed)
+
+
+def generate_device(lib, cfg: Config, ptr: int, n: int, queries: bool, row0: int = 0, device: int = 0) -> int:
+    """Rows [row0, row0+n) of a config's base (or query) stream straight into
+    device memory at ptr (gann_generate_u8 / gann_generate_f32). Returns the C
+    status code."""
+    seed = cfg.query_seed if queries else cfg.base_seed
+    if cfg.dtype == "f32":
+        return lib.gann_generate_f32(ptr, n, cfg.d, cfg.clusters, cfg.sigma, cfg.norm_sigma,
+                                     cfg.query_shift if queries else 0.0, cfg.center_seed, seed, row0, device)
+    return lib.gann_generate_u8(ptr, n, cfg.d, cfg.clusters, cfg.sigma, cfg.noise_frac, cfg.center_seed, seed, row0,
+                                device)

@@ -324,6 +324,22 @@ def test_generator_matches_numpy_restatement():
         assert (buf.cpu().numpy().reshape(n, d) == want).all()
 
 
+def test_f32_generator_matches_numpy_restatement():
+    """Config 3's generator: device rows equal the float64 restatement after
+    the one f32 rounding (tolerance: the warp-order sum of squares)."""
+    torch = pytest.importorskip("torch")
+    from paper_2305_04359_b200 import datagen
+    from paper_2305_04359_b200._lib import check, lib
+    for (n, d, cl, sig, ns, sh) in [(3000, 200, 2000, 0.5, 0.3, 0.0), (1000, 200, 2000, 0.5, 0.3, 0.5),
+                                    (500, 37, 7, 1.0, 0.0, 0.0)]:
+        buf = torch.empty(n * d, dtype=torch.float32, device="cuda")
+        check(lib().gann_generate_f32(buf.data_ptr(), n, d, cl, sig, ns, sh, 1, 2, 700, 0))
+        want = datagen.gen_f32_numpy(n, d, cl, sig, ns, sh, 1, 2, row0=700)
+        got = buf.cpu().numpy().reshape(n, d)
+        np.testing.assert_allclose(got, want, rtol=2e-6, atol=1e-7)
+        assert (got == want).mean() > 0.99
+
+
 def test_cpp_dropin_runs():
     """The reference's hand instances through include/gann.hpp (C++)."""
     import subprocess

@@ -84,6 +84,29 @@ def test_datagen_matches_config_distribution():
     assert y.shape == (20000, 16)
 
 
+def test_f32_datagen_config3_shape():
+    """Config 3 (TTI-like): per-point norms log-normal(0, 0.3); queries from
+    shifted centres are out of distribution (farther from their cluster)."""
+    from paper_2305_04359_b200 import datagen
+    cfg = datagen.CONFIGS["c3"].scaled(3000, 2000)
+    x = datagen.host_base(cfg)
+    q = datagen.host_queries(cfg)
+    assert x.dtype == np.float32 and x.shape == (3000, 200) and q.shape == (2000, 200)
+    ln = np.log(np.linalg.norm(x.astype(np.float64), axis=1))
+    assert abs(ln.mean()) < 0.03 and abs(ln.std() - 0.3) < 0.03
+    assert (datagen.gen_f32_numpy(100, 200, 2000, 0.5, 0.3, 0.0, 1, 2, row0=50) == x[50:150]).all()
+    # the cosine to the unshifted centre is lower for the shifted (query) stream
+    from paper_2305_04359_b200.datagen import K_CENTER, K_CLUSTER, _ih_normal, mix64_2
+
+    def cos_to_centre(rows, seed):
+        r = np.arange(len(rows), dtype=np.uint64)[:, None]
+        c = mix64_2(np.uint64(seed) ^ K_CLUSTER, r) % np.uint64(2000)
+        cen = _ih_normal(mix64_2(np.uint64(1) ^ K_CENTER, c * np.uint64(200) + np.arange(200, dtype=np.uint64)[None, :]))
+        return (rows * cen).sum(1) / np.linalg.norm(rows, axis=1) / np.linalg.norm(cen, axis=1)
+
+    assert cos_to_centre(q.astype(np.float64), cfg.query_seed).mean() < cos_to_centre(x.astype(np.float64)[:2000], cfg.base_seed).mean() - 0.02
+
+
 def test_recall_tie_rule():
     """recall_k_at_n tie rule (reference src/eval.cpp:14-33, tests/test_eval.cpp:12-38)."""
     from paper_2305_04359_b200.evalutil import recall_at_k
