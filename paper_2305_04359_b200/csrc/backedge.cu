@@ -181,6 +181,26 @@ __global__ void __launch_bounds__(NT)
   const int tid = threadIdx.x;
   const uint32_t R = a.R;
   const uint32_t nch = static_cast<uint32_t>(a.stride >> 4);
+  // re-prune list slots: one warp collects up to 32 group ids and claims
+  // their slots with one atomic (a per-group atomic on one counter serialises
+  // millions of operations per batch in L2)
+  uint32_t pend = 0, npend = 0;
+  auto flush_small = [&]() {
+    unsigned long long base = 0;
+    if (tid == 0) base = atomicAdd(a.counters + kCntPruneSmall, static_cast<unsigned long long>(npend));
+    base = __shfl_sync(0xFFFFFFFFu, base, 0);
+    if (static_cast<uint32_t>(tid) < npend) a.plist_small[base + tid] = pend;
+    npend = 0;
+  };
+  auto push_small = [&](uint32_t gg) {
+    if (NT == 32) {
+      if (static_cast<uint32_t>(tid) == npend) pend = gg;
+      if (++npend == 32) flush_small();
+    } else if (tid == 0) {
+      const uint32_t i = static_cast<uint32_t>(atomicAdd(a.counters + kCntPruneSmall, 1ull));
+      a.plist_small[i] = gg;
+    }
+  };
 
   for (uint32_t gi = blockIdx.x; gi < count; gi += gridDim.x) {
     const uint32_t g = glist ? glist[gi] : gi;
@@ -192,59 +212,95 @@ __global__ void __launch_bounds__(NT)
     }
     const uint32_t t = a.gtarget[g];
     const uint64_t go = a.goff[g];
-    uint32_t Mp = 32;
-    while (Mp < c) Mp <<= 1;
-    for (uint32_t i = tid; i < Mp; i += NT) ord[i] = i < c ? a.gsrc[go + i] : 0xFFFFFFFFu;
-    cta_sync<NT>();
-    cta_sort_u32<NT>(ord, Mp);  // input order inside the group (semisort.cpp:58-63)
-    if (MODE == 1) {
-      const uint32_t key = a.key_of_target ? a.key_of_target[t] : t;
-      for (uint32_t i = tid; i < c; i += NT) {
-        out_keys[go + i] = key;
-        out_vals[go + i] = pair_source(a, ord[i]);
+    uint32_t* trow = a.adj + uint64_t(t - a.base) * R;
+    uint32_t* pid = a.pid + a.poff[g];
+    uint32_t nm;
+    if (NT == 32 && c <= 32 && R <= 64) {
+      // one warp, registers: rank-sort the ordinals (distinct), the row as two
+      // ids per lane, each source tested against the row with one ballot
+      const int lane = tid;
+      const uint32_t FULL = 0xFFFFFFFFu;
+      const uint32_t o = static_cast<uint32_t>(lane) < c ? a.gsrc[go + lane] : 0xFFFFFFFFu;
+      uint32_t rk = 0;
+      for (uint32_t j = 0; j < c; j++) rk += __shfl_sync(FULL, o, j) < o ? 1u : 0u;
+      if (static_cast<uint32_t>(lane) < c) ord[rk] = o;  // input order inside the group (semisort.cpp:58-63)
+      __syncwarp();
+      if (MODE == 1) {
+        const uint32_t key = a.key_of_target ? a.key_of_target[t] : t;
+        if (static_cast<uint32_t>(lane) < c) {
+          out_keys[go + lane] = key;
+          out_vals[go + lane] = pair_source(a, ord[lane]);
+        }
+        __syncwarp();
+        if (lane == 0) a.tcount[t - a.base] = 0;
+        continue;
+      }
+      const uint32_t src = static_cast<uint32_t>(lane) < c ? pair_source(a, ord[lane]) : kNone;
+      const uint32_t r0 = static_cast<uint32_t>(lane) < R ? trow[lane] : kNone;
+      const uint32_t r1 = static_cast<uint32_t>(lane) + 32 < R ? trow[lane + 32] : kNone;
+      const uint32_t deg = __popc(__ballot_sync(FULL, r0 != kNone)) + __popc(__ballot_sync(FULL, r1 != kNone));
+      // first occurrence wins (builder_common.cpp:124-128)
+      uint32_t keepmask = 0;
+      for (uint32_t i = 0; i < c; i++) {
+        const uint32_t si = __shfl_sync(FULL, src, i);
+        bool dup = __ballot_sync(FULL, r0 == si || r1 == si) != 0;
+        if (!a.sources_distinct) dup = dup || __ballot_sync(FULL, static_cast<uint32_t>(lane) < i && src == si) != 0;
+        keepmask |= dup ? 0u : (1u << i);
+      }
+      if (static_cast<uint32_t>(lane) < deg) pid[lane] = r0;
+      if (static_cast<uint32_t>(lane) + 32 < deg) pid[lane + 32] = r1;
+      if ((keepmask >> lane) & 1u) pid[deg + __popc(keepmask & ((1u << lane) - 1u))] = src;
+      nm = deg + __popc(keepmask);
+      __syncwarp();
+    } else {
+      uint32_t Mp = 32;
+      while (Mp < c) Mp <<= 1;
+      for (uint32_t i = tid; i < Mp; i += NT) ord[i] = i < c ? a.gsrc[go + i] : 0xFFFFFFFFu;
+      cta_sync<NT>();
+      cta_sort_u32<NT>(ord, Mp);  // input order inside the group (semisort.cpp:58-63)
+      if (MODE == 1) {
+        const uint32_t key = a.key_of_target ? a.key_of_target[t] : t;
+        for (uint32_t i = tid; i < c; i += NT) {
+          out_keys[go + i] = key;
+          out_vals[go + i] = pair_source(a, ord[i]);
+        }
+        cta_sync<NT>();
+        if (tid == 0) a.tcount[t - a.base] = 0;
+        continue;
+      }
+      for (uint32_t i = tid; i < c; i += NT) ord[i] = pair_source(a, ord[i]);
+      if (tid == 0) sh_deg = 0;
+      cta_sync<NT>();
+      for (uint32_t i = tid; i < R; i += NT) {
+        const uint32_t v = trow[i];
+        row[i] = v;
+        if (v != kNone) atomicAdd(&sh_deg, 1u);
       }
       cta_sync<NT>();
-      if (tid == 0) a.tcount[t - a.base] = 0;
-      continue;
+      const uint32_t deg = sh_deg;
+      // first occurrence wins (builder_common.cpp:124-128)
+      for (uint32_t i = tid; i < c; i += NT) {
+        const uint32_t s = ord[i];
+        bool keep = true;
+        for (uint32_t j = 0; j < deg && keep; j++) keep = row[j] != s;
+        if (!a.sources_distinct)
+          for (uint32_t j = 0; j < i && keep; j++) keep = ord[j] != s;
+        kf[i] = keep ? 1 : 0;
+      }
+      cta_sync<NT>();
+      for (uint32_t i = tid; i < deg; i += NT) pid[i] = row[i];
+      const uint32_t kept = cta_stable_ranks<NT>(kf, c, warp_tot, [&](uint32_t i, uint32_t r) {
+        pid[deg + r] = ord[i];
+      });
+      nm = deg + kept;
+      cta_sync<NT>();
     }
-    for (uint32_t i = tid; i < c; i += NT) ord[i] = pair_source(a, ord[i]);
-    if (tid == 0) sh_deg = 0;
-    cta_sync<NT>();
-    uint32_t* trow = a.adj + uint64_t(t - a.base) * R;
-    for (uint32_t i = tid; i < R; i += NT) {
-      const uint32_t v = trow[i];
-      row[i] = v;
-      if (v != kNone) atomicAdd(&sh_deg, 1u);
-    }
-    cta_sync<NT>();
-    const uint32_t deg = sh_deg;
-    // first occurrence wins (builder_common.cpp:124-128)
-    for (uint32_t i = tid; i < c; i += NT) {
-      const uint32_t s = ord[i];
-      bool keep = true;
-      for (uint32_t j = 0; j < deg && keep; j++) keep = row[j] != s;
-      if (!a.sources_distinct)
-        for (uint32_t j = 0; j < i && keep; j++) keep = ord[j] != s;
-      kf[i] = keep ? 1 : 0;
-    }
-    cta_sync<NT>();
-    uint32_t* pid = a.pid + a.poff[g];
-    for (uint32_t i = tid; i < deg; i += NT) pid[i] = row[i];
-    const uint32_t kept = cta_stable_ranks<NT>(kf, c, warp_tot, [&](uint32_t i, uint32_t r) {
-      pid[deg + r] = ord[i];
-    });
-    const uint32_t nm = deg + kept;
-    cta_sync<NT>();
     if (nm <= R) {  // builder_common.cpp:129-131
       for (uint32_t i = tid; i < R; i += NT) trow[i] = i < nm ? pid[i] : kNone;
     } else if (nm <= a.prune_small_cap && !a.small_dists) {
       // the tensor-core prune gathers these rows anyway and computes d(t, .) itself
-      if (tid == 0) {
-        a.plen[g] = nm;
-        atomicMax(a.counters + kCntMaxMerged, static_cast<unsigned long long>(nm));
-        const uint32_t i = static_cast<uint32_t>(atomicAdd(a.counters + kCntPruneSmall, 1ull));
-        a.plist_small[i] = g;
-      }
+      if (tid == 0) a.plen[g] = nm;
+      push_small(g);
     } else {  // stage for alpha_prune with fresh distances (:133-138)
       const int sub = tid & (LPR - 1), grp = tid / LPR;
       uint4 tr[CPL];
@@ -280,21 +336,18 @@ __global__ void __launch_bounds__(NT)
           if (sub == 0 && r < nm) pd[r] = Op::finish(acc);
         }
       }
-      if (tid == 0) {
-        a.plen[g] = nm;
-        atomicMax(a.counters + kCntMaxMerged, static_cast<unsigned long long>(nm));
-        if (nm <= a.prune_small_cap) {
-          const uint32_t i = static_cast<uint32_t>(atomicAdd(a.counters + kCntPruneSmall, 1ull));
-          a.plist_small[i] = g;
-        } else {
-          const uint32_t i = static_cast<uint32_t>(atomicAdd(a.counters + kCntPruneBig, 1ull));
-          a.plist_big[i] = g;
-        }
+      if (tid == 0) a.plen[g] = nm;
+      if (nm <= a.prune_small_cap) {
+        push_small(g);
+      } else if (tid == 0) {
+        const uint32_t i = static_cast<uint32_t>(atomicAdd(a.counters + kCntPruneBig, 1ull));
+        a.plist_big[i] = g;
       }
     }
     cta_sync<NT>();
     if (tid == 0) a.tcount[t - a.base] = 0;
   }
+  if (NT == 32 && npend) flush_small();
 }
 
 // Hubs of the batch form (more sources than the small path handles, so the
