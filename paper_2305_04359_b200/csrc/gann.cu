@@ -133,6 +133,9 @@ struct gann_index {
   Geometry geom{};
   uint8_t* points = nullptr;
   uint32_t* adj = nullptr;
+  uint8_t* spre = nullptr;   // per row: length of its prune-output prefix (PruneArgs::spre)
+  float spre_alpha = -1.0f;  // the (alpha, rule) those prefixes were pruned with
+  int spre_rule = -1;
   uint32_t* tcount = nullptr;
   uint32_t* tgroup = nullptr;
   unsigned long long* stats = nullptr;  // kStCount
@@ -196,6 +199,7 @@ gann_index* new_index(uint64_t n, uint32_t d, int elem, int metric, uint32_t R, 
     const uint64_t rows = std::max<uint64_t>(idx->part_rows, 1);
     cu(cudaMalloc(&idx->points, nn * idx->stride), "cudaMalloc points");
     cu(cudaMalloc(&idx->adj, rows * std::max<uint32_t>(R, 1) * 4), "cudaMalloc graph");
+    cu(cudaMalloc(&idx->spre, std::max<uint64_t>(rows, 1)), "cudaMalloc row prefixes");
     cu(cudaMalloc(&idx->tcount, rows * 4), "cudaMalloc tcount");
     cu(cudaMalloc(&idx->tgroup, rows * 4), "cudaMalloc tgroup");
     cu(cudaMalloc(&idx->d_parts, sizeof(uint32_t*) * nparts), "cudaMalloc parts");
@@ -210,6 +214,7 @@ gann_index* new_index(uint64_t n, uint32_t d, int elem, int metric, uint32_t R, 
     cu(cudaMalloc(&idx->qctr, kQueryCounters * 4), "cudaMalloc query counters");
     cu(cudaMemsetAsync(idx->points, 0, nn * idx->stride, idx->stream), "memset");
     cu(cudaMemsetAsync(idx->adj, 0xFF, rows * std::max<uint32_t>(R, 1) * 4, idx->stream), "memset");
+    cu(cudaMemsetAsync(idx->spre, 0, std::max<uint64_t>(rows, 1), idx->stream), "memset");
     cu(cudaMemsetAsync(idx->tcount, 0, rows * 4, idx->stream), "memset");
     cu(cudaMemsetAsync(idx->stats, 0, sizeof(unsigned long long) * kStCount, idx->stream), "memset");
     cu(cudaMemsetAsync(idx->flags, 0, 16, idx->stream), "memset");
@@ -322,6 +327,13 @@ constexpr uint32_t kSmallGroupCap = 256;
 constexpr uint32_t kSortedGroupCap = 32768;
 
 PruneArgs base_prune_args(gann_index* idx, float alpha, int rule) {
+  // a row prefix is mutually non-culling only under the (alpha, rule) that
+  // pruned it: a launch with other parameters forgets every prefix first
+  if (alpha != idx->spre_alpha || rule != idx->spre_rule) {
+    cu(cudaMemsetAsync(idx->spre, 0, std::max<uint64_t>(idx->part_rows, 1), idx->stream), "clear row prefixes");
+    idx->spre_alpha = alpha;
+    idx->spre_rule = rule;
+  }
   PruneArgs p{};
   p.data = idx->points;
   p.stride = idx->stride;
@@ -330,6 +342,10 @@ PruneArgs base_prune_args(gann_index* idx, float alpha, int rule) {
   p.rule = rule;
   p.too_long = idx->flags + 1;
   p.stats = idx->stats;
+  // kernels writing rows into out_adj record the prune prefix (GANN_NO_SPRE=1:
+  // no prefixes, every re-prune tests all pairs — an A/B switch for tests)
+  static const bool no_spre = env_u32("GANN_NO_SPRE", 0) != 0;
+  p.spre = no_spre ? nullptr : idx->spre;
   return p;
 }
 
@@ -582,6 +598,7 @@ void apply_back(gann_index* idx, const uint32_t* bsrc, uint32_t B, const uint32_
   p.cand_dists = b.pdist;
   p.out_adj = idx->adj;
   p.out_base = idx->part_base;
+  p.row_lists = 1;  // merged lists start with the target's current row
   if (nps) {
     p.count = nps;
     p.list_index = b.plist_small;
@@ -705,7 +722,7 @@ void gann_index_free(gann_index* idx) {
   for (void* p : {static_cast<void*>(idx->points), static_cast<void*>(idx->adj),
                   static_cast<void*>(idx->tcount), static_cast<void*>(idx->tgroup),
                   static_cast<void*>(idx->stats), static_cast<void*>(idx->counters),
-                  static_cast<void*>(idx->flags), static_cast<void*>(idx->qctr)})
+                  static_cast<void*>(idx->flags), static_cast<void*>(idx->qctr), static_cast<void*>(idx->spre)})
     if (p) cudaFree(p);
   for (DevBuf* b : {&idx->q, &idx->qids, &idx->qdists, &idx->qnvis, &idx->qdc, &idx->qvids,
                     &idx->qvd, &idx->qstart, &idx->table, &idx->order, &idx->vis_ids, &idx->vis_d,
@@ -746,6 +763,7 @@ int gann_build(gann_index* idx, uint32_t L, float alpha, int rule, uint64_t seed
     idx->back_pairs = idx->back_groups = idx->back_pruned = 0;
     const uint64_t n = idx->n;
     cu(cudaMemsetAsync(idx->adj, 0xFF, n * idx->R * 4, idx->stream), "clear graph");
+    cu(cudaMemsetAsync(idx->spre, 0, n, idx->stream), "clear row prefixes");
     cu(cudaMemsetAsync(idx->tcount, 0, n * 4, idx->stream), "clear counts");
     Timer t0(idx->stream);
     const uint32_t start = choose_start_dev(idx);
@@ -835,6 +853,7 @@ int gann_import_graph(gann_index* idx, const uint32_t* adj, uint32_t start) {
     }
     set_device(idx);
     if (n) cu(cudaMemcpyAsync(idx->adj, adj, n * R * 4, cudaMemcpyHostToDevice, idx->stream), "upload graph");
+    if (n) cu(cudaMemsetAsync(idx->spre, 0, n, idx->stream), "clear row prefixes");  // rows of unknown origin
     idx->start = start;
     sync(idx);
   });
@@ -848,6 +867,7 @@ int gann_import_graph_device(gann_index* idx, const uint32_t* d_adj, uint32_t st
     set_device(idx);
     if (idx->n)
       cu(cudaMemcpyAsync(idx->adj, d_adj, idx->n * idx->R * 4, cudaMemcpyDeviceToDevice, idx->stream), "copy graph");
+    if (idx->n) cu(cudaMemsetAsync(idx->spre, 0, idx->n, idx->stream), "clear row prefixes");
     idx->start = start;
     sync(idx);
   });
@@ -1391,6 +1411,7 @@ int gann_load_graph(gann_index* idx, const char* path) {
     if (!in.eof()) fmt_fail("trailing bytes: " + ctx);
     set_device(idx);
     if (n) cu(cudaMemcpyAsync(idx->adj, adj.data(), adj.size() * 4, cudaMemcpyHostToDevice, idx->stream), "upload graph");
+    if (n) cu(cudaMemsetAsync(idx->spre, 0, n, idx->stream), "clear row prefixes");
     idx->start = start;
     sync(idx);
   });
@@ -1568,6 +1589,7 @@ int gann_part_build_begin(gann_index* idx, uint32_t L, float alpha, int rule, ui
     set_device(idx);
     const uint64_t n = idx->n;
     cu(cudaMemsetAsync(idx->adj, 0xFF, uint64_t(idx->part_rows) * idx->R * 4, idx->stream), "clear graph");
+    cu(cudaMemsetAsync(idx->spre, 0, std::max<uint64_t>(idx->part_rows, 1), idx->stream), "clear row prefixes");
     cu(cudaMemsetAsync(idx->tcount, 0, uint64_t(idx->part_rows) * 4, idx->stream), "clear counts");
     // every partition derives the same start and insertion order (src/diskann.cpp:47-51)
     idx->start = choose_start_dev(idx);

@@ -97,6 +97,12 @@ struct PruneArgs {
   int skip_long;               // lists longer than mcap: skip silently (binned launches)
   uint32_t* too_long;          // ... or count them here
   unsigned long long* stats;
+  // Per graph row: how many leading entries are a prune's output (<= 255;
+  // mutually non-culling). Written by every kernel that writes a row into
+  // out_adj (nullable). With row_lists set, a list of this launch starts with
+  // its point's current row, so that prefix needs no pair tests among itself.
+  uint8_t* spre;
+  int row_lists;
 };
 // threads = 32 for short lists, larger for hubs; smem from prune_smem_bytes.
 size_t prune_smem_bytes(uint32_t mcap, uint32_t R);

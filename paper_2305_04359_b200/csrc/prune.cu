@@ -194,6 +194,7 @@ __global__ void __launch_bounds__(NT) prune_kernel(const PruneArgs a, const uint
     for (uint32_t i = tid; i < R; i += NT) orow[i] = i < nsel ? sel[i] : kNone;
     if (tid == 0) {
       if (a.n_out) a.n_out[l] = nsel;
+      if (a.spre && !a.out_rows) a.spre[p - a.out_base] = static_cast<uint8_t>(nsel < 255 ? nsel : 255);
       if (a.stats) {
         atomicAdd(a.stats + kStPruneLists, 1ull);
         atomicAdd(a.stats + kStPruneCands, static_cast<unsigned long long>(m));
@@ -457,8 +458,8 @@ __global__ void __launch_bounds__(kMmaThreads)
     for (uint32_t i = tid; i + 1 < m; i += NT)
       if (!(tk[i] < tk[i + 1])) atomicMin(&sh_pre, i + 1);
     __syncthreads();
+    const uint32_t P = sh_pre;  // keys [0, P) ascend
     {
-      const uint32_t P = sh_pre;  // keys [0, P) ascend
       for (uint32_t i = tid; i < m; i += NT) {
         const uint64_t k = tk[i];
         if (k == kMaxKey) continue;
@@ -510,6 +511,65 @@ __global__ void __launch_bounds__(kMmaThreads)
       sn[i] = nrm;  // sorted norm (0 for IP and padding)
     }
     __syncthreads();
+    // Re-prune lists start with the target's row, whose first nS entries are a
+    // prune output: no entry of that prefix S culls a later one (same exact
+    // distances, same test). Only pairs with an entry of the unverified tail U
+    // need testing: U x S and U x U Gram tiles instead of the full triangle.
+    uint32_t nS = 0;
+    if (a.row_lists && a.spre && m2 == m) nS = min(static_cast<uint32_t>(a.spre[p - a.out_base]), m);
+    const bool su = nS >= 16 && nS < m && nS <= P;
+    if (su) {
+      uint16_t* ipos = reinterpret_cast<uint16_t*>(tk);  // input index -> sorted position
+      for (uint32_t r = tid; r < m2; r += NT) ipos[perm[r]] = static_cast<uint16_t>(r);
+      __syncthreads();
+      const uint32_t nu = m - nS;
+      const uint32_t mu = (nu + 15) >> 4;             // U row tiles
+      const uint32_t ncS = (nS + 15) >> 4, ncU = mu;  // S / U column tiles
+      const uint32_t items = mu * (ncS + ncU);
+      const int g = lane >> 2, tg = lane & 3;
+      for (uint32_t it = warp; it < items; it += NT / 32) {
+        const uint32_t ru = it / (ncS + ncU), cc = it - ru * (ncS + ncU);
+        const bool isU = cc >= ncS;
+        const uint32_t cb = isU ? cc - ncS : cc;
+        const uint32_t cbase = isU ? nS : 0u, cend = isU ? m : nS;
+        const uint32_t al = ru * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+        const uint32_t ia = nS + al < m ? nS + al : mc;
+        const uint32_t bl = cbase + cb * 16 + (lane & 7) + (lane >> 4) * 8;
+        const uint32_t ib = bl < cend ? bl : mc;
+        const uint8_t* arow = X + size_t(ia) * xs + (lane >> 4) * 16;
+        const uint8_t* brow = X + size_t(ib) * xs + ((lane >> 3) & 1) * 16;
+        int acc0[4] = {0, 0, 0, 0}, acc1[4] = {0, 0, 0, 0};
+        for (uint32_t kc = 0; kc < (kp >> 5); kc++) {
+          uint32_t af[4], bf[4];
+          ldsm_x4(af, arow + kc * 32);
+          ldsm_x4(bf, brow + kc * 32);
+          mma_i8<SIGNED>(acc0, af, bf[0], bf[1]);
+          mma_i8<SIGNED>(acc1, af, bf[2], bf[3]);
+        }
+#pragma unroll
+        for (int rr = 0; rr < 2; rr++) {
+          const uint32_t ui = nS + ru * 16 + g + rr * 8;
+          if (ui >= m) continue;
+          const uint32_t pu = ipos[ui];
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+#pragma unroll
+            for (int e2 = 0; e2 < 2; e2++) {
+              const uint32_t ci = cbase + cb * 16 + h * 8 + tg * 2 + e2;
+              if (ci >= cend || ci == ui) continue;
+              const uint32_t pc = ipos[ci];
+              if (isU && pc < pu) continue;  // the (ci, ui) entry tests this pair
+              const uint32_t x = pu < pc ? pu : pc, y = pu < pc ? pc : pu;  // x precedes y
+              if ((zmask[x >> 5] >> (x & 31)) & 1u) continue;  // prune.cpp:32
+              const int gram = h ? acc1[rr * 2 + e2] : acc0[rr * 2 + e2];
+              const int gm = M == kL2 ? -2 * gram : -gram;
+              const bool cull = RULE == 0 ? (sn[x] + gm <= ns[y]) : (sn[y] + gm <= ns[x]);
+              if (cull) atomicOr(&cm[x * W + (y >> 5)], 1u << (y & 31));
+            }
+          }
+        }
+      }
+    } else
     // all cull tests of the upper triangle (sorted positions), 16x16 tiles per warp
     {
       const uint32_t mt = mpad >> 4;
@@ -670,6 +730,9 @@ __global__ void __launch_bounds__(kWalkWarps * 32)
   }
   for (uint32_t i = nsel + lane; i < R; i += 32) orow[i] = kNone;
   if (lane == 0 && a.n_out) a.n_out[l] = nsel;
+  // a prune output: no entry culls a later one (exact int distances), so a
+  // later re-prune of this row + appended sources may skip those pairs
+  if (lane == 0 && a.spre && !a.out_rows) a.spre[p - a.out_base] = static_cast<uint8_t>(nsel < 255 ? nsel : 255);
 }
 
 // ---- length binning --------------------------------------------------------
@@ -939,6 +1002,7 @@ __global__ void __launch_bounds__(NT) prune_chunked_kernel(const PruneArgs a) {
     for (uint32_t i = tid; i < R; i += NT) orow[i] = i < nsel ? sel[i] : kNone;
     if (tid == 0) {
       if (a.n_out) a.n_out[l] = nsel;
+      if (a.spre && !a.out_rows) a.spre[p - a.out_base] = static_cast<uint8_t>(nsel < 255 ? nsel : 255);
       if (a.stats) {
         atomicAdd(a.stats + kStPruneLists, 1ull);
         atomicAdd(a.stats + kStPruneCands, static_cast<unsigned long long>(m));

@@ -212,6 +212,33 @@ def test_apply_back_edges_parity(oracle):
     assert (got == want).all()
 
 
+@pytest.mark.parametrize("alpha,rule", [(1.0, "scale_candidate"), (1.2, "scale_selected"), (1.2, "scale_candidate")])
+def test_apply_back_edges_after_gpu_build(oracle, alpha, rule):
+    """Re-prunes of rows the GPU build wrote (their prune prefixes are known to
+    be mutually non-culling under the build's alpha/rule): with the same
+    parameters the prefix pairs are skipped, with other ones they are not.
+    Either way the result is the reference's apply_back_edges."""
+    g = _g()
+    data = mixture(13, 3000, 32, clusters=12)
+    idx = g.build_diskann(data, "l2", g.DiskannParams(16, 32, 1.2))
+    adj, _, start = idx.export_graph()
+    rng = np.random.default_rng(9)
+    t = rng.integers(0, 3000, 12000).astype(np.uint32)
+    s = rng.integers(0, 3000, 12000).astype(np.uint32)
+    keep = t != s
+    t, s = t[keep], s[keep]
+    want = oracle.apply_back_edges(adj, data, t, s, alpha, rule=rule, workers=4)
+    idx.apply_back_edges(t, s, g.PruneParams(16, alpha, rule))
+    got, _, _ = idx.export_graph()
+    assert (got == want).all(), f"{int((got != want).any(axis=1).sum())} rows differ"
+    # and once more on top (prefixes now from these re-prunes)
+    want2 = oracle.apply_back_edges(want, data, s, t, alpha, rule=rule, workers=4)
+    idx.apply_back_edges(s, t, g.PruneParams(16, alpha, rule))
+    got2, _, _ = idx.export_graph()
+    assert (got2 == want2).all()
+    idx.close()
+
+
 @pytest.mark.parametrize("dtype", [np.uint8, np.int8])
 @pytest.mark.parametrize("cap", [0, 97])
 def test_build_bit_identical(oracle, dtype, cap):
