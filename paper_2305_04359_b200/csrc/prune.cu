@@ -780,7 +780,7 @@ cudaError_t launch_bin_lists(const PruneArgs& a, const uint32_t* d_bounds, int n
 // some earlier selection's test fires on it — the order of the tests does not
 // matter), then walked greedily as above. Most hubs finish inside the first
 // chunk because R selections are reached long before the list ends.
-constexpr uint32_t kChunk = 4096;
+constexpr uint32_t kChunk = 512;
 
 size_t prune_chunked_smem(uint32_t R) {
   size_t b = size_t(kChunk) * 8 + 2 * size_t(kChunk) * 2 + kChunk + size_t(R) * 8 + 256 * 4;
