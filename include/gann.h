@@ -257,6 +257,7 @@ typedef struct gann_stats {
   uint64_t survivors;       /* search: candidates inserted into the beam */
   uint64_t moved;           /* search: beam entries shifted by those inserts */
   uint64_t duplicates;      /* search: re-evaluated ids found already in the beam */
+  uint64_t guess_hits;      /* search: expansions whose row was prefetched by a right guess */
 } gann_stats;
 int gann_get_stats(const gann_index* idx, gann_stats* out);
 int gann_reset_stats(gann_index* idx);

@@ -41,6 +41,7 @@ class GannStats(C.Structure):
         ("survivors", C.c_uint64),
         ("moved", C.c_uint64),
         ("duplicates", C.c_uint64),
+        ("guess_hits", C.c_uint64),
     ]
 
 

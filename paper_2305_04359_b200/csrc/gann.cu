@@ -1688,6 +1688,7 @@ int gann_get_stats(const gann_index* idx, gann_stats* out) {
     out->survivors = s[kStSurvivors];
     out->moved = s[kStMoved];
     out->duplicates = s[kStDups];
+    out->guess_hits = s[kStGuess];
     out->back_pairs = idx->back_pairs;
     out->back_groups = idx->back_groups;
     out->back_pruned = idx->back_pruned;

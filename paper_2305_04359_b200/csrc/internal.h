@@ -35,7 +35,7 @@ __device__ __forceinline__ uint32_t* local_row(const GraphView& g, uint32_t v, u
 
 enum StatIdx {
   kStQueries = 0, kStExpansions, kStEvals, kStDrops, kStAdj,
-  kStPruneLists, kStPruneCands, kStPruneEvals, kStMerges, kStSurvivors, kStMoved, kStDups, kStCount
+  kStPruneLists, kStPruneCands, kStPruneEvals, kStMerges, kStSurvivors, kStMoved, kStDups, kStGuess, kStCount
 };
 
 struct SearchArgs {

@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_SEARCH_MINB)
     }
     uint32_t size = 1, nvis = 0, hint = 0, evict = 0;
     uint64_t evals = 1;
-    uint32_t adjsum = 0, merges = 0, survivors = 0, moved = 0, dups = 0;  // per query: 32 bits suffice
+    uint32_t adjsum = 0, merges = 0, survivors = 0, moved = 0, dups = 0, ghits = 0;  // per query: 32 bits suffice
     // speculative register prefetch of the next expansion's adjacency row
     // (R <= 64: two ids per lane); used when the guess turns out right
     const bool pf_ok = R <= 64;
@@ -307,6 +307,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_SEARCH_MINB)
         if (pf_id == cur) {
           nb0 = pf0;
           nb1 = pf1;
+          if (!F16) ghits++;
         } else {
           nb0 = lane < R ? __ldg(row + lane) : kNone;
           nb1 = lane + 32 < R ? __ldg(row + 32 + lane) : kNone;
@@ -519,6 +520,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_SEARCH_MINB)
           atomicAdd(a.stats + kStSurvivors, static_cast<unsigned long long>(survivors));
           atomicAdd(a.stats + kStMoved, static_cast<unsigned long long>(moved));
           atomicAdd(a.stats + kStDups, static_cast<unsigned long long>(dups));
+          atomicAdd(a.stats + kStGuess, static_cast<unsigned long long>(ghits));
         }
       }
     }
@@ -533,10 +535,9 @@ template <int E, int M, int LPR, int CPL>
 cudaError_t launch_one(const SearchArgs& a, cudaStream_t s) {
   const uint32_t per_warp = static_cast<uint32_t>(search_smem_per_warp(a.L, a.R, a.hash_log2, a.hash_bits != 0));
   const size_t smem = size_t(per_warp) * kWarpsPerBlock;
-  static const bool diag = [] {
-    const char* v = std::getenv("GANN_SEARCH_DIAG");
-    return v && *v && *v != '0';
-  }();
+  // read per launch (A/B runs flip it between launches)
+  const char* dv = std::getenv("GANN_SEARCH_DIAG");
+  const bool diag = dv && *dv && *dv != '0';
   const bool f16 = a.visited_mode == 0 && a.hash_bits != 0 && !diag;
   auto k = f16 ? search_kernel<E, M, LPR, CPL, true> : search_kernel<E, M, LPR, CPL, false>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
