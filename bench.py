@@ -42,6 +42,8 @@ sys.path.insert(0, str(ROOT))
 
 # BASELINE.json: "beam L swept 10..200"; --L-max widens it
 L_CANDIDATES = [10, 12, 14, 16, 20, 24, 28, 32, 40, 48, 56, 64, 80, 96, 128, 160, 200, 256, 320, 400, 512]
+# beams tried past the sweep when it ends below the recall target ("at_target")
+L_EXTEND = [256, 320, 400, 512, 640, 800, 1024, 1280, 1600, 2048]
 GT_DEPTH = 16
 CFG_INDEX = {"c0": 0, "c1": 1, "c2": 2, "c3": 3, "c4": 4}  # BASELINE.json configs[i]
 
@@ -75,6 +77,8 @@ def parse():
     ap.add_argument("--L-max", type=int, default=200, help="largest beam of the sweep (BASELINE: 10..200)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="CPU baseline sample length")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extend", action="store_true",
+                    help="do not search past the sweep for the beam that reaches the recall target")
     ap.add_argument("--ref-n", type=int, default=100_000, help="reference arm: points in its CPU build sample")
     ap.add_argument("--streams", type=int, default=2,
                     help="timed steps alternate over this many streams, so one step's tail overlaps the next "
@@ -283,13 +287,29 @@ def setup(args):
         chosen = curve[-1]["L"]
     recall = curve[-1]["recall@10"]
     sp = g.SearchParams(chosen, chosen, 0.0)
+    # the sweep ended below the target: continue past it until the target is
+    # reached (reported beside the headline as "at_target")
+    ext_curve, L_target = [], None
+    if not target_reached and not args.no_extend:
+        for L in [x for x in L_EXTEND if x > chosen]:
+            search_L(L)
+            torch.cuda.synchronize()
+            res = out_ids.cpu().numpy().view(np.uint32).reshape(nq, k)
+            rec = allreduce(float(evalutil.recall_at_k(gt_ids_h, gt_d_h, res, k).mean()), "mean")
+            ext_curve.append({"L": L, "recall@10": round(rec, 5)})
+            if rec >= args.target_recall:
+                L_target = L
+                break
+        search_L(chosen)
+        torch.cuda.synchronize()
 
     return dict(torch=torch, dist=dist, g=g, check=check, lib=lib, cfg=cfg, nq=nq, n=n, d=d, k=k, dev=dev,
                 rank=rank, world=world, barrier=barrier, allreduce=allreduce, base=base, qdev=qdev, idx=idx,
                 build_s=build_s, bstats=bstats, replicas_identical=replicas_identical, deg_mean=deg_mean,
                 build_mode=build_mode,
                 out_ids=out_ids, out_d=out_d, stream=stream, search_L=search_L, curve=curve, chosen=chosen,
-                recall=recall, target_reached=target_reached, sp=sp, gt_ids_h=gt_ids_h, gt_d_h=gt_d_h)
+                recall=recall, target_reached=target_reached, sp=sp, gt_ids_h=gt_ids_h, gt_d_h=gt_d_h,
+                ext_curve=ext_curve, L_target=L_target)
 
 
 def run_ours(args):
@@ -428,6 +448,35 @@ def run_ours(args):
             rec = float(evalutil.recall_at_k(gt_ids_h, gt_d_h, res, k).mean())
             secondary.append({"L": L, "k_gate": k, "eps": eps, "recall@10": round(allreduce(rec, "mean"), 5),
                               "qps": round(world * nq / (allreduce(best) / 1e3), 1)})
+    # ---- QPS at the beam that reaches the recall target past the sweep --------------------
+    at_target = None
+    if S["ext_curve"]:
+        at_target = {"L": S["L_target"], "reached": S["L_target"] is not None,
+                     "recall_curve_past_sweep": S["ext_curve"]}
+        if S["L_target"]:
+            spt = g.SearchParams(S["L_target"], S["L_target"], 0.0)
+            nt = max(3, min(10, args.steps))
+            idx.search_staged(spt, k, out_ids.data_ptr(), out_d.data_ptr(), stream)
+            torch.cuda.synchronize()
+            barrier()
+            t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0e.record(ext[0])
+            for es in ext[1:]:
+                es.wait_event(t0e)
+            for i in range(nt):
+                j = i % nstreams
+                idx.search_staged(spt, k, souts[j][0].data_ptr(), souts[j][1].data_ptr(), streams[j])
+            for es in ext[1:]:
+                ev = torch.cuda.Event()
+                ev.record(es)
+                ext[0].wait_event(ev)
+            t1e.record(ext[0])
+            torch.cuda.synchronize()
+            barrier()
+            tms = allreduce(t0e.elapsed_time(t1e))
+            at_target.update({"recall@10": S["ext_curve"][-1]["recall@10"], "qps": round(world * nq * nt / (tms / 1e3), 1),
+                              "ms_per_step": round(tms / nt, 4), "steps": nt,
+                              "timing": f"{nt} launches alternating over {nstreams} stream(s), as the headline"})
     search_L(chosen)  # out_ids back to the headline search (the CPU baseline compares against it)
     torch.cuda.synchronize()
 
@@ -500,6 +549,7 @@ def run_ours(args):
             "stats": {kk: v for kk, v in bstats.items() if kk != "build_ms"},
         },
         "recall_curve": curve,
+        "at_target": at_target,
         "secondary_sweep": {"semantics": "reference eval {L, k_gate=10, eps}, top-10, one serial launch (best of 3, L2 not flushed)",
                             "points": secondary},
     }
@@ -603,6 +653,13 @@ def run_reference(args):
                                       reps=1)
         secs.append(sec)
     value = nq * args.steps / sum(secs)
+    at_target = None
+    if S["L_target"]:  # our arm's recall-target beam past the sweep: one timed pass
+        LT = S["L_target"]
+        sec_t, ids_t, _ = orc.time_search(adj, start, data, q, LT, LT, 0.0, k_out=k, metric=cfg.metric, workers=0,
+                                          reps=1)
+        at_target = {"L": LT, "recall@10": S["ext_curve"][-1]["recall@10"], "qps": round(nq / sec_t, 1),
+                     "timing": "one pass over all queries"}
     # the reference's build speed on a bounded prefix (host cores)
     nb = min(args.ref_n, cfg.n)
     pref = data[:nb]
@@ -631,6 +688,7 @@ def run_reference(args):
         "build": {"points_per_s": round(nb / build_s, 1), "seconds": round(build_s, 3), "n": nb, "cores": cores,
                   "sample": f"graphann build_diskann loop on the first {nb} points (batch cap {cap})"},
         "recall_curve": S["curve"],
+        "at_target": at_target,
     }
     print(json.dumps(line), flush=True)
 

@@ -165,4 +165,15 @@ __device__ __forceinline__ uint32_t lower_bound_u64(const uint64_t* a, uint32_t 
   return lo;
 }
 
+// lower_bound_u64 without data-dependent branches: the count of entries < k,
+// found by power-of-two steps (floor(log2 n) + 1 probes, one LDS each).
+__device__ __forceinline__ uint32_t lower_bound_steps_u64(const uint64_t* a, uint32_t n, uint64_t k) {
+  uint32_t pos = 0;
+  for (uint32_t step = n ? 1u << (31 - __clz(n)) : 0u; step; step >>= 1) {
+    const uint32_t j = pos + step;
+    if (j <= n && a[j - 1] < k) pos = j;
+  }
+  return pos;
+}
+
 }  // namespace gann

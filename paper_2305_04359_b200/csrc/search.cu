@@ -414,7 +414,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_SEARCH_MINB)
         const uint64_t k = keep ? tmpk[j] : kMaxKey;
         uint32_t pb = 0;
         if (keep) {
-          pb = lower_bound_u64(beam, size, k);
+          pb = lower_bound_steps_u64(beam, size, k);
           if (pb < size && beam[pb] == k) {
             keep = false;
             if (!F16) dups++;
@@ -438,8 +438,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_SEARCH_MINB)
         bool in = false;
         if (j < s) {
           const uint64_t k = ck[j];
-          uint32_t r = 0;
-          for (uint32_t t = 0; t < s; t++) r += ck[t] < k ? 1u : 0u;
+          // rank among the survivors (ck is 16-byte aligned: two keys per load)
+          uint32_t r = 0, t = 0;
+          for (; t + 2 <= s; t += 2) {
+            const ulonglong2 p2 = *reinterpret_cast<const ulonglong2*>(ck + t);
+            r += (p2.x < k ? 1u : 0u) + (p2.y < k ? 1u : 0u);
+          }
+          if (t < s) r += ck[t] < k ? 1u : 0u;
           srt[r] = k;
           p0 = min(p0, posb[j]);
           const uint32_t fin = posb[j] + r;
