@@ -260,7 +260,7 @@ typedef struct gann_stats {
   uint64_t guess_hits;      /* search: expansions whose row was prefetched by a right guess */
 } gann_stats;
 int gann_get_stats(const gann_index* idx, gann_stats* out);
-int gann_reset_stats(gann_index* idx);
+int gann_reset_stats(gann_index* idx);  /* waits for all work queued on the device first */
 
 /* Device pointers of the resident index (points: padded rows of `stride`
  * bytes; adj: n*R uint32). For in-process callers that move the index with

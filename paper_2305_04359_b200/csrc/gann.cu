@@ -102,15 +102,23 @@ uint32_t env_u32(const char* name, uint32_t dflt) {
 // With n <= 2^(log2 + 15) a slot stores the 15-bit remainder of a bijective
 // hash of the id (half the bytes of an id slot, so twice the entries for the
 // same shared memory, still no false positives).
-void hash_config(uint32_t L, uint64_t n, uint32_t* log2, uint32_t* bits) {
+void hash_config(uint32_t L, uint64_t n, uint32_t* log2, uint32_t* bits, uint32_t* ways) {
   const uint32_t forced = std::min<uint32_t>(env_u32("GANN_HASH_LOG2", 0), 15);
   const bool narrow = env_u32("GANN_HASH16", 1) != 0;
   uint32_t l = forced ? std::max<uint32_t>(forced, 5) : 11;
-  if (narrow && n <= (uint64_t(1) << (l + 15))) {
+  // u16 remainder slots; 2-way buckets (the bucket's newest id in the low
+  // half) halve the conflict evictions of a direct-mapped table of the same size
+  const uint32_t w = env_u32("GANN_HASH_WAYS", 4);
+  const uint32_t wl = w >= 4 ? 2 : (w == 2 ? 1 : 0);  // log2(ways)
+  *ways = 1u << wl;
+  while (*ways > 1 && !(narrow && n <= (uint64_t(1) << (l + 15 - (31 - __builtin_clz(*ways)))))) *ways >>= 1;
+  const uint32_t b = l + 15 - (31 - __builtin_clz(*ways));
+  if (narrow && n <= (uint64_t(1) << b)) {
     *log2 = l;
-    *bits = l + 15;
+    *bits = b;
     return;
   }
+  *ways = 1;
   // u32 id slots; measured on B200 at 10M (tools/profile_search.py, HLOGS sweep)
   *log2 = forced ? std::max<uint32_t>(forced, 5) : (L <= 160 ? 10 : 9);
   *bits = 0;
@@ -274,7 +282,7 @@ SearchArgs base_search_args(gann_index* idx, uint32_t L, uint32_t k_gate, uint32
   a.k_out = k_out;
   a.eps = eps;
   a.visited_mode = mode;
-  hash_config(L, idx->n, &a.hash_log2, &a.hash_bits);
+  hash_config(L, idx->n, &a.hash_log2, &a.hash_bits, &a.hash_ways);
   a.dim = idx->d;
   a.row_bytes = idx->row_bytes;
   a.overflow = idx->flags;
@@ -1674,6 +1682,7 @@ int gann_get_stats(const gann_index* idx, gann_stats* out) {
   return guarded([&] {
     if (!idx || !out) fail(GANN_EINVAL, "NULL argument");
     cudaSetDevice(idx->device);
+    cu(cudaDeviceSynchronize(), "device sync");  // launches on any stream have counted
     unsigned long long s[kStCount];
     cu(cudaMemcpy(s, idx->stats, sizeof(s), cudaMemcpyDeviceToHost), "read stats");
     out->queries = s[kStQueries];
@@ -1700,6 +1709,8 @@ int gann_reset_stats(gann_index* idx) {
   return guarded([&] {
     if (!idx) fail(GANN_EINVAL, "index is NULL");
     set_device(idx);
+    // launches queued on other streams (any caller stream) count before the reset
+    cu(cudaDeviceSynchronize(), "device sync");
     cu(cudaMemsetAsync(idx->stats, 0, sizeof(unsigned long long) * kStCount, idx->stream), "memset");
     sync(idx);
   });

@@ -55,7 +55,10 @@ struct SearchArgs {
   uint32_t exact_slots;      // mode 2: slots per query (power of two)
   uint32_t hash_log2;        // fast mode table size (entries)
   uint32_t hash_bits;        // fast mode: 0 = u32 id slots; else u16 remainders of a
-                             // bijective hash over hash_bits = hash_log2 + 15 bits
+                             // bijective hash over hash_bits bits: direct mapped
+                             // (hash_ways 1: hash_log2 + 15 bits) or 2-way buckets of
+                             // two u16 slots (hash_ways 2: hash_log2 + 14 bits)
+  uint32_t hash_ways;
   uint32_t* ref_table;       // modes 1/2: per-query tables, initialised by the kernel
   uint32_t dim;              // real dimension (search_seed)
   uint32_t row_bytes;        // real bytes per row (search_seed)

@@ -870,7 +870,10 @@ __global__ void __launch_bounds__(NT) prune_chunked_kernel(const PruneArgs a) {
         }
         hi_key = sh_prefix;
       }
-      // gather the chunk (lo_key, hi_key] and sort it
+      // gather the chunk (lo_key, hi_key] and sort it; every thread has read
+      // rem = sh_cnt before it is reset (without this barrier a warp could
+      // read the reset count when rem <= kChunk skips the radix select's)
+      __syncthreads();
       if (tid == 0) sh_cnt = 0;
       __syncthreads();
       for (uint64_t i = tid; i < m; i += NT) {

@@ -263,7 +263,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_SEARCH_MINB)
         table[(start * 0x9E3779B1u) & (TS - 1)] = start;
       else if (vmode == 1)
         table[mix64(static_cast<uint64_t>(start) ^ seed) % LL] = start;
-      else if (F16 || hbits) {
+      else if ((F16 || hbits) && a.hash_ways == 4) {
+        const uint32_t h = (start * 0x9E3779B1u) & hmask;
+        reinterpret_cast<uint64_t*>(hash)[h >> 15] = 0xFFFFFFFFFFFF0000ull | (h & 0x7FFFu);
+      } else if ((F16 || hbits) && a.hash_ways == 2) {
+        const uint32_t h = (start * 0x9E3779B1u) & hmask;
+        hash[h >> 15] = 0xFFFF0000u | (h & 0x7FFFu);
+      } else if (F16 || hbits) {
         const uint32_t h = (start * 0x9E3779B1u) & hmask;
         h16[h >> 15] = static_cast<uint16_t>(h & 0x7FFFu);
       } else
@@ -368,6 +374,35 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_SEARCH_MINB)
           if (valid && last) table[slot] = nb;
           __syncwarp();
           fresh = valid && !seen;
+        } else if ((F16 || hbits) && a.hash_ways == 4) {
+          // 4-way buckets of u16 slots in one u64 (newest in the low half
+          // word), as the 2-way case below
+          const uint32_t h = (nb * 0x9E3779B1u) & hmask;
+          const uint32_t bucket = h >> 15, rem = h & 0x7FFFu;
+          uint64_t* h64 = reinterpret_cast<uint64_t*>(hash);
+          const uint64_t w = valid ? h64[bucket] : 0ull;
+          const uint32_t rr = rem | (rem << 16);
+          const uint32_t eq = __vcmpeq2(static_cast<uint32_t>(w), rr) | __vcmpeq2(static_cast<uint32_t>(w >> 32), rr);
+          fresh = valid && eq == 0u;
+          __syncwarp();
+          if (fresh) {
+            h64[bucket] = (w << 16) | rem;
+            if (!F16) evict += (w >> 48) != 0xFFFFu ? 1u : 0u;
+          }
+        } else if ((F16 || hbits) && a.hash_ways == 2) {
+          // 2-way buckets of u16 slots (word = older << 16 | newer): bucket and
+          // remainder of a bijection of the id over hbits bits, so a match is
+          // the same id; 0xFFFF (no 15-bit remainder) marks an empty slot. An
+          // insert shifts the newer slot up and evicts the older id.
+          const uint32_t h = (nb * 0x9E3779B1u) & hmask;
+          const uint32_t bucket = h >> 15, rem = h & 0x7FFFu;
+          const uint32_t w = valid ? hash[bucket] : 0u;
+          fresh = valid && (w & 0xFFFFu) != rem && (w >> 16) != rem;
+          __syncwarp();
+          if (fresh) {
+            hash[bucket] = (w << 16) | rem;
+            if (!F16) evict += (w >> 16) != 0xFFFFu ? 1u : 0u;
+          }
         } else if (F16 || hbits) {
           // direct-mapped u16 slots: slot and remainder of a bijection of the
           // id over hbits bits (id < 2^hbits), so a match is the same id;

@@ -83,16 +83,21 @@ if args.profile:
 for L in [int(x) for x in args.L.split(",")]:
     res = {i: [] for i in range(len(combos))}
     ref_ids = None
+    evq = {}
     for r in range(args.rounds):
         for i, c in enumerate(combos):
+            idx.reset_stats()
             ms, ids = run(L, c)
+            st = idx.stats()
+            evq[i] = st["evaluations"] / max(1, st["queries"])
             res[i].append(ms)
             if ref_ids is None:
                 ref_ids = ids
             assert (ids == ref_ids).all(), f"ids differ under {c}"
     for i, c in enumerate(combos):
         ms = min(res[i])
-        print(f"L={L} {c}: {ms:.3f} ms  {args.nq / ms * 1e3 / 1e6:.3f} MQPS  (runs {[round(x, 3) for x in res[i]]})")
+        print(f"L={L} {c}: {ms:.3f} ms  {args.nq / ms * 1e3 / 1e6:.3f} MQPS  evals/q {evq[i]:.1f}  "
+              f"(runs {[round(x, 3) for x in res[i]]})")
     # diagnostic counters (general kernel) for the first combo
     os.environ["GANN_SEARCH_DIAG"] = "1"
     for k, v in combos[-1].items():
