@@ -804,6 +804,8 @@ int gann_build(gann_index* idx, uint32_t L, float alpha, int rule, uint64_t seed
       const uint64_t ptotal = groups * idx->R + pairs;
       idx->pid.ensure(ptotal * 4);
       idx->pdist.ensure(ptotal * 4);
+      if (prune_uses_mma(idx->elem, 512, idx->stride, idx->R))
+        prune_reserve(static_cast<uint32_t>(std::min<uint64_t>(groups, 0xFFFFFFFFu)), idx->stride, idx->R, idx->stream);
     }
     const bool trace = env_u32("GANN_TRACE", 0) != 0;
     for (auto [lo, hi] : batch_ranges(n, max_batch)) {

@@ -116,6 +116,9 @@ cudaError_t launch_bin_lists(const PruneArgs& a, const uint32_t* d_bounds, int n
                              uint32_t* d_lists, cudaStream_t s);
 // Integer lists up to 512 candidates run on the tensor cores (IMMA tiles).
 bool prune_uses_mma(int elem, uint32_t mcap, uint64_t stride, uint32_t R);
+// Allocate the tensor-core prune's hand-off region up front for launches of
+// up to `lists` lists (a build sizes it once from its largest batch).
+void prune_reserve(uint32_t lists, uint64_t stride, uint32_t R, cudaStream_t s);
 
 // ---- back-edge grouping (phase 2) -----------------------------------------
 // Pairs (target, source) come either from the out-rows of the batch's points

@@ -280,18 +280,23 @@ __host__ __device__ inline MmaLayout mma_layout(uint32_t mcap, uint32_t stride, 
 constexpr int kMmaThreads = 128;
 
 // Stage-1 -> stage-2 hand-off buffer (grows; one per process and device).
+constexpr uint64_t kHandoffMax = 1ull << 30;  // launches are chunked to fit
+
 uint32_t* prune_handoff(uint64_t bytes, cudaStream_t s) {
   static uint32_t* buf[16] = {};
   static uint64_t cap[16] = {};
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev >= 16) return nullptr;
   if (bytes > cap[dev]) {
+    // grows geometrically (a build's lists per launch double batch by batch;
+    // every regrowth is a device-wide sync + a large cudaMalloc)
+    const uint64_t want = std::max<uint64_t>(bytes, std::min<uint64_t>(2 * cap[dev], kHandoffMax));
     cudaStreamSynchronize(s);
     if (buf[dev]) cudaFree(buf[dev]);
     buf[dev] = nullptr;
     cap[dev] = 0;
-    if (cudaMalloc(&buf[dev], bytes) != cudaSuccess) return nullptr;
-    cap[dev] = bytes;
+    if (cudaMalloc(&buf[dev], want) != cudaSuccess) return nullptr;
+    cap[dev] = want;
   }
   return buf[dev];
 }
@@ -1060,7 +1065,7 @@ cudaError_t launch_mma_w(const PruneArgs& a, const MmaLayout& ly, cudaStream_t s
   if (e != cudaSuccess) return e;
   // the hand-off region is reused chunk by chunk (~1 GiB)
   const uint64_t per = uint64_t(ly.stride) * 4;
-  const uint32_t chunk = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(a.count, (1ull << 30) / per)));
+  const uint32_t chunk = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(a.count, kHandoffMax / per)));
   uint32_t* hand = prune_handoff(uint64_t(chunk) * per, s);
   if (!hand) return cudaErrorMemoryAllocation;
   const size_t walk_smem = size_t(kWalkWarps) * ly.mc * W * 4;
@@ -1084,6 +1089,12 @@ cudaError_t launch_mma(const PruneArgs& a, cudaStream_t s) {
   if (ly.w == 4) return launch_mma_w<E, M, 4>(a, ly, s);
   if (ly.w == 8) return launch_mma_w<E, M, 8>(a, ly, s);
   return launch_mma_w<E, M, 16>(a, ly, s);
+}
+
+void prune_reserve(uint32_t lists, uint64_t stride, uint32_t R, cudaStream_t s) {
+  // the largest hand-off a launch of `lists` lists (up to 512 candidates) asks for
+  const uint64_t per = uint64_t(mma_layout(512, static_cast<uint32_t>(stride), R).stride) * 4;
+  prune_handoff(std::min<uint64_t>(uint64_t(lists) * per, kHandoffMax / per * per), s);
 }
 
 bool prune_uses_mma(int elem, uint32_t mcap, uint64_t stride, uint32_t R) {
