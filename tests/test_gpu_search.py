@@ -277,3 +277,34 @@ def test_search_async_concurrent_streams_equal_sync(dtype):
         idx.search_async(qh.data_ptr(), nq, sp, k, outs[0][0].data_ptr(), outs[0][1].data_ptr(),
                          scratch[0].data_ptr(), nbytes - 1, streams[0].cuda_stream)
     idx.close()
+
+
+@pytest.mark.parametrize("env", [
+    {"GANN_HASH_WAYS": "1"}, {"GANN_HASH_WAYS": "2"}, {"GANN_HASH_WAYS": "4"},
+    {"GANN_HASH_WAYS": "4", "GANN_HASH_LOG2": "5"},   # 32 slots: constant evictions
+    {"GANN_HASH_WAYS": "1", "GANN_HASH_LOG2": "5"},
+    {"GANN_HASH16": "0"},                             # u32 id slots
+    {"GANN_HASH16": "0", "GANN_HASH_LOG2": "5"},
+    {"GANN_SEARCH_DIAG": "1"},                        # general (diagnostic) kernel instance
+])
+def test_fast_filter_layouts_keep_results(oracle, monkeypatch, env):
+    """The FAST visited table is a performance knob only: every layout (direct
+    mapped or 2/4-way buckets of u16 remainders, u32 id slots, tiny tables that
+    evict constantly) returns the reference's ids, distances, |V| and visit
+    sequences; only the number of re-evaluations changes."""
+    g = _g()
+    data, qs = mixture(17, 4000, 48, clusters=16, nq=300)
+    adj, start = oracle.build(data, 24, 48, 1.2, workers=4)
+    idx = idx_with_graph(data, adj, start)
+    L = 64
+    vcap = 4 * L + 64
+    want = oracle.beam_search(adj, start, data, qs, L, L, 0.0, visited_mode=1, vcap=vcap, workers=4)
+    for k_, v_ in env.items():
+        monkeypatch.setenv(k_, v_)
+    got = idx.search(qs, g.SearchParams(L, L, 0.0), visited_mode="fast", vcap=vcap)
+    assert (got.ids == want["ids"]).all()
+    assert (got.dists == want["dists"]).all()
+    assert (got.n_visited == want["n_visited"]).all()
+    for i in range(len(qs)):
+        nv = int(want["n_visited"][i])
+        assert (got.visited_ids[i, :nv] == want["visited_ids"][i, :nv]).all()
