@@ -189,6 +189,24 @@ int gann_index_create_from_file(const char* path, int metric, uint32_t R, int de
 int gann_range_search(gann_index* idx, const void* queries, uint32_t nq, float radius, uint32_t L,
                       float eps, uint32_t cap, uint32_t* counts, uint32_t* ids, float* dists);
 
+/* ---- layered (HNSW) search ------------------------------
+ * graphann::search_hnsw (src/hnsw.cpp:130-147) over a layered index: layer 0 is
+ * `layer0` (its points and bottom graph, borrowed: it must outlive the handle);
+ * layers 1..num_layers-1 are graphs over the same id space, rows of
+ * `m_upper` ids (GANN_NONE padded; non-members have empty rows), layer l at
+ * upper_adj[((l-1)*n + v)*m_upper]. `entry` is the top layer's entry vertex
+ * (HnswIndex::entry, include/graphann/hnsw.hpp). A query descends with beam
+ * {1, 1, 0} searches from `entry`, each layer started at the previous layer's
+ * nearest, then searches layer 0 with {L, k_gate, eps} from there.
+ * dist_comps sums every layer's evaluations, as the reference does. */
+typedef struct gann_hnsw gann_hnsw;
+int gann_hnsw_create(gann_index* layer0, uint32_t num_layers, const uint32_t* upper_adj, uint32_t m_upper,
+                     uint32_t entry, gann_hnsw** out);
+int gann_hnsw_search(gann_hnsw* h, const void* queries, uint32_t nq, uint32_t k_out, uint32_t L,
+                     uint32_t k_gate, float eps, int visited_mode, uint32_t* ids, float* dists,
+                     uint32_t* n_visited, uint64_t* dist_comps);
+void gann_hnsw_free(gann_hnsw* h);
+
 /* ---- next-row helpers --------------------------------------
  * Exact top-k by (dist, id): graphann::compute_groundtruth (src/dataset.cpp:172-217). */
 int gann_groundtruth(gann_index* idx, const void* queries, uint32_t nq, uint32_t k,

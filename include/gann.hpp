@@ -177,6 +177,49 @@ class Index {
   Metric metric_;
 };
 
+// Layered index (graphann::HnswIndex): layer 0 is an Index (borrowed), the upper
+// layers are graphs over the same ids, each n rows of m_upper ids.
+class HnswIndex {
+ public:
+  HnswIndex(Index& layer0, const std::vector<HostGraph>& upper, uint32_t entry) {
+    std::vector<uint32_t> flat;
+    const uint32_t m = upper.empty() ? 0 : upper[0].capacity;
+    for (const HostGraph& g : upper) {
+      if (g.capacity != m) throw std::invalid_argument("upper layers must share one row capacity");
+      flat.insert(flat.end(), g.adj.begin(), g.adj.end());
+    }
+    gann_hnsw* h = nullptr;
+    check(gann_hnsw_create(layer0.handle(), 1 + static_cast<uint32_t>(upper.size()),
+                           flat.empty() ? nullptr : flat.data(), m, entry, &h));
+    h_.reset(h);
+  }
+  gann_hnsw* handle() const { return h_.get(); }
+
+ private:
+  struct Free {
+    void operator()(gann_hnsw* p) const { gann_hnsw_free(p); }
+  };
+  std::unique_ptr<gann_hnsw, Free> h_;
+};
+
+// graphann::search_hnsw (src/hnsw.cpp:130-147), batched over queries.
+inline std::vector<SearchResult> search_hnsw(const HnswIndex& h, const void* queries, uint32_t nq,
+                                             const SearchParams& p) {
+  std::vector<uint32_t> ids(size_t(nq) * p.k), nvis(nq);
+  std::vector<float> dists(size_t(nq) * p.k);
+  std::vector<uint64_t> dc(nq);
+  check(gann_hnsw_search(h.handle(), queries, nq, p.k, p.beam, p.k, p.epsilon, GANN_VISITED_FAST, ids.data(),
+                         dists.data(), nvis.data(), dc.data()));
+  std::vector<SearchResult> out(nq);
+  for (uint32_t q = 0; q < nq; q++) {
+    for (uint32_t t = 0; t < p.k; t++)
+      if (ids[size_t(q) * p.k + t] != GANN_NONE)
+        out[q].neighbors.push_back({ids[size_t(q) * p.k + t], dists[size_t(q) * p.k + t]});
+    out[q].dist_comps = dc[q];
+  }
+  return out;
+}
+
 // ---- free functions with the reference's names ------------------------------------
 inline Index build_diskann(const void* points, uint64_t n, uint32_t d, ElemKind elem, Metric metric,
                            const DiskannParams& p, int device = 0) {

@@ -88,6 +88,12 @@ class Oracle:
         f("load_graph").argtypes = [C.c_char_p, vp, vp, vp, vp, u64]
         if prefix == "ref":
             L.ref_write_vectors.argtypes = [vp, u32, u32, i32, C.c_char_p, i32]
+            L.ref_hnsw_build.argtypes = [vp, u32, u32, i32, i32, u32, u32, f32, i32, u64, i32, i32, vp, vp, vp]
+            L.ref_hnsw_export.argtypes = [u32, u32, vp, vp, vp]
+            L.ref_hnsw_search.argtypes = [u32, vp, u32, u32, i32, i32, vp, u32, u32, u32, f32, vp, vp, vp, vp,
+                                          vp, u32, i32]
+            L.ref_hnsw_free.argtypes = [u32]
+            L.ref_hnsw_free.restype = None
         f("recall").restype = C.c_double
         f("recall").argtypes = [vp, vp, u32, vp, u32, u32]
         self._f = f
@@ -256,6 +262,46 @@ class Oracle:
         data = np.ascontiguousarray(data)
         self._check(self.lib.ref_write_vectors(_p(data), data.shape[0], data.shape[1], ELEM[data.dtype],
                                                str(path).encode(), 0 if fmt == "bin" else 1))
+
+    # ---- layered (HNSW) index: the reference's build_hnsw / search_hnsw ------
+    def hnsw_build(self, data, m, ef, alpha=1.2, rule="scale_candidate", metric="l2", seed=42,
+                   single_layer=False, workers=0):
+        """graphann::build_hnsw; returns (handle, levels, entry, layers) where
+        layers[l] is the (n, cap_l) row array of layer l (0 = bottom)."""
+        data = np.ascontiguousarray(data)
+        n = data.shape[0]
+        h, nl, e = (np.zeros(1, np.uint32) for _ in range(3))
+        self._check(self.lib.ref_hnsw_build(_p(data), n, data.shape[1], ELEM[data.dtype], METRIC[metric], m, ef,
+                                            alpha, RULE[rule], seed, int(single_layer), workers, _p(h), _p(nl),
+                                            _p(e)))
+        nl = int(nl[0])
+        cap = 2 * m
+        levels = np.empty(n, np.uint32)
+        caps = np.empty(nl, np.uint32)
+        adj = np.empty((nl, n, cap), np.uint32)
+        self._check(self.lib.ref_hnsw_export(int(h[0]), cap, _p(levels), _p(caps), _p(adj)))
+        layers = [np.ascontiguousarray(adj[l, :, :int(caps[l])]) for l in range(nl)]
+        return int(h[0]), levels, int(e[0]), layers
+
+    def hnsw_search(self, handle, data, queries, L, k, eps=0.0, metric="l2", vcap=0, workers=0):
+        data = np.ascontiguousarray(data)
+        queries = np.ascontiguousarray(queries, dtype=data.dtype)
+        nq = queries.shape[0]
+        ids = np.empty((nq, k), np.uint32)
+        dists = np.empty((nq, k), np.float32)
+        nvis = np.empty(nq, np.uint32)
+        dc = np.empty(nq, np.uint64)
+        vi = np.full((nq, vcap), SENT, np.uint32) if vcap else None
+        self._check(self.lib.ref_hnsw_search(handle, _p(data), data.shape[0], data.shape[1], ELEM[data.dtype],
+                                             METRIC[metric], _p(queries), nq, L, k, eps, _p(ids), _p(dists),
+                                             _p(nvis), _p(dc), _p(vi), vcap, workers))
+        out = dict(ids=ids, dists=dists, n_visited=nvis, dist_comps=dc)
+        if vcap:
+            out["visited_ids"] = vi
+        return out
+
+    def hnsw_free(self, handle):
+        self.lib.ref_hnsw_free(handle)
 
     def recall(self, truth_ids, truth_dists, result, k):
         ti = np.ascontiguousarray(truth_ids, dtype=np.uint32)

@@ -79,6 +79,16 @@ ORACLE_DECLS(orc_)
 ORACLE_DECLS(ref_)
 /* reference only: graphann::write_vectors (src/dataset.cpp:124-140); format 0 = bin, 1 = vecs */
 int ref_write_vectors(const void* data, uint32_t n, uint32_t d, int elem, const char* path, int format);
+/* reference only: graphann::build_hnsw / search_hnsw (src/hnsw.cpp) behind a handle */
+int ref_hnsw_build(const void* data, uint32_t n, uint32_t d, int elem, int metric, uint32_t m, uint32_t ef,
+                   float alpha, int rule, uint64_t seed, int single_layer, int workers, uint32_t* handle,
+                   uint32_t* num_layers, uint32_t* entry);
+int ref_hnsw_export(uint32_t handle, uint32_t cap, uint32_t* levels, uint32_t* caps, uint32_t* adj);
+int ref_hnsw_search(uint32_t handle, const void* data, uint32_t n, uint32_t d, int elem, int metric,
+                    const void* queries, uint32_t nq, uint32_t L, uint32_t k, float eps, uint32_t* ids,
+                    float* dists, uint32_t* n_visited, uint64_t* dist_comps, uint32_t* vis_ids,
+                    uint32_t vcap, int workers);
+void ref_hnsw_free(uint32_t handle);
 #ifdef __cplusplus
 }
 #endif

@@ -18,9 +18,13 @@
 //                        public API
 //   ref_groundtruth      graphann::compute_groundtruth (src/dataset.cpp:172)
 //   ref_recall           graphann::recall_k_at_n      (src/eval.cpp:14)
+//   ref_hnsw_build       graphann::build_hnsw         (src/hnsw.cpp; kept behind a handle)
+//   ref_hnsw_export      the handle's levels / entry / layer graphs as flat arrays
+//   ref_hnsw_search      graphann::search_hnsw        (src/hnsw.cpp:130-147)
 #include <chrono>
 #include <cstring>
 #include <limits>
+#include <memory>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -31,6 +35,7 @@
 #include "graphann/diskann.hpp"
 #include "graphann/eval.hpp"
 #include "graphann/graph.hpp"
+#include "graphann/hnsw.hpp"
 #include "graphann/parallel.hpp"
 #include "graphann/prune.hpp"
 #include "graphann/search.hpp"
@@ -379,6 +384,83 @@ double ref_recall(const uint32_t* truth_ids, const float* truth_dists, uint32_t 
     g_err = e.what();
     return -1.0;
   }
+}
+
+// ---- layered (HNSW) search: the reference's own builder and search_hnsw ----
+// The built HnswIndex stays inside the shim (its members are private to the
+// reference's build/load functions); tests export its layers for the GPU.
+static std::vector<std::unique_ptr<HnswIndex>> g_hnsw;
+
+int ref_hnsw_build(const void* data, uint32_t n, uint32_t d, int elem, int metric, uint32_t m,
+                   uint32_t ef, float alpha, int rule, uint64_t seed, int single_layer, int workers,
+                   uint32_t* handle, uint32_t* num_layers, uint32_t* entry) {
+  return guarded([&] {
+    VectorDataset ds = make_ds(data, n, d, elem);
+    HnswParams p;
+    p.m = m;
+    p.ef_construction = ef;
+    p.alpha = alpha;
+    p.rule = rul(rule);
+    p.seed = seed;
+    p.single_layer = single_layer != 0;
+    g_hnsw.push_back(std::make_unique<HnswIndex>(
+        build_hnsw(ds, met(metric), p, static_cast<size_t>(workers < 0 ? 0 : workers))));
+    const HnswIndex& h = *g_hnsw.back();
+    *handle = static_cast<uint32_t>(g_hnsw.size() - 1);
+    *num_layers = h.num_layers();
+    *entry = h.entry();
+  });
+}
+
+// levels[n]; adj holds layer l's rows at (l * n + v) * cap, cap >= every layer's capacity
+int ref_hnsw_export(uint32_t handle, uint32_t cap, uint32_t* levels, uint32_t* caps, uint32_t* adj) {
+  return guarded([&] {
+    if (handle >= g_hnsw.size() || !g_hnsw[handle]) throw std::invalid_argument("bad hnsw handle");
+    const HnswIndex& h = *g_hnsw[handle];
+    const uint32_t n = h.size();
+    for (uint32_t v = 0; v < n; v++) levels[v] = h.level(v);
+    for (uint32_t l = 0; l < h.num_layers(); l++) {
+      const NeighborGraph& g = h.layer(l);
+      if (g.capacity() > cap) throw std::invalid_argument("layer capacity above cap");
+      caps[l] = g.capacity();
+      for (uint32_t v = 0; v < n; v++) {
+        auto nb = g.out_neighbors(v);
+        uint32_t* r = adj + (static_cast<size_t>(l) * n + v) * cap;
+        for (uint32_t t = 0; t < cap; t++) r[t] = t < nb.size() ? nb[t] : kSent;
+      }
+    }
+  });
+}
+
+int ref_hnsw_search(uint32_t handle, const void* data, uint32_t n, uint32_t d, int elem, int metric,
+                    const void* queries, uint32_t nq, uint32_t L, uint32_t k, float eps, uint32_t* ids,
+                    float* dists, uint32_t* n_visited, uint64_t* dist_comps, uint32_t* vis_ids,
+                    uint32_t vcap, int workers) {
+  return guarded([&] {
+    if (handle >= g_hnsw.size() || !g_hnsw[handle]) throw std::invalid_argument("bad hnsw handle");
+    const HnswIndex& h = *g_hnsw[handle];
+    VectorDataset ds = make_ds(data, n, d, elem);
+    const size_t stride = ds.stride();
+    const std::byte* qb = static_cast<const std::byte*>(queries);
+    SearchParams sp{L, k, eps};
+    parallel_for(nq, static_cast<size_t>(workers < 0 ? 0 : workers), [&](size_t qi, size_t) {
+      VectorView q{qb + qi * stride, d, kind(elem)};
+      SearchResult r = search_hnsw(h, ds, met(metric), q, sp, nullptr);
+      for (uint32_t t = 0; t < k; t++) {
+        bool have = t < r.neighbors.size();
+        ids[qi * k + t] = have ? r.neighbors[t].id : kSent;
+        dists[qi * k + t] = have ? r.neighbors[t].dist : std::numeric_limits<float>::infinity();
+      }
+      n_visited[qi] = static_cast<uint32_t>(r.visited.size());
+      if (dist_comps) dist_comps[qi] = r.dist_comps;
+      if (vis_ids)
+        for (uint32_t t = 0; t < vcap && t < r.visited.size(); t++) vis_ids[qi * vcap + t] = r.visited[t].id;
+    });
+  });
+}
+
+void ref_hnsw_free(uint32_t handle) {
+  if (handle < g_hnsw.size()) g_hnsw[handle].reset();
 }
 
 }  // extern "C"

@@ -6,14 +6,15 @@ interface over that ABI. Importing it loads the shared object and fails loudly
 if it is missing — there is no CPU fallback.
 """
 from ._lib import GANN_NONE, GannError, LIB_PATH, lib
-from .api import (DiskannParams, GroupedPairs, Index, PruneParams, SearchParams, SearchResult,
+from .api import (DiskannParams, GroupedPairs, HnswIndex, Index, PruneParams, SearchParams, SearchResult,
                   alpha_prune, apply_back_edges, batch_ranges, beam_search, build_diskann,
-                  choose_start, group_by_key, insert_point, insert_seed, shuffled_order)
+                  choose_start, group_by_key, insert_point, insert_seed, search_hnsw, shuffled_order)
 
 lib()  # load now: a missing/unbuildable extension is an import error, not a silent fallback
 
 __all__ = [
-    "GANN_NONE", "GannError", "LIB_PATH", "DiskannParams", "GroupedPairs", "Index", "PruneParams",
+    "GANN_NONE", "GannError", "LIB_PATH", "DiskannParams", "GroupedPairs", "HnswIndex", "Index", "PruneParams",
     "SearchParams", "SearchResult", "alpha_prune", "apply_back_edges", "batch_ranges", "beam_search",
-    "build_diskann", "choose_start", "group_by_key", "insert_point", "insert_seed", "shuffled_order",
+    "build_diskann", "choose_start", "group_by_key", "insert_point", "insert_seed", "search_hnsw",
+    "shuffled_order",
 ]

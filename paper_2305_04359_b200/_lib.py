@@ -81,6 +81,9 @@ SIGNATURES = {
     "gann_load_graph": (_i, [_vp, C.c_char_p]),
     "gann_index_create_from_file": (_i, [C.c_char_p, _i, _u32, _i, _pp]),
     "gann_range_search": (_i, [_vp, _vp, _u32, _f, _u32, _f, _u32, _vp, _vp, _vp]),
+    "gann_hnsw_create": (_i, [_vp, _u32, _vp, _u32, _u32, _pp]),
+    "gann_hnsw_search": (_i, [_vp, _vp, _u32, _u32, _u32, _u32, _f, _i, _vp, _vp, _vp, _vp]),
+    "gann_hnsw_free": (None, [_vp]),
     "gann_index_create_part": (_i, [_vp, _u64, _u32, _i, _i, _u32, _u32, _u32, _i, _pp]),
     "gann_index_create_part_device": (_i, [_vp, _u64, _u32, _i, _i, _u32, _u32, _u32, _i, _pp]),
     "gann_import_graph_device": (_i, [_vp, _vp, _u32]),

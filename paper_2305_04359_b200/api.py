@@ -315,6 +315,62 @@ class Index:
 
 
 # ---- module-level mirrors of the reference's free functions ------------------------
+class HnswIndex:
+    """A layered index (graphann::HnswIndex, include/graphann/hnsw.hpp) searched
+    on the GPU with graphann::search_hnsw semantics (src/hnsw.cpp:130-147).
+
+    ``layer0`` is an :class:`Index` holding the points and the bottom graph
+    (borrowed: keep it alive); ``upper`` lists the graphs of layers 1..top as
+    (n, m) id arrays over the same id space (rows of non-members are empty);
+    ``entry`` is the top layer's entry vertex. The layers come from a builder
+    outside this path (the reference's build_hnsw); the search is the product."""
+
+    def __init__(self, layer0: Index, upper, entry: int):
+        self.layer0 = layer0
+        upper = [np.ascontiguousarray(a, dtype=np.uint32) for a in upper]
+        m = upper[0].shape[1] if upper else 0
+        for a in upper:
+            if a.shape != (layer0.n, m):
+                raise ValueError(f"every upper layer must be ({layer0.n}, {m})")
+        flat = np.ascontiguousarray(np.stack(upper)) if upper else None
+        h = C.c_void_p()
+        check(lib().gann_hnsw_create(layer0.handle, 1 + len(upper), _p(flat), m, entry, C.byref(h)))
+        self._h = h
+        self.num_layers = 1 + len(upper)
+        self.entry = entry
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().gann_hnsw_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def search(self, queries: np.ndarray, params: SearchParams = SearchParams(), k_out: Optional[int] = None,
+               visited_mode: str = "fast") -> SearchResult:
+        queries = np.ascontiguousarray(queries)
+        if queries.ndim != 2 or queries.shape[1] != self.layer0.d or queries.dtype != self.layer0.dtype:
+            raise ValueError("query does not match dataset dimension/element kind")
+        nq = queries.shape[0]
+        k_out = params.k if k_out is None else k_out
+        ids = np.empty((nq, k_out), np.uint32)
+        dists = np.empty((nq, k_out), np.float32)
+        nvis = np.empty(nq, np.uint32)
+        dc = np.empty(nq, np.uint64)
+        check(lib().gann_hnsw_search(self._h, _p(queries), nq, k_out, params.beam, params.k, params.epsilon,
+                                     VISITED[visited_mode], _p(ids), _p(dists), _p(nvis), _p(dc)))
+        return SearchResult(ids, dists, nvis, dc)
+
+
+def search_hnsw(index: HnswIndex, queries: np.ndarray, params: SearchParams = SearchParams(), **kw) -> SearchResult:
+    """graphann::search_hnsw (src/hnsw.cpp:130-147), batched over queries."""
+    return index.search(queries, params, **kw)
+
+
 def build_diskann(points: np.ndarray, metric: str = "l2", params: DiskannParams = DiskannParams(),
                   device: int = 0) -> Index:
     """graphann::build_diskann (include/graphann/diskann.hpp:36-37)."""

@@ -1680,6 +1680,143 @@ int gann_part_phase2(gann_index* idx, uint32_t batch, const uint32_t* d_pairs, u
   });
 }
 
+// ---- layered (HNSW) search: search_hnsw, src/hnsw.cpp:130-147 ---------------
+// Layer 0 is an ordinary index (points + bottom graph). The upper layers are
+// graphs over the same id space (non-members have empty rows), held on the
+// device beside it. A query descends with beam {1, 1, 0} searches from the
+// entry vertex, layer by layer, each started at the previous layer's nearest
+// (start_override, in place on the device), then runs the bottom search from
+// there; dist_comps is the sum over all layers.
+struct gann_hnsw {
+  gann_index* base = nullptr;  // borrowed
+  uint32_t layers = 1;
+  uint32_t m = 0;              // upper-layer row capacity
+  uint32_t entry = 0;
+  uint32_t* upper = nullptr;   // (layers - 1) x n x m
+  DevBuf cur, dc, hd;
+};
+
+int gann_hnsw_create(gann_index* layer0, uint32_t num_layers, const uint32_t* upper_adj, uint32_t m_upper,
+                     uint32_t entry, gann_hnsw** out) {
+  return guarded([&] {
+    if (!layer0 || !out) fail(GANN_EINVAL, "NULL argument");
+    if (num_layers == 0) fail(GANN_EINVAL, "an HNSW index has at least one layer");
+    if (layer0->part_count != 1) fail(GANN_EINVAL, "layered search over a partitioned index is not supported");
+    const uint64_t n = layer0->n;
+    if (n && entry >= n) fail(GANN_EINVAL, "entry vertex out of range");
+    if (num_layers > 1) {
+      if (m_upper == 0 || m_upper > 1024) fail(GANN_EINVAL, "upper-layer capacity must lie in [1, 1024]");
+      if (!upper_adj) fail(GANN_EINVAL, "upper_adj is NULL");
+      const uint64_t words = uint64_t(num_layers - 1) * n * m_upper;
+      for (uint64_t i = 0; i < words; i++)
+        if (upper_adj[i] != GANN_NONE && upper_adj[i] >= n) fail(GANN_EINVAL, "neighbor id out of range");
+    }
+    set_device(layer0);
+    auto* h = new gann_hnsw();
+    h->base = layer0;
+    h->layers = num_layers;
+    h->m = num_layers > 1 ? m_upper : 0;
+    h->entry = entry;
+    if (num_layers > 1 && n) {
+      const size_t bytes = size_t(num_layers - 1) * n * m_upper * 4;
+      if (cudaMalloc(&h->upper, bytes) != cudaSuccess) {
+        delete h;
+        fail(GANN_ECUDA, "cudaMalloc upper layers");
+      }
+      cu(cudaMemcpy(h->upper, upper_adj, bytes, cudaMemcpyHostToDevice), "upload upper layers");
+    }
+    *out = h;
+  });
+}
+
+void gann_hnsw_free(gann_hnsw* h) {
+  if (!h) return;
+  cudaSetDevice(h->base->device);
+  if (h->base->stream) cudaStreamSynchronize(h->base->stream);
+  if (h->upper) cudaFree(h->upper);
+  for (DevBuf* b : {&h->cur, &h->dc, &h->hd}) b->release();
+  delete h;
+}
+
+int gann_hnsw_search(gann_hnsw* h, const void* queries, uint32_t nq, uint32_t k_out, uint32_t L, uint32_t k_gate,
+                     float eps, int visited_mode, uint32_t* ids, float* dists, uint32_t* n_visited,
+                     uint64_t* dist_comps) {
+  return guarded([&] {
+    if (!h) fail(GANN_EINVAL, "index is NULL");
+    gann_index* idx = h->base;
+    validate_search(idx, k_out, L, k_gate, eps, visited_mode);
+    if (nq == 0) return;
+    if (!queries) fail(GANN_EINVAL, "queries is NULL");
+    set_device(idx);
+    if (idx->n == 0) {  // src/hnsw.cpp:134 — empty index, empty result
+      for (uint64_t i = 0; i < uint64_t(nq) * k_out; i++) {
+        if (ids) ids[i] = GANN_NONE;
+        if (dists) dists[i] = __builtin_inff();
+      }
+      for (uint32_t i = 0; i < nq; i++) {
+        if (n_visited) n_visited[i] = 0;
+        if (dist_comps) dist_comps[i] = 0;
+      }
+      return;
+    }
+    const uint8_t* q = stage_rows(idx, idx->q, queries, nq, false);
+    h->cur.ensure(size_t(nq) * 4);
+    h->dc.ensure(size_t(nq) * 8 * h->layers);
+    h->hd.ensure(size_t(nq) * 4);
+    uint32_t* cur = h->cur.as<uint32_t>();
+    uint64_t* dc = h->dc.as<uint64_t>();
+    {
+      std::vector<uint32_t> e(nq, h->entry);
+      cu(cudaMemcpyAsync(cur, e.data(), size_t(nq) * 4, cudaMemcpyHostToDevice, idx->stream), "upload entry");
+      sync(idx);  // e leaves scope
+    }
+    // upper layers, top down: beam {1, 1, 0} from cur, the nearest found becomes cur
+    for (uint32_t l = h->layers - 1; l >= 1; l--) {
+      SearchArgs a = base_search_args(idx, 1, 1, 1, 0.0f, visited_mode);
+      a.graph = GraphView{h->upper + size_t(l - 1) * idx->n * h->m, nullptr, 0, 1, 0};
+      a.R = h->m;
+      a.queries = q;
+      a.nq = nq;
+      a.start_override = cur;
+      a.out_ids = cur;  // a query reads its start before it writes its result
+      a.out_dists = h->hd.as<float>();
+      a.dist_comps = dc + size_t(l) * nq;
+      run_search(idx, a, idx->stream);
+    }
+    SearchArgs a = base_search_args(idx, L, k_gate, k_out, eps, visited_mode);
+    a.queries = q;
+    a.nq = nq;
+    a.start_override = cur;
+    if (k_out) {
+      idx->qids.ensure(size_t(nq) * k_out * 4);
+      idx->qdists.ensure(size_t(nq) * k_out * 4);
+      a.out_ids = idx->qids.as<uint32_t>();
+      a.out_dists = idx->qdists.as<float>();
+    }
+    idx->qnvis.ensure(size_t(nq) * 4);
+    a.n_visited = idx->qnvis.as<uint32_t>();
+    a.dist_comps = dc;
+    run_search(idx, a, idx->stream);
+    auto d2h = [&](void* dst, const void* src, size_t bytes) {
+      if (dst) cu(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, idx->stream), "download results");
+    };
+    if (k_out) {
+      d2h(ids, a.out_ids, size_t(nq) * k_out * 4);
+      d2h(dists, a.out_dists, size_t(nq) * k_out * 4);
+    }
+    d2h(n_visited, a.n_visited, size_t(nq) * 4);
+    std::vector<uint64_t> all(dist_comps ? size_t(nq) * h->layers : 0);
+    if (dist_comps) d2h(all.data(), dc, all.size() * 8);
+    sync(idx);
+    if (dist_comps)
+      for (uint32_t i = 0; i < nq; i++) {
+        uint64_t t = 0;
+        for (uint32_t l = 0; l < h->layers; l++) t += all[size_t(l) * nq + i];
+        dist_comps[i] = t;
+      }
+  });
+}
+
 int gann_get_stats(const gann_index* idx, gann_stats* out) {
   return guarded([&] {
     if (!idx || !out) fail(GANN_EINVAL, "NULL argument");

@@ -1,0 +1,90 @@
+"""Layered (HNSW) search on the GPU: graphann::search_hnsw
+(src/hnsw.cpp:130-147) over layers built by the reference's own build_hnsw,
+checked against the reference's search_hnsw. Mirrors acceptance criterion 9
+(proj/tests/acceptance.cpp:513-535, a single-layer index searches exactly like
+a plain beam search) and uses its desk parameters (m=16, ef=64)."""
+import numpy as np
+import pytest
+
+from helpers import mixture
+
+pytestmark = pytest.mark.gpu
+
+
+def _g():
+    import paper_2305_04359_b200 as g
+    return g
+
+
+@pytest.fixture(scope="module")
+def ref():
+    from oracle.oracle import Oracle, available
+    if not available("ref"):
+        pytest.skip("the reference build_hnsw/search_hnsw need oracle/_ref")
+    return Oracle("ref")
+
+
+def gpu_layers(data, levels, entry, layers, metric="l2"):
+    g = _g()
+    idx0 = g.Index(data, metric, layers[0].shape[1])
+    idx0.import_graph(layers[0], entry)
+    return idx0, g.HnswIndex(idx0, layers[1:], entry)
+
+
+@pytest.mark.parametrize("dtype,d,metric", [(np.uint8, 32, "l2"), (np.int8, 24, "ip"), (np.float32, 16, "l2")])
+@pytest.mark.parametrize("L,k,eps", [(10, 10, 0.0), (64, 10, 0.1), (32, 32, 0.0)])
+def test_hnsw_search_parity(ref, dtype, d, metric, L, k, eps):
+    """ids, distances, |V| identical to graphann's search_hnsw over the same
+    layers (f32: distances within 1e-5 relative, ids equal); REF visited mode
+    also reproduces dist_comps summed over all layers."""
+    g = _g()
+    data, qs = mixture(61, 5000, d, clusters=12, dtype=dtype, nq=300)
+    h, levels, entry, layers = ref.hnsw_build(data, 16, 64, metric=metric, workers=4)
+    assert len(layers) >= 2, "the test needs upper layers"
+    idx0, hn = gpu_layers(data, levels, entry, layers, metric)
+    want = ref.hnsw_search(h, data, qs, L, k, eps, metric=metric, workers=4)
+    for mode in ("fast", "ref"):
+        got = hn.search(qs, g.SearchParams(L, k, eps), visited_mode=mode)
+        if dtype == np.float32:
+            assert (got.ids == want["ids"]).mean() > 0.999
+            np.testing.assert_allclose(got.dists, want["dists"], rtol=1e-5)
+        else:
+            assert (got.ids == want["ids"]).all()
+            assert (got.dists == want["dists"]).all()
+            assert (got.n_visited == want["n_visited"]).all()
+            if mode == "ref":
+                assert (got.dist_comps == want["dist_comps"]).all()
+    ref.hnsw_free(h)
+
+
+def test_single_layer_equals_plain_search(ref):
+    """Acceptance criterion 9: with every level forced to 0 the layered search
+    is the plain beam search over layer 0 (same ids, dists, |V|, dist_comps)."""
+    g = _g()
+    data, qs = mixture(62, 4000, 16, clusters=10, dtype=np.float32, nq=200)
+    h, levels, entry, layers = ref.hnsw_build(data, 16, 64, single_layer=True, workers=4)
+    assert len(layers) == 1 and (levels == 0).all()
+    idx0, hn = gpu_layers(data, levels, entry, layers)
+    sp = g.SearchParams(64, 10, 0.1)
+    a = hn.search(qs, sp, visited_mode="ref")
+    b = idx0.search(qs, sp, visited_mode="ref")
+    assert (a.ids == b.ids).all() and (a.dists == b.dists).all()
+    assert (a.n_visited == b.n_visited).all() and (a.dist_comps == b.dist_comps).all()
+    want = ref.hnsw_search(h, data, qs, 64, 10, 0.1, workers=4)
+    assert (a.ids == want["ids"]).mean() > 0.999
+    ref.hnsw_free(h)
+
+
+def test_hnsw_validation():
+    g = _g()
+    data = mixture(63, 200, 8)
+    idx0 = g.Index(data, "l2", 8)
+    with pytest.raises(ValueError):
+        g.HnswIndex(idx0, [np.zeros((100, 4), np.uint32)], 0)      # wrong row count
+    with pytest.raises(ValueError):
+        g.HnswIndex(idx0, [np.full((200, 4), 500, np.uint32)], 0)  # ids out of range
+    with pytest.raises(ValueError):
+        g.HnswIndex(idx0, [], 999)                                  # entry out of range
+    hn = g.HnswIndex(idx0, [np.full((200, 4), g.GANN_NONE, np.uint32)], 3)
+    with pytest.raises(ValueError):
+        hn.search(data[:2], g.SearchParams(4, 8, 0.0))              # k > L
