@@ -93,6 +93,10 @@ class Oracle:
             L.ref_hnsw_search.argtypes = [u32, vp, u32, u32, i32, i32, vp, u32, u32, u32, f32, vp, vp, vp, vp,
                                           vp, u32, i32]
             L.ref_hnsw_free.argtypes = [u32]
+            d64 = C.c_double
+            L.ref_pareto.argtypes = [u32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+            L.ref_write_csv.argtypes = [C.c_char_p, C.c_char_p, u32, d64, u64, u32, vp, vp, vp, vp, vp, vp, vp,
+                                        C.c_char_p]
             L.ref_hnsw_free.restype = None
         f("recall").restype = C.c_double
         f("recall").argtypes = [vp, vp, u32, vp, u32, u32]
@@ -302,6 +306,31 @@ class Oracle:
 
     def hnsw_free(self, handle):
         self.lib.ref_hnsw_free(handle)
+
+    # ---- eval harness -----------------------------------------------------------
+    @staticmethod
+    def _row_arrays(rows):
+        return (np.array([r.beam for r in rows], np.uint32), np.array([r.k for r in rows], np.uint32),
+                np.array([r.epsilon for r in rows], np.float32), np.array([r.recall for r in rows], np.float64),
+                np.array([r.qps for r in rows], np.float64), np.array([r.latency_ms for r in rows], np.float64),
+                np.array([r.dist_comps for r in rows], np.float64))
+
+    def pareto(self, rows):
+        """graphann::pareto_frontier; returns (beam, k, eps, recall, qps) tuples."""
+        a = self._row_arrays(rows)
+        n = len(rows)
+        no = np.zeros(1, np.uint32)
+        outs = [np.empty(n, np.uint32), np.empty(n, np.uint32), np.empty(n, np.float32), np.empty(n, np.float64),
+                np.empty(n, np.float64)]
+        self._check(self.lib.ref_pareto(n, *[_p(x) for x in a], _p(no), *[_p(x) for x in outs]))
+        m = int(no[0])
+        return [(int(outs[0][i]), int(outs[1][i]), float(outs[2][i]), float(outs[3][i]), float(outs[4][i]))
+                for i in range(m)]
+
+    def write_csv(self, meta, rows, path):
+        a = self._row_arrays(rows)
+        self._check(self.lib.ref_write_csv(meta.algorithm.encode(), meta.dataset.encode(), meta.n, meta.build_seconds,
+                                           meta.threads, len(rows), *[_p(x) for x in a], str(path).encode()))
 
     def recall(self, truth_ids, truth_dists, result, k):
         ti = np.ascontiguousarray(truth_ids, dtype=np.uint32)

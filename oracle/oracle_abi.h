@@ -89,6 +89,13 @@ int ref_hnsw_search(uint32_t handle, const void* data, uint32_t n, uint32_t d, i
                     float* dists, uint32_t* n_visited, uint64_t* dist_comps, uint32_t* vis_ids,
                     uint32_t vcap, int workers);
 void ref_hnsw_free(uint32_t handle);
+/* reference only: graphann::pareto_frontier / write_csv (src/eval.cpp:205-254) on given rows */
+int ref_pareto(uint32_t nrows, const uint32_t* beams, const uint32_t* ks, const float* eps, const double* recall,
+               const double* qps, const double* lat, const double* dc, uint32_t* n_out, uint32_t* beams_o,
+               uint32_t* ks_o, float* eps_o, double* recall_o, double* qps_o);
+int ref_write_csv(const char* algorithm, const char* dataset, uint32_t n, double build_seconds, uint64_t threads,
+                  uint32_t nrows, const uint32_t* beams, const uint32_t* ks, const float* eps, const double* recall,
+                  const double* qps, const double* lat, const double* dc, const char* path);
 #ifdef __cplusplus
 }
 #endif

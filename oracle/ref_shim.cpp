@@ -21,7 +21,11 @@
 //   ref_hnsw_build       graphann::build_hnsw         (src/hnsw.cpp; kept behind a handle)
 //   ref_hnsw_export      the handle's levels / entry / layer graphs as flat arrays
 //   ref_hnsw_search      graphann::search_hnsw        (src/hnsw.cpp:130-147)
+//   ref_pareto           graphann::pareto_frontier    (src/eval.cpp:205-225)
+//   ref_write_csv        graphann::write_csv          (src/eval.cpp:236-254)
 #include <chrono>
+#include <cstdio>
+#include <sstream>
 #include <cstring>
 #include <limits>
 #include <memory>
@@ -461,6 +465,56 @@ int ref_hnsw_search(uint32_t handle, const void* data, uint32_t n, uint32_t d, i
 
 void ref_hnsw_free(uint32_t handle) {
   if (handle < g_hnsw.size()) g_hnsw[handle].reset();
+}
+
+// ---- eval harness: pareto_frontier / write_csv on caller-given rows ----------
+static std::vector<EvalRow> rows_of(uint32_t nrows, const uint32_t* beams, const uint32_t* ks, const float* eps,
+                                    const double* recall, const double* qps, const double* lat, const double* dc) {
+  std::vector<EvalRow> rows(nrows);
+  for (uint32_t i = 0; i < nrows; i++) rows[i] = {beams[i], ks[i], eps[i], recall[i], qps[i], lat[i], dc[i]};
+  return rows;
+}
+
+int ref_pareto(uint32_t nrows, const uint32_t* beams, const uint32_t* ks, const float* eps, const double* recall,
+               const double* qps, const double* lat, const double* dc, uint32_t* n_out, uint32_t* beams_o,
+               uint32_t* ks_o, float* eps_o, double* recall_o, double* qps_o) {
+  return guarded([&] {
+    std::vector<EvalRow> rows = rows_of(nrows, beams, ks, eps, recall, qps, lat, dc);
+    std::vector<EvalRow> f = pareto_frontier(rows);
+    *n_out = static_cast<uint32_t>(f.size());
+    for (size_t i = 0; i < f.size(); i++) {
+      beams_o[i] = f[i].beam;
+      ks_o[i] = f[i].k;
+      eps_o[i] = f[i].epsilon;
+      recall_o[i] = f[i].recall;
+      qps_o[i] = f[i].qps;
+    }
+  });
+}
+
+int ref_write_csv(const char* algorithm, const char* dataset, uint32_t n, double build_seconds, uint64_t threads,
+                  uint32_t nrows, const uint32_t* beams, const uint32_t* ks, const float* eps, const double* recall,
+                  const double* qps, const double* lat, const double* dc, const char* path) {
+  return guarded([&] {
+    EvalReport r;
+    r.meta.algorithm = algorithm;
+    r.meta.dataset = dataset;
+    r.meta.n = n;
+    r.meta.build_seconds = build_seconds;
+    r.meta.threads = threads;
+    r.rows = rows_of(nrows, beams, ks, eps, recall, qps, lat, dc);
+    // the stream overload (src/eval.cpp:236-245) into memory, then plain stdio:
+    // the path overload's std::ofstream crashes inside a process that has
+    // loaded numpy's bundled runtime libraries
+    std::ostringstream os;
+    write_csv(r, os);
+    const std::string text = os.str();
+    FILE* f = std::fopen(path, "wb");
+    if (!f) throw io_error(std::string("cannot open for writing: ") + path);
+    const size_t wrote = std::fwrite(text.data(), 1, text.size(), f);
+    std::fclose(f);
+    if (wrote != text.size()) throw io_error(std::string("write failed: ") + path);
+  });
 }
 
 }  // extern "C"

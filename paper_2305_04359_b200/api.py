@@ -220,6 +220,18 @@ class Index:
             vd[pad] = np.inf
         return SearchResult(ids, dists, nvis, dc, vi, vd)
 
+    def run_sweep(self, queries: np.ndarray, truth_ids: np.ndarray, truth_dists: np.ndarray, sweep, meta,
+                  visited_mode: str = "fast"):
+        """graphann::run_sweep (src/eval.cpp:127-168) with this index's batched
+        search as the dispatch: one gann_search call over all queries per sweep
+        point and repetition (evalutil.run_sweep)."""
+        from .evalutil import run_sweep
+
+        def one(beam, k, eps):
+            r = self.search(queries, SearchParams(beam, k, eps), k_out=k, visited_mode=visited_mode)
+            return r.ids, r.dist_comps
+        return run_sweep(one, truth_ids, truth_dists, sweep, meta)
+
     def search_device(self, q_ptr: int, nq: int, params: SearchParams, k_out: int, ids_ptr: int,
                       dists_ptr: int, nvis_ptr: int = 0, dc_ptr: int = 0, stream: int = 0,
                       visited_mode: str = "fast") -> None:
@@ -364,6 +376,19 @@ class HnswIndex:
         check(lib().gann_hnsw_search(self._h, _p(queries), nq, k_out, params.beam, params.k, params.epsilon,
                                      VISITED[visited_mode], _p(ids), _p(dists), _p(nvis), _p(dc)))
         return SearchResult(ids, dists, nvis, dc)
+
+
+def _hnsw_run_sweep(self, queries, truth_ids, truth_dists, sweep, meta, visited_mode: str = "fast"):
+    """run_sweep with search_hnsw as the dispatch (the reference's layered_dispatch)."""
+    from .evalutil import run_sweep
+
+    def one(beam, k, eps):
+        r = self.search(queries, SearchParams(beam, k, eps), k_out=k, visited_mode=visited_mode)
+        return r.ids, r.dist_comps
+    return run_sweep(one, truth_ids, truth_dists, sweep, meta)
+
+
+HnswIndex.run_sweep = _hnsw_run_sweep
 
 
 def search_hnsw(index: HnswIndex, queries: np.ndarray, params: SearchParams = SearchParams(), **kw) -> SearchResult:

@@ -88,3 +88,39 @@ def test_hnsw_validation():
     hn = g.HnswIndex(idx0, [np.full((200, 4), g.GANN_NONE, np.uint32)], 3)
     with pytest.raises(ValueError):
         hn.search(data[:2], g.SearchParams(4, 8, 0.0))              # k > L
+
+
+def test_run_sweep_over_gpu_indexes(ref, tmp_path):
+    """The eval harness over the flat and the layered GPU
+    index: every (beam, k, eps) row's recall is graphann's recall_k_at_n of the
+    reference's own search results at the same parameters (the ids are equal),
+    dist_comps is the per-query mean, and the CSV has graphann's layout."""
+    g = _g()
+    from paper_2305_04359_b200 import evalutil as E
+    data, qs = mixture(64, 5000, 32, clusters=12, nq=200)
+    tid, td = ref.groundtruth(data, qs, 20, workers=4)
+    adj, start = ref.build(data, 24, 48, 1.2, workers=4)
+    idx = g.Index(data, "l2", 24)
+    idx.import_graph(adj, start)
+    sweep = E.SweepConfig(beams=[10, 32], ks=[10], epsilons=[0.0, 0.1], repetitions=2)
+    rep = idx.run_sweep(qs, tid, td, sweep, E.EvalMeta("diskann", "mixture", len(data)))
+    assert len(rep.rows) == 4
+    for r in rep.rows:
+        want = ref.beam_search(adj, start, data, qs, r.beam, r.k, r.epsilon, workers=4)
+        assert r.recall == pytest.approx(ref.mean_recall(tid, td, want["ids"], r.k), abs=1e-12)
+        got = idx.search(qs, g.SearchParams(r.beam, r.k, r.epsilon))
+        assert r.dist_comps == pytest.approx(got.dist_comps.mean())
+    assert [(r.recall, r.qps) for r in E.pareto_frontier(rep.rows)] == \
+        [(b[3], b[4]) for b in ref.pareto(rep.rows)]
+    h, levels, entry, layers = ref.hnsw_build(data, 16, 64, workers=4)
+    _, hn = gpu_layers(data, levels, entry, layers)
+    hrep = hn.run_sweep(qs, tid, td, sweep, E.EvalMeta("hnsw", "mixture", len(data)))
+    for r in hrep.rows:
+        want = ref.hnsw_search(h, data, qs, r.beam, r.k, r.epsilon, workers=4)
+        assert r.recall == pytest.approx(ref.mean_recall(tid, td, want["ids"], r.k), abs=1e-12)
+    ref.hnsw_free(h)
+    import io
+    buf = io.StringIO()
+    E.write_csv(rep, buf)
+    ref.write_csv(rep.meta, rep.rows, tmp_path / "r.csv")
+    assert buf.getvalue() == (tmp_path / "r.csv").read_text()
