@@ -247,7 +247,12 @@ def setup(args):
             build_mode = "replicated: every rank builds the whole graph"
         bstats = idx.stats()
     adj_t = _tensor_from_ptr(idx.device_ptrs()[2], n * cfg.R * 4).view(torch.int32)  # a view, no copy
-    checksum = int(adj_t.to(torch.int64).mul_(1 + torch.arange(n * cfg.R, device="cuda") % 7919).sum().item())
+    checksum, CH = 0, 1 << 28  # chunked: an int64 copy of a 100M-row graph would not fit beside it
+    for c0 in range(0, n * cfg.R, CH):
+        c1 = min(n * cfg.R, c0 + CH)
+        w = 1 + torch.arange(c0, c1, device="cuda") % 7919
+        checksum += int(adj_t[c0:c1].to(torch.int64).mul_(w).sum().item())
+    checksum &= (1 << 63) - 1
     replicas_identical = distutil.replicas_identical(checksum, dist if world > 1 else None)
     deg_mean = float((adj_t != -1).sum().item()) / n
     del adj_t

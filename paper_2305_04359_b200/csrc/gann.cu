@@ -96,12 +96,13 @@ uint32_t env_u32(const char* name, uint32_t dflt) {
   return v && *v ? static_cast<uint32_t>(std::strtoul(v, nullptr, 10)) : dflt;
 }
 
-// Shared-memory visited table size of the fast search mode (direct mapped,
-// overwrite on collision): a pure performance knob — it trades re-evaluated
-// rows against per-warp shared memory, i.e. resident warps.
-// With n <= 2^(log2 + 15) a slot stores the 15-bit remainder of a bijective
-// hash of the id (half the bytes of an id slot, so twice the entries for the
-// same shared memory, still no false positives).
+// Shared-memory visited table of the fast search mode: a pure performance
+// knob — it trades re-evaluated rows against per-warp shared memory, i.e.
+// resident warps; it never reports a false positive, so results do not
+// depend on it. A slot stores the 15-bit remainder of a bijective hash of the
+// id while n fits (half the bytes of an id slot, so twice the entries); a
+// bucket of 4 (2, 1) slots then covers n <= 2^(log2 + 13) (+14, +15). Larger
+// n store whole ids, in buckets of 4 as well.
 void hash_config(uint32_t L, uint64_t n, uint32_t* log2, uint32_t* bits, uint32_t* ways) {
   const uint32_t forced = std::min<uint32_t>(env_u32("GANN_HASH_LOG2", 0), 15);
   const bool narrow = env_u32("GANN_HASH16", 1) != 0;
@@ -118,9 +119,11 @@ void hash_config(uint32_t L, uint64_t n, uint32_t* log2, uint32_t* bits, uint32_
     *bits = b;
     return;
   }
-  *ways = 1;
-  // u32 id slots; measured on B200 at 10M (tools/profile_search.py, HLOGS sweep)
-  *log2 = forced ? std::max<uint32_t>(forced, 5) : (L <= 160 ? 10 : 9);
+  // u32 id slots (n above 2^26); 4-way buckets unless GANN_HASH_WAYS is 1 or 2
+  // (measured at 100M, c4 generator: 1024 slots in buckets of 4 beat 512 / 2048,
+  // and direct mapping, at L = 64 and 200)
+  *ways = w >= 4 ? 4 : 1;
+  *log2 = forced ? std::max<uint32_t>(forced, 5) : (*ways == 4 || L <= 160 ? 10 : 9);
   *bits = 0;
 }
 
@@ -823,6 +826,15 @@ int gann_build(gann_index* idx, uint32_t L, float alpha, int rule, uint64_t seed
       }
     }
     sync(idx);
+    // the batch scratch is sized for the largest batch (tens of GB at 100M
+    // points): hand it back, the index keeps only points and graph
+    if (env_u32("GANN_KEEP_BUILD_SCRATCH", 0) == 0) {
+      for (DevBuf* b : {&idx->order, &idx->vis_ids, &idx->vis_d, &idx->nvis, &idx->gtarget, &idx->gcnt, &idx->goff,
+                        &idx->gcursor, &idx->gsrc, &idx->poff, &idx->plen, &idx->pid, &idx->pdist, &idx->bigg,
+                        &idx->pls, &idx->plb, &idx->bins})
+        b->release();
+      prune_release();
+    }
   });
 }
 

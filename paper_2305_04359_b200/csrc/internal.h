@@ -119,6 +119,7 @@ bool prune_uses_mma(int elem, uint32_t mcap, uint64_t stride, uint32_t R);
 // Allocate the tensor-core prune's hand-off region up front for launches of
 // up to `lists` lists (a build sizes it once from its largest batch).
 void prune_reserve(uint32_t lists, uint64_t stride, uint32_t R, cudaStream_t s);
+void prune_release();  // frees this device's hand-off region (after a build)
 
 // ---- back-edge grouping (phase 2) -----------------------------------------
 // Pairs (target, source) come either from the out-rows of the batch's points

@@ -282,9 +282,21 @@ constexpr int kMmaThreads = 128;
 // Stage-1 -> stage-2 hand-off buffer (grows; one per process and device).
 constexpr uint64_t kHandoffMax = 1ull << 30;  // launches are chunked to fit
 
+static uint32_t* g_hand_buf[16] = {};
+static uint64_t g_hand_cap[16] = {};
+
+void prune_release() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 16 || !g_hand_buf[dev]) return;
+  cudaDeviceSynchronize();
+  cudaFree(g_hand_buf[dev]);
+  g_hand_buf[dev] = nullptr;
+  g_hand_cap[dev] = 0;
+}
+
 uint32_t* prune_handoff(uint64_t bytes, cudaStream_t s) {
-  static uint32_t* buf[16] = {};
-  static uint64_t cap[16] = {};
+  uint32_t** buf = g_hand_buf;
+  uint64_t* cap = g_hand_cap;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev >= 16) return nullptr;
   if (bytes > cap[dev]) {

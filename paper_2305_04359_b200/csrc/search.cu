@@ -272,6 +272,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_SEARCH_MINB)
       } else if (F16 || hbits) {
         const uint32_t h = (start * 0x9E3779B1u) & hmask;
         h16[h >> 15] = static_cast<uint16_t>(h & 0x7FFFu);
+      } else if (a.hash_ways == 4) {
+        reinterpret_cast<uint4*>(hash)[(start * 0x9E3779B1u) >> (34 - hlog2)] = make_uint4(start, kNone, kNone, kNone);
       } else
         hash[(start * 0x9E3779B1u) >> (32 - hlog2)] = start;
     }
@@ -415,6 +417,19 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_SEARCH_MINB)
           if (fresh) {
             h16[slot] = static_cast<uint16_t>(rem);
             if (!F16) evict += old != 0xFFFFu ? 1u : 0u;
+          }
+        } else if (a.hash_ways == 4) {
+          // ids too wide for u16 remainders (n > 2^26): 4-way buckets of u32
+          // ids, one 16-byte load; an insert shifts the bucket, dropping its
+          // oldest id
+          uint4* h4 = reinterpret_cast<uint4*>(hash);
+          const uint32_t bucket = (nb * 0x9E3779B1u) >> (34 - hlog2);
+          const uint4 w = valid ? h4[bucket] : make_uint4(kNone, kNone, kNone, kNone);
+          fresh = valid && w.x != nb && w.y != nb && w.z != nb && w.w != nb;
+          __syncwarp();
+          if (fresh) {
+            h4[bucket] = make_uint4(nb, w.x, w.y, w.z);
+            evict += w.w != kNone ? 1u : 0u;
           }
         } else {
           // direct-mapped, overwrite on collision: never a false positive

@@ -283,8 +283,10 @@ def test_search_async_concurrent_streams_equal_sync(dtype):
     {"GANN_HASH_WAYS": "1"}, {"GANN_HASH_WAYS": "2"}, {"GANN_HASH_WAYS": "4"},
     {"GANN_HASH_WAYS": "4", "GANN_HASH_LOG2": "5"},   # 32 slots: constant evictions
     {"GANN_HASH_WAYS": "1", "GANN_HASH_LOG2": "5"},
-    {"GANN_HASH16": "0"},                             # u32 id slots
+    {"GANN_HASH16": "0"},                             # u32 id slots (4-way buckets)
     {"GANN_HASH16": "0", "GANN_HASH_LOG2": "5"},
+    {"GANN_HASH16": "0", "GANN_HASH_WAYS": "1"},      # u32 id slots, direct mapped
+    {"GANN_HASH16": "0", "GANN_HASH_WAYS": "1", "GANN_HASH_LOG2": "5"},
     {"GANN_SEARCH_DIAG": "1"},                        # general (diagnostic) kernel instance
 ])
 def test_fast_filter_layouts_keep_results(oracle, monkeypatch, env):
