@@ -387,13 +387,33 @@ __global__ void __launch_bounds__(kMmaThreads)
   for (uint32_t c = tid; c < kch; c += NT) *reinterpret_cast<uint4*>(X + size_t(mc) * xs + c * 16) = make_uint4(0, 0, 0, 0);
   if (tid == 0) norm[mc] = 0;
 
-  for (uint32_t rel = blockIdx.x; rel < lcount; rel += gridDim.x) {
+  // A list's header (index, length, point, offset, verified-prefix length)
+  // is loaded up front, one iteration ahead when a CTA takes several lists
+  // (one CTA per list measured faster than a resident grid: the CTAs'
+  // phases overlap better than one CTA's consecutive lists).
+  struct Head {
+    uint32_t l, m, p, spre;
+    uint64_t beg;
+  };
+  auto head = [&](uint32_t rel) {
+    Head h{0, 0, 0, 0, 0};
+    if (rel >= lcount) return h;
     const uint32_t li = l0 + rel;
-    const uint32_t l = a.list_index ? a.list_index[li] : li;
-    const uint32_t m = a.lengths[l];
+    h.l = a.list_index ? a.list_index[li] : li;
+    h.m = a.lengths[h.l];
+    h.p = a.points[h.l];
+    h.beg = a.begins ? a.begins[h.l] : uint64_t(h.l) * a.fixed_stride;
+    h.spre = (a.row_lists && a.spre) ? a.spre[h.p - a.out_base] : 0u;
+    return h;
+  };
+  Head nxt = head(blockIdx.x);
+  for (uint32_t rel = blockIdx.x; rel < lcount; rel += gridDim.x) {
+    const Head cur = nxt;
+    nxt = head(rel + gridDim.x);
+    const uint32_t m = cur.m;
     if (m < a.mmin || m > a.mcap) continue;  // another launch's bin (the walk skips it too)
-    const uint32_t p = a.points[l];
-    const uint64_t beg = a.begins ? a.begins[l] : uint64_t(l) * a.fixed_stride;
+    const uint32_t p = cur.p;
+    const uint64_t beg = cur.beg;
     uint32_t* out = hand + size_t(rel) * ly.stride;
     __syncthreads();
     if (tid == 0) {
@@ -533,7 +553,7 @@ __global__ void __launch_bounds__(kMmaThreads)
     // distances, same test). Only pairs with an entry of the unverified tail U
     // need testing: U x S and U x U Gram tiles instead of the full triangle.
     uint32_t nS = 0;
-    if (a.row_lists && a.spre && m2 == m) nS = min(static_cast<uint32_t>(a.spre[p - a.out_base]), m);
+    if (a.row_lists && a.spre && m2 == m) nS = min(cur.spre, m);
     const bool su = nS >= 16 && nS < m && nS <= P;
     if (su) {
       uint16_t* ipos = reinterpret_cast<uint16_t*>(tk);  // input index -> sorted position
