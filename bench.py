@@ -154,6 +154,25 @@ def search_bytes(stats: dict, row_bytes: int, nq: int, k: int) -> float:
             + nq * row_bytes + 8.0 * k * nq)
 
 
+def gathered_obj(sstats: dict, steps: int, row_bytes: int, nq: int, k: int, R: int, launch_s: float, peak: float,
+                 traffic):
+    """What the fast kernel actually moves per launch: every row it scores
+    (re-evaluations of ids its visited table dropped included) plus the
+    adjacency rows, against the same HBM peak; and the ncu DRAM traffic of the
+    same launch as a bandwidth. The roofline's `achieved` counts distinct
+    evaluations only, so it is the conservative one."""
+    per = search_bytes(dict(sstats, evaluations=sstats["evaluations"] / steps,
+                            expansions=sstats["expansions"] / steps, adj_entries=0, R=R), row_bytes, nq, k)
+    rate = per / launch_s / 1e9
+    out = {"basis": "scored rows x row bytes + R-wide adjacency rows per expansion (the fast visited table's "
+                    "re-evaluations included; many are L2 hits)",
+           "bytes_per_launch": round(per), "rate": round(rate, 1), "unit": "GB/s", "frac": round(rate / peak, 4)}
+    if traffic:
+        out["dram_traffic_rate"] = round(traffic / launch_s / 1e9, 1)
+        out["dram_traffic_frac"] = round(traffic / launch_s / 1e9 / peak, 4)
+    return out
+
+
 def traffic_from_profile(workload: str, L: int):
     """dram bytes (read + write) of one timed launch from an ncu --set full
     capture of the same workload and beam (profiles/traffic.json), else None."""
@@ -530,6 +549,8 @@ def run_ours(args):
             "note": ("algorithmic bytes count each query's rows; rows shared across queries (hubs) are served "
                      "from the 126 MB L2, so achieved can exceed the HBM peak" if achieved > peak else None),
             "traffic": traffic_from_profile(cfg.name, chosen),
+            "gathered": gathered_obj(sstats, args.steps, d * s_el, nq, k, cfg.R, avg_launch_s, peak,
+                                    traffic_from_profile(cfg.name, chosen)),
             "distinct_evals_per_query": round(xstats["evaluations"] / nq, 1),
             "evals_per_query_fast_filter": round(sstats["evaluations"] / (nq * args.steps), 1),
             "expansions_per_query": round(xstats["expansions"] / nq, 1),
