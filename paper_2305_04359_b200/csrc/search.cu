@@ -524,23 +524,23 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_SEARCH_MINB)
           const uint32_t t = static_cast<uint32_t>(c) * 32 + lane;
           const uint32_t before = running + __popc(w & lanemask_lt(lane));
           const bool act = t >= p0 && t < nsz;
+          // one load from either source (no divergent branch)
+          const bool mine = (w >> lane) & 1u;
+          const uint64_t* src = mine ? srt + before : beam + (t - before);
           uint64_t key = 0;
           uint8_t f = 0;
           if (act) {
-            if ((w >> lane) & 1u) {
-              key = srt[before];
-            } else {
-              key = beam[t - before];
-              f = fl[t - before];
-            }
+            key = *src;
+            f = mine ? 0 : fl[t - before];
           }
-          __syncwarp();
+          __syncwarp();  // every read of this chunk's old entries precedes its writes
           if (act) {
             beam[t] = key;
             fl[t] = f;
           }
           if (lane == 0) bm[c] = 0;
-          __syncwarp();
+          // no second sync: the next (lower) chunk reads only positions below
+          // this chunk, none written yet
         }
       }
       size = min(L, size + s);
