@@ -25,6 +25,7 @@
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/gann.h"
@@ -155,6 +156,7 @@ struct gann_index {
   uint32_t* qctr = nullptr;   // kQueryCounters per-launch query counters (round robin)
   std::atomic<uint32_t> qslot{0};
   double build_ms[6] = {0, 0, 0, 0, 0, 0};
+  std::vector<std::tuple<cudaEvent_t, cudaEvent_t, int>> timers;  // recorded, not yet read
   uint64_t back_pairs = 0, back_groups = 0, back_pruned = 0;
   // scratch
   DevBuf q, qids, qdists, qnvis, qdc, qvids, qvd, qstart, table;
@@ -236,7 +238,13 @@ gann_index* new_index(uint64_t n, uint32_t d, int elem, int metric, uint32_t R, 
   return idx;
 }
 
-void sync(gann_index* idx) { cu(cudaStreamSynchronize(idx->stream), "stream sync"); }
+void flush_timers(gann_index* idx);
+// Stream sync; the phase events recorded before it are complete, so their
+// times are collected here at no extra cost.
+void sync(gann_index* idx) {
+  cu(cudaStreamSynchronize(idx->stream), "stream sync");
+  flush_timers(idx);
+}
 
 template <class T>
 T read_dev(gann_index* idx, const T* p) {
@@ -365,6 +373,9 @@ void check_prune_params(float alpha, int rule) {
   if (rule != GANN_SCALE_CANDIDATE && rule != GANN_SCALE_SELECTED) fail(GANN_EINVAL, "unknown prune rule");
 }
 
+// Phase timer of the build: a pair of events on the index's stream. stop()
+// does not wait; the elapsed times are added to build_ms[phase] when the
+// build ends (flush_timers), so the phases add no host round trips.
 struct Timer {
   cudaEvent_t a, b;
   cudaStream_t s;
@@ -373,16 +384,26 @@ struct Timer {
     cudaEventCreate(&b);
     cudaEventRecord(a, s);
   }
-  double stop() {
-    cudaEventRecord(b, s);
+  void stop(gann_index* idx, int phase);  // phase < 0: not accumulated
+};
+
+void Timer::stop(gann_index* idx, int phase) {
+  cudaEventRecord(b, s);
+  idx->timers.emplace_back(a, b, phase);
+}
+
+// Waits for the recorded phase events and adds their times to build_ms.
+void flush_timers(gann_index* idx) {
+  for (auto& [a, b, phase] : idx->timers) {
     cudaEventSynchronize(b);
     float ms = 0;
     cudaEventElapsedTime(&ms, a, b);
+    if (phase >= 0) idx->build_ms[phase] += ms;
     cudaEventDestroy(a);
     cudaEventDestroy(b);
-    return ms;
   }
-};
+  idx->timers.clear();
+}
 
 // alpha_prune over lists of length <= maxlen, each by the smallest kernel that
 // fits: integer rows on the tensor-core kernel in 128/256/512 bins, f32 rows
@@ -447,7 +468,7 @@ void insert_batch(gann_index* idx, const uint32_t* d_ids, uint32_t B, uint32_t L
   a.vcap = vcap;
   Timer ts(idx->stream);
   run_search(idx, a, idx->stream);
-  if (timed) idx->build_ms[1] += ts.stop(); else ts.stop();
+  ts.stop(idx, timed ? 1 : -1);
   PruneArgs p = base_prune_args(idx, alpha, rule);
   p.count = B;
   p.points = d_ids;
@@ -460,7 +481,7 @@ void insert_batch(gann_index* idx, const uint32_t* d_ids, uint32_t B, uint32_t L
   p.mcap = vcap;
   Timer tp(idx->stream);
   prune_binned(idx, p, vcap);
-  if (timed) idx->build_ms[2] += tp.stop(); else tp.stop();
+  tp.stop(idx, timed ? 2 : -1);
   uint32_t fl[2];
   cu(cudaMemcpyAsync(fl, idx->flags, 8, cudaMemcpyDeviceToHost, idx->stream), "read flags");
   sync(idx);
@@ -582,7 +603,7 @@ void apply_back(gann_index* idx, const uint32_t* bsrc, uint32_t B, const uint32_
   if ((out_keys || !b.sources_distinct) && cnt[kCntMaxGroup] > kSortedGroupCap)
     fail(GANN_EINVAL, "a group of " + std::to_string(cnt[kCntMaxGroup]) + " pairs exceeds the ordered-group cap " +
                           std::to_string(kSortedGroupCap));
-  if (timed) idx->build_ms[3] += tg.stop(); else tg.stop();
+  tg.stop(idx, timed ? 3 : -1);
   if (out_keys) {  // group_by_key mode
     cu(backedge_write_groups(b, ng, nbig, out_keys, out_vals, idx->stream), "group write");
     sync(idx);
@@ -593,7 +614,7 @@ void apply_back(gann_index* idx, const uint32_t* bsrc, uint32_t B, const uint32_
   cu(backedge_merge(b, ng, nbig, idx->elem, idx->metric, idx->geom, idx->stream), "back-edge merge");
   cu(cudaMemcpyAsync(cnt, idx->counters, sizeof(cnt), cudaMemcpyDeviceToHost, idx->stream), "read");
   sync(idx);
-  if (timed) idx->build_ms[4] += tm.stop(); else tm.stop();
+  tm.stop(idx, timed ? 4 : -1);
   if (cnt[kCntTooBig]) fail(GANN_ECUDA, "back-edge group exceeded the merge capacity");
   const uint32_t nps = static_cast<uint32_t>(cnt[kCntPruneSmall]);
   const uint32_t npb = static_cast<uint32_t>(cnt[kCntPruneBig]);
@@ -625,7 +646,7 @@ void apply_back(gann_index* idx, const uint32_t* bsrc, uint32_t B, const uint32_
     cu(launch_prune(p, idx->elem, idx->metric, idx->geom, 256, idx->stream), "reprune big");
   }
   sync(idx);
-  if (timed) idx->build_ms[5] += tp.stop(); else tp.stop();
+  tp.stop(idx, timed ? 5 : -1);
 }
 
 std::vector<std::pair<uint32_t, uint32_t>> batch_ranges(uint64_t n, uint32_t cap) {
@@ -726,6 +747,7 @@ void gann_index_free(gann_index* idx) {
   if (!idx) return;
   cudaSetDevice(idx->device);
   if (idx->stream) cudaStreamSynchronize(idx->stream);
+  flush_timers(idx);
   for (void* p : idx->ipc_open)
     if (p) cudaIpcCloseMemHandle(p);
   if (idx->d_parts) cudaFree(idx->d_parts);
@@ -785,7 +807,7 @@ int gann_build(gann_index* idx, uint32_t L, float alpha, int rule, uint64_t seed
     idx->order.ensure(n * 4);
     cu(cudaMemcpyAsync(idx->order.p, order.data(), n * 4, cudaMemcpyHostToDevice, idx->stream),
        "upload order");
-    idx->build_ms[0] += t0.stop();
+    t0.stop(idx, 0);
     const uint32_t* d_order = idx->order.as<uint32_t>();
     // size the per-batch scratch once, from the largest batch: a cudaFree /
     // cudaMalloc inside the loop stalls the device for tens of milliseconds
