@@ -259,6 +259,14 @@ def setup(args):
         else:
             pidx.close()
     if build_mode == "single-gpu":
+        # warm-up: one small build of the same kind first, so the timed build
+        # does not pay CUDA's lazy loading of the kernels it launches first
+        nw = min(n, 20_000)
+        widx = g.Index.from_device(base.data_ptr(), nw, d, cfg.np_dtype, cfg.metric, cfg.R, dev)
+        widx.build(g.DiskannParams(cfg.R, cfg.L, cfg.alpha, seed=42, max_batch=int(nw * cfg.batch_cap_frac)))
+        widx.close()
+        del widx
+        barrier()
         barrier()
         t0 = time.perf_counter()
         idx.build(params)
@@ -268,6 +276,7 @@ def setup(args):
             build_mode = "replicated: every rank builds the whole graph"
         bstats = idx.stats()
     build_clocks = bclock.stop()
+    idx.release_scratch()  # after the timed build: the search needs none of it
     adj_t = _tensor_from_ptr(idx.device_ptrs()[2], n * cfg.R * 4).view(torch.int32)  # a view, no copy
     checksum, CH = 0, 1 << 28  # chunked: an int64 copy of a 100M-row graph would not fit beside it
     for c0 in range(0, n * cfg.R, CH):
@@ -569,6 +578,8 @@ def run_ours(args):
         "clocks": clocks,
         "build": {
             "points_per_s": round(n / build_s, 1), "seconds": round(build_s, 3), "mode": build_mode,
+            "warmup": "one 20k-point build of the same config first (kernel module loading); the timed "
+                      "build allocates its own scratch",
             "phases_ms": {kk: round(v, 1) for kk, v in bstats["build_ms"].items()},
             "mean_degree": round(deg_mean, 3), "replicas_identical": replicas_identical,
             "clocks": S["build_clocks"],

@@ -278,6 +278,10 @@ typedef struct gann_stats {
   uint64_t guess_hits;      /* search: expansions whose row was prefetched by a right guess */
 } gann_stats;
 int gann_get_stats(const gann_index* idx, gann_stats* out);
+/* Frees the build's batch scratch (sized for the largest batch: ~10 GB at 10M
+ * points). gann_build keeps it for the next build unless device memory is
+ * tight; the next build reallocates it. */
+int gann_release_scratch(gann_index* idx);
 int gann_reset_stats(gann_index* idx);  /* waits for all work queued on the device first */
 
 /* Device pointers of the resident index (points: padded rows of `stride`

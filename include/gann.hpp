@@ -112,6 +112,7 @@ class Index {
     check(gann_build(h_.get(), p.build_beam, p.alpha, static_cast<int>(p.rule), p.seed, p.max_batch));
   }
   void import_graph(const HostGraph& g) { check(gann_import_graph(h_.get(), g.adj.data(), g.start)); }
+  void release_scratch() { check(gann_release_scratch(h_.get())); }
   HostGraph export_graph() const {
     uint64_t n = 0;
     uint32_t R = 0, start = 0;

@@ -95,6 +95,7 @@ SIGNATURES = {
     "gann_part_phase2": (_i, [_vp, _u32, _vp, _u64]),
     "gann_get_stats": (_i, [_vp, C.POINTER(GannStats)]),
     "gann_reset_stats": (_i, [_vp]),
+    "gann_release_scratch": (_i, [_vp]),
     "gann_index_device_ptrs": (_i, [_vp, _pp, C.POINTER(C.c_uint64), _pp]),
 }
 

@@ -319,6 +319,10 @@ class Index:
     def reset_stats(self) -> None:
         check(lib().gann_reset_stats(self._h))
 
+    def release_scratch(self) -> None:
+        """Free the build's batch scratch (gann_release_scratch)."""
+        check(lib().gann_release_scratch(self._h))
+
     def device_ptrs(self):
         pts, adj = C.c_void_p(), C.c_void_p()
         stride = C.c_uint64()

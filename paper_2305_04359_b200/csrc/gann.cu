@@ -239,6 +239,16 @@ gann_index* new_index(uint64_t n, uint32_t d, int elem, int metric, uint32_t R, 
 }
 
 void flush_timers(gann_index* idx);
+
+// The build's batch scratch and the prune hand-off (the index keeps its
+// points, graph and query buffers).
+void release_build_scratch(gann_index* idx) {
+  for (DevBuf* b : {&idx->order, &idx->vis_ids, &idx->vis_d, &idx->nvis, &idx->gtarget, &idx->gcnt, &idx->goff,
+                    &idx->gcursor, &idx->gsrc, &idx->poff, &idx->plen, &idx->pid, &idx->pdist, &idx->bigg,
+                    &idx->pls, &idx->plb, &idx->bins})
+    b->release();
+  prune_release();
+}
 // Stream sync; the phase events recorded before it are complete, so their
 // times are collected here at no extra cost.
 void sync(gann_index* idx) {
@@ -849,14 +859,20 @@ int gann_build(gann_index* idx, uint32_t L, float alpha, int rule, uint64_t seed
     }
     sync(idx);
     // the batch scratch is sized for the largest batch (tens of GB at 100M
-    // points): hand it back, the index keeps only points and graph
-    if (env_u32("GANN_KEEP_BUILD_SCRATCH", 0) == 0) {
-      for (DevBuf* b : {&idx->order, &idx->vis_ids, &idx->vis_d, &idx->nvis, &idx->gtarget, &idx->gcnt, &idx->goff,
-                        &idx->gcursor, &idx->gsrc, &idx->poff, &idx->plen, &idx->pid, &idx->pdist, &idx->bigg,
-                        &idx->pls, &idx->plb, &idx->bins})
-        b->release();
-      prune_release();
-    }
+    // points): kept for the next build unless device memory is tight (freeing
+    // ~10 GB costs ~0.15 s); gann_release_scratch hands it back on request
+    size_t fr = 0, tot = 0;
+    cu(cudaMemGetInfo(&fr, &tot), "cudaMemGetInfo");
+    if (env_u32("GANN_KEEP_BUILD_SCRATCH", 0) == 0 && fr < tot / 4) release_build_scratch(idx);
+  });
+}
+
+int gann_release_scratch(gann_index* idx) {
+  return guarded([&] {
+    if (!idx) fail(GANN_EINVAL, "index is NULL");
+    set_device(idx);
+    sync(idx);
+    release_build_scratch(idx);
   });
 }
 
