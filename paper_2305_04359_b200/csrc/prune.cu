@@ -1090,6 +1090,62 @@ cudaError_t dispatch(const PruneArgs& a, const Geometry& g, int threads, cudaStr
 }
 }  // namespace
 
+// Stage 2, one lane per list: the greedy walk is a serial bit loop that every
+// lane of a warp-per-list walk repeats in lockstep; here each lane walks its
+// own list, streaming its cull rows from the hand-off region (consecutive rows
+// of one list share cache lines), so a warp walks 32 lists for about the
+// instructions the warp-per-list form spends on one.
+template <int W>
+__global__ void __launch_bounds__(128)
+    prune_walk_lane_kernel(const PruneArgs a, const MmaLayout ly, const uint32_t* hand, uint32_t l0,
+                           uint32_t lcount) {
+  const uint32_t rel = blockIdx.x * blockDim.x + threadIdx.x;
+  if (rel >= lcount) return;
+  const uint32_t li = l0 + rel;
+  const uint32_t l = a.list_index ? a.list_index[li] : li;
+  const uint32_t m = a.lengths[l];
+  if (m < a.mmin || m > a.mcap) return;
+  const uint32_t p = a.points[l];
+  const uint32_t R = a.R;
+  uint32_t* orow = a.out_rows ? a.out_rows + uint64_t(l) * R : a.out_adj + uint64_t(p - a.out_base) * R;
+  const uint32_t* in = hand + size_t(rel) * ly.stride;
+  const uint32_t m2 = in[0];
+  const uint32_t* ids = in + 4;
+  const uint32_t* zm = ids + ly.mc;
+  const uint4* rows = reinterpret_cast<const uint4*>(zm + W);
+  uint32_t culled[W], z[W];
+#pragma unroll
+  for (int w = 0; w < W; w++) {
+    culled[w] = 0u;
+    z[w] = __ldg(zm + w);
+  }
+  uint32_t nsel = 0;
+#pragma unroll
+  for (int w = 0; w < W; w++) {
+    if (32u * w >= m2 || nsel == R) break;
+    for (uint32_t b = 0; b < 32; b++) {
+      const uint32_t i = 32u * w + b;
+      if (i >= m2) break;
+      if ((culled[w] >> b) & 1u) continue;  // prune.cpp:28-29
+      orow[nsel] = __ldg(ids + i);
+      nsel++;
+      if (nsel == R) break;
+      if ((z[w] >> b) & 1u) continue;  // prune.cpp:32: a zero-distance pick culls nothing
+#pragma unroll
+      for (int q = 0; q < W / 4; q++) {
+        const uint4 c = __ldg(rows + size_t(i) * (W / 4) + q);
+        culled[4 * q + 0] |= c.x;
+        culled[4 * q + 1] |= c.y;
+        culled[4 * q + 2] |= c.z;
+        culled[4 * q + 3] |= c.w;
+      }
+    }
+  }
+  for (uint32_t i = nsel; i < R; i++) orow[i] = kNone;
+  if (a.n_out) a.n_out[l] = nsel;
+  if (a.spre && !a.out_rows) a.spre[p - a.out_base] = static_cast<uint8_t>(nsel < 255 ? nsel : 255);
+}
+
 template <int E, int M, int W>
 cudaError_t launch_mma_w(const PruneArgs& a, const MmaLayout& ly, cudaStream_t s) {
   auto kp = a.rule == 0 ? prune_prep_kernel<E, M, W, 0> : prune_prep_kernel<E, M, W, 1>;
@@ -1104,11 +1160,20 @@ cudaError_t launch_mma_w(const PruneArgs& a, const MmaLayout& ly, cudaStream_t s
   if ((e = cudaFuncSetAttribute(prune_walk_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(walk_smem))) !=
       cudaSuccess)
     return e;
+  // lane-per-list walks for the long insert-time lists (W >= 8: -8% prune
+  // time at c1); the short re-prune lists stay on the warp walk with rows
+  // staged in shared memory (the lane walk's dependent row loads made them
+  // 6% slower). GANN_WALK_LANE=0/1 forces either.
+  const char* wl = std::getenv("GANN_WALK_LANE");
+  const bool walk_lane = wl && *wl ? *wl == '1' : W >= 8;
   for (uint32_t l0 = 0; l0 < a.count; l0 += chunk) {
     const uint32_t n = std::min(chunk, a.count - l0);
     kp<<<n, kMmaThreads, ly.total, s>>>(a, ly, hand, l0, n);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    prune_walk_kernel<W><<<(n + kWalkWarps - 1) / kWalkWarps, kWalkWarps * 32, walk_smem, s>>>(a, ly, hand, l0, n);
+    if (walk_lane)
+      prune_walk_lane_kernel<W><<<(n + 127) / 128, 128, 0, s>>>(a, ly, hand, l0, n);
+    else
+      prune_walk_kernel<W><<<(n + kWalkWarps - 1) / kWalkWarps, kWalkWarps * 32, walk_smem, s>>>(a, ly, hand, l0, n);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   return cudaSuccess;
