@@ -1090,15 +1090,15 @@ cudaError_t dispatch(const PruneArgs& a, const Geometry& g, int threads, cudaStr
 }
 }  // namespace
 
-// Stage 2, one lane per list: the greedy walk is a serial bit loop that every
-// lane of a warp-per-list walk repeats in lockstep; here each lane walks its
-// own list, streaming its cull rows from the hand-off region (consecutive rows
-// of one list share cache lines), so a warp walks 32 lists for about the
-// instructions the warp-per-list form spends on one.
-template <int W>
+// One lane per list, rows streamed through a D-deep register ring: row i + D
+// is loaded while candidate i is decided (selected or not), so the walk's bit
+// tests do not wait on memory. W/4 16-byte loads per row; D * W registers of
+// ring (64 at the depths used).
+template <int W, int D>
 __global__ void __launch_bounds__(128)
-    prune_walk_lane_kernel(const PruneArgs a, const MmaLayout ly, const uint32_t* hand, uint32_t l0,
+    prune_walk_ring_kernel(const PruneArgs a, const MmaLayout ly, const uint32_t* hand, uint32_t l0,
                            uint32_t lcount) {
+  constexpr int Q = W / 4;  // uint4 per cull row
   const uint32_t rel = blockIdx.x * blockDim.x + threadIdx.x;
   if (rel >= lcount) return;
   const uint32_t li = l0 + rel;
@@ -1113,31 +1113,45 @@ __global__ void __launch_bounds__(128)
   const uint32_t* ids = in + 4;
   const uint32_t* zm = ids + ly.mc;
   const uint4* rows = reinterpret_cast<const uint4*>(zm + W);
-  uint32_t culled[W], z[W];
+  uint32_t cul[W];
 #pragma unroll
-  for (int w = 0; w < W; w++) {
-    culled[w] = 0u;
-    z[w] = __ldg(zm + w);
-  }
+  for (int w = 0; w < W; w++) cul[w] = 0u;
+  uint4 ring[D][Q];
+#pragma unroll
+  for (int d = 0; d < D; d++)
+#pragma unroll
+    for (int q = 0; q < Q; q++)
+      ring[d][q] = d < static_cast<int>(m2) ? __ldg(rows + size_t(d) * Q + q) : make_uint4(0u, 0u, 0u, 0u);
   uint32_t nsel = 0;
 #pragma unroll
   for (int w = 0; w < W; w++) {
     if (32u * w >= m2 || nsel == R) break;
-    for (uint32_t b = 0; b < 32; b++) {
-      const uint32_t i = 32u * w + b;
-      if (i >= m2) break;
-      if ((culled[w] >> b) & 1u) continue;  // prune.cpp:28-29
-      orow[nsel] = __ldg(ids + i);
-      nsel++;
-      if (nsel == R) break;
-      if ((z[w] >> b) & 1u) continue;  // prune.cpp:32: a zero-distance pick culls nothing
+    const uint32_t zw = __ldg(zm + w);
+    for (uint32_t g = 0; g < 32; g += D) {
+      const uint32_t i0 = 32u * w + g;
+      if (i0 >= m2 || nsel == R) break;
 #pragma unroll
-      for (int q = 0; q < W / 4; q++) {
-        const uint4 c = __ldg(rows + size_t(i) * (W / 4) + q);
-        culled[4 * q + 0] |= c.x;
-        culled[4 * q + 1] |= c.y;
-        culled[4 * q + 2] |= c.z;
-        culled[4 * q + 3] |= c.w;
+      for (int d = 0; d < D; d++) {
+        const uint32_t i = i0 + d, b = g + d;
+        uint4 cur[Q];
+#pragma unroll
+        for (int q = 0; q < Q; q++) {
+          cur[q] = ring[d][q];
+          ring[d][q] = i + D < m2 ? __ldg(rows + size_t(i + D) * Q + q) : make_uint4(0u, 0u, 0u, 0u);
+        }
+        if (i < m2 && nsel < R && !((cul[w] >> b) & 1u)) {  // prune.cpp:28-29
+          orow[nsel] = __ldg(ids + i);
+          nsel++;
+          if (!((zw >> b) & 1u)) {  // prune.cpp:32: a zero-distance pick culls nothing
+#pragma unroll
+            for (int q = 0; q < Q; q++) {
+              cul[4 * q + 0] |= cur[q].x;
+              cul[4 * q + 1] |= cur[q].y;
+              cul[4 * q + 2] |= cur[q].z;
+              cul[4 * q + 3] |= cur[q].w;
+            }
+          }
+        }
       }
     }
   }
@@ -1164,14 +1178,17 @@ cudaError_t launch_mma_w(const PruneArgs& a, const MmaLayout& ly, cudaStream_t s
   // time at c1); the short re-prune lists stay on the warp walk with rows
   // staged in shared memory (the lane walk's dependent row loads made them
   // 6% slower). GANN_WALK_LANE=0/1 forces either.
-  const char* wl = std::getenv("GANN_WALK_LANE");
-  const bool walk_lane = wl && *wl ? *wl == '1' : W >= 8;
+  // walk: one lane per list through a register ring (measured at c1: -5% re-prune
+  // time at W = 4, -8% insert prune time at W >= 8 against a warp per list);
+  // GANN_WALK_RING=0 selects the warp walk
+  const char* wr = std::getenv("GANN_WALK_RING");
+  const bool ring = !(wr && *wr == '0');
   for (uint32_t l0 = 0; l0 < a.count; l0 += chunk) {
     const uint32_t n = std::min(chunk, a.count - l0);
     kp<<<n, kMmaThreads, ly.total, s>>>(a, ly, hand, l0, n);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    if (walk_lane)
-      prune_walk_lane_kernel<W><<<(n + 127) / 128, 128, 0, s>>>(a, ly, hand, l0, n);
+    if (ring)
+      prune_walk_ring_kernel<W, (W == 4 ? 16 : (W == 8 ? 8 : 4))><<<(n + 127) / 128, 128, 0, s>>>(a, ly, hand, l0, n);
     else
       prune_walk_kernel<W><<<(n + kWalkWarps - 1) / kWalkWarps, kWalkWarps * 32, walk_smem, s>>>(a, ly, hand, l0, n);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
