@@ -424,7 +424,8 @@ void prune_binned(gann_index* idx, PruneArgs p, uint32_t maxlen) {
                    !std::getenv("GANN_NO_MMA");
   // bins: (0,128] (128,256] (256,512] on the tensor cores, or (0,512] on the
   // warp kernel for f32; then anything longer on the chunked kernel
-  std::vector<uint32_t> bounds = mma ? std::vector<uint32_t>{128, 256, 512} : std::vector<uint32_t>{kPruneSmallCap};
+  const uint32_t bin0 = env_u32("GANN_PRUNE_BIN0", 80);  // a first, smaller tensor-core bin (0: none)
+  std::vector<uint32_t> bounds = mma ? (bin0 ? std::vector<uint32_t>{bin0, 128, 256, 512} : std::vector<uint32_t>{128, 256, 512}) : std::vector<uint32_t>{kPruneSmallCap};
   const int nb = static_cast<int>(bounds.size());
   idx->bins.ensure(size_t(p.count) * (nb + 1) * 4 + 64 + 16 * 4);
   uint32_t* d_counts = idx->bins.as<uint32_t>();
