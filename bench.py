@@ -232,8 +232,6 @@ def setup(args):
     params = g.DiskannParams(cfg.R, cfg.L, cfg.alpha, seed=42, max_batch=cfg.max_batch)
     idx.reset_stats()
     build_mode = "single-gpu"
-    bclock = ClockSampler(dev)  # the build's clocks, beside the search's
-    bclock.start()
     if world > 1 and not args.replicated_build:
         # one vertex-partitioned build over the N GPUs (peer rows over NVLink,
         # NCCL all-to-all-v of the reverse pairs), then every rank gathers the
@@ -275,7 +273,6 @@ def setup(args):
         if world > 1:
             build_mode = "replicated: every rank builds the whole graph"
         bstats = idx.stats()
-    build_clocks = bclock.stop()
     idx.release_scratch()  # after the timed build: the search needs none of it
     adj_t = _tensor_from_ptr(idx.device_ptrs()[2], n * cfg.R * 4).view(torch.int32)  # a view, no copy
     checksum, CH = 0, 1 << 28  # chunked: an int64 copy of a 100M-row graph would not fit beside it
@@ -342,7 +339,7 @@ def setup(args):
     return dict(torch=torch, dist=dist, g=g, check=check, lib=lib, cfg=cfg, nq=nq, n=n, d=d, k=k, dev=dev,
                 rank=rank, world=world, barrier=barrier, allreduce=allreduce, base=base, qdev=qdev, idx=idx,
                 build_s=build_s, bstats=bstats, replicas_identical=replicas_identical, deg_mean=deg_mean,
-                build_mode=build_mode, build_clocks=build_clocks,
+                build_mode=build_mode,
                 out_ids=out_ids, out_d=out_d, stream=stream, search_L=search_L, curve=curve, chosen=chosen,
                 recall=recall, target_reached=target_reached, sp=sp, gt_ids_h=gt_ids_h, gt_d_h=gt_d_h,
                 ext_curve=ext_curve, L_target=L_target)
@@ -582,7 +579,6 @@ def run_ours(args):
                       "build allocates its own scratch",
             "phases_ms": {kk: round(v, 1) for kk, v in bstats["build_ms"].items()},
             "mean_degree": round(deg_mean, 3), "replicas_identical": replicas_identical,
-            "clocks": S["build_clocks"],
             "search_gather_rate": {
                 "value": round(build_bytes / (build_search_ms / 1e3) / 1e9, 1) if build_search_ms else None, "unit": "GB/s",
                 "basis": "fast-mode evaluations x row bytes + adjacency rows, / the build's search time; "
