@@ -44,6 +44,10 @@ constexpr int kWarpsPerBlock = 4;
 #define GANN_SEARCH_MINB 6  // resident CTAs per SM the register budget targets (80 regs; 7 CTAs at 72 regs
                             // rematerialised more and measured 1.2% slower)
 #endif
+#ifndef GANN_SEARCH_MINB_WIDE
+#define GANN_SEARCH_MINB_WIDE 7  // rows of 16 lanes (256-byte u8 rows): left free the compiler takes 76
+                                 // registers, 6 CTAs, and c2 ran 7% slower than at 7 CTAs
+#endif
 
 // Rows in flight per lane group per pass: U <= LPR so the transposed
 // reduction can hand every lane of the group (at most) one finished row.
@@ -187,7 +191,7 @@ size_t search_smem_per_warp(uint32_t L, uint32_t R, uint32_t hash_log2, bool has
 // entries, merges, survivors, moved, duplicates); the general instance keeps
 // them (GANN_SEARCH_DIAG=1 selects it for the fast mode too)
 template <int E, int M, int LPR, int CPL, bool F16>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_SEARCH_MINB)
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_MINB_WIDE : GANN_SEARCH_MINB)
     search_kernel(const SearchArgs a, const uint32_t per_warp) {
   using Op = DistOp<E, M>;
   extern __shared__ __align__(16) uint8_t smem[];
