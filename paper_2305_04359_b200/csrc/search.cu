@@ -190,14 +190,15 @@ size_t search_smem_per_warp(uint32_t L, uint32_t R, uint32_t hash_log2, bool has
 // branches and without the diagnostic counters (filter drops, adjacency
 // entries, merges, survivors, moved, duplicates); the general instance keeps
 // them (GANN_SEARCH_DIAG=1 selects it for the fast mode too)
-template <int E, int M, int LPR, int CPL, bool F16>
+// R64: the degree bound is 64 (every BASELINE config), fixed at compile time
+template <int E, int M, int LPR, int CPL, bool F16, bool R64 = false>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_MINB_WIDE : GANN_SEARCH_MINB)
     search_kernel(const SearchArgs a, const uint32_t per_warp) {
   using Op = DistOp<E, M>;
   extern __shared__ __align__(16) uint8_t smem[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  const uint32_t L = a.L, R = a.R;
+  const uint32_t L = a.L, R = R64 ? 64u : a.R;
   const uint32_t Lp = (L + 31) & ~31u, Rp = (R + 31) & ~31u;
   const uint32_t hlog2 = a.hash_log2;
   const uint32_t H = 1u << hlog2;
@@ -599,7 +600,12 @@ cudaError_t launch_one(const SearchArgs& a, cudaStream_t s) {
   const char* dv = std::getenv("GANN_SEARCH_DIAG");
   const bool diag = dv && *dv && *dv != '0';
   const bool f16 = a.visited_mode == 0 && a.hash_bits != 0 && !diag;
-  auto k = f16 ? search_kernel<E, M, LPR, CPL, true> : search_kernel<E, M, LPR, CPL, false>;
+  // R = 64 fixed at compile time helps the 16-lane rows (c2: -5% at L=200,
+  // faster build search) but not the 8-lane ones (c1 build search +6%)
+  const char* rv = std::getenv("GANN_SEARCH_R64");
+  const bool r64 = a.R == 64 && (rv && *rv ? *rv == '1' : LPR >= 16);
+  auto k = !f16 ? search_kernel<E, M, LPR, CPL, false>
+                : (r64 ? search_kernel<E, M, LPR, CPL, true, true> : search_kernel<E, M, LPR, CPL, true, false>);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
