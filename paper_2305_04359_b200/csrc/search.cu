@@ -600,10 +600,12 @@ cudaError_t launch_one(const SearchArgs& a, cudaStream_t s) {
   const char* dv = std::getenv("GANN_SEARCH_DIAG");
   const bool diag = dv && *dv && *dv != '0';
   const bool f16 = a.visited_mode == 0 && a.hash_bits != 0 && !diag;
-  // R = 64 fixed at compile time helps the 16-lane rows (c2: -5% at L=200,
-  // faster build search) but not the 8-lane ones (c1 build search +6%)
+  // R = 64 fixed at compile time (measured): 16-lane rows -5% at L=200 (c2)
+  // and a faster build search; 8-lane rows (c1) -1% for queries at L=200,
+  // even at 128, +1.4% at L=64, and +4.5% for the build's searches (which
+  // record their visited lists)
   const char* rv = std::getenv("GANN_SEARCH_R64");
-  const bool r64 = a.R == 64 && (rv && *rv ? *rv == '1' : LPR >= 16);
+  const bool r64 = a.R == 64 && (rv && *rv ? *rv == '1' : (LPR >= 16 || (a.L >= 192 && !a.vis_ids)));
   auto k = !f16 ? search_kernel<E, M, LPR, CPL, false>
                 : (r64 ? search_kernel<E, M, LPR, CPL, true, true> : search_kernel<E, M, LPR, CPL, true, false>);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
