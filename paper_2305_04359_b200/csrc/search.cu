@@ -601,11 +601,11 @@ cudaError_t launch_one(const SearchArgs& a, cudaStream_t s) {
   const bool diag = dv && *dv && *dv != '0';
   const bool f16 = a.visited_mode == 0 && a.hash_bits != 0 && !diag;
   // R = 64 fixed at compile time (measured): 16-lane rows -5% at L=200 (c2)
-  // and a faster build search; 8-lane rows (c1) -1% for queries at L=200,
-  // even at 128, +1.4% at L=64, and +4.5% for the build's searches (which
-  // record their visited lists)
+  // and a faster build search; 8-lane rows (c1): -1% for a serial launch at
+  // L=200 but -1% bench QPS (pipelined), +1.4% at L=64, +4.5% for the build's
+  // searches — so only the 16-lane instance is specialised
   const char* rv = std::getenv("GANN_SEARCH_R64");
-  const bool r64 = a.R == 64 && (rv && *rv ? *rv == '1' : (LPR >= 16 || (a.L >= 192 && !a.vis_ids)));
+  const bool r64 = a.R == 64 && (rv && *rv ? *rv == '1' : LPR >= 16);
   auto k = !f16 ? search_kernel<E, M, LPR, CPL, false>
                 : (r64 ? search_kernel<E, M, LPR, CPL, true, true> : search_kernel<E, M, LPR, CPL, true, false>);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
