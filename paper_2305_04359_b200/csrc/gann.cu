@@ -418,14 +418,24 @@ void flush_timers(gann_index* idx) {
 // alpha_prune over lists of length <= maxlen, each by the smallest kernel that
 // fits: integer rows on the tensor-core kernel in 128/256/512 bins, f32 rows
 // on the warp kernel; anything longer on the chunked kernel.
-void prune_binned(gann_index* idx, PruneArgs p, uint32_t maxlen) {
+void prune_binned(gann_index* idx, PruneArgs p, uint32_t maxlen, bool fine = false) {
   if (p.count == 0) return;
   const bool mma = prune_uses_mma(idx->elem, std::min<uint32_t>(maxlen, 512), idx->stride, idx->R) &&
                    !std::getenv("GANN_NO_MMA");
   // bins: (0,128] (128,256] (256,512] on the tensor cores, or (0,512] on the
   // warp kernel for f32; then anything longer on the chunked kernel
   const uint32_t bin0 = env_u32("GANN_PRUNE_BIN0", 80);  // a first, smaller tensor-core bin (0: none)
-  std::vector<uint32_t> bounds = mma ? (bin0 ? std::vector<uint32_t>{bin0, 128, 256, 512} : std::vector<uint32_t>{128, 256, 512}) : std::vector<uint32_t>{kPruneSmallCap};
+  // the staging area of a bin is sized by its bound, so finer bins fit more
+  // CTAs per SM; insert-time lists (|V| ~ 1.3 L, spread out) take the finer
+  // set (-16% prune time at c1 against 128/256/512), re-prune lists (a row
+  // plus a few sources) the coarser one (their extra launches cost more)
+  std::vector<uint32_t> bounds;
+  if (!mma)
+    bounds = {kPruneSmallCap};
+  else if (fine)
+    bounds = {bin0 ? bin0 : 80, 128, 160, 192, 224, 256, 320, 512};
+  else
+    bounds = {bin0 ? bin0 : 80, 128, 192, 256, 512};
   const int nb = static_cast<int>(bounds.size());
   idx->bins.ensure(size_t(p.count) * (nb + 1) * 4 + 64 + 16 * 4);
   uint32_t* d_counts = idx->bins.as<uint32_t>();
@@ -491,7 +501,7 @@ void insert_batch(gann_index* idx, const uint32_t* d_ids, uint32_t B, uint32_t L
   p.out_base = idx->part_base;
   p.mcap = vcap;
   Timer tp(idx->stream);
-  prune_binned(idx, p, vcap);
+  prune_binned(idx, p, vcap, true);
   tp.stop(idx, timed ? 2 : -1);
   uint32_t fl[2];
   cu(cudaMemcpyAsync(fl, idx->flags, 8, cudaMemcpyDeviceToHost, idx->stream), "read flags");
