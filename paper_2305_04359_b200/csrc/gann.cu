@@ -852,6 +852,10 @@ int gann_build(gann_index* idx, uint32_t L, float alpha, int rule, uint64_t seed
       idx->pdist.ensure(ptotal * 4);
       if (prune_uses_mma(idx->elem, 512, idx->stride, idx->R))
         prune_reserve(static_cast<uint32_t>(std::min<uint64_t>(groups, 0xFFFFFFFFu)), idx->stride, idx->R, idx->stream);
+      // the prune's length bins: lists x (bins + 1) ids, for the largest count
+      // a batch can prune (every group) — growing it batch by batch meant a
+      // cudaFree/cudaMalloc pair inside the timed batches
+      idx->bins.ensure(size_t(std::max<uint64_t>(groups, bmax)) * 9 * 4 + 64 + 16 * 4);
     }
     const bool trace = env_u32("GANN_TRACE", 0) != 0;
     for (auto [lo, hi] : batch_ranges(n, max_batch)) {
