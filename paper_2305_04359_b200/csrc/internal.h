@@ -74,6 +74,20 @@ struct SearchArgs {
   unsigned long long* stats; // kStCount counters (nullable)
 };
 size_t search_smem_per_warp(uint32_t L, uint32_t R, uint32_t hash_log2, bool hash16);
+
+// Kernel preloading. CUDA loads a kernel's code at its first launch (lazy
+// module loading), which put 15-200 ms of one-time stalls into the first
+// build of a process; index creation touches the kernels the index will use
+// (cudaFuncGetAttributes) so the build and the searches start warm.
+void preload_search(int elem, int metric, const Geometry& g);
+void preload_prune(int elem, int metric, const Geometry& g);
+void preload_backedge(int elem, int metric, const Geometry& g);
+void preload_misc(int elem, int metric);
+template <class K>
+inline void touch_kernel(K k) {
+  cudaFuncAttributes attr;
+  (void)cudaFuncGetAttributes(&attr, reinterpret_cast<const void*>(k));
+}
 cudaError_t launch_search(const SearchArgs& a, int elem, int metric, const Geometry& g,
                           cudaStream_t s);
 

@@ -283,6 +283,17 @@ cudaError_t launch_choose_start(const uint8_t* data, uint64_t stride, uint64_t n
   return cudaGetLastError();
 }
 
+void preload_misc(int elem, int metric) {
+  touch_kernel(centroid_kernel);
+#define GANN_PL(E, M) (touch_kernel(colsum_kernel<E>), touch_kernel(start_dist_kernel<E, M>))
+  if (metric == kL2) {
+    if (elem == kU8) GANN_PL(kU8, kL2); else if (elem == kI8) GANN_PL(kI8, kL2); else GANN_PL(kF32, kL2);
+  } else {
+    if (elem == kU8) GANN_PL(kU8, kIP); else if (elem == kI8) GANN_PL(kI8, kIP); else GANN_PL(kF32, kIP);
+  }
+#undef GANN_PL
+}
+
 cudaError_t launch_generate_u8(uint8_t* out, uint64_t out_stride, uint64_t n, uint32_t d,
                                uint32_t clusters, float sigma, float noise_frac,
                                uint64_t center_seed, uint64_t stream_seed, uint64_t row0,

@@ -1244,6 +1244,51 @@ void prune_reserve(uint32_t lists, uint64_t stride, uint32_t R, cudaStream_t s) 
   prune_handoff(std::min<uint64_t>(uint64_t(lists) * per, kHandoffMax / per * per), s);
 }
 
+namespace {
+template <int E, int M, int LPR, int CPL>
+void preload_prune_one() {
+  touch_kernel(prune_kernel<E, M, LPR, CPL, 32>);
+  touch_kernel(prune_chunked_kernel<E, M, LPR, CPL, 256>);
+  if (E != kF32) {
+    touch_kernel(prune_prep_kernel<E, M, 4, 0>);
+    touch_kernel(prune_prep_kernel<E, M, 4, 1>);
+    touch_kernel(prune_prep_kernel<E, M, 8, 0>);
+    touch_kernel(prune_prep_kernel<E, M, 8, 1>);
+    touch_kernel(prune_prep_kernel<E, M, 16, 0>);
+    touch_kernel(prune_prep_kernel<E, M, 16, 1>);
+  }
+}
+template <int E, int M>
+void preload_prune_geom(const Geometry& g) {
+  switch (g.lpr) {
+    case 1: return preload_prune_one<E, M, 1, 1>();
+    case 2: return preload_prune_one<E, M, 2, 1>();
+    case 4: return preload_prune_one<E, M, 4, 1>();
+    case 8: return preload_prune_one<E, M, 8, 1>();
+    case 16: return preload_prune_one<E, M, 16, 1>();
+    default:
+      if (g.cpl == 1) return preload_prune_one<E, M, 32, 1>();
+      if (g.cpl == 2) return preload_prune_one<E, M, 32, 2>();
+      return preload_prune_one<E, M, 32, 4>();
+  }
+}
+}  // namespace
+
+void preload_prune(int elem, int metric, const Geometry& g) {
+  touch_kernel(bin_lists_kernel);
+  touch_kernel(prune_walk_ring_kernel<4, 16>);
+  touch_kernel(prune_walk_ring_kernel<8, 8>);
+  touch_kernel(prune_walk_ring_kernel<16, 4>);
+  if (metric == kL2) {
+    if (elem == kU8) return preload_prune_geom<kU8, kL2>(g);
+    if (elem == kI8) return preload_prune_geom<kI8, kL2>(g);
+    return preload_prune_geom<kF32, kL2>(g);
+  }
+  if (elem == kU8) return preload_prune_geom<kU8, kIP>(g);
+  if (elem == kI8) return preload_prune_geom<kI8, kIP>(g);
+  return preload_prune_geom<kF32, kIP>(g);
+}
+
 bool prune_uses_mma(int elem, uint32_t mcap, uint64_t stride, uint32_t R) {
   if (elem == kF32 || mcap > 512 || mcap == 0) return false;
   return mma_layout(mcap, static_cast<uint32_t>(stride), R).total <= 200 * 1024;

@@ -640,6 +640,40 @@ cudaError_t dispatch_geom(const SearchArgs& a, const Geometry& g, cudaStream_t s
 }
 }  // namespace
 
+namespace {
+template <int E, int M, int LPR, int CPL>
+void preload_one() {
+  touch_kernel(search_kernel<E, M, LPR, CPL, false>);
+  touch_kernel(search_kernel<E, M, LPR, CPL, true, false>);
+  touch_kernel(search_kernel<E, M, LPR, CPL, true, true>);
+}
+template <int E, int M>
+void preload_geom(const Geometry& g) {
+  switch (g.lpr) {
+    case 1: return preload_one<E, M, 1, 1>();
+    case 2: return preload_one<E, M, 2, 1>();
+    case 4: return preload_one<E, M, 4, 1>();
+    case 8: return preload_one<E, M, 8, 1>();
+    case 16: return preload_one<E, M, 16, 1>();
+    default:
+      if (g.cpl == 1) return preload_one<E, M, 32, 1>();
+      if (g.cpl == 2) return preload_one<E, M, 32, 2>();
+      return preload_one<E, M, 32, 4>();
+  }
+}
+}  // namespace
+
+void preload_search(int elem, int metric, const Geometry& g) {
+  if (metric == kL2) {
+    if (elem == kU8) return preload_geom<kU8, kL2>(g);
+    if (elem == kI8) return preload_geom<kI8, kL2>(g);
+    return preload_geom<kF32, kL2>(g);
+  }
+  if (elem == kU8) return preload_geom<kU8, kIP>(g);
+  if (elem == kI8) return preload_geom<kI8, kIP>(g);
+  return preload_geom<kF32, kIP>(g);
+}
+
 Geometry make_geometry(uint32_t nch) {
   Geometry g{nch, 32, 1};
   if (nch <= 32) {
