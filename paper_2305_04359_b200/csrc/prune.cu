@@ -280,6 +280,9 @@ __host__ __device__ inline MmaLayout mma_layout(uint32_t mcap, uint32_t stride, 
 }
 
 constexpr int kMmaThreads = 128;
+#ifndef GANN_PREP_GU
+#define GANN_PREP_GU 4  // candidate rows in flight per thread in the prep gather
+#endif
 
 // Stage-1 -> stage-2 hand-off buffer (grows; one per process and device).
 constexpr uint64_t kHandoffMax = 1ull << 30;  // launches are chunked to fit
@@ -429,7 +432,7 @@ __global__ void __launch_bounds__(kMmaThreads)
     if ((kch & (kch - 1)) == 0 && kch <= NT) {
       // a thread keeps one chunk column; 4 rows' loads in flight per thread
       const uint32_t lk = __ffs(kch) - 1, c = tid & (kch - 1), step = NT >> lk;
-      constexpr int GU = 4;
+      constexpr int GU = GANN_PREP_GU;
       for (uint32_t r0 = tid >> lk; r0 < rows_g; r0 += GU * step) {
         uint4 v[GU];
 #pragma unroll
@@ -455,7 +458,7 @@ __global__ void __launch_bounds__(kMmaThreads)
         *reinterpret_cast<uint4*>(dst + c * 16) = v;
       }
     }
-    for (uint32_t t = tid; t < m * W; t += NT) cm[t] = 0u;
+    for (uint32_t t = tid; t < m * (W / 4); t += NT) reinterpret_cast<uint4*>(cm)[t] = make_uint4(0u, 0u, 0u, 0u);
     __syncthreads();
     // keys (distances from the caller, or d(p, .) — src/builder_common.cpp:136)
     // and the rows' norms. Re-prunes (d(p, .) computed here, ~70 rows): two
