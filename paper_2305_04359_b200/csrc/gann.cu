@@ -27,6 +27,7 @@
 #include <string>
 #include <mutex>
 #include <set>
+#include <thread>
 #include <tuple>
 #include <vector>
 
@@ -835,19 +836,27 @@ int gann_build(gann_index* idx, uint32_t L, float alpha, int rule, uint64_t seed
     cu(cudaMemsetAsync(idx->spre, 0, n, idx->stream), "clear row prefixes");
     cu(cudaMemsetAsync(idx->tcount, 0, n * 4, idx->stream), "clear counts");
     Timer t0(idx->stream);
-    const uint32_t start = choose_start_dev(idx);
-    idx->start = start;
-    // shuffled_order — src/builder_common.cpp:99-107 (same libstdc++ calls)
+    // shuffled_order — src/builder_common.cpp:99-107 (same libstdc++ calls):
+    // the shuffle does not depend on the start vertex (only the final swap
+    // does), so it runs on a host thread while the device picks the start
+    // and the batch scratch is allocated
     std::vector<uint32_t> order(n);
-    gann_shuffled_order(static_cast<uint32_t>(n), mix64(seed, 0x696e73657274ULL), start, order.data());
-    idx->order.ensure(n * 4);
-    cu(cudaMemcpyAsync(idx->order.p, order.data(), n * 4, cudaMemcpyHostToDevice, idx->stream),
-       "upload order");
-    t0.stop(idx, 0);
-    const uint32_t* d_order = idx->order.as<uint32_t>();
+    std::thread shuffler([&] {
+      for (uint64_t i = 0; i < n; i++) order[i] = static_cast<uint32_t>(i);
+      std::mt19937_64 rng(mix64(seed, 0x696e73657274ULL));
+      std::shuffle(order.begin(), order.end(), rng);
+    });
+    uint32_t start = 0;
+    try {
+      start = choose_start_dev(idx);
+    } catch (...) {
+      shuffler.join();
+      throw;
+    }
+    idx->start = start;
     // size the per-batch scratch once, from the largest batch: a cudaFree /
     // cudaMalloc inside the loop stalls the device for tens of milliseconds
-    {
+    try {
       uint32_t bmax = 0;
       for (auto [lo, hi] : batch_ranges(n, max_batch)) bmax = std::max(bmax, hi - lo);
       const uint32_t vcap = std::max<uint32_t>(64, 3 * L);
@@ -871,7 +880,17 @@ int gann_build(gann_index* idx, uint32_t L, float alpha, int rule, uint64_t seed
       // a batch can prune (every group) — growing it batch by batch meant a
       // cudaFree/cudaMalloc pair inside the timed batches
       idx->bins.ensure(size_t(std::max<uint64_t>(groups, bmax)) * 9 * 4 + 64 + 16 * 4);
+      idx->order.ensure(n * 4);
+    } catch (...) {
+      shuffler.join();
+      throw;
     }
+    shuffler.join();
+    std::iter_swap(order.begin(), std::find(order.begin(), order.end(), start));
+    cu(cudaMemcpyAsync(idx->order.p, order.data(), n * 4, cudaMemcpyHostToDevice, idx->stream),
+       "upload order");
+    t0.stop(idx, 0);
+    const uint32_t* d_order = idx->order.as<uint32_t>();
     const bool trace = env_u32("GANN_TRACE", 0) != 0;
     for (auto [lo, hi] : batch_ranges(n, max_batch)) {
       const uint32_t B = hi - lo;
