@@ -23,6 +23,7 @@
 // Groups are size-binned: 32-thread CTAs for <= small_group_cap sources,
 // 512-thread CTAs for hubs up to big_group_cap.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "internal.h"
@@ -448,7 +449,19 @@ cudaError_t merge_launch(const BackEdgeArgs& a, uint32_t ng, uint32_t nbig, uint
     const size_t smem = backedge_merge_smem(a.small_group_cap, a.R);
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
-    k<<<ng, 32, smem, s>>>(a, ng, nullptr, a.small_group_cap, ok, ov);
+    // resident one-warp CTAs walking the groups (grid-stride) rather than one
+    // CTA per group: millions of tiny CTAs per batch cost their launch, and a
+    // warp with several groups claims re-prune slots 32 groups per atomic
+    uint32_t grid = ng;
+    const char* pg = std::getenv("GANN_MERGE_GRID");
+    if (!(pg && *pg == '0')) {
+      int dev = 0, sms = 0, per_sm = 0;
+      if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+      if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+      if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 32, smem)) != cudaSuccess) return e;
+      grid = std::min<uint32_t>(ng, static_cast<uint32_t>(std::max(1, per_sm) * sms));
+    }
+    k<<<grid, 32, smem, s>>>(a, ng, nullptr, a.small_group_cap, ok, ov);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   if (nbig > 0 && MODE == 0 && a.sources_distinct) {
