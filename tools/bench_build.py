@@ -25,10 +25,10 @@ ap.add_argument("--reps", type=int, default=2)
 args = ap.parse_args()
 cfg = datagen.CONFIGS[args.config].scaled(args.n)
 torch.cuda.set_stream(torch.cuda.Stream())
-base = torch.empty(cfg.n * cfg.d, dtype=torch.uint8, device="cuda")
-check(lib().gann_generate_u8(base.data_ptr(), cfg.n, cfg.d, cfg.clusters, cfg.sigma, cfg.noise_frac,
-                             cfg.center_seed, cfg.base_seed, 0, 0))
-idx = g.Index.from_device(base.data_ptr(), cfg.n, cfg.d, np.uint8, "l2", cfg.R)
+tdt = {"u8": torch.uint8, "i8": torch.int8, "f32": torch.float32}[cfg.dtype]
+base = torch.empty(cfg.n * cfg.d, dtype=tdt, device="cuda")
+check(datagen.generate_device(lib(), cfg, base.data_ptr(), cfg.n, queries=False))
+idx = g.Index.from_device(base.data_ptr(), cfg.n, cfg.d, cfg.np_dtype, cfg.metric, cfg.R)
 sums = []
 for r in range(args.reps):
     idx.reset_stats()
