@@ -365,12 +365,15 @@ __device__ __forceinline__ int last_true(Pred pred, float e) {
   return lo;
 }
 
-// Threads per CTA by mask width (measured at c1): 128 for the short lists
-// (W = 4: re-prunes, +42% time at 256), 256 for the long insert-time lists
-// (W >= 8: -10% time against 128).
+// Threads per CTA by mask width (measured at c1): 96 for the short lists
+// (W = 4, mostly re-prunes of ~70 candidates: -5% against 128, +20% at 64,
+// +42% at 256), 256 for the long insert-time lists (W >= 8: -10% against 128).
+#ifndef GANN_PREP_NT4
+#define GANN_PREP_NT4 96
+#endif
 template <int W>
 struct PrepThreads {
-  static constexpr int value = W >= 8 ? 256 : 128;
+  static constexpr int value = W >= 8 ? 256 : GANN_PREP_NT4;
 };
 
 template <int E, int M, int W, int RULE>
