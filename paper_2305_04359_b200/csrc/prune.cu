@@ -371,9 +371,12 @@ __device__ __forceinline__ int last_true(Pred pred, float e) {
 #ifndef GANN_PREP_NT4
 #define GANN_PREP_NT4 96
 #endif
+#ifndef GANN_PREP_NT8
+#define GANN_PREP_NT8 256
+#endif
 template <int W>
 struct PrepThreads {
-  static constexpr int value = W >= 8 ? 256 : GANN_PREP_NT4;
+  static constexpr int value = W >= 8 ? GANN_PREP_NT8 : GANN_PREP_NT4;
 };
 
 template <int E, int M, int W, int RULE>
