@@ -252,7 +252,7 @@ __host__ __device__ inline MmaLayout mma_layout(uint32_t mcap, uint32_t stride, 
   l.w = mcap <= 128 ? 4 : (mcap <= 256 ? 8 : 16);
   // short lists (re-prunes: a row of R plus a few sources) get a smaller
   // staging area, so more CTAs fit an SM; the mask rows stay W words
-  l.mc = (std::min(mcap, l.w * 32) + 15) & ~15u;
+  l.mc = ((mcap < l.w * 32 ? mcap : l.w * 32) + 15) & ~15u;
   l.kp = (stride + 31) & ~31u;
   l.xs = l.kp + 16;
   l.stride = 4 + l.mc + l.w + l.mc * l.w;  // [m2, pad x3][ids mc][zero mask W][cull rows mc*W]
