@@ -279,7 +279,6 @@ __host__ __device__ inline MmaLayout mma_layout(uint32_t mcap, uint32_t stride, 
   return l;
 }
 
-constexpr int kMmaThreads = 128;
 #ifndef GANN_PREP_GU
 #define GANN_PREP_GU 4  // candidate rows in flight per thread in the prep gather
 #endif
