@@ -220,8 +220,12 @@ int gann_groundtruth_device(gann_index* idx, const void* d_queries, uint32_t nq,
 int gann_generate_u8(void* d_out, uint64_t n, uint32_t d, uint32_t clusters, float sigma,
                      float noise_frac, uint64_t center_seed, uint64_t stream_seed, uint64_t row0,
                      int device);
+/* The generators' normal deviates: out[u] = Phi^-1((u + 1/2) / 2^16) for
+ * u < 65536, on a 2^-16 grid (host only, no GPU needed). A deviate is
+ * out[hash & 0xFFFF]: an exact Gaussian up to the 16-bit discretisation. */
+int gann_normal_table(float* out);
 /* Seeded synthetic f32 rows (BASELINE config 3, TTI-like): a `clusters`-
- * component mixture, v = c + sigma z (c, z ~ Irwin-Hall(4) normals), scaled
+ * component mixture, v = c + sigma z (c, z ~ N(0, 1), gann_normal_table), scaled
  * to norm exp(norm_sigma g) (log-normal per-point norms); shift > 0 moves
  * every centre by shift * N(0, 1) (the out-of-distribution query set).
  * Computed in double, rounded to f32 once. */

@@ -77,6 +77,7 @@ SIGNATURES = {
     "gann_groundtruth_device": (_i, [_vp, _vp, _u32, _u32, _vp, _vp, _vp]),
     "gann_generate_u8": (_i, [_vp, _u64, _u32, _u32, _f, _f, _u64, _u64, _u64, _i]),
     "gann_generate_f32": (_i, [_vp, _u64, _u32, _u32, _f, _f, _f, _u64, _u64, _u64, _i]),
+    "gann_normal_table": (_i, [_vp]),
     "gann_save_graph": (_i, [_vp, C.c_char_p]),
     "gann_load_graph": (_i, [_vp, C.c_char_p]),
     "gann_index_create_from_file": (_i, [C.c_char_p, _i, _u32, _i, _pp]),

@@ -162,11 +162,12 @@ struct gann_index {
   std::vector<std::tuple<cudaEvent_t, cudaEvent_t, int>> timers;  // recorded, not yet read
   uint64_t back_pairs = 0, back_groups = 0, back_pruned = 0;
   // scratch
-  DevBuf q, qids, qdists, qnvis, qdc, qvids, qvd, qstart, table;
+  DevBuf q, qstaged, qids, qdists, qnvis, qdc, qvids, qvd, qstart, table;
   DevBuf order, vis_ids, vis_d, nvis;
   DevBuf gtarget, gcnt, goff, gcursor, gsrc, poff, plen, pid, pdist, bigg, pls, plb;
   DevBuf pt, ps, ok, ov, misc, gt, bins;
   uint32_t staged_nq = 0;
+  bool staged = false;  // gann_stage_queries has run
   // vertex partitioning (1 partition = the whole graph)
   uint32_t part_rank = 0, part_count = 1, part_size = 0, part_base = 0, part_rows = 0;
   uint32_t** d_parts = nullptr;            // device table of partition row pointers
@@ -177,6 +178,7 @@ struct gann_index {
   uint32_t bL = 0, brule = 0;
   float balpha = 0.0f;
   DevBuf pair_out, pair_cnt, lids;
+  PruneHandoff hand;  // the tensor-core prune's hand-off region (this index only)
 };
 
 namespace {
@@ -263,8 +265,27 @@ void release_build_scratch(gann_index* idx) {
                     &idx->gcursor, &idx->gsrc, &idx->poff, &idx->plen, &idx->pid, &idx->pdist, &idx->bigg,
                     &idx->pls, &idx->plb, &idx->bins})
     b->release();
-  prune_release();
+  prune_release(&idx->hand, idx->stream);
 }
+// Rows of an imported graph must satisfy set_neighbors (src/graph.cpp:42-59)
+// and the reference's invariant of distinct neighbours (check_graph_invariants,
+// src/graph.cpp:80-92; the search kernel relies on it), checked on the device.
+void validate_graph_rows(gann_index* idx, const uint32_t* d_rows, uint64_t rows, uint32_t R, uint64_t n,
+                         uint64_t row0, const std::string& what) {
+  if (rows == 0) return;
+  idx->misc.ensure(64);
+  auto* bad = idx->misc.as<unsigned long long>();
+  cu(launch_validate_rows(d_rows, rows, R, n, row0, bad, idx->stream), "validate rows");
+  unsigned long long b = 0;
+  cu(cudaMemcpyAsync(&b, bad, 8, cudaMemcpyDeviceToHost, idx->stream), "read back");
+  cu(cudaStreamSynchronize(idx->stream), "stream sync");
+  if (b == ~0ull) return;
+  const uint64_t v = row0 + (b >> 3);
+  static const char* why[] = {"", "id after GANN_NONE padding", "neighbor id out of range", "self loop",
+                              "duplicate neighbor"};
+  fail(GANN_EINVAL, what + why[b & 7] + " at vertex " + std::to_string(v));
+}
+
 // Stream sync; the phase events recorded before it are complete, so their
 // times are collected here at no extra cost.
 void sync(gann_index* idx) {
@@ -391,6 +412,7 @@ PruneArgs base_prune_args(gann_index* idx, float alpha, int rule) {
   // no prefixes, every re-prune tests all pairs — an A/B switch for tests)
   static const bool no_spre = env_u32("GANN_NO_SPRE", 0) != 0;
   p.spre = no_spre ? nullptr : idx->spre;
+  p.hand = &idx->hand;
   return p;
 }
 
@@ -478,9 +500,12 @@ void prune_binned(gann_index* idx, PruneArgs p, uint32_t maxlen, bool fine = fal
     lo = bounds[b];
   }
   if (total < p.count) {  // the rest is longer than the last bound
+    // lists longer than maxlen (insert-time walks that outgrew the visited
+    // buffer: only maxlen entries were written) are skipped here; the search
+    // flagged them and insert_batch re-runs them with a larger buffer
     PruneArgs q = p;
     q.mmin = lo + 1;
-    q.mcap = 0xFFFFFFFFu;
+    q.mcap = maxlen;
     q.skip_long = 1;
     cu(launch_prune(q, idx->elem, idx->metric, idx->geom, 256, idx->stream), "prune kernel (chunked)");
   }
@@ -794,12 +819,13 @@ void gann_index_free(gann_index* idx) {
                   static_cast<void*>(idx->stats), static_cast<void*>(idx->counters),
                   static_cast<void*>(idx->flags), static_cast<void*>(idx->qctr), static_cast<void*>(idx->spre)})
     if (p) cudaFree(p);
-  for (DevBuf* b : {&idx->q, &idx->qids, &idx->qdists, &idx->qnvis, &idx->qdc, &idx->qvids,
+  for (DevBuf* b : {&idx->q, &idx->qstaged, &idx->qids, &idx->qdists, &idx->qnvis, &idx->qdc, &idx->qvids,
                     &idx->qvd, &idx->qstart, &idx->table, &idx->order, &idx->vis_ids, &idx->vis_d,
                     &idx->nvis, &idx->gtarget, &idx->gcnt, &idx->goff, &idx->gcursor, &idx->gsrc,
                     &idx->poff, &idx->plen, &idx->pid, &idx->pdist, &idx->bigg, &idx->pls,
                     &idx->plb, &idx->pt, &idx->ps, &idx->ok, &idx->ov, &idx->misc, &idx->gt, &idx->bins})
     b->release();
+  prune_release(&idx->hand, idx->stream);
   if (idx->stream) cudaStreamDestroy(idx->stream);
   delete idx;
 }
@@ -875,7 +901,7 @@ int gann_build(gann_index* idx, uint32_t L, float alpha, int rule, uint64_t seed
       idx->pid.ensure(ptotal * 4);
       idx->pdist.ensure(ptotal * 4);
       if (prune_uses_mma(idx->elem, 512, idx->stride, idx->R))
-        prune_reserve(static_cast<uint32_t>(std::min<uint64_t>(groups, 0xFFFFFFFFu)), idx->stride, idx->R, idx->stream);
+        prune_reserve(&idx->hand, static_cast<uint32_t>(std::min<uint64_t>(groups, 0xFFFFFFFFu)), idx->stride, idx->R, idx->stream);
       // the prune's length bins: lists x (bins + 1) ids, for the largest count
       // a batch can prune (every group) — growing it batch by batch meant a
       // cudaFree/cudaMalloc pair inside the timed batches
@@ -947,21 +973,15 @@ int gann_import_graph(gann_index* idx, const uint32_t* adj, uint32_t start) {
     const uint64_t n = idx->n;
     const uint32_t R = idx->R;
     if (n && start >= n) fail(GANN_EINVAL, "start vertex out of range");
-    for (uint64_t v = 0; v < n; v++) {  // set_neighbors checks, src/graph.cpp:42-59
-      const uint32_t* r = adj + v * R;
-      bool ended = false;
-      for (uint32_t t = 0; t < R; t++) {
-        if (r[t] == GANN_NONE) {
-          ended = true;
-          continue;
-        }
-        if (ended) fail(GANN_EINVAL, "row " + std::to_string(v) + ": id after GANN_NONE padding");
-        if (r[t] >= n) fail(GANN_EINVAL, "neighbor id " + std::to_string(r[t]) + " out of range at vertex " + std::to_string(v));
-        if (r[t] == v) fail(GANN_EINVAL, "self loop at vertex " + std::to_string(v));
-      }
-    }
     set_device(idx);
     if (n) cu(cudaMemcpyAsync(idx->adj, adj, n * R * 4, cudaMemcpyHostToDevice, idx->stream), "upload graph");
+    try {
+      validate_graph_rows(idx, idx->adj, n, R, n, 0, "");
+    } catch (...) {  // leave an empty graph, not a half-valid one
+      cudaMemsetAsync(idx->adj, 0xFF, n * R * 4, idx->stream);
+      cudaStreamSynchronize(idx->stream);
+      throw;
+    }
     if (n) cu(cudaMemsetAsync(idx->spre, 0, n, idx->stream), "clear row prefixes");  // rows of unknown origin
     idx->start = start;
     sync(idx);
@@ -974,6 +994,7 @@ int gann_import_graph_device(gann_index* idx, const uint32_t* d_adj, uint32_t st
     if (idx->part_count != 1) fail(GANN_EINVAL, "import_graph needs an unpartitioned index");
     if (idx->n && start >= idx->n) fail(GANN_EINVAL, "start vertex out of range");
     set_device(idx);
+    validate_graph_rows(idx, d_adj, idx->n, idx->R, idx->n, 0, "");
     if (idx->n)
       cu(cudaMemcpyAsync(idx->adj, d_adj, idx->n * idx->R * 4, cudaMemcpyDeviceToDevice, idx->stream), "copy graph");
     if (idx->n) cu(cudaMemsetAsync(idx->spre, 0, idx->n, idx->stream), "clear row prefixes");
@@ -1113,8 +1134,9 @@ int gann_stage_queries(gann_index* idx, const void* d_queries, uint32_t nq) {
   return guarded([&] {
     if (!idx) fail(GANN_EINVAL, "index is NULL");
     set_device(idx);
-    stage_rows(idx, idx->q, d_queries, nq, true);
+    stage_rows(idx, idx->qstaged, d_queries, nq, true);
     idx->staged_nq = nq;
+    idx->staged = true;
     sync(idx);
   });
 }
@@ -1125,9 +1147,11 @@ int gann_search_staged(gann_index* idx, uint32_t k_out, uint32_t L, uint32_t k_g
     if (!idx) fail(GANN_EINVAL, "index is NULL");
     validate_search(idx, k_out, L, k_gate, eps, GANN_VISITED_FAST);
     if (idx->n == 0) fail(GANN_EINVAL, "search over an empty index");
+    if (!idx->staged) fail(GANN_EINVAL, "no queries staged (call gann_stage_queries first)");
+    set_device(idx);
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : idx->stream;
     SearchArgs a = base_search_args(idx, L, k_gate, k_out, eps, GANN_VISITED_FAST);
-    a.queries = idx->q.as<uint8_t>();
+    a.queries = idx->qstaged.as<uint8_t>();
     a.nq = idx->staged_nq;
     a.out_ids = d_ids;
     a.out_dists = d_dists;
@@ -1202,6 +1226,20 @@ int gann_alpha_prune(gann_index* idx, const uint32_t* p, const uint64_t* offsets
     }
     for (uint64_t i = 0; i < total; i++)
       if (cand_ids[i] >= idx->n) fail(GANN_EINVAL, "candidate id out of range");
+    // A candidate list is a visited set or a merged row: distinct ids (copies
+    // of p are dropped anyway, src/prune.cpp:16-18). The kernels' rank sort
+    // needs distinct keys, so a repeated id is rejected rather than guessed at.
+    {
+      std::vector<uint32_t> tmp;
+      for (uint32_t i = 0; i < count; i++) {
+        tmp.clear();
+        for (uint64_t j = offsets[i]; j < offsets[i + 1]; j++)
+          if (cand_ids[j] != p[i]) tmp.push_back(cand_ids[j]);
+        std::sort(tmp.begin(), tmp.end());
+        if (std::adjacent_find(tmp.begin(), tmp.end()) != tmp.end())
+          fail(GANN_EINVAL, "candidate list " + std::to_string(i) + " repeats an id");
+      }
+    }
     // one scratch block: p | beg | len | small | big | ids | dists | out | nout
     idx->pt.ensure(size_t(count) * 4 * 4 + size_t(count) * 8 + total * 8 + size_t(count) * idx->R * 4 + 64);
     uint8_t* base = idx->pt.as<uint8_t>();
@@ -1395,6 +1433,13 @@ int gann_generate_u8(void* d_out, uint64_t n, uint32_t d, uint32_t clusters, flo
                           center_seed, stream_seed, row0, nullptr),
        "generate");
     cu(cudaDeviceSynchronize(), "generate sync");
+  });
+}
+
+int gann_normal_table(float* out) {
+  return guarded([&] {
+    if (!out) fail(GANN_EINVAL, "NULL argument");
+    normal_table(out);
   });
 }
 
@@ -1806,9 +1851,6 @@ int gann_hnsw_create(gann_index* layer0, uint32_t num_layers, const uint32_t* up
     if (num_layers > 1) {
       if (m_upper == 0 || m_upper > 1024) fail(GANN_EINVAL, "upper-layer capacity must lie in [1, 1024]");
       if (!upper_adj) fail(GANN_EINVAL, "upper_adj is NULL");
-      const uint64_t words = uint64_t(num_layers - 1) * n * m_upper;
-      for (uint64_t i = 0; i < words; i++)
-        if (upper_adj[i] != GANN_NONE && upper_adj[i] >= n) fail(GANN_EINVAL, "neighbor id out of range");
     }
     set_device(layer0);
     auto* h = new gann_hnsw();
@@ -1823,6 +1865,15 @@ int gann_hnsw_create(gann_index* layer0, uint32_t num_layers, const uint32_t* up
         fail(GANN_ECUDA, "cudaMalloc upper layers");
       }
       cu(cudaMemcpy(h->upper, upper_adj, bytes, cudaMemcpyHostToDevice), "upload upper layers");
+      try {
+        for (uint32_t l = 1; l < num_layers; l++)
+          validate_graph_rows(layer0, h->upper + uint64_t(l - 1) * n * m_upper, n, m_upper, n, 0,
+                              "layer " + std::to_string(l) + ": ");
+      } catch (...) {
+        cudaFree(h->upper);
+        delete h;
+        throw;
+      }
     }
     *out = h;
   });

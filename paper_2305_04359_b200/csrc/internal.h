@@ -91,6 +91,14 @@ inline void touch_kernel(K k) {
 cudaError_t launch_search(const SearchArgs& a, int elem, int metric, const Geometry& g,
                           cudaStream_t s);
 
+// The tensor-core prune's stage-1 -> stage-2 hand-off region. One per index
+// (host-side bookkeeping; kernels only see the device pointer), so two
+// indexes pruning on one device from different host threads never share it.
+struct PruneHandoff {
+  uint32_t* buf = nullptr;
+  uint64_t cap = 0;
+};
+
 struct PruneArgs {
   const uint8_t* data;
   uint64_t stride;
@@ -120,6 +128,7 @@ struct PruneArgs {
   // its point's current row, so that prefix needs no pair tests among itself.
   uint8_t* spre;
   int row_lists;
+  PruneHandoff* hand;          // host pointer: the calling index's hand-off region
 };
 // threads = 32 for short lists, larger for hubs; smem from prune_smem_bytes.
 size_t prune_smem_bytes(uint32_t mcap, uint32_t R);
@@ -132,8 +141,8 @@ cudaError_t launch_bin_lists(const PruneArgs& a, const uint32_t* d_bounds, int n
 bool prune_uses_mma(int elem, uint32_t mcap, uint64_t stride, uint32_t R);
 // Allocate the tensor-core prune's hand-off region up front for launches of
 // up to `lists` lists (a build sizes it once from its largest batch).
-void prune_reserve(uint32_t lists, uint64_t stride, uint32_t R, cudaStream_t s);
-void prune_release();  // frees this device's hand-off region (after a build)
+void prune_reserve(PruneHandoff* h, uint32_t lists, uint64_t stride, uint32_t R, cudaStream_t s);
+void prune_release(PruneHandoff* h, cudaStream_t s);  // frees an index's hand-off region
 
 // ---- back-edge grouping (phase 2) -----------------------------------------
 // Pairs (target, source) come either from the out-rows of the batch's points
@@ -202,6 +211,9 @@ cudaError_t part_pairs_scatter(const uint32_t* adj_local, uint32_t base, uint32_
 cudaError_t launch_choose_start(const uint8_t* data, uint64_t stride, uint64_t n, uint32_t d,
                                 int elem, int metric, double* colsum, float* centroid,
                                 unsigned long long* best, cudaStream_t s);
+// table[u] = Phi^-1((u + 1/2) / 2^16) on a 2^-16 grid (host, 65536 floats)
+void normal_table(float* out);
+const float* device_normal_table();
 cudaError_t launch_generate_f32(float* out, uint64_t n, uint32_t d, uint32_t clusters, float sigma,
                                 float norm_sigma, float shift, uint64_t center_seed, uint64_t stream_seed,
                                 uint64_t row0, cudaStream_t s);
@@ -214,5 +226,10 @@ cudaError_t launch_groundtruth(const uint8_t* data, uint64_t stride, uint64_t n,
                                int metric, uint32_t nch, unsigned long long* partial,
                                uint32_t splits, uint32_t* ids, float* dists, cudaStream_t s);
 uint32_t groundtruth_splits(uint64_t n, uint32_t nq);
+// Validate rows [0, rows) of an n-vertex graph (row r is vertex row0 + r):
+// *bad = ~0 if fine, else (first bad row << 3) | code (1 id after padding,
+// 2 id out of range, 3 self loop, 4 repeated id).
+cudaError_t launch_validate_rows(const uint32_t* adj, uint64_t rows, uint32_t R, uint64_t n, uint64_t row0,
+                                 unsigned long long* bad, cudaStream_t s);
 
 }  // namespace gann

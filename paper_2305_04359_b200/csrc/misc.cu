@@ -1,5 +1,8 @@
 // misc.cu — start vertex, synthetic data generator, brute-force ground truth.
 #include <algorithm>
+#include <cmath>
+#include <mutex>
+#include <vector>
 
 #include "common.cuh"
 #include "internal.h"
@@ -67,9 +70,11 @@ __global__ void start_dist_kernel(const uint8_t* data, uint64_t stride, uint64_t
 
 // ---- synthetic data ---------------------------------------------------------
 // A pure function of (seeds, row, column), restated bit-for-bit in numpy by
-// paper_2305_04359_b200/datagen.py. Gaussian noise is Irwin-Hall(4) over
-// 16-bit uniforms (unit variance), i.e. integer arithmetic plus three IEEE f32
-// ops, so host and device agree exactly.
+// paper_2305_04359_b200/datagen.py. A standard normal deviate is the Gaussian
+// quantile of a 16-bit uniform, z = Phi^-1((u + 1/2) / 2^16), looked up in a
+// 2^16-entry table (normal_table below: an exact Gaussian up to the 16-bit
+// discretisation, tails to +-4.32 sigma) that host and device share, so the
+// rest is IEEE f32 (u8 rows) or double (f32 rows) arithmetic on both sides.
 constexpr uint64_t kKCenter = 0xC3A5C85C97CB3127ull;
 constexpr uint64_t kKCluster = 0x2545F4914F6CDD1Dull;
 constexpr uint64_t kKNoiseRow = 0x9E3779B97F4A7C15ull;
@@ -78,10 +83,9 @@ constexpr uint64_t kKNormal = 0xA0761D6478BD642Full;
 
 __global__ void gen_u8_kernel(uint8_t* out, uint64_t out_stride, uint64_t n, uint32_t d,
                               uint32_t clusters, float sigma, uint32_t noise_thr,
-                              uint64_t cseed, uint64_t sseed, uint64_t row0) {
+                              uint64_t cseed, uint64_t sseed, uint64_t row0, const float* __restrict__ ntab) {
   const uint64_t total = n * d;
   const uint64_t step = uint64_t(gridDim.x) * blockDim.x;
-  const float inv_sd = 1.0f / 37837.2227f;
   for (uint64_t idx = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total; idx += step) {
     const uint64_t i = idx / d;
     const uint32_t j = static_cast<uint32_t>(idx - i * d);
@@ -93,10 +97,7 @@ __global__ void gen_u8_kernel(uint8_t* out, uint64_t out_stride, uint64_t n, uin
     } else {
       const uint64_t c = mix64(sseed ^ kKCluster, r) % clusters;
       const uint32_t center = static_cast<uint32_t>(mix64(cseed ^ kKCenter, c * d + j) >> 56);
-      const uint64_t h = mix64(sseed ^ kKNormal, el);
-      const int s = static_cast<int>((h & 0xFFFF) + ((h >> 16) & 0xFFFF) + ((h >> 32) & 0xFFFF) +
-                                     ((h >> 48) & 0xFFFF)) - 131070;
-      const float z = __fmul_rn(static_cast<float>(s), inv_sd);
+      const float z = __ldg(ntab + (mix64(sseed ^ kKNormal, el) & 0xFFFF));
       const float x = __fadd_rn(static_cast<float>(center), __fmul_rn(sigma, z));
       const float rx = rintf(x);
       v = rx < 0.0f ? 0u : (rx > 255.0f ? 255u : static_cast<uint32_t>(rx));
@@ -105,20 +106,16 @@ __global__ void gen_u8_kernel(uint8_t* out, uint64_t out_stride, uint64_t n, uin
   }
 }
 
-// f32 mixture rows (config 3): one warp per row. Normals are Irwin-Hall(4)
-// over 16-bit uniforms (integer exact), the rest is double arithmetic, one
-// rounding to f32 at the end (datagen.gen_f32_numpy restates it).
+// f32 mixture rows (config 3): one warp per row. Normals come from the same
+// quantile table; the rest is double arithmetic, one rounding to f32 at the
+// end (datagen.gen_f32_numpy restates it).
 constexpr uint64_t kKShift = 0x8CB92BA72F3D8DD7ull;
 constexpr uint64_t kKNorm = 0x3C6EF372FE94F82Bull;
 
-__device__ __forceinline__ double ih_normal(uint64_t h) {
-  const int s = static_cast<int>((h & 0xFFFF) + ((h >> 16) & 0xFFFF) + ((h >> 32) & 0xFFFF) + ((h >> 48) & 0xFFFF)) -
-                131070;
-  return static_cast<double>(s) / 37837.22269;
-}
-
 __global__ void gen_f32_kernel(float* out, uint64_t n, uint32_t d, uint32_t clusters, double sigma,
-                               double norm_sigma, double shift, uint64_t cseed, uint64_t sseed, uint64_t row0) {
+                               double norm_sigma, double shift, uint64_t cseed, uint64_t sseed, uint64_t row0,
+                               const float* __restrict__ ntab) {
+  auto ih_normal = [&](uint64_t h) { return static_cast<double>(__ldg(ntab + (h & 0xFFFF))); };
   const int lane = threadIdx.x & 31;
   const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x >> 5);
   for (uint64_t i = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {
@@ -294,14 +291,77 @@ void preload_misc(int elem, int metric) {
 #undef GANN_PL
 }
 
+// Phi^-1(p): Acklam's rational approximation (relative error < 1.2e-9)
+// refined by one Halley step on erfc, i.e. to about double precision.
+static double norm_ppf(double p) {
+  static const double a[6] = {-3.969683028665376e+01, 2.209460984245205e+02, -2.759285104469687e+02,
+                              1.383577518672690e+02, -3.066479806614716e+01, 2.506628277459239e+00};
+  static const double b[5] = {-5.447609879822406e+01, 1.615858368580409e+02, -1.556989798598866e+02,
+                              6.680131188771972e+01, -1.328068155288572e+01};
+  static const double c[6] = {-7.784894002430293e-03, -3.223964580411365e-01, -2.400758277161838e+00,
+                              -2.549732539343734e+00, 4.374664141464968e+00, 2.938163982698783e+00};
+  static const double d[4] = {7.784695709041462e-03, 3.224671290700398e-01, 2.445134137142996e+00,
+                              3.754408661907416e+00};
+  const double plow = 0.02425;
+  double x;
+  if (p < plow) {
+    const double q = std::sqrt(-2.0 * std::log(p));
+    x = (((((c[0] * q + c[1]) * q + c[2]) * q + c[3]) * q + c[4]) * q + c[5]) /
+        ((((d[0] * q + d[1]) * q + d[2]) * q + d[3]) * q + 1.0);
+  } else if (p <= 1.0 - plow) {
+    const double q = p - 0.5, r = q * q;
+    x = (((((a[0] * r + a[1]) * r + a[2]) * r + a[3]) * r + a[4]) * r + a[5]) * q /
+        (((((b[0] * r + b[1]) * r + b[2]) * r + b[3]) * r + b[4]) * r + 1.0);
+  } else {
+    const double q = std::sqrt(-2.0 * std::log(1.0 - p));
+    x = -(((((c[0] * q + c[1]) * q + c[2]) * q + c[3]) * q + c[4]) * q + c[5]) /
+        ((((d[0] * q + d[1]) * q + d[2]) * q + d[3]) * q + 1.0);
+  }
+  const double e = 0.5 * std::erfc(-x / std::sqrt(2.0)) - p;
+  const double u = e * std::sqrt(2.0 * 3.14159265358979323846) * std::exp(x * x / 2.0);
+  return x - u / (1.0 + x * u / 2.0);
+}
+
+// table[u] = Phi^-1((u + 1/2) / 2^16) on a 2^-16 grid (the grid makes the
+// table immune to last-ulp differences between libm builds).
+void normal_table(float* out) {
+  for (uint32_t u = 0; u < 65536; u++) {
+    const double z = norm_ppf((static_cast<double>(u) + 0.5) / 65536.0);
+    out[u] = static_cast<float>(std::nearbyint(z * 65536.0) / 65536.0);
+  }
+}
+
+// The table in device memory, uploaded once per device (read-only).
+const float* device_normal_table() {
+  static std::mutex mu;
+  static float* tabs[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!tabs[dev]) {
+    std::vector<float> h(65536);
+    normal_table(h.data());
+    float* p = nullptr;
+    if (cudaMalloc(&p, 65536 * sizeof(float)) != cudaSuccess) return nullptr;
+    if (cudaMemcpy(p, h.data(), 65536 * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess) {
+      cudaFree(p);
+      return nullptr;
+    }
+    tabs[dev] = p;
+  }
+  return tabs[dev];
+}
+
 cudaError_t launch_generate_u8(uint8_t* out, uint64_t out_stride, uint64_t n, uint32_t d,
                                uint32_t clusters, float sigma, float noise_frac,
                                uint64_t center_seed, uint64_t stream_seed, uint64_t row0,
                                cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   const uint32_t thr = static_cast<uint32_t>(static_cast<double>(noise_frac) * 16777216.0);
+  const float* tab = device_normal_table();
+  if (!tab) return cudaErrorMemoryAllocation;
   gen_u8_kernel<<<148 * 16, 256, 0, s>>>(out, out_stride, n, d, clusters, sigma, thr, center_seed,
-                                         stream_seed, row0);
+                                         stream_seed, row0, tab);
   return cudaGetLastError();
 }
 
@@ -309,8 +369,10 @@ cudaError_t launch_generate_f32(float* out, uint64_t n, uint32_t d, uint32_t clu
                                 float norm_sigma, float shift, uint64_t center_seed, uint64_t stream_seed,
                                 uint64_t row0, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
+  const float* tab = device_normal_table();
+  if (!tab) return cudaErrorMemoryAllocation;
   gen_f32_kernel<<<148 * 16, 256, 0, s>>>(out, n, d, clusters, sigma, norm_sigma, shift, center_seed, stream_seed,
-                                          row0);
+                                          row0, tab);
   return cudaGetLastError();
 }
 
@@ -337,6 +399,57 @@ cudaError_t launch_groundtruth(const uint8_t* data, uint64_t stride, uint64_t n,
 #undef GANN_GT
   if (e != cudaSuccess) return e;
   gt_merge_kernel<<<(nq + 127) / 128, 128, 0, s>>>(partial, nq, splits, k, ids, dists);
+  return cudaGetLastError();
+}
+
+
+// ---- graph row validation ----------------------------------------------------
+// The reference's set_neighbors checks (src/graph.cpp:42-59: id in range, no
+// self loop) plus its graph invariant of distinct neighbours
+// (check_graph_invariants, src/graph.cpp:80-92), and our padding rule (ids
+// first, then GANN_NONE). One warp per row; the first bad row (lowest index)
+// wins: bad = min(row << 3 | code).
+namespace {
+__global__ void validate_rows_kernel(const uint32_t* adj, uint64_t rows, uint32_t R, uint64_t n, uint64_t row0,
+                                     unsigned long long* bad) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x >> 5);
+  for (uint64_t r = uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += warps) {
+    const uint32_t* row = adj + r * R;
+    const uint64_t v = row0 + r;
+    uint32_t code = 0;
+    bool ended = false;
+    for (uint32_t t0 = 0; t0 < R; t0 += 32) {
+      const uint32_t t = t0 + lane;
+      const uint32_t id = t < R ? row[t] : kNone;
+      const bool none = id == kNone;
+      const uint32_t nb = __ballot_sync(0xFFFFFFFFu, none && t < R);
+      const bool after_pad = !none && (ended || (nb & ((1u << lane) - 1u)) != 0);
+      if (after_pad) code = max(code, 1u);
+      if (!none && id >= n) code = max(code, 2u);
+      if (!none && id == v) code = max(code, 3u);
+      // duplicates against this chunk's lower lanes and every earlier chunk
+      for (uint32_t c0 = 0; c0 <= t0; c0 += 32) {
+        const uint32_t other = c0 + lane < R ? row[c0 + lane] : kNone;
+        for (int j = 0; j < 32; j++) {
+          const uint32_t o = __shfl_sync(0xFFFFFFFFu, other, j);
+          if (!none && o == id && (c0 < t0 || j < lane)) code = max(code, 4u);
+        }
+      }
+      ended = ended || nb != 0;
+    }
+    code = __reduce_max_sync(0xFFFFFFFFu, code);
+    if (lane == 0 && code) atomicMin(bad, (static_cast<unsigned long long>(r) << 3) | code);
+  }
+}
+}  // namespace
+
+cudaError_t launch_validate_rows(const uint32_t* adj, uint64_t rows, uint32_t R, uint64_t n, uint64_t row0,
+                                 unsigned long long* bad, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(bad, 0xFF, sizeof(unsigned long long), s);
+  if (e != cudaSuccess || rows == 0 || R == 0) return e;
+  const uint64_t blocks = std::min<uint64_t>((rows + 7) / 8, 148ull * 16);
+  validate_rows_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(adj, rows, R, n, row0, bad);
   return cudaGetLastError();
 }
 

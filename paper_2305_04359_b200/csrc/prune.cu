@@ -286,35 +286,30 @@ __host__ __device__ inline MmaLayout mma_layout(uint32_t mcap, uint32_t stride, 
 // Stage-1 -> stage-2 hand-off buffer (grows; one per process and device).
 constexpr uint64_t kHandoffMax = 1ull << 30;  // launches are chunked to fit
 
-static uint32_t* g_hand_buf[16] = {};
-static uint64_t g_hand_cap[16] = {};
-
-void prune_release() {
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 16 || !g_hand_buf[dev]) return;
-  cudaDeviceSynchronize();
-  cudaFree(g_hand_buf[dev]);
-  g_hand_buf[dev] = nullptr;
-  g_hand_cap[dev] = 0;
+void prune_release(PruneHandoff* h, cudaStream_t s) {
+  if (!h || !h->buf) return;
+  cudaStreamSynchronize(s);
+  cudaFree(h->buf);
+  h->buf = nullptr;
+  h->cap = 0;
 }
 
-uint32_t* prune_handoff(uint64_t bytes, cudaStream_t s) {
-  uint32_t** buf = g_hand_buf;
-  uint64_t* cap = g_hand_cap;
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 16) return nullptr;
-  if (bytes > cap[dev]) {
+// The index's hand-off region, grown to `bytes`. Only the owning index's
+// stream uses it, so a regrowth needs to wait for that stream alone.
+uint32_t* prune_handoff(PruneHandoff* h, uint64_t bytes, cudaStream_t s) {
+  if (!h) return nullptr;
+  if (bytes > h->cap) {
     // grows geometrically (a build's lists per launch double batch by batch;
-    // every regrowth is a device-wide sync + a large cudaMalloc)
-    const uint64_t want = std::max<uint64_t>(bytes, std::min<uint64_t>(2 * cap[dev], kHandoffMax));
+    // every regrowth is a stream sync + a large cudaMalloc)
+    const uint64_t want = std::max<uint64_t>(bytes, std::min<uint64_t>(2 * h->cap, kHandoffMax));
     cudaStreamSynchronize(s);
-    if (buf[dev]) cudaFree(buf[dev]);
-    buf[dev] = nullptr;
-    cap[dev] = 0;
-    if (cudaMalloc(&buf[dev], want) != cudaSuccess) return nullptr;
-    cap[dev] = want;
+    if (h->buf) cudaFree(h->buf);
+    h->buf = nullptr;
+    h->cap = 0;
+    if (cudaMalloc(&h->buf, want) != cudaSuccess) return nullptr;
+    h->cap = want;
   }
-  return buf[dev];
+  return h->buf;
 }
 
 // Stage 1 of the integer prune (one CTA per list, no serial part): gather the
@@ -933,6 +928,10 @@ __global__ void __launch_bounds__(NT) prune_chunked_kernel(const PruneArgs a) {
     const uint64_t m = a.lengths[l];
     uint32_t* orow = a.out_rows ? a.out_rows + uint64_t(l) * R : a.out_adj + uint64_t(p - a.out_base) * R;
     if (m < a.mmin) continue;
+    if (m > a.mcap) {  // only mcap entries exist (a walk that outgrew its buffer): re-run by the caller
+      if (tid == 0 && !a.skip_long) atomicAdd(a.too_long, 1u);
+      continue;
+    }
     auto key_at = [&](uint64_t i) -> uint64_t {
       const uint32_t id = a.cand_ids[beg + i];
       return id == p ? kMaxKey : make_key(a.cand_dists[beg + i], id);
@@ -1247,7 +1246,7 @@ cudaError_t launch_mma_w(const PruneArgs& a, const MmaLayout& ly, cudaStream_t s
   // the hand-off region is reused chunk by chunk (~1 GiB)
   const uint64_t per = uint64_t(ly.stride) * 4;
   const uint32_t chunk = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(a.count, kHandoffMax / per)));
-  uint32_t* hand = prune_handoff(uint64_t(chunk) * per, s);
+  uint32_t* hand = prune_handoff(a.hand, uint64_t(chunk) * per, s);
   if (!hand) return cudaErrorMemoryAllocation;
   const size_t walk_smem = size_t(kWalkWarps) * ly.mc * W * 4;
   if ((e = cudaFuncSetAttribute(prune_walk_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(walk_smem))) !=
@@ -1284,10 +1283,10 @@ cudaError_t launch_mma(const PruneArgs& a, cudaStream_t s) {
   return launch_mma_w<E, M, 16>(a, ly, s);
 }
 
-void prune_reserve(uint32_t lists, uint64_t stride, uint32_t R, cudaStream_t s) {
+void prune_reserve(PruneHandoff* h, uint32_t lists, uint64_t stride, uint32_t R, cudaStream_t s) {
   // the largest hand-off a launch of `lists` lists (up to 512 candidates) asks for
   const uint64_t per = uint64_t(mma_layout(512, static_cast<uint32_t>(stride), R).stride) * 4;
-  prune_handoff(std::min<uint64_t>(uint64_t(lists) * per, kHandoffMax / per * per), s);
+  prune_handoff(h, std::min<uint64_t>(uint64_t(lists) * per, kHandoffMax / per * per), s);
 }
 
 namespace {

@@ -8,8 +8,10 @@ function of (seeds, row, column): the device kernel (``csrc/misc.cu``,
 restates it bit-for-bit on the host (tests pin the two together) so the CPU
 reference arm can regenerate any prefix without a GPU.
 
-Noise is Irwin-Hall(4) over 16-bit uniforms (unit variance): integer
-arithmetic plus three IEEE f32 operations, identical on host and device.
+Noise is Gaussian: a deviate is the normal quantile of a 16-bit uniform,
+``z = Phi^-1((u + 1/2) / 2^16)``, read from a 65,536-entry table on a 2^-16
+grid (:func:`normal_table`; the library's ``gann_normal_table`` computes the
+same table and a CPU test pins the two), so host and device agree exactly.
 """
 from __future__ import annotations
 
@@ -40,6 +42,52 @@ def mix64_2(a, b):
     return mix64(np.asarray(a, np.uint64) ^ mix64(b))
 
 
+_ACKLAM_A = (-3.969683028665376e+01, 2.209460984245205e+02, -2.759285104469687e+02,
+             1.383577518672690e+02, -3.066479806614716e+01, 2.506628277459239e+00)
+_ACKLAM_B = (-5.447609879822406e+01, 1.615858368580409e+02, -1.556989798598866e+02,
+             6.680131188771972e+01, -1.328068155288572e+01)
+_ACKLAM_C = (-7.784894002430293e-03, -3.223964580411365e-01, -2.400758277161838e+00,
+             -2.549732539343734e+00, 4.374664141464968e+00, 2.938163982698783e+00)
+_ACKLAM_D = (7.784695709041462e-03, 3.224671290700398e-01, 2.445134137142996e+00, 3.754408661907416e+00)
+
+
+def _norm_ppf(p):
+    """Phi^-1(p): Acklam's rational approximation + one Halley step on erfc
+    (restates ``norm_ppf`` in csrc/misc.cu with the same libm calls)."""
+    import math
+    a, b, c, d = _ACKLAM_A, _ACKLAM_B, _ACKLAM_C, _ACKLAM_D
+    plow = 0.02425
+    if p < plow:
+        q = math.sqrt(-2.0 * math.log(p))
+        x = (((((c[0] * q + c[1]) * q + c[2]) * q + c[3]) * q + c[4]) * q + c[5]) / \
+            ((((d[0] * q + d[1]) * q + d[2]) * q + d[3]) * q + 1.0)
+    elif p <= 1.0 - plow:
+        q = p - 0.5
+        r = q * q
+        x = (((((a[0] * r + a[1]) * r + a[2]) * r + a[3]) * r + a[4]) * r + a[5]) * q / \
+            (((((b[0] * r + b[1]) * r + b[2]) * r + b[3]) * r + b[4]) * r + 1.0)
+    else:
+        q = math.sqrt(-2.0 * math.log(1.0 - p))
+        x = -(((((c[0] * q + c[1]) * q + c[2]) * q + c[3]) * q + c[4]) * q + c[5]) / \
+            ((((d[0] * q + d[1]) * q + d[2]) * q + d[3]) * q + 1.0)
+    e = 0.5 * math.erfc(-x / math.sqrt(2.0)) - p
+    u = e * math.sqrt(2.0 * 3.14159265358979323846) * math.exp(x * x / 2.0)
+    return x - u / (1.0 + x * u / 2.0)
+
+
+_NTAB = None
+
+
+def normal_table() -> np.ndarray:
+    """float32[65536]: table[u] = Phi^-1((u + 1/2) / 2^16) rounded to a 2^-16 grid."""
+    global _NTAB
+    if _NTAB is None:
+        t = np.array([round(_norm_ppf((u + 0.5) / 65536.0) * 65536.0) / 65536.0 for u in range(65536)],
+                     dtype=np.float64)
+        _NTAB = t.astype(np.float32)
+    return _NTAB
+
+
 def gen_u8_numpy(n, d, clusters, sigma, noise_frac, center_seed, stream_seed, row0=0):
     """Host restatement of ``gen_u8_kernel`` (csrc/misc.cu)."""
     r = np.arange(row0, row0 + n, dtype=np.uint64)[:, None]
@@ -49,23 +97,16 @@ def gen_u8_numpy(n, d, clusters, sigma, noise_frac, center_seed, stream_seed, ro
     noise_row = (mix64_2(np.uint64(stream_seed) ^ K_NOISE_ROW, r) >> np.uint64(40)) < thr
     c = mix64_2(np.uint64(stream_seed) ^ K_CLUSTER, r) % np.uint64(clusters)
     center = (mix64_2(np.uint64(center_seed) ^ K_CENTER, c * np.uint64(d) + j) >> np.uint64(56)).astype(np.float32)
-    h = mix64_2(np.uint64(stream_seed) ^ K_NORMAL, el)
-    s = ((h & np.uint64(0xFFFF)) + ((h >> np.uint64(16)) & np.uint64(0xFFFF)) +
-         ((h >> np.uint64(32)) & np.uint64(0xFFFF)) + ((h >> np.uint64(48)) & np.uint64(0xFFFF))).astype(np.int64)
-    s = (s - 131070).astype(np.float32)
-    inv_sd = np.float32(1.0) / np.float32(37837.2227)
-    z = s * inv_sd
+    z = normal_table()[(mix64_2(np.uint64(stream_seed) ^ K_NORMAL, el) & np.uint64(0xFFFF)).astype(np.int64)]
     x = center + np.float32(sigma) * z
     v = np.clip(np.rint(x), 0, 255).astype(np.uint8)
     uni = (mix64_2(np.uint64(stream_seed) ^ K_UNIFORM, el) >> np.uint64(56)).astype(np.uint8)
     return np.where(noise_row, uni, v)
 
 
-def _ih_normal(h):
-    """Irwin-Hall(4) over the four 16-bit fields of h, unit variance (float64)."""
-    s = ((h & np.uint64(0xFFFF)) + ((h >> np.uint64(16)) & np.uint64(0xFFFF)) +
-         ((h >> np.uint64(32)) & np.uint64(0xFFFF)) + ((h >> np.uint64(48)) & np.uint64(0xFFFF))).astype(np.int64)
-    return (s - 131070).astype(np.float64) / 37837.22269
+def _normal(h):
+    """The N(0, 1) deviate of hash h: normal_table()[h & 0xFFFF], as float64."""
+    return normal_table()[(h & np.uint64(0xFFFF)).astype(np.int64)].astype(np.float64)
 
 
 def gen_f32_numpy(n, d, clusters, sigma, norm_sigma, shift, center_seed, stream_seed, row0=0):
@@ -75,11 +116,11 @@ def gen_f32_numpy(n, d, clusters, sigma, norm_sigma, shift, center_seed, stream_
     r = np.arange(row0, row0 + n, dtype=np.uint64)[:, None]
     j = np.arange(d, dtype=np.uint64)[None, :]
     c = mix64_2(np.uint64(stream_seed) ^ K_CLUSTER, r) % np.uint64(clusters)
-    v = _ih_normal(mix64_2(np.uint64(center_seed) ^ K_CENTER, c * np.uint64(d) + j))
+    v = _normal(mix64_2(np.uint64(center_seed) ^ K_CENTER, c * np.uint64(d) + j))
     if shift > 0:
-        v = v + float(np.float32(shift)) * _ih_normal(mix64_2(np.uint64(center_seed) ^ K_SHIFT, c * np.uint64(d) + j))
-    v = v + float(np.float32(sigma)) * _ih_normal(mix64_2(np.uint64(stream_seed) ^ K_NORMAL, r * np.uint64(d) + j))
-    g = _ih_normal(mix64_2(np.uint64(stream_seed) ^ K_NORM, r))
+        v = v + float(np.float32(shift)) * _normal(mix64_2(np.uint64(center_seed) ^ K_SHIFT, c * np.uint64(d) + j))
+    v = v + float(np.float32(sigma)) * _normal(mix64_2(np.uint64(stream_seed) ^ K_NORMAL, r * np.uint64(d) + j))
+    g = _normal(mix64_2(np.uint64(stream_seed) ^ K_NORM, r))
     scale = np.exp(float(np.float32(norm_sigma)) * g) / np.sqrt((v * v).sum(axis=1, keepdims=True))
     return (v * scale).astype(np.float32)
 

@@ -377,3 +377,31 @@ def test_cpp_dropin_runs():
                        timeout=120)
     assert r.returncode == 0, r.stderr
     assert "ok" in r.stdout
+
+
+def test_build_long_walks_beyond_every_bin(oracle, monkeypatch):
+    """Walks longer than both the visited buffer and the largest prune bin
+    (|V| > max(vcap, 512), the chunked kernel's range) are skipped by the
+    first prune pass and re-run: the graph stays bit-identical."""
+    g = _g()
+    data = mixture(24, 3000, 16, clusters=10)
+    want, ws = oracle.build(data, 16, 600, 1.2, workers=8)
+    monkeypatch.setenv("GANN_VCAP", "64")
+    idx = g.build_diskann(data, "l2", g.DiskannParams(16, 600, 1.2))
+    got, _, s = idx.export_graph()
+    assert s == ws and (got == want).all()
+
+
+def test_alpha_prune_rejects_repeated_candidates():
+    """A candidate list repeating an id is rejected (the kernels' rank sort
+    needs distinct keys); copies of p itself are dropped as in prune.cpp:16-18."""
+    g = _g()
+    data = mixture(25, 200, 8, clusters=3)
+    idx = g.Index(data, "l2", 8)
+    p = g.PruneParams(8, 1.2)
+    ids = np.array([3, 4, 5, 4], np.uint32)
+    with pytest.raises(ValueError, match="repeats"):
+        idx.alpha_prune_many([0], [ids], [np.array(l2_cands(data, 0, ids), np.float32)], p)
+    ids = np.array([0, 3, 0, 4], np.uint32)  # p twice: fine
+    got = idx.alpha_prune_many([0], [ids], [np.array(l2_cands(data, 0, ids), np.float32)], p)
+    assert 0 not in list(got[0])

@@ -310,3 +310,29 @@ def test_fast_filter_layouts_keep_results(oracle, monkeypatch, env):
     for i in range(len(qs)):
         nv = int(want["n_visited"][i])
         assert (got.visited_ids[i, :nv] == want["visited_ids"][i, :nv]).all()
+
+
+def test_import_rejects_invalid_rows():
+    """set_neighbors' checks (src/graph.cpp:42-59) and the distinct-neighbour
+    invariant (check_graph_invariants, src/graph.cpp:80-92) at import; a
+    failed import leaves an empty graph."""
+    g = _g()
+    data, adj = path_fixture(6)
+    idx = g.Index(data, "l2", 2)
+    for bad, msg in [((2, [1, 1]), "duplicate"), ((3, [3, 4]), "self loop"), ((4, [9, 5]), "out of range"),
+                     ((5, [0xFFFFFFFF, 4]), "padding")]:
+        a = adj.copy()
+        a[bad[0]] = bad[1]
+        with pytest.raises(ValueError, match=msg):
+            idx.import_graph(a, 0)
+        assert (idx.export_graph()[1] == 0).all()
+    idx.import_graph(adj, 0)
+    assert (idx.export_graph()[0] == adj).all()
+
+
+def test_search_staged_needs_staged_queries():
+    g = _g()
+    data, adj = path_fixture(5)
+    idx = idx_with_graph(data, adj, 0)
+    with pytest.raises(ValueError, match="staged"):
+        idx.search_staged(g.SearchParams(2, 1, 0.0), 1, 0, 0)

@@ -65,6 +65,24 @@ def test_datagen_is_deterministic_and_prefix_stable():
     assert not (a == datagen.gen_u8_numpy(500, 128, 1000, 20.0, 0.0, 1, 3)).all()
 
 
+def test_normal_table_pinned_to_library():
+    """The generators' Gaussian quantile table: numpy restatement == the
+    library's host table, bit for bit; it is a standard normal."""
+    from paper_2305_04359_b200 import datagen
+    from paper_2305_04359_b200._lib import check, lib
+    want = np.empty(65536, np.float32)
+    check(lib().gann_normal_table(want.ctypes.data))
+    got = datagen.normal_table()
+    assert (got == want).all()
+    assert (got[::-1] == -got).all()  # symmetric
+    assert abs(float(got.astype(np.float64).mean())) < 1e-9
+    assert abs(float(got.astype(np.float64).std()) - 1.0) < 2e-3
+    assert 4.3 < float(got.max()) < 4.35
+    from math import erf, sqrt
+    for zq in (-2.0, -1.0, 0.5, 1.5):  # empirical CDF of the 2^16 levels == Phi
+        assert abs((got <= zq).mean() - 0.5 * (1 + erf(zq / sqrt(2)))) < 2e-5
+
+
 def test_datagen_matches_config_distribution():
     """Noise ~ N(0, sigma^2) around U[0,255] centres (BASELINE configs 0/1),
     10% uniform rows for config 2."""
@@ -96,12 +114,12 @@ def test_f32_datagen_config3_shape():
     assert abs(ln.mean()) < 0.03 and abs(ln.std() - 0.3) < 0.03
     assert (datagen.gen_f32_numpy(100, 200, 2000, 0.5, 0.3, 0.0, 1, 2, row0=50) == x[50:150]).all()
     # the cosine to the unshifted centre is lower for the shifted (query) stream
-    from paper_2305_04359_b200.datagen import K_CENTER, K_CLUSTER, _ih_normal, mix64_2
+    from paper_2305_04359_b200.datagen import K_CENTER, K_CLUSTER, _normal, mix64_2
 
     def cos_to_centre(rows, seed):
         r = np.arange(len(rows), dtype=np.uint64)[:, None]
         c = mix64_2(np.uint64(seed) ^ K_CLUSTER, r) % np.uint64(2000)
-        cen = _ih_normal(mix64_2(np.uint64(1) ^ K_CENTER, c * np.uint64(200) + np.arange(200, dtype=np.uint64)[None, :]))
+        cen = _normal(mix64_2(np.uint64(1) ^ K_CENTER, c * np.uint64(200) + np.arange(200, dtype=np.uint64)[None, :]))
         return (rows * cen).sum(1) / np.linalg.norm(rows, axis=1) / np.linalg.norm(cen, axis=1)
 
     assert cos_to_centre(q.astype(np.float64), cfg.query_seed).mean() < cos_to_centre(x.astype(np.float64)[:2000], cfg.base_seed).mean() - 0.02
