@@ -190,6 +190,45 @@ def host_base(cfg: Config, n: int | None = None) -> np.ndarray:
     return gen_u8_numpy(n, cfg.d, cfg.clusters, cfg.sigma, cfg.noise_frac, cfg.center_seed, cfg.base_seed)
 
 
+def _u8_rows_fast(out, row0, n, d, clusters, sigma, noise_frac, center_seed, stream_seed, centers):
+    """gen_u8_numpy for rows [row0, row0+n) into out[row0:row0+n], with the
+    cluster centres precomputed (the same values, fewer hashes)."""
+    r = np.arange(row0, row0 + n, dtype=np.uint64)[:, None]
+    c = (mix64_2(np.uint64(stream_seed) ^ K_CLUSTER, r) % np.uint64(clusters)).astype(np.int64)
+    el = r * np.uint64(d) + np.arange(d, dtype=np.uint64)[None, :]
+    z = normal_table()[(mix64_2(np.uint64(stream_seed) ^ K_NORMAL, el) & np.uint64(0xFFFF)).astype(np.int64)]
+    x = centers[c[:, 0]] + np.float32(sigma) * z
+    v = np.clip(np.rint(x), 0, 255).astype(np.uint8)
+    if noise_frac > 0:
+        thr = np.uint64(int(float(noise_frac) * 16777216.0))
+        noise_row = (mix64_2(np.uint64(stream_seed) ^ K_NOISE_ROW, r) >> np.uint64(40)) < thr
+        uni = (mix64_2(np.uint64(stream_seed) ^ K_UNIFORM, el) >> np.uint64(56)).astype(np.uint8)
+        v = np.where(noise_row, uni, v)
+    out[row0:row0 + n] = v
+
+
+def host_base_parallel(cfg: Config, n: int | None = None, threads: int | None = None,
+                       chunk: int = 65536) -> np.ndarray:
+    """host_base for the u8 configs at full size: row chunks on a thread pool
+    (numpy releases the GIL), cluster centres computed once. Bit-identical to
+    gen_u8_numpy (tests pin it) and to the device generator."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+    n = cfg.n if n is None else n
+    if cfg.dtype == "f32":
+        return host_base(cfg, n)
+    d = cfg.d
+    cj = np.arange(d, dtype=np.uint64)[None, :]
+    cc = np.arange(cfg.clusters, dtype=np.uint64)[:, None]
+    centers = (mix64_2(np.uint64(cfg.center_seed) ^ K_CENTER, cc * np.uint64(d) + cj) >> np.uint64(56)).astype(np.float32)
+    out = np.empty((n, d), np.uint8)
+    starts = range(0, n, chunk)
+    with ThreadPoolExecutor(threads or os.cpu_count() or 1) as ex:
+        list(ex.map(lambda r0: _u8_rows_fast(out, r0, min(chunk, n - r0), d, cfg.clusters, cfg.sigma, cfg.noise_frac,
+                                             cfg.center_seed, cfg.base_seed, centers), starts))
+    return out
+
+
 def host_queries(cfg: Config, nq: int | None = None) -> np.ndarray:
     nq = cfg.n_queries if nq is None else nq
     if cfg.dtype == "f32":
