@@ -1,8 +1,11 @@
 #!/usr/bin/env python
-"""Benchmark: batched beam-search QPS at recall@10 >= 0.95 over a B200-built
-Vamana graph (BASELINE config 1: 10M x 128 u8, R64 L128 alpha 1.2), plus the
-build's points/s, the search kernel's HBM roofline, the end-to-end QPS through
-the C ABI with host buffers, and the reference's CPU search timed beside it.
+"""Benchmark: batched beam-search QPS over a Vamana graph built from BASELINE
+config 1 (10M x 128 u8, R64 L128 alpha 1.2), at the smallest beam of the
+BASELINE sweep (10..200) reaching recall@10 0.95, else at L=200; plus the
+QPS / recall curve over every beam of the sweep and past it, the build's
+points/s and roofline, the search kernel's HBM roofline, the end-to-end QPS
+through the C ABI with host buffers, and the reference's CPU search timed
+beside it.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1] [--n N]
   python bench.py --impl reference ...     # the reference's own CPU path
@@ -21,11 +24,20 @@ per rank (checksum all-gather verifies them); each rank searches its own
 10k-query shard — no data-path collective ("scaling": "weak"). Timing: CUDA
 events on the launching streams, barrier + synchronize on both sides, max
 over ranks.
+
+The reference arm (--impl reference) never imports the package: it
+regenerates the config's points on the host (datagen's numpy restatement,
+bit-identical to the device generator), builds the graph with graphann's own
+build loop (oracle/_ref: the reference's sources), computes graphann's ground
+truth, and times graphann's beam_search on all host threads. Both arms print
+the same `config`, the graph's and the headline ids' SHA-256 (`parity`), and a
+QPS / recall curve (`qps_curve`).
 """
 from __future__ import annotations
 
 import argparse
 import ctypes
+import hashlib
 import importlib.util
 import json
 import os
@@ -42,10 +54,15 @@ sys.path.insert(0, str(ROOT))
 
 # BASELINE.json: "beam L swept 10..200"; --L-max widens it
 L_CANDIDATES = [10, 12, 14, 16, 20, 24, 28, 32, 40, 48, 56, 64, 80, 96, 128, 160, 200, 256, 320, 400, 512]
-# beams tried past the sweep when it ends below the recall target ("at_target")
-L_EXTEND = [256, 320, 400, 512, 640, 800, 1024, 1280, 1600, 2048]
+# beams tried past the sweep while the recall target is not reached (both arms;
+# ours stops at the kernel's on-chip beam limit, gann_search_max_beam)
+L_EXTEND = [256, 320, 400, 512, 640, 800, 1024, 1280, 1600, 2048, 2560, 3200, 4096, 5120, 6400, 8192]
+EXT_SAMPLE = 1000  # the reference arm times the extension on the first 1000 queries
 GT_DEPTH = 16
 CFG_INDEX = {"c0": 0, "c1": 1, "c2": 2, "c3": 3, "c4": 4}  # BASELINE.json configs[i]
+B200_L2_BYTES = 126 * 2**20
+METRIC = ("search QPS (Alg.1 beam {L,L,0}, top-10) at the smallest beam of the BASELINE sweep 10..200 reaching "
+          "recall@10 0.95, else at L=200 (config carries L and its recall; qps_curve every beam)")
 
 
 def load_module(name, rel):
@@ -79,13 +96,76 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extend", action="store_true",
                     help="do not search past the sweep for the beam that reaches the recall target")
-    ap.add_argument("--ref-n", type=int, default=100_000, help="reference arm: points in its CPU build sample")
+    ap.add_argument("--ref-build", default="full", choices=["full", "prefix"],
+                    help="reference arm: build the config's whole graph with graphann (default) or only a "
+                         "--ref-n prefix (quick checks; then the search runs over that prefix's graph)")
+    ap.add_argument("--ref-n", type=int, default=100_000, help="reference arm: points of a prefix build")
     ap.add_argument("--streams", type=int, default=2,
                     help="timed steps alternate over this many streams, so one step's tail overlaps the next "
                          "step's start (1 = serial launches; forced to 1 when steps flush L2)")
+    ap.add_argument("--no-build-roofline", action="store_true",
+                    help="skip the untimed exact-count rebuild behind build.roofline")
     ap.add_argument("--replicated-build", action="store_true",
                     help="N>1: every rank builds the whole graph (default: one vertex-partitioned build)")
     return ap.parse_args()
+
+
+def workload(args):
+    cfg = datagen.CONFIGS[args.config]
+    if args.n:
+        cfg = cfg.scaled(args.n)
+    return cfg, (args.nq or cfg.n_queries)
+
+
+def sweep_beams(args):
+    return [args.L] if args.L else [x for x in L_CANDIDATES if x <= args.L_max]
+
+
+def choose_beam(args, curve):
+    """The smallest swept beam reaching the target, else the sweep's largest
+    (identical rule in both arms, applied to each arm's own recall)."""
+    if args.L:
+        return args.L
+    for c in curve:
+        if c["recall@10"] >= args.target_recall:
+            return c["L"]
+    return curve[-1]["L"]
+
+
+def config_obj(args, cfg, nq, L, recall):
+    """The workload both arms print, key for key."""
+    index_bytes = cfg.n * (cfg.d * cfg.elem_bytes + 4 * cfg.R)
+    return {
+        "workload": f"BASELINE configs[{CFG_INDEX.get(args.config, '?')}]: {cfg.name}",
+        "n": cfg.n, "d": cfg.d, "dtype": cfg.dtype, "metric": cfg.metric, "R": cfg.R, "L_build": cfg.L,
+        "alpha": cfg.alpha, "max_batch": cfg.max_batch, "queries_per_gpu": nq, "k": cfg.k,
+        "L_search": L, "recall@10": round(recall, 5), "target_recall": args.target_recall,
+        "target_reached_in_sweep": recall >= args.target_recall,
+        "graph": "built from the config's points by each arm (ours: gann_build on the GPU; reference: graphann's "
+                 "build loop on the host); parity.graph_sha256 compares them",
+        "l2": ("flushed between steps" if index_bytes < 2 * B200_L2_BYTES
+               else f"inputs larger than L2 ({index_bytes / 1e9:.2f} GB index)"),
+    }
+
+
+def sha16(a) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).view(np.uint8).tobytes()).hexdigest()[:16]
+
+
+def build_bytes(st: dict, n: int, row_bytes: int, R: int):
+    """Algorithmic bytes of a whole build: per inserted point j
+    B_search(j) + |V_j| d s (prune rows) + 4R (its row written), per batch
+    16 E_b (pairs written + read) + per target 4(1+deg) read + 4(1+deg') written
+    + |M_t| d s when the merged list is re-pruned. `st` must come from a build
+    whose searches counted distinct evaluations (EXACT visited mode): then
+    st["evaluations"] = sum_j U_j. |V_j| = the expansions; the re-prune lists'
+    candidates = all prune candidates - the insert lists'."""
+    U, V = st["evaluations"], st["expansions"]
+    reprune_cands = max(0, st["prune_candidates"] - V)
+    search = U * row_bytes + 4.0 * V * (1 + R) + n * row_bytes
+    prune = V * row_bytes + 4.0 * R * n
+    back = 16.0 * st["back_pairs"] + 8.0 * (1 + R) * st["back_groups"] + reprune_cands * row_bytes
+    return {"search": search, "prune": prune, "back_edges": back, "total": search + prune + back}
 
 
 class ClockSampler:
@@ -204,10 +284,7 @@ def setup(args):
     import paper_2305_04359_b200 as g
     from paper_2305_04359_b200._lib import check, lib
 
-    cfg = datagen.CONFIGS[args.config]
-    if args.n:
-        cfg = cfg.scaled(args.n)
-    nq = args.nq or cfg.n_queries
+    cfg, nq = workload(args)
     n, d, k = cfg.n, cfg.d, cfg.k
     dev = local
 
@@ -275,18 +352,12 @@ def setup(args):
             build_mode = "replicated: every rank builds the whole graph"
         bstats = idx.stats()
     idx.release_scratch()  # after the timed build: the search needs none of it
-    adj_t = _tensor_from_ptr(idx.device_ptrs()[2], n * cfg.R * 4).view(torch.int32)  # a view, no copy
-    checksum, CH = 0, 1 << 28  # chunked: an int64 copy of a 100M-row graph would not fit beside it
-    for c0 in range(0, n * cfg.R, CH):
-        c1 = min(n * cfg.R, c0 + CH)
-        w = 1 + torch.arange(c0, c1, device="cuda") % 7919
-        checksum += int(adj_t[c0:c1].to(torch.int64).mul_(w).sum().item())
-    checksum &= (1 << 63) - 1
-    replicas_identical = distutil.replicas_identical(checksum, dist if world > 1 else None)
-    deg_mean = float((adj_t != -1).sum().item()) / n
-    del adj_t
+    adj_h, deg_h, start_h = idx.export_graph()  # host copy: the graph's checksum (and the CPU baseline)
+    graph_sha = sha16(adj_h)
+    replicas_identical = distutil.replicas_identical(int(graph_sha, 16), dist if world > 1 else None)
+    deg_mean = float(deg_h.mean())
 
-    # ---- ground truth (GPU brute force) and the beam giving recall >= target -----------------
+    # ---- ground truth (GPU brute force) -------------------------------------------
     if d * cfg.elem_bytes <= 256:
         gt_ids = torch.empty(nq * GT_DEPTH, dtype=torch.int32, device="cuda")
         gt_d = torch.empty(nq * GT_DEPTH, dtype=torch.float32, device="cuda")
@@ -300,50 +371,94 @@ def setup(args):
     out_ids = torch.empty(nq * k, dtype=torch.int32, device="cuda")
     out_d = torch.empty(nq * k, dtype=torch.float32, device="cuda")
     stream = torch.cuda.current_stream().cuda_stream
+    # L2: flushed between steps when the index fits in it (serial launches then)
+    l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
+    index_bytes = n * (d * cfg.elem_bytes + 4 * cfg.R)
+    flush = index_bytes < 2 * l2_bytes
+    flush_buf = torch.empty(max(4 * l2_bytes, 1), dtype=torch.uint8, device="cuda") if flush else None
+    nstreams = 1 if flush else max(1, args.streams)
+    streams = [stream] + [torch.cuda.Stream().cuda_stream for _ in range(nstreams - 1)]
+    souts = [(out_ids, out_d)] + [(torch.empty_like(out_ids), torch.empty_like(out_d)) for _ in range(nstreams - 1)]
+    ext = [torch.cuda.ExternalStream(sp_) for sp_ in streams]
 
     def search_L(L):
         idx.search_staged(g.SearchParams(L, L, 0.0), k, out_ids.data_ptr(), out_d.data_ptr(), stream)
 
+    def timed(sp, nt):
+        """ms per launch of nt launches alternating over the streams (serial
+        launches with L2 flushes when the index fits in L2), max over ranks."""
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nt)]
+        t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        t0e.record(ext[0])
+        for es in ext[1:]:
+            es.wait_event(t0e)
+        for i, (e0, e1) in enumerate(evs):
+            j = i % nstreams
+            if flush:
+                flush_buf.fill_(1)
+            e0.record(ext[j])
+            idx.search_staged(sp, k, souts[j][0].data_ptr(), souts[j][1].data_ptr(), streams[j])
+            e1.record(ext[j])
+        for es in ext[1:]:
+            ev = torch.cuda.Event()
+            ev.record(es)
+            ext[0].wait_event(ev)
+        t1e.record(ext[0])
+        torch.cuda.synchronize()
+        barrier()
+        spans = [e0.elapsed_time(e1) for e0, e1 in evs]
+        total = sum(spans) if nstreams == 1 else t0e.elapsed_time(t1e)
+        return allreduce(total) / nt, spans
+
+    def recall_of(res, rows=None):
+        ti, td = (gt_ids_h, gt_d_h) if rows is None else (gt_ids_h[:rows], gt_d_h[:rows])
+        r = res if rows is None else res[:rows]
+        return allreduce(float(evalutil.recall_at_k(ti, td, r, k).mean()), "mean")
+
+    # ---- QPS / recall at every beam of the sweep, then the headline beam -------------------
     curve = []
-    chosen = args.L
-    for L in ([args.L] if args.L else [x for x in L_CANDIDATES if x <= args.L_max]):
-        search_L(L)
+    for L in sweep_beams(args):
+        sp = g.SearchParams(L, L, 0.0)
+        search_L(L)  # warm + results for the recall
         torch.cuda.synchronize()
         res = out_ids.cpu().numpy().view(np.uint32).reshape(nq, k)
-        rec = float(evalutil.recall_at_k(gt_ids_h, gt_d_h, res, k).mean())
-        rec = allreduce(rec, "mean")
-        curve.append({"L": L, "recall@10": round(rec, 5)})
-        if not args.L and rec >= args.target_recall:
-            chosen = L
-            break
-    target_reached = bool(chosen) or args.L > 0
-    if not chosen:  # not reached inside the sweep: report the sweep's largest beam
-        chosen = curve[-1]["L"]
-    recall = curve[-1]["recall@10"]
+        ms, _ = timed(sp, 4)
+        curve.append({"L": L, "recall@10": round(recall_of(res), 5), "qps": round(world * nq / (ms / 1e3), 1),
+                      "ms_per_launch": round(ms, 4)})
+    chosen = choose_beam(args, curve)
+    recall = next(c["recall@10"] for c in curve if c["L"] == chosen)
+    target_reached = recall >= args.target_recall
     sp = g.SearchParams(chosen, chosen, 0.0)
-    # the sweep ended below the target: continue past it until the target is
-    # reached (reported beside the headline as "at_target")
-    ext_curve, L_target = [], None
-    if not target_reached and not args.no_extend:
-        for L in [x for x in L_EXTEND if x > chosen]:
+    # past the sweep while the target is not reached, up to the on-chip beam limit
+    ext_curve, L_target, max_beam = [], None, idx.max_beam()
+    if not target_reached and not args.no_extend and not args.L:
+        for L in [x for x in L_EXTEND if x > curve[-1]["L"]]:
+            if L > max_beam:
+                break
             search_L(L)
             torch.cuda.synchronize()
             res = out_ids.cpu().numpy().view(np.uint32).reshape(nq, k)
-            rec = allreduce(float(evalutil.recall_at_k(gt_ids_h, gt_d_h, res, k).mean()), "mean")
-            ext_curve.append({"L": L, "recall@10": round(rec, 5)})
+            ms, _ = timed(g.SearchParams(L, L, 0.0), 2)
+            rec = recall_of(res)
+            ext_curve.append({"L": L, "recall@10": round(rec, 5), "qps": round(world * nq / (ms / 1e3), 1),
+                              f"recall@10_first{EXT_SAMPLE}": round(recall_of(res, EXT_SAMPLE), 5)})
             if rec >= args.target_recall:
                 L_target = L
                 break
-        search_L(chosen)
-        torch.cuda.synchronize()
+    search_L(chosen)
+    torch.cuda.synchronize()
+    ids_sha = sha16(out_ids.cpu().numpy().view(np.uint32).reshape(nq, k))
 
     return dict(torch=torch, dist=dist, g=g, check=check, lib=lib, cfg=cfg, nq=nq, n=n, d=d, k=k, dev=dev,
                 rank=rank, world=world, barrier=barrier, allreduce=allreduce, base=base, qdev=qdev, idx=idx,
                 build_s=build_s, bstats=bstats, replicas_identical=replicas_identical, deg_mean=deg_mean,
-                build_mode=build_mode,
+                build_mode=build_mode, adj_h=adj_h, start_h=start_h, graph_sha=graph_sha, ids_sha=ids_sha,
                 out_ids=out_ids, out_d=out_d, stream=stream, search_L=search_L, curve=curve, chosen=chosen,
                 recall=recall, target_reached=target_reached, sp=sp, gt_ids_h=gt_ids_h, gt_d_h=gt_d_h,
-                ext_curve=ext_curve, L_target=L_target)
+                ext_curve=ext_curve, L_target=L_target, max_beam=max_beam, timed=timed, flush=flush,
+                flush_buf=flush_buf, nstreams=nstreams, streams=streams, souts=souts, ext=ext,
+                index_bytes=index_bytes, params=params)
 
 
 def run_ours(args):
@@ -355,17 +470,11 @@ def run_ours(args):
     build_mode = S["build_mode"]
     out_ids, out_d, stream, search_L, curve = S["out_ids"], S["out_d"], S["stream"], S["search_L"], S["curve"]
     chosen, recall, target_reached, sp = S["chosen"], S["recall"], S["target_reached"], S["sp"]
+    flush, flush_buf, nstreams, streams, souts, ext = (S["flush"], S["flush_buf"], S["nstreams"], S["streams"],
+                                                       S["souts"], S["ext"])
+    s_el = cfg.elem_bytes
 
     # ---- timed search steps --------------------------------------------------------
-    l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
-    s_el = cfg.elem_bytes
-    index_bytes = n * (d * s_el + 4 * cfg.R)
-    flush = index_bytes < 2 * l2_bytes
-    flush_buf = torch.empty(max(4 * l2_bytes, 1), dtype=torch.uint8, device="cuda") if flush else None
-    nstreams = 1 if flush else max(1, args.streams)
-    streams = [stream] + [torch.cuda.Stream().cuda_stream for _ in range(nstreams - 1)]
-    souts = [(out_ids, out_d)] + [(torch.empty_like(out_ids), torch.empty_like(out_d)) for _ in range(nstreams - 1)]
-    ext = [torch.cuda.ExternalStream(sp_) for sp_ in streams]
     for _ in range(args.warmup):
         search_L(chosen)
     idx.reset_stats()
@@ -429,6 +538,8 @@ def run_ours(args):
     scratch_b = idx.async_scratch_bytes(nq, k)
     scratch = [torch.empty(scratch_b, dtype=torch.uint8, device="cuda") for _ in range(nstreams)]
     L_ = lib()
+    search_L(chosen)
+    torch.cuda.synchronize()
 
     def e2e_async(i):
         j = i % nstreams
@@ -470,59 +581,56 @@ def run_ours(args):
     for eps in (0.0, 0.1, 0.25):
         for L in [x for x in (16, 32, 64, 128, 200) if x <= args.L_max]:
             spx = g.SearchParams(L, k, eps)
-            best = float("inf")
-            for _ in range(3):
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(ext[0])
-                idx.search_staged(spx, k, out_ids.data_ptr(), out_d.data_ptr(), stream)
-                e1.record(ext[0])
-                torch.cuda.synchronize()
-                best = min(best, e0.elapsed_time(e1))
+            idx.search_staged(spx, k, out_ids.data_ptr(), out_d.data_ptr(), stream)
+            torch.cuda.synchronize()
             res = out_ids.cpu().numpy().view(np.uint32).reshape(nq, k)
             rec = float(evalutil.recall_at_k(gt_ids_h, gt_d_h, res, k).mean())
+            ms, _ = S["timed"](spx, 3)
             secondary.append({"L": L, "k_gate": k, "eps": eps, "recall@10": round(allreduce(rec, "mean"), 5),
-                              "qps": round(world * nq / (allreduce(best) / 1e3), 1)})
-    # ---- QPS at the beam that reaches the recall target past the sweep --------------------
-    at_target = None
-    if S["ext_curve"]:
-        at_target = {"L": S["L_target"], "reached": S["L_target"] is not None,
-                     "recall_curve_past_sweep": S["ext_curve"]}
-        if S["L_target"]:
-            spt = g.SearchParams(S["L_target"], S["L_target"], 0.0)
-            nt = max(3, min(10, args.steps))
-            idx.search_staged(spt, k, out_ids.data_ptr(), out_d.data_ptr(), stream)
-            torch.cuda.synchronize()
-            barrier()
-            t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            t0e.record(ext[0])
-            for es in ext[1:]:
-                es.wait_event(t0e)
-            for i in range(nt):
-                j = i % nstreams
-                idx.search_staged(spt, k, souts[j][0].data_ptr(), souts[j][1].data_ptr(), streams[j])
-            for es in ext[1:]:
-                ev = torch.cuda.Event()
-                ev.record(es)
-                ext[0].wait_event(ev)
-            t1e.record(ext[0])
-            torch.cuda.synchronize()
-            barrier()
-            tms = allreduce(t0e.elapsed_time(t1e))
-            at_target.update({"recall@10": S["ext_curve"][-1]["recall@10"], "qps": round(world * nq * nt / (tms / 1e3), 1),
-                              "ms_per_step": round(tms / nt, 4), "steps": nt,
-                              "timing": f"{nt} launches alternating over {nstreams} stream(s), as the headline"})
+                              "qps": round(world * nq / (ms / 1e3), 1)})
     search_L(chosen)  # out_ids back to the headline search (the CPU baseline compares against it)
     torch.cuda.synchronize()
 
     # ---- CPU baseline: the reference's beam_search over the same graph, rank 0 at N=1 ------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline_search(idx, base, qh.numpy(), chosen, k, args.cpu_seconds, out_ids, nq, cfg.metric)
+        cpu = cpu_baseline_search(S["adj_h"], S["start_h"], base.view(n, d).cpu().numpy(), qh.numpy(), chosen, k,
+                                  args.cpu_seconds, out_ids, nq, cfg.metric)
 
-    build_bytes = search_bytes(dict(bstats, R=cfg.R), d * s_el, bstats["queries"], 0)
-    build_search_ms = bstats["build_ms"]["search"]
+    # ---- the build's roofline: its algorithmic bytes (an untimed rebuild whose
+    # searches count distinct evaluations, EXACT visited mode) over the timed
+    # build's wall time and its kernel time --------------------------------------------------
+    build_roof = None
+    if build_mode == "single-gpu" and not args.no_build_roofline:
+        os.environ["GANN_BUILD_VISITED"] = "exact"
+        xi = g.Index.from_device(base.data_ptr(), n, d, cfg.np_dtype, cfg.metric, cfg.R, dev)
+        xi.reset_stats()
+        xi.build(S["params"])
+        torch.cuda.synchronize()
+        del os.environ["GANN_BUILD_VISITED"]
+        xb = xi.stats()
+        same = sha16(xi.export_graph()[0]) == S["graph_sha"]
+        xi.close()
+        del xi
+        bb = build_bytes(xb, n, d * s_el, cfg.R)
+        kern_ms = sum(bstats["build_ms"].values())
+        build_roof = {
+            "bound": "hbm", "unit": "GB/s", "peak": peak,
+            "achieved": round(bb["total"] / build_s / 1e9, 1), "frac": round(bb["total"] / build_s / 1e9 / peak, 4),
+            "basis": "algorithmic bytes of the whole build (SURVEY.md §8d: per point B_search + |V| d s + 4R, per batch "
+                     "16 E + target rows read/written + re-pruned lists' rows) / the timed build's wall time",
+            "algorithmic_bytes": {kk: round(v) for kk, v in bb.items()},
+            "bytes_per_point": round(bb["total"] / n, 1),
+            "kernel_time_frac": round(bb["total"] / (kern_ms / 1e3) / 1e9 / peak, 4) if kern_ms else None,
+            "distinct_evals_per_point": round(xb["evaluations"] / n, 1),
+            "fast_filter_evals_per_point": round(bstats["evaluations"] / n, 1),
+            "exact_count_rebuild_graph_identical": same,
+        }
+
+    peak_note = ("algorithmic bytes count each query's rows; rows shared across queries (hubs) are served "
+                 "from the 126 MB L2, so achieved can exceed the HBM peak" if achieved > peak else None)
     line = {
-        "metric": "search QPS at recall@10>=0.95 (Alg.1 beam {L,L,0}, top-10) over a B200-built Vamana graph",
+        "metric": METRIC,
         "value": round(qps, 1),
         "unit": "queries/s",
         "n_gpus": world,
@@ -534,18 +642,15 @@ def run_ours(args):
         "vs_baseline": None,
         "dtype": cfg.dtype,
         "data": "synthetic: seeded Gaussian mixture with BASELINE config shapes (datagen.py), generated in HBM",
-        "config": {
-            "workload": f"BASELINE configs[{CFG_INDEX.get(args.config, '?')}]: {cfg.name}",
-            "n": n, "d": d, "metric": cfg.metric, "R": cfg.R, "L_build": cfg.L, "alpha": cfg.alpha,
-            "max_batch": cfg.max_batch, "queries_per_gpu": nq, "k": k,
-            "L_search": chosen, "recall@10": recall, "target_recall": args.target_recall,
-            "target_reached_in_sweep": target_reached,
-            "l2": "flushed between steps" if flush else f"inputs larger than L2 ({index_bytes / 1e9:.2f} GB index)",
-            "streams": nstreams,
-            "step_pipelining": ("steps alternate over 2 streams: a step's tail overlaps the next step's start; every "
-                                "step searches its whole batch; value = K*nq / elapsed of all K" if nstreams > 1
-                                else "serial launches"),
-        },
+        "config": config_obj(args, cfg, nq, chosen, recall),
+        "parity": {"graph_sha256": S["graph_sha"], "start": int(S["start_h"]), "ids_sha256": S["ids_sha"],
+                   "basis": "sha256[:16] of the n x R uint32 graph rows (GANN_NONE padded) and of the headline "
+                            "search's nq x k ids; the reference arm prints the same over graphann's own build "
+                            "and search"},
+        "streams": nstreams,
+        "step_pipelining": ("steps alternate over 2 streams: a step's tail overlaps the next step's start; every "
+                            "step searches its whole batch; value = K*nq / elapsed of all K" if nstreams > 1
+                            else "serial launches"),
         "roofline": {
             "bound": "hbm", "kernel": "search_kernel", "achieved": round(achieved, 1), "peak": peak,
             "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
@@ -556,8 +661,7 @@ def run_ours(args):
                                 else "mean of the launches' own event spans"),
             "launch_event_span_ms_mean": round(statistics.mean(step_ms), 4),
             "outputs_agree_across_streams": outs_agree,
-            "note": ("algorithmic bytes count each query's rows; rows shared across queries (hubs) are served "
-                     "from the 126 MB L2, so achieved can exceed the HBM peak" if achieved > peak else None),
+            "note": peak_note,
             "traffic": traffic_from_profile(cfg.name, chosen),
             "gathered": gathered_obj(sstats, args.steps, d * s_el, nq, k, cfg.R, avg_launch_s, peak,
                                     traffic_from_profile(cfg.name, chosen)),
@@ -579,15 +683,18 @@ def run_ours(args):
             "warmup": "none: one build, including its scratch allocation",
             "phases_ms": {kk: round(v, 1) for kk, v in bstats["build_ms"].items()},
             "mean_degree": round(deg_mean, 3), "replicas_identical": replicas_identical,
-            "search_gather_rate": {
-                "value": round(build_bytes / (build_search_ms / 1e3) / 1e9, 1) if build_search_ms else None, "unit": "GB/s",
-                "basis": "fast-mode evaluations x row bytes + adjacency rows, / the build's search time; "
-                         "re-evaluations are partly L2 hits, so this is a gather rate, not DRAM bandwidth"},
+            "roofline": build_roof,
             "stats": {kk: v for kk, v in bstats.items() if kk != "build_ms"},
         },
-        "recall_curve": curve,
-        "at_target": at_target,
-        "secondary_sweep": {"semantics": "reference eval {L, k_gate=10, eps}, top-10, one serial launch (best of 3, L2 not flushed)",
+        "qps_curve": {"basis": "every beam of the sweep: recall over all queries, QPS of 4 launches timed as the "
+                               "headline (extension: 2 launches)",
+                      "sweep": curve,
+                      "extension": {"beams": S["ext_curve"], "reached_target_at": S["L_target"],
+                                    "stopped": ("target reached" if S["L_target"] else
+                                                f"on-chip beam limit {S['max_beam']} of this index" if S["ext_curve"]
+                                                and S["ext_curve"][-1]["L"] < L_EXTEND[-1] else "end of the list")
+                                    } if S["ext_curve"] else None},
+        "secondary_sweep": {"semantics": "reference eval {L, k_gate=10, eps}, top-10, 3 launches timed as the headline",
                             "points": secondary},
     }
     if rank == 0:
@@ -641,91 +748,130 @@ def groundtruth_wide_f32(torch, X, Q, metric, depth, pre=64, chunk=200_000):
     return (np.take_along_axis(ih, order, 1).astype(np.uint32), np.take_along_axis(dh, order, 1).astype(np.float32))
 
 
-def cpu_baseline_search(idx, base, q_host, L, k, seconds, out_ids, nq, metric="l2"):
+def cpu_baseline_search(adj, start, data, q_host, L, k, seconds, out_ids, nq, metric="l2"):
+    """graphann's beam_search (oracle/_ref, all host threads) over our graph,
+    the same queries and beam: a bounded ~10 s sample beside the GPU number."""
     from oracle.oracle import Oracle, available
     kind = "reference" if available("ref") else "port"
     orc = Oracle("ref" if kind == "reference" else "orc")
-    adj, _, start = idx.export_graph()
-    data = base.view(idx.n, idx.d).cpu().numpy()
     secs, ids, reps = orc.time_search(adj, start, data, q_host, L, L, 0.0, k_out=k, metric=metric, workers=0,
                                       reps=1, min_seconds=seconds)
     gpu_ids = out_ids.cpu().numpy().view(np.uint32).reshape(nq, k)
     cores = os.cpu_count()
     return {"value": round(nq / secs, 1), "unit": "queries/s", "cores": cores, "kind": kind,
             "sample": f"all {nq} queries per pass, best of {reps} passes (>= {seconds:.0f} s), beam {{L={L},L,0}} over "
-                      f"the same {idx.n}-point graph, parallel_for over queries on {cores} threads",
+                      f"the same {len(adj)}-point graph, parallel_for over queries on {cores} threads",
             "ids_identical_to_gpu": float((ids == gpu_ids).all(axis=1).mean())}
+
+
+def host_points(cfg, n):
+    """The config's first n points on the host (numpy; bit-identical to the
+    device generator the GPU arm uses). u8 configs on a thread pool."""
+    if cfg.dtype == "f32":
+        out = np.empty((n, cfg.d), np.float32)
+        for r0 in range(0, n, 200_000):  # bounded float64 temporaries
+            r1 = min(n, r0 + 200_000)
+            out[r0:r1] = datagen.gen_f32_numpy(r1 - r0, cfg.d, cfg.clusters, cfg.sigma, cfg.norm_sigma, 0.0,
+                                               cfg.center_seed, cfg.base_seed, row0=r0)
+        return out
+    return datagen.host_base_parallel(cfg, n)
 
 
 # ---------------------------------------------------------------------------------
 def run_reference(args):
-    """The reference's own CPU search (oracle/_ref = graphann's sources,
-    beam_search through its public API, parallel_for over all host threads)
-    on this arm's workload: the same 10M-point index, the same 10k queries and
-    the same recall-selected beam L. The index and L are set up exactly as in
-    our arm (setup(): GPU build, untimed); only the search is timed. The
-    reference's build of 10M points would take ~8 min on the host, so its
-    build speed is measured on a bounded 100k-point prefix and reported
-    beside it. Under torchrun only rank 0 runs."""
+    """The reference's own CPU path, end to end, on this arm's workload: the
+    config's points regenerated on the host (no GPU, no import of our
+    package), graphann's build loop over them (build_diskann's prefix-doubling
+    batches with the config's cap: src/diskann.cpp:31-70), graphann's
+    compute_groundtruth (src/dataset.cpp:172-217), and graphann's beam_search
+    timed per step over all queries with parallel_for on every host thread
+    (measure_qps, src/eval.cpp:57-101). The beam is chosen by the same rule as
+    our arm from graphann's own recall curve. Under torchrun only rank 0 runs."""
     if int(os.environ.get("RANK", 0)) != 0:
         return
-    os.environ["WORLD_SIZE"] = "1"  # rank 0 alone: no process group
     from oracle.oracle import Oracle, available
 
     kind = "reference" if available("ref") else "port"
     orc = Oracle("ref" if kind == "reference" else "orc")
-    S = setup(args)
-    cfg, idx, nq, k, chosen = S["cfg"], S["idx"], S["nq"], S["k"], S["chosen"]
-    adj, _, start = idx.export_graph()
-    data = S["base"].view(idx.n, idx.d).cpu().numpy()
-    q = S["qdev"].view(nq, idx.d).cpu().numpy()
-    gpu_ids = S["out_ids"].cpu().numpy().view(np.uint32).reshape(nq, k)
+    cfg, nq = workload(args)
+    k = cfg.k
     cores = os.cpu_count()
-    # one graphann pass per step (warm-up passes untimed)
+    prefix = args.ref_build == "prefix"
+    n = min(args.ref_n, cfg.n) if prefix else cfg.n
+    t0 = time.perf_counter()
+    data = host_points(cfg, n)
+    queries = datagen.host_queries(cfg, nq)
+    gen_s = time.perf_counter() - t0
+    # ---- graphann's build (timed) ---------------------------------------------------------
+    cap = (int(n * cfg.batch_cap_frac) if cfg.batch_cap_frac else 0) if prefix else cfg.max_batch
+    t0 = time.perf_counter()
+    adj, start = orc.build(data, cfg.R, cfg.L, cfg.alpha, metric=cfg.metric, cap=cap, workers=0)
+    build_s = time.perf_counter() - t0
+    graph_sha = sha16(adj)
+    # ---- graphann's ground truth ------------------------------------------------------------
+    t0 = time.perf_counter()
+    gt_ids, gt_d = orc.groundtruth(data, queries, GT_DEPTH, metric=cfg.metric, workers=0)
+    gt_s = time.perf_counter() - t0
+
+    def one_pass(L, q=queries):
+        sec, ids, _ = orc.time_search(adj, start, data, q, L, L, 0.0, k_out=k, metric=cfg.metric, workers=0, reps=1)
+        return sec, ids
+
+    def recall_of(ids, rows=None):
+        ti, td = (gt_ids, gt_d) if rows is None else (gt_ids[:rows], gt_d[:rows])
+        return float(evalutil.recall_at_k(ti, td, ids if rows is None else ids[:rows], k).mean())
+
+    # ---- QPS / recall at every beam of the sweep (one pass each) ------------------------------
+    curve = []
+    for L in sweep_beams(args):
+        sec, ids = one_pass(L)
+        curve.append({"L": L, "recall@10": round(recall_of(ids), 5), "qps": round(nq / sec, 1),
+                      "ms_per_pass": round(1e3 * sec, 2)})
+    chosen = choose_beam(args, curve)
+    recall = next(c["recall@10"] for c in curve if c["L"] == chosen)
+    # ---- timed steps at the headline beam --------------------------------------------------------
     for _ in range(args.warmup):
-        orc.time_search(adj, start, data, q, chosen, chosen, 0.0, k_out=k, metric=cfg.metric, workers=0, reps=1)
+        one_pass(chosen)
     secs, ids = [], None
     for _ in range(args.steps):
-        sec, ids, _ = orc.time_search(adj, start, data, q, chosen, chosen, 0.0, k_out=k, metric=cfg.metric, workers=0,
-                                      reps=1)
+        sec, ids = one_pass(chosen)
         secs.append(sec)
     value = nq * args.steps / sum(secs)
-    at_target = None
-    if S["L_target"]:  # our arm's recall-target beam past the sweep: one timed pass
-        LT = S["L_target"]
-        sec_t, ids_t, _ = orc.time_search(adj, start, data, q, LT, LT, 0.0, k_out=k, metric=cfg.metric, workers=0,
-                                          reps=1)
-        at_target = {"L": LT, "recall@10": S["ext_curve"][-1]["recall@10"], "qps": round(nq / sec_t, 1),
-                     "timing": "one pass over all queries"}
-    # the reference's build speed on a bounded prefix (host cores)
-    nb = min(args.ref_n, cfg.n)
-    pref = data[:nb]
-    cap = int(nb * cfg.batch_cap_frac) if cfg.batch_cap_frac else 0
-    t0 = time.perf_counter()
-    orc.build(pref, cfg.R, cfg.L, cfg.alpha, metric=cfg.metric, cap=cap, workers=0)
-    build_s = time.perf_counter() - t0
-    sample = (f"graphann beam_search {{L={chosen},L,0}} top-{k}, one pass over all {nq} queries per step, over the "
-              f"same {idx.n}-point index as our arm (built by our GPU build, bit-identical to graphann's for u8), "
-              f"parallel_for on {cores} threads")
+    # ---- past the sweep (first EXT_SAMPLE queries) while the target is not reached ----------------
+    ext = []
+    if recall < args.target_recall and not args.no_extend and not args.L:
+        qs = queries[:EXT_SAMPLE]
+        for L in [x for x in L_EXTEND if x > curve[-1]["L"]]:
+            sec, ids_e = one_pass(L, qs)
+            rec = recall_of(ids_e, EXT_SAMPLE)
+            ext.append({"L": L, f"recall@10_first{EXT_SAMPLE}": round(rec, 5), "qps": round(len(qs) / sec, 1)})
+            if rec >= args.target_recall or sec > 120:
+                break
+    sample = (f"graphann beam_search {{L={chosen},L,0}} top-{k}, one pass over all {nq} queries per step, over "
+              f"graphann's own {n}-point graph of the config (built here), parallel_for on {cores} threads")
     line = {
         "impl": "reference",
-        "metric": "search QPS at recall@10>=0.95 (Alg.1 beam {L,L,0}, top-10) over a B200-built Vamana graph",
+        "metric": METRIC,
         "value": round(value, 1), "unit": "queries/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(1e3 * sum(secs) / args.steps, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": cfg.dtype,
-        "data": "synthetic: seeded Gaussian mixture with BASELINE config shapes (datagen.py)",
-        "config": {"workload": f"BASELINE configs[{CFG_INDEX.get(args.config, '?')}]: {cfg.name}", "n": idx.n,
-                   "d": idx.d, "metric": cfg.metric, "R": cfg.R,
-                   "L_build": cfg.L, "alpha": cfg.alpha, "max_batch": cfg.max_batch, "queries": nq, "k": k,
-                   "L_search": chosen, "recall@10": S["recall"]},
+        "data": "synthetic: seeded Gaussian mixture with BASELINE config shapes (datagen.py numpy restatement, "
+                "bit-identical to the device generator)",
+        "config": config_obj(args, cfg.scaled(n) if prefix else cfg, nq, chosen, recall),
+        "parity": {"graph_sha256": graph_sha, "start": int(start), "ids_sha256": sha16(ids),
+                   "basis": "sha256[:16] of graphann's n x R uint32 graph rows (0xFFFFFFFF padded) and of its "
+                            "headline search's nq x k ids"},
         "cpu_baseline": {"value": round(value, 1), "unit": "queries/s", "cores": cores, "kind": kind,
                          "sample": sample},
         "e2e": {"value": round(value, 1), "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "ids_identical_to_gpu": float((ids == gpu_ids).all(axis=1).mean()),
-        "build": {"points_per_s": round(nb / build_s, 1), "seconds": round(build_s, 3), "n": nb, "cores": cores,
-                  "sample": f"graphann build_diskann loop on the first {nb} points (batch cap {cap})"},
-        "recall_curve": S["curve"],
-        "at_target": at_target,
+        "build": {"points_per_s": round(n / build_s, 1), "seconds": round(build_s, 3), "n": n, "cores": cores,
+                  "batch_cap": cap, "graph_sha256": graph_sha,
+                  "sample": ("graphann's build loop over the config's whole point set" if not prefix else
+                             f"graphann's build loop over the first {n} points")},
+        "setup_seconds": {"generate": round(gen_s, 1), "groundtruth": round(gt_s, 1)},
+        "qps_curve": {"basis": "every beam of the sweep: recall and QPS of one pass over all queries; extension: "
+                               f"the first {EXT_SAMPLE} queries",
+                      "sweep": curve, "extension": {"beams": ext} if ext else None},
     }
     print(json.dumps(line), flush=True)
 

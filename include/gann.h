@@ -111,6 +111,10 @@ int gann_search_device(gann_index* idx, const void* d_queries, uint32_t nq, uint
                        uint32_t L, uint32_t k_gate, float eps, int visited_mode,
                        uint32_t* d_ids, float* d_dists, uint32_t* d_n_visited,
                        uint64_t* d_dist_comps, void* stream);
+/* The largest beam L this index's search kernel holds on chip (beam, candidate
+ * lists and visited table of a query live in shared memory; L above it is
+ * rejected with GANN_EINVAL). The reference has no such limit. */
+int gann_search_max_beam(const gann_index* idx, uint32_t* max_L);
 /* Stage a query batch once (padded device layout) so repeated
  * gann_search_staged calls time only the search kernel. */
 int gann_stage_queries(gann_index* idx, const void* d_queries, uint32_t nq);

@@ -240,6 +240,12 @@ class Index:
                                        C.c_void_p(nvis_ptr or None), C.c_void_p(dc_ptr or None),
                                        C.c_void_p(stream or None)))
 
+    def max_beam(self) -> int:
+        """The largest search beam L this index holds on chip (gann_search_max_beam)."""
+        v = C.c_uint32(0)
+        check(lib().gann_search_max_beam(self._h, C.byref(v)))
+        return int(v.value)
+
     def stage_queries(self, q_ptr: int, nq: int) -> None:
         check(lib().gann_stage_queries(self._h, C.c_void_p(q_ptr), nq))
 

@@ -25,6 +25,7 @@
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <map>
 #include <mutex>
 #include <set>
 #include <thread>
@@ -313,6 +314,33 @@ const uint8_t* stage_rows(gann_index* idx, DevBuf& buf, const void* src, uint32_
   return buf.as<uint8_t>();
 }
 
+// The largest beam the search kernel holds on chip: a CTA's warps keep their
+// beams (8 B a slot), candidate lists and visited tables in shared memory,
+// and a CTA may use up to the device's opt-in maximum (227 KB on a B200).
+uint32_t search_max_beam(const gann_index* idx) {
+  static std::mutex mu;
+  static std::map<int, int> optin;
+  int mx = 0;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = optin.find(idx->device);
+    if (it == optin.end()) {
+      if (cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, idx->device) != cudaSuccess) mx = 0;
+      optin[idx->device] = mx;
+    } else {
+      mx = it->second;
+    }
+  }
+  uint32_t lo = 0;
+  for (uint32_t L = 32; L <= (1u << 20); L += 32) {
+    uint32_t lg = 0, bits = 0, ways = 0;
+    hash_config(L, idx->n, &lg, &bits, &ways);
+    if (search_smem_per_block(L, idx->R, lg, bits != 0) > static_cast<size_t>(mx)) break;
+    lo = L;
+  }
+  return lo;
+}
+
 void validate_search(const gann_index* idx, uint32_t k_out, uint32_t L, uint32_t k_gate,
                      float eps, int mode) {
   // validate_search_args — src/search.cpp:32-48
@@ -324,6 +352,12 @@ void validate_search(const gann_index* idx, uint32_t k_out, uint32_t L, uint32_t
   if (mode != GANN_VISITED_FAST && mode != GANN_VISITED_REF && mode != GANN_VISITED_EXACT)
     fail(GANN_EINVAL, "unknown visited mode");
   if (idx->n > 0 && idx->start >= idx->n) fail(GANN_EINVAL, "start vertex out of range");
+  if (L > 32) {
+    const uint32_t mx = search_max_beam(idx);
+    if (L > mx)
+      fail(GANN_EINVAL, "beam " + std::to_string(L) + " exceeds the on-chip beam limit " + std::to_string(mx) +
+                            " of this index (gann_search_max_beam)");
+  }
 }
 
 SearchArgs base_search_args(gann_index* idx, uint32_t L, uint32_t k_gate, uint32_t k_out, float eps,
@@ -521,7 +555,12 @@ void insert_batch(gann_index* idx, const uint32_t* d_ids, uint32_t B, uint32_t L
   idx->vis_d.ensure(size_t(B) * vcap * 4);
   idx->nvis.ensure(size_t(B) * 4);
   cu(cudaMemsetAsync(idx->flags, 0, 8, idx->stream), "memset flags");
-  SearchArgs a = base_search_args(idx, L, L, 0, 0.0f, GANN_VISITED_FAST);
+  // GANN_BUILD_VISITED=exact: the build's searches count distinct evaluations
+  // (a diagnostic for the build roofline's algorithmic bytes; the graph is
+  // the same in every visited mode)
+  const char* bv = std::getenv("GANN_BUILD_VISITED");
+  const int bmode = bv && std::string(bv) == "exact" ? GANN_VISITED_EXACT : GANN_VISITED_FAST;
+  SearchArgs a = base_search_args(idx, L, L, 0, 0.0f, bmode);
   a.query_rows = d_ids;
   a.nq = B;
   a.n_visited = idx->nvis.as<uint32_t>();
@@ -849,6 +888,9 @@ int gann_build(gann_index* idx, uint32_t L, float alpha, int rule, uint64_t seed
     // src/diskann.cpp:33-42
     if (idx->n == 0) fail(GANN_EINVAL, "cannot build over an empty dataset");
     if (L == 0 || idx->R == 0) fail(GANN_EINVAL, "build beam and degree bound must be positive");
+    if (L > 32 && L > search_max_beam(idx))
+      fail(GANN_EINVAL, "build beam " + std::to_string(L) + " exceeds the on-chip beam limit " +
+                            std::to_string(search_max_beam(idx)));
     check_prune_params(alpha, rule);
     if (L < idx->R)
       std::fprintf(stderr, "warning: build beam %u below degree bound %u; lists will be thin\n", L,
@@ -1127,6 +1169,14 @@ int gann_search_device(gann_index* idx, const void* d_queries, uint32_t nq, uint
     a.n_visited = d_n_visited;
     a.dist_comps = d_dist_comps;
     run_search(idx, a, s);
+  });
+}
+
+int gann_search_max_beam(const gann_index* idx, uint32_t* max_L) {
+  return guarded([&] {
+    if (!idx || !max_L) fail(GANN_EINVAL, "NULL argument");
+    set_device(idx);
+    *max_L = search_max_beam(idx);
   });
 }
 
