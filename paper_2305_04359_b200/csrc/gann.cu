@@ -180,6 +180,7 @@ struct gann_index {
   float balpha = 0.0f;
   DevBuf pair_out, pair_cnt, lids;
   PruneHandoff hand;  // the tensor-core prune's hand-off region (this index only)
+  std::atomic<uint32_t> max_beam{0};  // search_max_beam, computed once
 };
 
 namespace {
@@ -314,10 +315,12 @@ const uint8_t* stage_rows(gann_index* idx, DevBuf& buf, const void* src, uint32_
   return buf.as<uint8_t>();
 }
 
-// The largest beam the search kernel holds on chip: a CTA's warps keep their
-// beams (8 B a slot), candidate lists and visited tables in shared memory,
-// and a CTA may use up to the device's opt-in maximum (227 KB on a B200).
+// The largest beam the search kernel holds on chip: a warp keeps its query's
+// beam (9 B a slot), candidate lists and visited table in shared memory, and
+// a CTA (down to one warp for large beams) may use up to the device's opt-in
+// maximum (227 KB on a B200): L up to ~24k.
 uint32_t search_max_beam(const gann_index* idx) {
+  if (const uint32_t c = idx->max_beam.load()) return c;
   static std::mutex mu;
   static std::map<int, int> optin;
   int mx = 0;
@@ -335,9 +338,10 @@ uint32_t search_max_beam(const gann_index* idx) {
   for (uint32_t L = 32; L <= (1u << 20); L += 32) {
     uint32_t lg = 0, bits = 0, ways = 0;
     hash_config(L, idx->n, &lg, &bits, &ways);
-    if (search_smem_per_block(L, idx->R, lg, bits != 0) > static_cast<size_t>(mx)) break;
+    if (search_smem_min_block(L, idx->R, lg, bits != 0) > static_cast<size_t>(mx)) break;
     lo = L;
   }
+  const_cast<gann_index*>(idx)->max_beam.store(lo);
   return lo;
 }
 

@@ -75,7 +75,7 @@ struct SearchArgs {
 };
 size_t search_smem_per_warp(uint32_t L, uint32_t R, uint32_t hash_log2, bool hash16);
 constexpr int kSearchWarpsPerBlock = 4;  // one query per warp
-size_t search_smem_per_block(uint32_t L, uint32_t R, uint32_t hash_log2, bool hash16);
+size_t search_smem_min_block(uint32_t L, uint32_t R, uint32_t hash_log2, bool hash16);
 
 // Kernel preloading. CUDA loads a kernel's code at its first launch (lazy
 // module loading), which put 15-200 ms of one-time stalls into the first

@@ -41,9 +41,10 @@ size_t search_smem_per_warp(uint32_t L, uint32_t R, uint32_t hash_log2, bool has
   return (b + 15) & ~size_t(15);
 }
 
-// Shared memory of one search CTA (its warps' regions side by side).
-size_t search_smem_per_block(uint32_t L, uint32_t R, uint32_t hash_log2, bool hash16) {
-  return search_smem_per_warp(L, R, hash_log2, hash16) * kSearchWarpsPerBlock;
+// Shared memory of the narrowest search CTA: one warp (one query). Wider
+// CTAs (up to kSearchWarpsPerBlock) are used while their regions fit.
+size_t search_smem_min_block(uint32_t L, uint32_t R, uint32_t hash_log2, bool hash16) {
+  return search_smem_per_warp(L, R, hash_log2, hash16);
 }
 
 cudaError_t launch_search_u8(const SearchArgs& a, int metric, const Geometry& g, cudaStream_t s);

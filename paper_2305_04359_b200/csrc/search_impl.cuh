@@ -601,7 +601,15 @@ namespace {
 template <int E, int M, int LPR, int CPL>
 cudaError_t launch_one(const SearchArgs& a, cudaStream_t s) {
   const uint32_t per_warp = static_cast<uint32_t>(search_smem_per_warp(a.L, a.R, a.hash_log2, a.hash_bits != 0));
-  const size_t smem = size_t(per_warp) * kWarpsPerBlock;
+  int dev = 0, optin = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if ((e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess) return e;
+  // large beams: fewer warps (queries) per CTA so one CTA's regions fit the
+  // opt-in shared memory (the kernel works per warp at any CTA width)
+  int wpb = kWarpsPerBlock;
+  while (wpb > 1 && size_t(per_warp) * wpb > static_cast<size_t>(optin)) wpb >>= 1;
+  const size_t smem = size_t(per_warp) * wpb;
   // read per launch (A/B runs flip it between launches)
   const char* dv = std::getenv("GANN_SEARCH_DIAG");
   const bool diag = dv && *dv && *dv != '0';
@@ -617,19 +625,17 @@ cudaError_t launch_one(const SearchArgs& a, cudaStream_t s) {
                 : (r64 ? (fit ? search_kernel<E, M, LPR, CPL, true, true, true> : search_kernel<E, M, LPR, CPL, true, true>)
                        : (fit ? search_kernel<E, M, LPR, CPL, true, false, true>
                               : search_kernel<E, M, LPR, CPL, true, false>));
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
-  if (e != cudaSuccess) return e;
-  if (a.nq == 0) return cudaSuccess;
-  int per_sm = 0, sms = 0, dev = 0;
-  if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
-  if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
-  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kWarpsPerBlock * 32, smem)) != cudaSuccess)
+  if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem))) !=
+      cudaSuccess)
     return e;
-  const uint32_t want = (a.nq + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  if (a.nq == 0) return cudaSuccess;
+  int per_sm = 0, sms = 0;
+  if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, wpb * 32, smem)) != cudaSuccess) return e;
+  const uint32_t want = (a.nq + wpb - 1) / wpb;
   const uint32_t blocks = std::min<uint32_t>(want, static_cast<uint32_t>(std::max(1, per_sm) * sms));
   if ((e = cudaMemsetAsync(a.next_query, 0, sizeof(uint32_t), s)) != cudaSuccess) return e;
-  k<<<blocks, kWarpsPerBlock * 32, smem, s>>>(a, per_warp);
+  k<<<blocks, wpb * 32, smem, s>>>(a, per_warp);
   return cudaGetLastError();
 }
 
