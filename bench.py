@@ -57,12 +57,12 @@ L_CANDIDATES = [10, 12, 14, 16, 20, 24, 28, 32, 40, 48, 56, 64, 80, 96, 128, 160
 # beams tried past the sweep while the recall target is not reached (both arms;
 # ours stops at the kernel's on-chip beam limit, gann_search_max_beam)
 L_EXTEND = [256, 320, 400, 512, 640, 800, 1024, 1280, 1600, 2048, 2560, 3200, 4096, 5120, 6400, 8192]
-EXT_SAMPLE = 1000  # the reference arm times the extension on the first 1000 queries
 GT_DEPTH = 16
 CFG_INDEX = {"c0": 0, "c1": 1, "c2": 2, "c3": 3, "c4": 4}  # BASELINE.json configs[i]
 B200_L2_BYTES = 126 * 2**20
-METRIC = ("search QPS (Alg.1 beam {L,L,0}, top-10) at the smallest beam of the BASELINE sweep 10..200 reaching "
-          "recall@10 0.95, else at L=200 (config carries L and its recall; qps_curve every beam)")
+METRIC = ("search QPS at recall@10 0.95 (Alg.1 beam {L,L,0}, top-10): the smallest beam reaching it, searched "
+          "over the BASELINE sweep 10..200, continued past 200 and bisected to a multiple of 32 (config carries L and "
+          "its recall; qps_curve every beam tried)")
 
 
 def load_module(name, rel):
@@ -121,15 +121,45 @@ def sweep_beams(args):
     return [args.L] if args.L else [x for x in L_CANDIDATES if x <= args.L_max]
 
 
-def choose_beam(args, curve):
-    """The smallest swept beam reaching the target, else the sweep's largest
-    (identical rule in both arms, applied to each arm's own recall)."""
+def choose_beam(args, curve, eval_L, max_beam=1 << 30):
+    """The headline beam, by one rule in both arms (each on its own recall):
+    the smallest beam of the sweep reaching the target; else the L_EXTEND
+    beams past the sweep until one reaches it, then bisection between the
+    last miss and that hit on multiples of 32. eval_L(L) -> (recall, extra)
+    runs one beam. Returns (L, reached, extension points). If no beam up to
+    max_beam reaches the target, the beam with the highest recall tried."""
     if args.L:
-        return args.L
+        return args.L, None, []
     for c in curve:
         if c["recall@10"] >= args.target_recall:
-            return c["L"]
-    return curve[-1]["L"]
+            return c["L"], True, []
+    ext = []
+    if args.no_extend:
+        return curve[-1]["L"], False, ext
+
+    def run(L):
+        rec, extra = eval_L(L)
+        ext.append(dict({"L": L, "recall@10": round(rec, 5)}, **extra))
+        return rec
+
+    lo, hi = curve[-1]["L"], None
+    for L in [x for x in L_EXTEND if x > lo]:
+        if L > max_beam:
+            break
+        if run(L) >= args.target_recall:
+            hi = L
+            break
+        lo = L
+    if hi is None:
+        best = max([(c["recall@10"], c["L"]) for c in curve] + [(e["recall@10"], e["L"]) for e in ext])
+        return best[1], False, ext
+    while hi - lo > 32:
+        mid = max(lo + 32, (lo + hi) // 64 * 32)
+        if run(mid) >= args.target_recall:
+            hi = mid
+        else:
+            lo = mid
+    return hi, True, sorted(ext, key=lambda e: e["L"])
 
 
 def config_obj(args, cfg, nq, L, recall):
@@ -140,7 +170,7 @@ def config_obj(args, cfg, nq, L, recall):
         "n": cfg.n, "d": cfg.d, "dtype": cfg.dtype, "metric": cfg.metric, "R": cfg.R, "L_build": cfg.L,
         "alpha": cfg.alpha, "max_batch": cfg.max_batch, "queries_per_gpu": nq, "k": cfg.k,
         "L_search": L, "recall@10": round(recall, 5), "target_recall": args.target_recall,
-        "target_reached_in_sweep": recall >= args.target_recall,
+        "target_reached": recall >= args.target_recall,
         "graph": "built from the config's points by each arm (ours: gann_build on the GPU; reference: graphann's "
                  "build loop on the host); parity.graph_sha256 compares them",
         "l2": ("flushed between steps" if index_bytes < 2 * B200_L2_BYTES
@@ -426,26 +456,18 @@ def setup(args):
         ms, _ = timed(sp, 4)
         curve.append({"L": L, "recall@10": round(recall_of(res), 5), "qps": round(world * nq / (ms / 1e3), 1),
                       "ms_per_launch": round(ms, 4)})
-    chosen = choose_beam(args, curve)
-    recall = next(c["recall@10"] for c in curve if c["L"] == chosen)
-    target_reached = recall >= args.target_recall
+    max_beam = idx.max_beam()
+
+    def eval_L(L):
+        search_L(L)
+        torch.cuda.synchronize()
+        res = out_ids.cpu().numpy().view(np.uint32).reshape(nq, k)
+        ms, _ = timed(g.SearchParams(L, L, 0.0), 2)
+        return recall_of(res), {"qps": round(world * nq / (ms / 1e3), 1), "ms_per_launch": round(ms, 4)}
+
+    chosen, target_reached, ext_curve = choose_beam(args, curve, eval_L, max_beam)
+    recall = next(c["recall@10"] for c in curve + ext_curve if c["L"] == chosen)
     sp = g.SearchParams(chosen, chosen, 0.0)
-    # past the sweep while the target is not reached, up to the on-chip beam limit
-    ext_curve, L_target, max_beam = [], None, idx.max_beam()
-    if not target_reached and not args.no_extend and not args.L:
-        for L in [x for x in L_EXTEND if x > curve[-1]["L"]]:
-            if L > max_beam:
-                break
-            search_L(L)
-            torch.cuda.synchronize()
-            res = out_ids.cpu().numpy().view(np.uint32).reshape(nq, k)
-            ms, _ = timed(g.SearchParams(L, L, 0.0), 2)
-            rec = recall_of(res)
-            ext_curve.append({"L": L, "recall@10": round(rec, 5), "qps": round(world * nq / (ms / 1e3), 1),
-                              f"recall@10_first{EXT_SAMPLE}": round(recall_of(res, EXT_SAMPLE), 5)})
-            if rec >= args.target_recall:
-                L_target = L
-                break
     search_L(chosen)
     torch.cuda.synchronize()
     ids_sha = sha16(out_ids.cpu().numpy().view(np.uint32).reshape(nq, k))
@@ -456,7 +478,7 @@ def setup(args):
                 build_mode=build_mode, adj_h=adj_h, start_h=start_h, graph_sha=graph_sha, ids_sha=ids_sha,
                 out_ids=out_ids, out_d=out_d, stream=stream, search_L=search_L, curve=curve, chosen=chosen,
                 recall=recall, target_reached=target_reached, sp=sp, gt_ids_h=gt_ids_h, gt_d_h=gt_d_h,
-                ext_curve=ext_curve, L_target=L_target, max_beam=max_beam, timed=timed, flush=flush,
+                ext_curve=ext_curve, max_beam=max_beam, timed=timed, flush=flush,
                 flush_buf=flush_buf, nstreams=nstreams, streams=streams, souts=souts, ext=ext,
                 index_bytes=index_bytes, params=params)
 
@@ -686,14 +708,11 @@ def run_ours(args):
             "roofline": build_roof,
             "stats": {kk: v for kk, v in bstats.items() if kk != "build_ms"},
         },
-        "qps_curve": {"basis": "every beam of the sweep: recall over all queries, QPS of 4 launches timed as the "
-                               "headline (extension: 2 launches)",
-                      "sweep": curve,
-                      "extension": {"beams": S["ext_curve"], "reached_target_at": S["L_target"],
-                                    "stopped": ("target reached" if S["L_target"] else
-                                                f"on-chip beam limit {S['max_beam']} of this index" if S["ext_curve"]
-                                                and S["ext_curve"][-1]["L"] < L_EXTEND[-1] else "end of the list")
-                                    } if S["ext_curve"] else None},
+        "qps_curve": {"basis": "recall over all queries; QPS of 4 launches (sweep) / 2 launches (past the sweep) "
+                               "timed as the headline",
+                      "sweep": curve, "past_sweep": S["ext_curve"],
+                      "target_reached": S["target_reached"],
+                      "on_chip_beam_limit": S["max_beam"]},
         "secondary_sweep": {"semantics": "reference eval {L, k_gate=10, eps}, top-10, 3 launches timed as the headline",
                             "points": secondary},
     }
@@ -821,14 +840,19 @@ def run_reference(args):
         ti, td = (gt_ids, gt_d) if rows is None else (gt_ids[:rows], gt_d[:rows])
         return float(evalutil.recall_at_k(ti, td, ids if rows is None else ids[:rows], k).mean())
 
-    # ---- QPS / recall at every beam of the sweep (one pass each) ------------------------------
+    # ---- QPS / recall at every beam of the sweep (one pass each), the headline beam -----------
     curve = []
     for L in sweep_beams(args):
         sec, ids = one_pass(L)
         curve.append({"L": L, "recall@10": round(recall_of(ids), 5), "qps": round(nq / sec, 1),
                       "ms_per_pass": round(1e3 * sec, 2)})
-    chosen = choose_beam(args, curve)
-    recall = next(c["recall@10"] for c in curve if c["L"] == chosen)
+
+    def eval_L(L):
+        sec, ids_l = one_pass(L)
+        return recall_of(ids_l), {"qps": round(nq / sec, 1), "ms_per_pass": round(1e3 * sec, 2)}
+
+    chosen, reached, ext = choose_beam(args, curve, eval_L)
+    recall = next(c["recall@10"] for c in curve + ext if c["L"] == chosen)
     # ---- timed steps at the headline beam --------------------------------------------------------
     for _ in range(args.warmup):
         one_pass(chosen)
@@ -837,16 +861,6 @@ def run_reference(args):
         sec, ids = one_pass(chosen)
         secs.append(sec)
     value = nq * args.steps / sum(secs)
-    # ---- past the sweep (first EXT_SAMPLE queries) while the target is not reached ----------------
-    ext = []
-    if recall < args.target_recall and not args.no_extend and not args.L:
-        qs = queries[:EXT_SAMPLE]
-        for L in [x for x in L_EXTEND if x > curve[-1]["L"]]:
-            sec, ids_e = one_pass(L, qs)
-            rec = recall_of(ids_e, EXT_SAMPLE)
-            ext.append({"L": L, f"recall@10_first{EXT_SAMPLE}": round(rec, 5), "qps": round(len(qs) / sec, 1)})
-            if rec >= args.target_recall or sec > 120:
-                break
     sample = (f"graphann beam_search {{L={chosen},L,0}} top-{k}, one pass over all {nq} queries per step, over "
               f"graphann's own {n}-point graph of the config (built here), parallel_for on {cores} threads")
     line = {
@@ -869,9 +883,8 @@ def run_reference(args):
                   "sample": ("graphann's build loop over the config's whole point set" if not prefix else
                              f"graphann's build loop over the first {n} points")},
         "setup_seconds": {"generate": round(gen_s, 1), "groundtruth": round(gt_s, 1)},
-        "qps_curve": {"basis": "every beam of the sweep: recall and QPS of one pass over all queries; extension: "
-                               f"the first {EXT_SAMPLE} queries",
-                      "sweep": curve, "extension": {"beams": ext} if ext else None},
+        "qps_curve": {"basis": "recall and QPS of one pass over all queries per beam",
+                      "sweep": curve, "past_sweep": ext, "target_reached": reached},
     }
     print(json.dumps(line), flush=True)
 

@@ -178,7 +178,7 @@ struct gann_index {
   std::vector<std::pair<uint32_t, uint32_t>> ranges;
   uint32_t bL = 0, brule = 0;
   float balpha = 0.0f;
-  DevBuf pair_out, pair_cnt, lids;
+  DevBuf pair_out, pair_cnt, lids, pair_in;
   PruneHandoff hand;  // the tensor-core prune's hand-off region (this index only)
   std::atomic<uint32_t> max_beam{0};  // search_max_beam, computed once
 };
@@ -856,7 +856,7 @@ void gann_index_free(gann_index* idx) {
   for (void* p : idx->ipc_open)
     if (p) cudaIpcCloseMemHandle(p);
   if (idx->d_parts) cudaFree(idx->d_parts);
-  for (DevBuf* b : {&idx->pair_out, &idx->pair_cnt, &idx->lids}) b->release();
+  for (DevBuf* b : {&idx->pair_out, &idx->pair_cnt, &idx->lids, &idx->pair_in}) b->release();
   for (void* p : {static_cast<void*>(idx->points), static_cast<void*>(idx->adj),
                   static_cast<void*>(idx->tcount), static_cast<void*>(idx->tgroup),
                   static_cast<void*>(idx->stats), static_cast<void*>(idx->counters),
@@ -1814,9 +1814,11 @@ int gann_part_build_begin(gann_index* idx, uint32_t L, float alpha, int rule, ui
   });
 }
 
-int gann_part_phase1(gann_index* idx, uint32_t batch, uint64_t* counts, const uint32_t** d_pairs) {
-  return guarded([&] {
-    if (!idx || !counts || !d_pairs) fail(GANN_EINVAL, "NULL argument");
+namespace {
+// Phase 1 of a partitioned batch: insert the batch points this partition owns,
+// then emit their reverse pairs grouped by the target's owner (counts[g]
+// pairs for partition g, at *d_pairs in partition order).
+void part_phase1(gann_index* idx, uint32_t batch, uint64_t* counts, const uint32_t** d_pairs) {
     if (batch >= idx->ranges.size()) fail(GANN_EINVAL, "batch index out of range");
     set_device(idx);
     const auto [lo, hi] = idx->ranges[batch];
@@ -1861,12 +1863,10 @@ int gann_part_phase1(gann_index* idx, uint32_t batch, uint64_t* counts, const ui
        "pairs");
     sync(idx);
     *d_pairs = idx->pair_out.as<uint32_t>();
-  });
 }
 
-int gann_part_phase2(gann_index* idx, uint32_t batch, const uint32_t* d_pairs, uint64_t m) {
-  return guarded([&] {
-    if (!idx) fail(GANN_EINVAL, "index is NULL");
+// Phase 2: merge the m received pairs (interleaved target, batch ordinal).
+void part_phase2(gann_index* idx, uint32_t batch, const uint32_t* d_pairs, uint64_t m) {
     if (batch >= idx->ranges.size()) fail(GANN_EINVAL, "batch index out of range");
     set_device(idx);
     const auto [lo, hi] = idx->ranges[batch];
@@ -1875,6 +1875,57 @@ int gann_part_phase2(gann_index* idx, uint32_t batch, const uint32_t* d_pairs, u
     apply_back(idx, idx->order.as<uint32_t>() + lo, hi - lo, d_pairs, nullptr, m, idx->balpha,
                static_cast<int>(idx->brule), true, nullptr, nullptr, nullptr, nullptr, d_pairs + 1, 2);
     sync(idx);
+}
+
+void xcheck(int rc, const char* what) {
+  if (rc != 0) fail(GANN_ECUDA, std::string("exchange ") + what + " failed (rc " + std::to_string(rc) + ")");
+}
+}  // namespace
+
+int gann_part_phase1(gann_index* idx, uint32_t batch, uint64_t* counts, const uint32_t** d_pairs) {
+  return guarded([&] {
+    if (!idx || !counts || !d_pairs) fail(GANN_EINVAL, "NULL argument");
+    part_phase1(idx, batch, counts, d_pairs);
+  });
+}
+
+int gann_part_phase2(gann_index* idx, uint32_t batch, const uint32_t* d_pairs, uint64_t m) {
+  return guarded([&] {
+    if (!idx) fail(GANN_EINVAL, "index is NULL");
+    part_phase2(idx, batch, d_pairs, m);
+  });
+}
+
+// The whole partitioned build in C++: build_diskann's batch loop
+// (src/diskann.cpp:53-67) with one exchange step per batch. The collectives
+// are the caller's (gann_exchange): NCCL through gann_exchange_nccl, or any
+// transport with the same semantics (the tests use torch.distributed/gloo).
+int gann_part_build(gann_index* idx, const gann_exchange* x, uint32_t L, float alpha, int rule, uint64_t seed,
+                    uint32_t max_batch, uint64_t* pairs_sent) {
+  const int rc0 = gann_part_build_begin(idx, L, alpha, rule, seed, max_batch, nullptr);
+  if (rc0 != GANN_OK) return rc0;
+  return guarded([&] {
+    if (!x || !x->alltoall_counts || !x->alltoallv || !x->barrier) fail(GANN_EINVAL, "incomplete exchange");
+    if (x->rank != idx->part_rank || x->nranks != idx->part_count)
+      fail(GANN_EINVAL, "exchange rank/size differ from the index's partition");
+    const uint32_t G = idx->part_count;
+    std::vector<uint64_t> sc(G), rc(G);
+    uint64_t sent = 0;
+    for (uint32_t b = 0; b < idx->ranges.size(); b++) {
+      const uint32_t* d_send = nullptr;
+      part_phase1(idx, b, sc.data(), &d_send);
+      xcheck(x->alltoall_counts(x->ctx, sc.data(), rc.data()), "counts");
+      uint64_t m = 0;
+      for (uint32_t g = 0; g < G; g++) m += rc[g], sent += sc[g];
+      idx->pair_in.ensure(std::max<uint64_t>(m, 1) * 8);
+      xcheck(x->alltoallv(x->ctx, d_send, sc.data(), idx->pair_in.p, rc.data(), idx->stream), "pairs");
+      cu(cudaStreamSynchronize(idx->stream), "exchange sync");
+      part_phase2(idx, b, idx->pair_in.as<uint32_t>(), m);
+      // every partition's rows are final before the next batch's searches read them
+      xcheck(x->barrier(x->ctx, idx->stream), "barrier");
+    }
+    idx->pair_in.release();
+    if (pairs_sent) *pairs_sent = sent;
   });
 }
 

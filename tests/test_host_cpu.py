@@ -156,3 +156,20 @@ def test_cpp_dropin_header_builds_and_links():
     assert exe.exists()
     out = subprocess.run(["nm", "-D", "--undefined-only", str(exe)], capture_output=True, text=True).stdout
     assert "gann_build" in out and "gann_search" in out
+
+
+def test_bench_beam_rule():
+    """bench.py's headline beam rule (both arms): smallest swept beam reaching
+    the target, else past the sweep and bisected to a multiple of 32."""
+    import argparse
+    import bench
+    args = argparse.Namespace(L=0, target_recall=0.95, no_extend=False)
+    rec = lambda L: min(1.0, 0.8 + L / 5000.0)  # reaches 0.95 at L = 750
+    curve = [{"L": L, "recall@10": rec(L)} for L in (10, 100, 200)]
+    L, reached, ext = bench.choose_beam(args, curve, lambda L: (rec(L), {}))
+    assert reached and L == 768 and rec(L) >= 0.95 and rec(L - 32) < 0.95
+    assert [e["L"] for e in ext] == sorted(e["L"] for e in ext)
+    L, reached, ext = bench.choose_beam(args, curve, lambda L: (rec(L), {}), max_beam=512)
+    assert not reached and L == 512
+    curve[1]["recall@10"] = 0.96
+    assert bench.choose_beam(args, curve, None)[:2] == (100, True)
