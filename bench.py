@@ -105,6 +105,9 @@ def parse():
                          "step's start (1 = serial launches; forced to 1 when steps flush L2)")
     ap.add_argument("--no-build-roofline", action="store_true",
                     help="skip the untimed exact-count rebuild behind build.roofline")
+    ap.add_argument("--search-on", default="auto", choices=["auto", "replica", "partitions"],
+                    help="N>1 after the partitioned build: gather a full graph replica per rank (when it fits) "
+                         "or search the partitions in place (peer rows over NVLink)")
     ap.add_argument("--replicated-build", action="store_true",
                     help="N>1: every rank builds the whole graph (default: one vertex-partitioned build)")
     return ap.parse_args()
@@ -327,43 +330,74 @@ def setup(args):
         return distutil.reduce_scalar(x, op, dist if world > 1 else None, "cuda")
 
     # ---- data: generated straight into HBM ------------------------------------------
+    # (N>1, partitioned build of rows that need no padding: straight into the
+    # partition index's own buffer — a 1B-point set fits once, not twice)
     tdt = {"u8": torch.uint8, "i8": torch.int8, "f32": torch.float32}[cfg.dtype]
-    base = torch.empty(n * d, dtype=tdt, device="cuda")
-    check(datagen.generate_device(lib(), cfg, base.data_ptr(), n, queries=False, device=dev))
+    in_place = world > 1 and not args.replicated_build and (d * cfg.elem_bytes) % 16 == 0
+    base = None if in_place else torch.empty(n * d, dtype=tdt, device="cuda")
+    if base is not None:
+        check(datagen.generate_device(lib(), cfg, base.data_ptr(), n, queries=False, device=dev))
     qdev = torch.empty(nq * d, dtype=tdt, device="cuda")
     row0, _ = distutil.query_rows(rank, nq)  # each rank searches its own query shard
     check(datagen.generate_device(lib(), cfg, qdev.data_ptr(), nq, queries=True, row0=row0, device=dev))
-    idx = g.Index.from_device(base.data_ptr(), n, d, cfg.np_dtype, cfg.metric, cfg.R, dev)
-
     # ---- build (timed once) ---------------------------------------------------------------
     params = g.DiskannParams(cfg.R, cfg.L, cfg.alpha, seed=42, max_batch=cfg.max_batch)
-    idx.reset_stats()
-    build_mode = "single-gpu"
+    build_mode, search_on, build_extra, pidx, idx = "single-gpu", "replica", {}, None, None
     if world > 1 and not args.replicated_build:
-        # one vertex-partitioned build over the N GPUs (peer rows over NVLink,
-        # NCCL all-to-all-v of the reverse pairs), then every rank gathers the
-        # full graph for its replica
-        from paper_2305_04359_b200.partition import PartitionedIndex
-        pidx = PartitionedIndex(base.data_ptr(), cfg.metric, cfg.R, dist, device=dev, shape=(n, d), dtype=cfg.np_dtype)
+        # one vertex-partitioned build over the N GPUs: the C++ batch loop
+        # (gann_part_build) with the library's NCCL transport; peer rows over
+        # NVLink (CUDA IPC). The batch cap is the config's, shrunk to what the
+        # free device memory holds (0.2-0.5% of n at 1B).
+        from paper_2305_04359_b200.partition import NcclExchange, PartitionedIndex
+        pidx = PartitionedIndex(base.data_ptr() if base is not None else 0, cfg.metric, cfg.R, dist, device=dev,
+                                shape=(n, d), dtype=cfg.np_dtype)
+        if base is None:
+            pts_ptr, _ = pidx.device_points()
+            check(datagen.generate_device(lib(), cfg, pts_ptr, n, queries=False, device=dev))
+            base = _tensor_from_ptr(pts_ptr, n * d * cfg.elem_bytes).view(tdt)  # a view of the index's points
         if pidx.peers_ok:
+            free_b, _ = torch.cuda.mem_get_info(dev)
+            # the full replica (points are already resident: graph rows only)
+            # is gathered for the search when it fits; else the search reads
+            # the partitions in place
+            replica_b = n * cfg.R * 4 + n * d * cfg.elem_bytes
+            search_on = args.search_on if args.search_on != "auto" else (
+                "replica" if replica_b < 0.4 * free_b else "partitions")
+            mem_cap = pidx.batch_cap(cfg.L, int(0.8 * free_b))
+            cap = int(allreduce(min(cfg.max_batch or n, mem_cap), "min"))
+            params = g.DiskannParams(cfg.R, cfg.L, cfg.alpha, seed=42, max_batch=cap)
+            xch = NcclExchange(dist, dev)
             barrier()
             t0 = time.perf_counter()
-            pidx.build(params, nccl=True)
+            info = pidx.build_native(params, xch)
             torch.cuda.synchronize()
             build_s = allreduce(time.perf_counter() - t0)
-            P = -(-n // world)
-            rows = torch.full((P * cfg.R,), -1, dtype=torch.int32, device="cuda")
-            rows[: pidx.rows * cfg.R] = pidx.device_rows()
-            full = torch.empty((world * P * cfg.R,), dtype=torch.int32, device="cuda")
-            dist.all_gather_into_tensor(full, rows)
-            check(lib().gann_import_graph_device(idx._h, ctypes.c_void_p(full.data_ptr()), pidx.start()))
+            xch.close()
             bstats = pidx.stats()  # this rank's share of the build
-            del full, rows
-            pidx.close()
-            build_mode = f"vertex-partitioned over {world} GPUs (NCCL all-to-all-v)"
+            build_mode = f"vertex-partitioned over {world} GPUs (gann_part_build, NCCL send/recv exchange)"
+            build_extra = {"max_batch_used": cap, "max_batch_memory_cap": mem_cap, "pairs_sent": info["pairs_sent"],
+                           "search_on": search_on}
+            if search_on == "replica":
+                P = -(-n // world)
+                rows = torch.full((P * cfg.R,), -1, dtype=torch.int32, device="cuda")
+                rows[: pidx.rows * cfg.R] = pidx.device_rows()
+                full = torch.empty((world * P * cfg.R,), dtype=torch.int32, device="cuda")
+                dist.all_gather_into_tensor(full, rows)
+                idx = g.Index.from_device(base.data_ptr(), n, d, cfg.np_dtype, cfg.metric, cfg.R, dev)
+                check(lib().gann_import_graph_device(idx._h, ctypes.c_void_p(full.data_ptr()), pidx.start()))
+                del full, rows
+                pidx.close()
+                pidx = None
+                if in_place:  # the view into the closed partition's points moves to the replica's
+                    base = _tensor_from_ptr(idx.device_ptrs()[0], n * d * cfg.elem_bytes).view(tdt)
+            else:
+                idx = pidx.as_index()  # searches read every partition in place
         else:
             pidx.close()
-    if build_mode == "single-gpu":
+            pidx = None
+    if idx is None:
+        idx = g.Index.from_device(base.data_ptr(), n, d, cfg.np_dtype, cfg.metric, cfg.R, dev)
+        idx.reset_stats()
         # optional warm-up build (GANN_BENCH_WARM_BUILD=<points>); off by default:
         # measured no faster, and the timed build's re-prune then varied more
         nw = min(n, int(os.environ.get("GANN_BENCH_WARM_BUILD", 0)))
@@ -383,9 +417,16 @@ def setup(args):
         bstats = idx.stats()
     idx.release_scratch()  # after the timed build: the search needs none of it
     adj_h, deg_h, start_h = idx.export_graph()  # host copy: the graph's checksum (and the CPU baseline)
-    graph_sha = sha16(adj_h)
-    replicas_identical = distutil.replicas_identical(int(graph_sha, 16), dist if world > 1 else None)
-    deg_mean = float(deg_h.mean())
+    if search_on == "partitions":  # each rank holds its own rows: the checksum of the rank checksums
+        shas = [None] * world
+        dist.all_gather_object(shas, sha16(adj_h))
+        graph_sha = hashlib.sha256("".join(shas).encode()).hexdigest()[:16]
+        replicas_identical = None
+        deg_mean = allreduce(float(deg_h.sum()), "sum") / n
+    else:
+        graph_sha = sha16(adj_h)
+        replicas_identical = distutil.replicas_identical(int(graph_sha, 16), dist if world > 1 else None)
+        deg_mean = float(deg_h.mean())
 
     # ---- ground truth (GPU brute force) -------------------------------------------
     if d * cfg.elem_bytes <= 256:
@@ -480,7 +521,7 @@ def setup(args):
                 recall=recall, target_reached=target_reached, sp=sp, gt_ids_h=gt_ids_h, gt_d_h=gt_d_h,
                 ext_curve=ext_curve, max_beam=max_beam, timed=timed, flush=flush,
                 flush_buf=flush_buf, nstreams=nstreams, streams=streams, souts=souts, ext=ext,
-                index_bytes=index_bytes, params=params)
+                index_bytes=index_bytes, params=params, build_extra=build_extra, search_on=search_on)
 
 
 def run_ours(args):
@@ -704,7 +745,7 @@ def run_ours(args):
             "points_per_s": round(n / build_s, 1), "seconds": round(build_s, 3), "mode": build_mode,
             "warmup": "none: one build, including its scratch allocation",
             "phases_ms": {kk: round(v, 1) for kk, v in bstats["build_ms"].items()},
-            "mean_degree": round(deg_mean, 3), "replicas_identical": replicas_identical,
+            "mean_degree": round(deg_mean, 3), "replicas_identical": replicas_identical, **S["build_extra"],
             "roofline": build_roof,
             "stats": {kk: v for kk, v in bstats.items() if kk != "build_ms"},
         },

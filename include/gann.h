@@ -252,6 +252,8 @@ int gann_generate_f32(void* d_out, uint64_t n, uint32_t d, uint32_t clusters, fl
  * partition's own rows. */
 int gann_index_create_part(const void* points, uint64_t n, uint32_t d, int elem, int metric,
                            uint32_t R, uint32_t rank, uint32_t nparts, int device, gann_index** out);
+/* d_points may be NULL: the index's points are then zero for the caller to
+ * fill in place (gann_index_device_ptrs), so 1B points need no second copy. */
 int gann_index_create_part_device(const void* d_points, uint64_t n, uint32_t d, int elem, int metric,
                                   uint32_t R, uint32_t rank, uint32_t nparts, int device,
                                   gann_index** out);
@@ -263,6 +265,46 @@ int gann_part_build_begin(gann_index* idx, uint32_t L, float alpha, int rule, ui
                           uint32_t max_batch, uint32_t* nbatches);
 int gann_part_phase1(gann_index* idx, uint32_t batch, uint64_t* counts, const uint32_t** d_pairs);
 int gann_part_phase2(gann_index* idx, uint32_t batch, const uint32_t* d_pairs, uint64_t m);
+
+/* The collectives of a partitioned build, supplied by the caller (one per
+ * rank). Every callback returns 0 on success. `stream` is the index's CUDA
+ * stream (cudaStream_t); device buffers hold interleaved u32 pairs (8 bytes a
+ * pair), counts are in pairs.
+ *   alltoall_counts: send[nranks] -> recv[nranks] (host arrays)
+ *   alltoallv:       d_send holds send_counts[g] pairs for rank g, in rank
+ *                    order; d_recv receives recv_counts[g] pairs from rank g,
+ *                    in rank order (device pointers)
+ *   barrier:         all ranks' work queued so far is complete
+ * gann_exchange_nccl fills one from an NCCL communicator; any transport with
+ * these semantics works (the tests drive it with torch.distributed/gloo). */
+typedef struct gann_exchange {
+  void* ctx;
+  uint32_t rank, nranks;
+  int (*alltoall_counts)(void* ctx, const uint64_t* send, uint64_t* recv);
+  int (*alltoallv)(void* ctx, const void* d_send, const uint64_t* send_counts, void* d_recv,
+                   const uint64_t* recv_counts, void* stream);
+  int (*barrier)(void* ctx, void* stream);
+} gann_exchange;
+
+/* The whole vertex-partitioned build of build_diskann (src/diskann.cpp:31-70):
+ * begin + per batch phase1 -> exchange -> phase2 -> barrier, driven in C++.
+ * Collective: every rank calls it with the same parameters. */
+int gann_part_build(gann_index* idx, const gann_exchange* x, uint32_t L, float alpha, int rule, uint64_t seed,
+                    uint32_t max_batch, uint64_t* pairs_sent);
+/* The largest global batch (points, all ranks together) whose build scratch
+ * fits `budget_bytes` on each rank, for build beam L; a cap for max_batch at
+ * 1B points (0.2-0.5% of n instead of 2%). */
+int gann_part_batch_cap(const gann_index* idx, uint32_t L, uint64_t budget_bytes, uint32_t* max_batch);
+
+/* NCCL (loaded at run time: the libnccl.so.2 already in the process, e.g.
+ * torch's, else the system one). A communicator of nranks ranks from a
+ * 128-byte unique id made by rank 0 (gann_nccl_unique_id) and shared by the
+ * caller; gann_exchange_nccl wraps it (ncclSend/ncclRecv groups on the
+ * index's stream). */
+int gann_nccl_unique_id(void* id128);
+int gann_nccl_comm_init(const void* id128, uint32_t rank, uint32_t nranks, int device, void** comm);
+int gann_nccl_comm_destroy(void* comm);
+int gann_exchange_nccl(void* comm, uint32_t rank, uint32_t nranks, gann_exchange* out);
 
 /* ---- counters (roofline) ----------------------------------------------------
  * Totals accumulated by the kernels since the last reset. */

@@ -95,6 +95,12 @@ SIGNATURES = {
     "gann_part_build_begin": (_i, [_vp, _u32, _f, _i, _u64, _u32, _vp]),
     "gann_part_phase1": (_i, [_vp, _u32, _vp, _pp]),
     "gann_part_phase2": (_i, [_vp, _u32, _vp, _u64]),
+    "gann_part_build": (_i, [_vp, _vp, _u32, _f, _i, _u64, _u32, _vp]),
+    "gann_part_batch_cap": (_i, [_vp, _u32, _u64, _vp]),
+    "gann_nccl_unique_id": (_i, [_vp]),
+    "gann_nccl_comm_init": (_i, [_vp, _u32, _u32, _i, _pp]),
+    "gann_nccl_comm_destroy": (_i, [_vp]),
+    "gann_exchange_nccl": (_i, [_vp, _u32, _u32, _vp]),
     "gann_get_stats": (_i, [_vp, C.POINTER(GannStats)]),
     "gann_reset_stats": (_i, [_vp]),
     "gann_release_scratch": (_i, [_vp]),

@@ -53,6 +53,13 @@ void cu(cudaError_t e, const char* what) {
   if (e != cudaSuccess) fail(GANN_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+}  // namespace
+
+// gann_last_error() text for failures reported outside gann.cu
+void gann::set_last_error(const std::string& msg) { g_err = msg; }
+
+namespace {
+
 template <class F>
 int guarded(F&& f) {
   try {
@@ -108,10 +115,18 @@ uint32_t env_u32(const char* name, uint32_t dflt) {
 // id while n fits (half the bytes of an id slot, so twice the entries); a
 // bucket of 4 (2, 1) slots then covers n <= 2^(log2 + 13) (+14, +15). Larger
 // n store whole ids, in buckets of 4 as well.
+// Past L = 256 the table grows with the beam (GANN_HASH_PER_BEAM slots per
+// beam slot, default 8): a walk of beam L evaluates ~10 L distinct ids, and a
+// table far smaller than that re-gathers each evicted row again and again
+// (measured at c1, L = 1024 with 2048 slots: 3x the distinct rows gathered).
 void hash_config(uint32_t L, uint64_t n, uint32_t* log2, uint32_t* bits, uint32_t* ways) {
   const uint32_t forced = std::min<uint32_t>(env_u32("GANN_HASH_LOG2", 0), 15);
   const bool narrow = env_u32("GANN_HASH16", 1) != 0;
-  uint32_t l = forced ? std::max<uint32_t>(forced, 5) : 11;
+  const uint64_t per_beam = env_u32("GANN_HASH_PER_BEAM", 8);
+  uint32_t grow = 0;  // doublings past the base table for large beams
+  if (L > 256)
+    while (grow < 4 && (uint64_t(2048) << grow) < per_beam * L) grow++;
+  uint32_t l = forced ? std::max<uint32_t>(forced, 5) : 11 + grow;
   // u16 remainder slots; 2-way buckets (the bucket's newest id in the low
   // half) halve the conflict evictions of a direct-mapped table of the same size
   const uint32_t w = env_u32("GANN_HASH_WAYS", 4);
@@ -128,7 +143,7 @@ void hash_config(uint32_t L, uint64_t n, uint32_t* log2, uint32_t* bits, uint32_
   // (measured at 100M, c4 generator: 1024 slots in buckets of 4 beat 512 / 2048,
   // and direct mapping, at L = 64 and 200)
   *ways = w >= 4 ? 4 : 1;
-  *log2 = forced ? std::max<uint32_t>(forced, 5) : (*ways == 4 || L <= 160 ? 10 : 9);
+  *log2 = forced ? std::max<uint32_t>(forced, 5) : (*ways == 4 || L <= 160 ? 10 : 9) + grow;
   *bits = 0;
 }
 
@@ -1734,10 +1749,12 @@ int gann_index_create_part(const void* points, uint64_t n, uint32_t d, int elem,
 int gann_index_create_part_device(const void* d_points, uint64_t n, uint32_t d, int elem, int metric, uint32_t R,
                                   uint32_t rank, uint32_t nparts, int device, gann_index** out) {
   return guarded([&] {
-    if (!out || (n && !d_points)) fail(GANN_EINVAL, "NULL argument");
+    if (!out) fail(GANN_EINVAL, "NULL argument");
     gann_index* idx = new_index(n, d, elem, metric, R, device, rank, nparts);
     try {
-      if (n)
+      // d_points NULL: the points stay zero for the caller to write in place
+      // (gann_index_device_ptrs) — at 1B points a second copy would not fit
+      if (n && d_points)
         cu(cudaMemcpy2DAsync(idx->points, idx->stride, d_points, idx->row_bytes, idx->row_bytes, n,
                              cudaMemcpyDeviceToDevice, idx->stream),
            "copy points");
@@ -1893,6 +1910,28 @@ int gann_part_phase2(gann_index* idx, uint32_t batch, const uint32_t* d_pairs, u
   return guarded([&] {
     if (!idx) fail(GANN_EINVAL, "index is NULL");
     part_phase2(idx, batch, d_pairs, m);
+  });
+}
+
+int gann_part_batch_cap(const gann_index* idx, uint32_t L, uint64_t budget_bytes, uint32_t* max_batch) {
+  return guarded([&] {
+    if (!idx || !max_batch) fail(GANN_EINVAL, "NULL argument");
+    if (L == 0) fail(GANN_EINVAL, "build beam must be positive");
+    // per point of a global batch, on one of G ranks: its 1/G share of the
+    // inserts (visited ids + dists of 3L slots, counters, bins, pair output)
+    // and of the received reverse pairs (<= R per point, 1.5x for skew across
+    // owners): the pair itself, the group-by arrays and the merged lists at
+    // ~0.25 groups per pair (measured 0.22 at 10M) of R + 1 slots each
+    const double G = idx->part_count, R = idx->R;
+    const uint32_t vcap = std::max<uint32_t>(64, 3 * L);
+    const double insert = 8.0 * vcap + 48.0 + 8.0 * R;
+    const double per_pair = 8.0 + 4.0 + 4.0 + 0.25 * 40.0 + (0.25 * R + 1.0) * 8.0;
+    const double per_point = (insert + 1.5 * R * per_pair) / G;
+    const double fixed = double(1ull << 30) + 64.0 * (1 << 20);  // prune hand-off + small buffers
+    const double room = double(budget_bytes) - fixed;
+    const double cap = room > 0 ? room / per_point : 0.0;
+    *max_batch = static_cast<uint32_t>(std::min(cap, double(idx->n)));
+    if (*max_batch == 0) fail(GANN_EINVAL, "budget leaves no room for a build batch");
   });
 }
 

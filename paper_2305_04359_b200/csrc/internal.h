@@ -4,7 +4,11 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <string>
+
 namespace gann {
+
+void set_last_error(const std::string& msg);  // gann_last_error() text (gann.cu)
 
 // Row geometry: LPR lanes per row, up to CPL 16-byte chunks per lane.
 struct Geometry {

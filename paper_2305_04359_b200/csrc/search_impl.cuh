@@ -605,11 +605,12 @@ cudaError_t launch_one(const SearchArgs& a, cudaStream_t s) {
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   if ((e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess) return e;
-  // large beams: fewer warps (queries) per CTA so one CTA's regions fit the
-  // opt-in shared memory (the kernel works per warp at any CTA width)
+  // CTA width (warps = queries per CTA; the kernel works per warp at any
+  // width): the widest whose regions fit the opt-in shared memory, narrowed
+  // further while that leaves more warps resident (large beams: 3 CTAs of 4
+  // warps at 59 KB each waste 50 KB that 1-warp CTAs use)
   int wpb = kWarpsPerBlock;
   while (wpb > 1 && size_t(per_warp) * wpb > static_cast<size_t>(optin)) wpb >>= 1;
-  const size_t smem = size_t(per_warp) * wpb;
   // read per launch (A/B runs flip it between launches)
   const char* dv = std::getenv("GANN_SEARCH_DIAG");
   const bool diag = dv && *dv && *dv != '0';
@@ -625,13 +626,26 @@ cudaError_t launch_one(const SearchArgs& a, cudaStream_t s) {
                 : (r64 ? (fit ? search_kernel<E, M, LPR, CPL, true, true, true> : search_kernel<E, M, LPR, CPL, true, true>)
                        : (fit ? search_kernel<E, M, LPR, CPL, true, false, true>
                               : search_kernel<E, M, LPR, CPL, true, false>));
-  if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem))) !=
-      cudaSuccess)
+  if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                size_t(per_warp) * wpb > 48 * 1024 ? static_cast<int>(size_t(per_warp) * wpb)
+                                                                   : 48 * 1024)) != cudaSuccess)
     return e;
   if (a.nq == 0) return cudaSuccess;
   int per_sm = 0, sms = 0;
   if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
-  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, wpb * 32, smem)) != cudaSuccess) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, wpb * 32, size_t(per_warp) * wpb)) !=
+      cudaSuccess)
+    return e;
+  for (int w = wpb >> 1; w >= 1; w >>= 1) {
+    int ps = 0;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, k, w * 32, size_t(per_warp) * w)) != cudaSuccess)
+      return e;
+    if (ps * w > per_sm * wpb) {
+      per_sm = ps;
+      wpb = w;
+    }
+  }
+  const size_t smem = size_t(per_warp) * wpb;
   const uint32_t want = (a.nq + wpb - 1) / wpb;
   const uint32_t blocks = std::min<uint32_t>(want, static_cast<uint32_t>(std::max(1, per_sm) * sms));
   if ((e = cudaMemsetAsync(a.next_query, 0, sizeof(uint32_t), s)) != cudaSuccess) return e;

