@@ -115,14 +115,17 @@ uint32_t env_u32(const char* name, uint32_t dflt) {
 // id while n fits (half the bytes of an id slot, so twice the entries); a
 // bucket of 4 (2, 1) slots then covers n <= 2^(log2 + 13) (+14, +15). Larger
 // n store whole ids, in buckets of 4 as well.
-// Past L = 256 the table grows with the beam (GANN_HASH_PER_BEAM slots per
-// beam slot, default 8): a walk of beam L evaluates ~10 L distinct ids, and a
-// table far smaller than that re-gathers each evicted row again and again
-// (measured at c1, L = 1024 with 2048 slots: 3x the distinct rows gathered).
+// Past L = 1024 the table grows with the beam (GANN_HASH_PER_BEAM slots per
+// beam slot, default 2). A walk of beam L evaluates ~10 L distinct ids and a
+// small table re-gathers evicted rows (c1, L = 1024, 2048 slots: 3.7x the
+// distinct rows), but the shared memory a larger table takes costs resident
+// warps, and that costs more: measured at c1, L = 832 / 1024, 2048 slots ->
+// 20.5 / 26.5 ms per 10k queries; 4, 8, 16 slots per beam slot -> 21.6 /
+// 26.5, 27.5 / 34.0, 38.4 / 47.0 ms.
 void hash_config(uint32_t L, uint64_t n, uint32_t* log2, uint32_t* bits, uint32_t* ways) {
   const uint32_t forced = std::min<uint32_t>(env_u32("GANN_HASH_LOG2", 0), 15);
   const bool narrow = env_u32("GANN_HASH16", 1) != 0;
-  const uint64_t per_beam = env_u32("GANN_HASH_PER_BEAM", 8);
+  const uint64_t per_beam = env_u32("GANN_HASH_PER_BEAM", 2);
   uint32_t grow = 0;  // doublings past the base table for large beams
   if (L > 256)
     while (grow < 4 && (uint64_t(2048) << grow) < per_beam * L) grow++;
