@@ -77,7 +77,7 @@ struct SearchArgs {
   uint32_t* next_query;      // persistent warps: dynamic query counter (zeroed per launch)
   unsigned long long* stats; // kStCount counters (nullable)
 };
-size_t search_smem_per_warp(uint32_t L, uint32_t R, uint32_t hash_log2, bool hash16, bool spec = false);
+size_t search_smem_per_warp(uint32_t L, uint32_t R, uint32_t hash_log2, bool hash16);
 constexpr int kSearchWarpsPerBlock = 4;  // one query per warp
 size_t search_smem_min_block(uint32_t L, uint32_t R, uint32_t hash_log2, bool hash16);
 

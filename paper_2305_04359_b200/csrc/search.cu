@@ -35,16 +35,16 @@ namespace gann {
 
 // Per-warp shared memory: beam keys + flags (single buffer, merged in place),
 // candidate scratch, and the direct-mapped visited table.
-size_t search_smem_per_warp(uint32_t L, uint32_t R, uint32_t hash_log2, bool hash16, bool spec) {
-  const size_t Lp = (L + 31) & ~31u, Rp = (R + 31) & ~31u, Rc = spec ? 2 * Rp : Rp;
-  size_t b = Lp * 8 + 2 * Rc * 8 + Rc * 4 + (size_t(1) << hash_log2) * (hash16 ? 2 : 4) + Lp / 8 + Lp;
+size_t search_smem_per_warp(uint32_t L, uint32_t R, uint32_t hash_log2, bool hash16) {
+  const size_t Lp = (L + 31) & ~31u, Rp = (R + 31) & ~31u;
+  size_t b = Lp * 8 + 2 * Rp * 8 + Rp * 4 + (size_t(1) << hash_log2) * (hash16 ? 2 : 4) + Lp / 8 + Lp;
   return (b + 15) & ~size_t(15);
 }
 
 // Shared memory of the narrowest search CTA: one warp (one query). Wider
 // CTAs (up to kSearchWarpsPerBlock) are used while their regions fit.
 size_t search_smem_min_block(uint32_t L, uint32_t R, uint32_t hash_log2, bool hash16) {
-  return search_smem_per_warp(L, R, hash_log2, hash16, R <= 64);
+  return search_smem_per_warp(L, R, hash_log2, hash16);
 }
 
 cudaError_t launch_search_u8(const SearchArgs& a, int metric, const Geometry& g, cudaStream_t s);

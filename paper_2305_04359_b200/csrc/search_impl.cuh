@@ -98,12 +98,11 @@ __device__ __forceinline__ const uint4* row_chunk(const uint8_t* base, uint32_t 
 // One pass: lane group g (LPR lanes) takes UU consecutive rows from b0 + g*UU,
 // their ids from one vectorised shared load. FIT: the row is exactly LPR*CPL
 // chunks (d = 128 u8 at 8 lanes), so no chunk is predicated off.
-template <class Op, int LPR, int CPL, int UU, bool FIT, bool SPLIT>
+template <class Op, int LPR, int CPL, int UU, bool FIT>
 __device__ __forceinline__ void eval_pass(uint32_t b0, const uint32_t* ids, uint32_t m, uint32_t stride,
                                           const uint8_t* const (&cb)[CPL], const bool (&chv)[CPL],
                                           uint64_t* out, const uint4 (&qr)[CPL], int sub, int grp,
-                                          uint64_t worst, uint32_t& n_out, int lane, uint32_t split,
-                                          uint32_t& n_split) {
+                                          uint64_t worst, uint32_t& n_out, int lane) {
   const uint32_t rb = b0 + grp * UU;
   uint32_t id[UU];
   if (UU % 4 == 0) {
@@ -144,8 +143,6 @@ __device__ __forceinline__ void eval_pass(uint32_t b0, const uint32_t* ids, uint
   const uint32_t bal = __ballot_sync(0xFFFFFFFFu, keep);
   if (keep) out[n_out + __popc(bal & ((1u << lane) - 1u))] = key;
   n_out += __popc(bal);
-  // keys of rows before `split` (rows keep their order in out: lane order is row order)
-  if (SPLIT) n_split += __popc(__ballot_sync(0xFFFFFFFFu, keep && r < split));
 }
 
 // Distances from the lane's query chunks qr to rows ids[0..m); the keys below
@@ -157,12 +154,11 @@ __device__ __forceinline__ void eval_pass(uint32_t b0, const uint32_t* ids, uint
 // address is one IMAD.WIDE.U32 (id * stride + the lane's hoisted chunk base).
 // A chunk index beyond the row (nch not a multiple of LPR) is clamped to the
 // row's last chunk and its contribution predicated off.
-template <class Op, int LPR, int CPL, bool FIT, bool SPLIT = false>
+template <class Op, int LPR, int CPL, bool FIT>
 __device__ __forceinline__ uint32_t eval_rows(const uint8_t* __restrict__ data, uint32_t stride,
                                               uint32_t nch, const uint32_t* ids, uint32_t m,
                                               uint64_t* out, const uint4 (&qr)[CPL], int lane,
-                                              uint64_t worst, uint32_t split = 0, uint32_t* n_split = nullptr) {
-  uint32_t ns = 0;
+                                              uint64_t worst) {
   constexpr int RPP = 32 / LPR;
   constexpr int U = Unroll<LPR, CPL>::U;
   const int sub = lane & (LPR - 1);
@@ -177,65 +173,23 @@ __device__ __forceinline__ uint32_t eval_rows(const uint8_t* __restrict__ data, 
   }
   uint32_t b0 = 0, n_out = 0;
   for (; b0 + RPP * U <= m; b0 += RPP * U)
-    eval_pass<Op, LPR, CPL, U, FIT, SPLIT>(b0, ids, m, stride, cb, chv, out, qr, sub, grp, worst, n_out, lane, split, ns);
+    eval_pass<Op, LPR, CPL, U, FIT>(b0, ids, m, stride, cb, chv, out, qr, sub, grp, worst, n_out, lane);
   const uint32_t rem = m - b0;
-  if (SPLIT) *n_split = ns;
   if (rem == 0) return n_out;
   if (U >= 8 && rem <= RPP * (U / 4))
-    eval_pass<Op, LPR, CPL, (U >= 8 ? U / 4 : 1), FIT, SPLIT>(b0, ids, m, stride, cb, chv, out, qr, sub, grp, worst, n_out,
-                                                                lane, split, ns);
+    eval_pass<Op, LPR, CPL, (U >= 8 ? U / 4 : 1), FIT>(b0, ids, m, stride, cb, chv, out, qr, sub, grp, worst, n_out, lane);
   else if (U >= 4 && rem <= RPP * (U / 2))
-    eval_pass<Op, LPR, CPL, (U >= 4 ? U / 2 : 1), FIT, SPLIT>(b0, ids, m, stride, cb, chv, out, qr, sub, grp, worst, n_out,
-                                                                lane, split, ns);
+    eval_pass<Op, LPR, CPL, (U >= 4 ? U / 2 : 1), FIT>(b0, ids, m, stride, cb, chv, out, qr, sub, grp, worst, n_out, lane);
   else
-    eval_pass<Op, LPR, CPL, U, FIT, SPLIT>(b0, ids, m, stride, cb, chv, out, qr, sub, grp, worst, n_out, lane, split, ns);
-  if (SPLIT) *n_split = ns;
+    eval_pass<Op, LPR, CPL, U, FIT>(b0, ids, m, stride, cb, chv, out, qr, sub, grp, worst, n_out, lane);
   return n_out;
-}
-
-// The fast mode's u16 visited table (F16 instances: 1, 2 or 4 slots a
-// bucket; see the filter in search_kernel): read-only test and insert.
-__device__ __forceinline__ bool u16_seen(const uint32_t* hash, uint32_t ways, uint32_t hmask, uint32_t nb) {
-  const uint32_t h = (nb * 0x9E3779B1u) & hmask;
-  const uint32_t bucket = h >> 15, rem = h & 0x7FFFu;
-  if (ways == 4) {
-    const uint64_t w = reinterpret_cast<const uint64_t*>(hash)[bucket];
-    const uint32_t rr = rem | (rem << 16);
-    return (__vcmpeq2(static_cast<uint32_t>(w), rr) | __vcmpeq2(static_cast<uint32_t>(w >> 32), rr)) != 0u;
-  }
-  if (ways == 2) {
-    const uint32_t w = hash[bucket];
-    return (w & 0xFFFFu) == rem || (w >> 16) == rem;
-  }
-  return reinterpret_cast<const uint16_t*>(hash)[bucket] == rem;
-}
-__device__ __forceinline__ void u16_insert(uint32_t* hash, uint32_t ways, uint32_t hmask, uint32_t nb) {
-  const uint32_t h = (nb * 0x9E3779B1u) & hmask;
-  const uint32_t bucket = h >> 15, rem = h & 0x7FFFu;
-  if (ways == 4) {
-    uint64_t* h64 = reinterpret_cast<uint64_t*>(hash);
-    h64[bucket] = (h64[bucket] << 16) | rem;
-  } else if (ways == 2) {
-    hash[bucket] = (hash[bucket] << 16) | rem;
-  } else {
-    reinterpret_cast<uint16_t*>(hash)[bucket] = static_cast<uint16_t>(rem);
-  }
-}
-
-// Warp-wide minimum of a u64 (every lane gets it).
-__device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    const uint64_t w = __shfl_xor_sync(0xFFFFFFFFu, v, o);
-    v = w < v ? w : v;
-  }
-  return v;
 }
 
 __device__ __forceinline__ uint32_t lanemask_lt(int lane) { return (1u << lane) - 1u; }
 
 }  // namespace
 
+size_t search_smem_per_warp(uint32_t L, uint32_t R, uint32_t hash_log2, bool hash16);
 
 // F16: the fast mode with u16 slots, compiled without the other modes'
 // branches and without the diagnostic counters (filter drops, adjacency
@@ -243,11 +197,9 @@ __device__ __forceinline__ uint32_t lanemask_lt(int lane) { return (1u << lane) 
 // them (GANN_SEARCH_DIAG=1 selects it for the fast mode too)
 // R64: the degree bound is 64 (every BASELINE config), fixed at compile time
 // FIT: rows are exactly LPR * CPL chunks (no chunk predicate in the gather)
-// SPEC: two expansions per step (Alg. 1, {L, L, 0}: see the loop)
-template <int E, int M, int LPR, int CPL, bool F16, bool R64 = false, bool FIT = false, bool SPEC = false>
+template <int E, int M, int LPR, int CPL, bool F16, bool R64 = false, bool FIT = false>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_MINB_WIDE : GANN_SEARCH_MINB)
     search_kernel(const SearchArgs a, const uint32_t per_warp) {
-  static_assert(!SPEC || F16, "two-expansion steps run in the fast visited mode");
   using Op = DistOp<E, M>;
   extern __shared__ __align__(16) uint8_t smem[];
   const int lane = threadIdx.x & 31;
@@ -263,14 +215,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_M
   // ck: candidate keys; tmpk: keys below the L-th (dead after the duplicate
   // pass, so it also holds the sorted survivors srt); cid: candidate ids
   // (dead after the gather, so it also holds the insertion points posb)
-  // (SPEC: room for two rows' candidates)
-  const uint32_t Rc = SPEC ? 2 * Rp : Rp;
   uint64_t* ck = beam + Lp;
-  uint64_t* tmpk = ck + Rc;
+  uint64_t* tmpk = ck + Rp;
   uint64_t* srt = tmpk;
-  uint32_t* cid = reinterpret_cast<uint32_t*>(tmpk + Rc);
+  uint32_t* cid = reinterpret_cast<uint32_t*>(tmpk + Rp);
   uint32_t* posb = cid;
-  uint32_t* hash = cid + Rc;
+  uint32_t* hash = cid + Rp;
   uint16_t* h16 = reinterpret_cast<uint16_t*>(hash);
   const uint32_t hbits = a.hash_bits;  // F16 implies hbits != 0
   const int vmode = F16 ? 0 : a.visited_mode;
@@ -346,9 +296,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_M
     // (R <= 64: two ids per lane); used when the guess turns out right
     const bool pf_ok = R <= 64;
     uint32_t pf_id = kNone, pf0 = kNone, pf1 = kNone;
-    // two expansions per step: Alg. 1 (k = L, eps = 0, so the gate always
-    // passes inside the beam), fast visited mode, rows of <= 64 ids
-    const bool spec = SPEC && pf_ok && a.k_gate == L && a.eps == 0.0f;
     __syncwarp();
 
     while (true) {
@@ -376,17 +323,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_M
       hint = fu + 1;
       const uint32_t* row = graph_row(a.graph, cur, R);
       uint32_t nb0 = kNone, nb1 = kNone;
-      // SPEC: the second unexpanded key v2 (at gi) is expanded in the same
-      // step when, once v1's candidates are merged, it is still the first
-      // unexpanded key — i.e. every surviving v1 candidate sorts after it —
-      // which is exactly the reference's next expansion (the gate passes
-      // inside the beam for k = L, eps = 0). Its candidates are gathered with
-      // v1's; they are merged (and its neighbours entered in the visited
-      // table) only then, else dropped. v2's row is read now and the row of
-      // the unexpanded key after it (v3) prefetched for the next step.
-      int gi = -1;
-      uint32_t v2 = kNone, nb2a = kNone, nb2b = kNone, p3 = kNone, p3a = kNone, p3b = kNone;
-      uint64_t k2 = kMaxKey;
       if (pf_ok) {
         if (pf_id == cur) {
           nb0 = pf0;
@@ -398,46 +334,17 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_M
         }
         // guess the next expansion: the next unexpanded key after fu
         const uint32_t above = fbal & ~((2u << (fu - fb0)) - 1u);
-        gi = above ? static_cast<int>(fb0 + __ffs(above) - 1) : -1;
+        int gi = above ? static_cast<int>(fb0 + __ffs(above) - 1) : -1;
         if (gi < 0 && fb0 + 32 < size) {
           const uint32_t i = fb0 + 32 + lane;
           const uint32_t bal = __ballot_sync(FULL, i < size && fl[i] == 0);
           if (bal) gi = static_cast<int>(fb0 + 32 + __ffs(bal) - 1);
         }
-        if (SPEC && spec) {
-          if (gi >= 0) {
-            k2 = beam[gi];
-            v2 = key_id(k2);
-            if (pf_id == v2) {
-              nb2a = pf0;
-              nb2b = pf1;
-            } else {
-              const uint32_t* r2 = graph_row(a.graph, v2, R);
-              nb2a = lane < R ? __ldg(r2 + lane) : kNone;
-              nb2b = lane + 32 < R ? __ldg(r2 + 32 + lane) : kNone;
-            }
-            const uint32_t b3 = static_cast<uint32_t>(gi) & ~31u;
-            uint32_t bal3 = __ballot_sync(FULL, b3 + lane > static_cast<uint32_t>(gi) && b3 + lane < size &&
-                                                    fl[b3 + lane] == 0);
-            int g3 = bal3 ? static_cast<int>(b3 + __ffs(bal3) - 1) : -1;
-            if (g3 < 0 && b3 + 32 < size) {
-              bal3 = __ballot_sync(FULL, b3 + 32 + lane < size && fl[b3 + 32 + lane] == 0);
-              if (bal3) g3 = static_cast<int>(b3 + 32 + __ffs(bal3) - 1);
-            }
-            if (g3 >= 0) {
-              p3 = key_id(beam[g3]);
-              const uint32_t* r3 = graph_row(a.graph, p3, R);
-              p3a = lane < R ? __ldg(r3 + lane) : kNone;
-              p3b = lane + 32 < R ? __ldg(r3 + 32 + lane) : kNone;
-            }
-          }
-        } else {
-          pf_id = gi >= 0 ? key_id(beam[gi]) : kNone;
-          if (pf_id != kNone) {
-            const uint32_t* prow = graph_row(a.graph, pf_id, R);
-            pf0 = lane < R ? __ldg(prow + lane) : kNone;
-            pf1 = lane + 32 < R ? __ldg(prow + 32 + lane) : kNone;
-          }
+        pf_id = gi >= 0 ? key_id(beam[gi]) : kNone;
+        if (pf_id != kNone) {
+          const uint32_t* prow = graph_row(a.graph, pf_id, R);
+          pf0 = lane < R ? __ldg(prow + lane) : kNone;
+          pf1 = lane + 32 < R ? __ldg(prow + 32 + lane) : kNone;
         }
       }
       __syncwarp();
@@ -449,7 +356,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_M
         }
       }
       nvis++;
-      bool lost = false;  // SPEC: a v1 table insert lost to a same-bucket race in its chunk
 
       // ---- neighbours through the visited filter (adjacency order kept) ----
       uint32_t m = 0;
@@ -551,79 +457,19 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_M
         const uint32_t bal = __ballot_sync(FULL, fresh);
         if (fresh) cid[m + __popc(bal & lanemask_lt(lane))] = nb;
         m += __popc(bal);
-        if (SPEC && spec) {
-          __syncwarp();
-          lost = lost || __any_sync(FULL, fresh && !u16_seen(hash, a.hash_ways, hmask, nb));
-        }
       }
-      // SPEC: v2's neighbours, tested against the table (now holding v1's) but
-      // not entered in it unless v2 commits; a race-lost v1 id is caught by
-      // comparing with v1's candidates
-      const uint32_t m1 = m;
-      uint32_t f2a = kNone, f2b = kNone;
-      bool commit = false;
-      if (SPEC && spec && v2 != kNone) {
-        for (uint32_t t0 = 0; t0 < R; t0 += 32) {
-          const uint32_t nb = t0 == 0 ? nb2a : nb2b;
-          bool fresh = nb != kNone && nb != cur && !u16_seen(hash, a.hash_ways, hmask, nb);
-          if (lost)
-            for (uint32_t t = 0; t < m1; t++) fresh = fresh && cid[t] != nb;
-          const uint32_t bal = __ballot_sync(FULL, fresh);
-          if (fresh) cid[m + __popc(bal & lanemask_lt(lane))] = nb;
-          m += __popc(bal);
-        }
-        __syncwarp();
-        f2a = m1 + lane < m ? cid[m1 + lane] : kNone;
-        f2b = m1 + 32 + lane < m ? cid[m1 + 32 + lane] : kNone;
-      }
-      // v2 joins the walk: marked expanded and recorded after v1, its
-      // neighbours entered in the table; the next step starts after it
-      auto commit_v2 = [&]() {
-        if (lane == 0) {
-          fl[gi] = 1;
-          if (a.vis_ids && nvis < a.vcap) {
-            a.vis_ids[static_cast<uint64_t>(q) * a.vcap + nvis] = v2;
-            a.vis_dists[static_cast<uint64_t>(q) * a.vcap + nvis] = key_dist(k2);
-          }
-        }
-        nvis++;
-        if (f2a != kNone) u16_insert(hash, a.hash_ways, hmask, f2a);
-        __syncwarp();
-        if (f2b != kNone) u16_insert(hash, a.hash_ways, hmask, f2b);
-        hint = static_cast<uint32_t>(gi) + 1;
-        pf_id = p3;
-        pf0 = p3a;
-        pf1 = p3b;
-      };
-      if (SPEC && spec) {  // next step's prefetch when v2 does not commit: v2's row
-        pf_id = v2;
-        pf0 = nb2a;
-        pf1 = nb2b;
-      }
-      if (m == 0) {
-        if (SPEC && spec && v2 != kNone) commit_v2();  // no candidates: v2 is next
-        __syncwarp();
-        continue;
-      }
+      if (m == 0) continue;
       if (m + lane < ((m + 31) & ~31u)) cid[m + lane] = cur;  // pad to a whole pass
       __syncwarp();
       evals += m;
-      // distances; keys below the L-th beam key go to tmpk (c1 of them; the
-      // first c1a from v1's rows)
+      // distances; keys below the L-th beam key go to tmpk (c1 of them)
       const uint64_t worst = size == L ? beam[L - 1] : kMaxKey;
-      uint32_t c1a = 0;
-      const uint32_t c1 = eval_rows<Op, LPR, CPL, FIT, SPEC>(a.data, stride32, nch, cid, m, tmpk, qr, lane, worst,
-                                                              m1, &c1a);
-      if (c1 == 0) {
-        if (SPEC && spec && v2 != kNone) commit_v2();  // no candidate below the L-th key: v2 is next
-        __syncwarp();
-        continue;
-      }
+      const uint32_t c1 = eval_rows<Op, LPR, CPL, FIT>(a.data, stride32, nch, cid, m, tmpk, qr, lane, worst);
+      if (c1 == 0) continue;
       __syncwarp();
       // ---- merge: top-L of beam U new, exact duplicates dropped ----
       // insertion points; exact (dist, id) duplicates of beam keys drop
-      uint32_t s = 0, s1 = 0;
-      uint64_t kmin1 = kMaxKey;  // SPEC: the smallest surviving v1 candidate
+      uint32_t s = 0;
       for (uint32_t j0 = 0; j0 < c1; j0 += 32) {
         const uint32_t j = j0 + lane;
         bool keep = j < c1;
@@ -643,23 +489,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_M
           posb[o] = pb;
         }
         s += __popc(bal);
-        if (SPEC && spec) {  // v1's keys precede v2's in tmpk, so its survivors are ck[0, s1)
-          const bool k1 = keep && j < c1a;
-          if (k1) kmin1 = k < kmin1 ? k : kmin1;
-          s1 += __popc(__ballot_sync(FULL, k1));
-        }
       }
-      if (SPEC && spec && v2 != kNone) {
-        commit = warp_min_u64(kmin1) > k2;
-        if (commit)
-          commit_v2();
-        else
-          s = s1;  // v2's candidates are dropped with it
-      }
-      if (s == 0) {
-        __syncwarp();
-        continue;
-      }
+      if (s == 0) continue;
       __syncwarp();
       // survivors sorted (srt), final positions fin = insertion point + rank
       // marked in a bitmap of beam positions (only fin < L is kept)
@@ -769,15 +600,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_M
 namespace {
 template <int E, int M, int LPR, int CPL>
 cudaError_t launch_one(const SearchArgs& a, cudaStream_t s) {
-  // read per launch (A/B runs flip them between launches)
-  const char* dv = std::getenv("GANN_SEARCH_DIAG");
-  const bool diag = dv && *dv && *dv != '0';
-  const bool f16 = a.visited_mode == 0 && a.hash_bits != 0 && !diag;
-  // two expansions per step (measured: see DESIGN.md §4); GANN_SEARCH_SPEC=0 disables
-  const char* sv = std::getenv("GANN_SEARCH_SPEC");
-  const bool spec = f16 && a.R <= 64 && a.k_gate == a.L && a.eps == 0.0f && !(sv && *sv == '0');
-  const uint32_t per_warp =
-      static_cast<uint32_t>(search_smem_per_warp(a.L, a.R, a.hash_log2, a.hash_bits != 0, spec));
+  const uint32_t per_warp = static_cast<uint32_t>(search_smem_per_warp(a.L, a.R, a.hash_log2, a.hash_bits != 0));
   int dev = 0, optin = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
@@ -788,6 +611,10 @@ cudaError_t launch_one(const SearchArgs& a, cudaStream_t s) {
   // warps at 59 KB each waste 50 KB that 1-warp CTAs use)
   int wpb = kWarpsPerBlock;
   while (wpb > 1 && size_t(per_warp) * wpb > static_cast<size_t>(optin)) wpb >>= 1;
+  // read per launch (A/B runs flip it between launches)
+  const char* dv = std::getenv("GANN_SEARCH_DIAG");
+  const bool diag = dv && *dv && *dv != '0';
+  const bool f16 = a.visited_mode == 0 && a.hash_bits != 0 && !diag;
   // R = 64 fixed at compile time (measured): 16-lane rows -5% at L=200 (c2)
   // and a faster build search; 8-lane rows (c1): -1% for a serial launch at
   // L=200 but -1% bench QPS (pipelined), +1.4% at L=64, +4.5% for the build's
@@ -796,13 +623,9 @@ cudaError_t launch_one(const SearchArgs& a, cudaStream_t s) {
   const bool r64 = a.R == 64 && (rv && *rv ? *rv == '1' : LPR >= 16);
   const bool fit = a.stride == uint64_t(16) * LPR * CPL;
   auto k = !f16 ? search_kernel<E, M, LPR, CPL, false>
-          : spec ? (r64 ? (fit ? search_kernel<E, M, LPR, CPL, true, true, true, true>
-                               : search_kernel<E, M, LPR, CPL, true, true, false, true>)
-                        : (fit ? search_kernel<E, M, LPR, CPL, true, false, true, true>
-                               : search_kernel<E, M, LPR, CPL, true, false, false, true>))
-                 : (r64 ? (fit ? search_kernel<E, M, LPR, CPL, true, true, true> : search_kernel<E, M, LPR, CPL, true, true>)
-                        : (fit ? search_kernel<E, M, LPR, CPL, true, false, true>
-                               : search_kernel<E, M, LPR, CPL, true, false>));
+                : (r64 ? (fit ? search_kernel<E, M, LPR, CPL, true, true, true> : search_kernel<E, M, LPR, CPL, true, true>)
+                       : (fit ? search_kernel<E, M, LPR, CPL, true, false, true>
+                              : search_kernel<E, M, LPR, CPL, true, false>));
   if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 size_t(per_warp) * wpb > 48 * 1024 ? static_cast<int>(size_t(per_warp) * wpb)
                                                                    : 48 * 1024)) != cudaSuccess)
@@ -854,10 +677,6 @@ void preload_one() {
   touch_kernel(search_kernel<E, M, LPR, CPL, true, true>);
   touch_kernel(search_kernel<E, M, LPR, CPL, true, false, true>);
   touch_kernel(search_kernel<E, M, LPR, CPL, true, true, true>);
-  touch_kernel(search_kernel<E, M, LPR, CPL, true, false, false, true>);
-  touch_kernel(search_kernel<E, M, LPR, CPL, true, true, false, true>);
-  touch_kernel(search_kernel<E, M, LPR, CPL, true, false, true, true>);
-  touch_kernel(search_kernel<E, M, LPR, CPL, true, true, true, true>);
 }
 template <int E, int M>
 void preload_geom(const Geometry& g) {
