@@ -129,7 +129,12 @@ void hash_config(uint32_t L, uint64_t n, uint32_t* log2, uint32_t* bits, uint32_
   uint32_t grow = 0;  // doublings past the base table for large beams
   if (L > 256)
     while (grow < 4 && (uint64_t(2048) << grow) < per_beam * L) grow++;
-  uint32_t l = forced ? std::max<uint32_t>(forced, 5) : 11 + grow;
+  // 512 < L <= 2048: half the table (1024 slots) leaves room for more
+  // resident warps, which pays more than the re-gathers it adds (c1, L = 832:
+  // 19.8 vs 20.5 ms per 10k queries; L = 1024: 25.8 vs 26.5; L = 200: 4.91 vs
+  // 4.74, so small beams keep 2048)
+  const uint32_t base = (L > 512 && L <= 2048) ? 10 : 11;
+  uint32_t l = forced ? std::max<uint32_t>(forced, 5) : base + grow;
   // u16 remainder slots; 2-way buckets (the bucket's newest id in the low
   // half) halve the conflict evictions of a direct-mapped table of the same size
   const uint32_t w = env_u32("GANN_HASH_WAYS", 4);
