@@ -306,6 +306,12 @@ int gann_nccl_comm_init(const void* id128, uint32_t rank, uint32_t nranks, int d
 int gann_nccl_comm_destroy(void* comm);
 int gann_exchange_nccl(void* comm, uint32_t rank, uint32_t nranks, gann_exchange* out);
 
+/* Checked builds (compiled with -DGANN_CHECKED; tools/build_variant.sh):
+ * the kernels test the index bounds of their shared-memory and output writes
+ * on the device. Reports the largest source line of a failed check since the
+ * last call (0: none) and whether this library is a checked build. */
+int gann_debug_check(int device, uint32_t* failed_line, int* checked_build);
+
 /* ---- counters (roofline) ----------------------------------------------------
  * Totals accumulated by the kernels since the last reset. */
 typedef struct gann_stats {

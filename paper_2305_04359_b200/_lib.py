@@ -63,6 +63,7 @@ SIGNATURES = {
     "gann_search_device": (_i, [_vp, _vp, _u32, _u32, _u32, _u32, _f, _i, _vp, _vp, _vp, _vp, _vp]),
     "gann_stage_queries": (_i, [_vp, _vp, _u32]),
     "gann_search_max_beam": (_i, [_vp, C.POINTER(C.c_uint32)]),
+    "gann_debug_check": (_i, [_i, _vp, _vp]),
     "gann_search_staged": (_i, [_vp, _u32, _u32, _u32, _f, _vp, _vp, _vp]),
     "gann_search_async_scratch": (_u64, [_vp, _u32, _u32]),
     "gann_search_async": (_i, [_vp, _vp, _u32, _u32, _u32, _u32, _f, _vp, _vp, _vp, _u64, _vp]),

@@ -104,6 +104,7 @@ __global__ void be_scatter_kernel(const BackEdgeArgs a) {
     if (t == kNone) continue;
     const uint32_t g = a.tgroup[t - a.base];
     const uint32_t pos = atomicAdd(a.gcursor + g, 1u);
+    GANN_CHECK(pos < a.gcnt[g] && a.goff[g] + pos < a.npairs);
     a.gsrc[a.goff[g] + pos] = a.pordinal ? a.pordinal[e * a.pstride] : static_cast<uint32_t>(e);
   }
 }
@@ -250,6 +251,7 @@ __global__ void __launch_bounds__(NT)
       }
       if (static_cast<uint32_t>(lane) < deg) pid[lane] = r0;
       if (static_cast<uint32_t>(lane) + 32 < deg) pid[lane + 32] = r1;
+      GANN_CHECK(!((keepmask >> lane) & 1u) || deg + __popc(keepmask & ((1u << lane) - 1u)) < a.R + c);
       if ((keepmask >> lane) & 1u) pid[deg + __popc(keepmask & ((1u << lane) - 1u))] = src;
       nm = deg + __popc(keepmask);
       __syncwarp();
@@ -646,5 +648,7 @@ cudaError_t backedge_write_groups(const BackEdgeArgs& a, uint32_t ng, uint32_t n
   Geometry g{1, 1, 1};
   return merge_geom<kU8, kL2, 1>(a, ng, nbig, g, out_keys, out_vals, s);
 }
+
+GANN_CHECK_READER(check_line_backedge)
 
 }  // namespace gann

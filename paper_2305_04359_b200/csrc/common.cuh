@@ -19,6 +19,37 @@
 
 namespace gann {
 
+// Checked builds (-DGANN_CHECKED, tools/build_variant.sh; the GPU test
+// tests/test_gpu_checked.py): index bounds of the kernels' shared-memory and
+// output writes are tested on the device; a failure records its source line
+// (the largest failing line wins) instead of writing out of bounds, and
+// gann_debug_check_line() reports it. compute-sanitizer is not available on
+// the GPU pool, so this is the memory-safety evidence. Release builds compile
+// the checks away.
+#ifdef GANN_CHECKED
+static __device__ unsigned int g_check_line = 0;
+#define GANN_CHECK(c)                                         \
+  do {                                                        \
+    if (!(c)) atomicMax(&::gann::g_check_line, __LINE__);     \
+  } while (0)
+#define GANN_CHECKED_ONLY(x) x
+// a translation unit's reader: the largest failing line, then cleared
+#define GANN_CHECK_READER(name)                                   \
+  unsigned name() {                                               \
+    unsigned v = 0, z = 0;                                        \
+    cudaMemcpyFromSymbol(&v, ::gann::g_check_line, sizeof(v));    \
+    cudaMemcpyToSymbol(::gann::g_check_line, &z, sizeof(z));      \
+    return v;                                                     \
+  }
+#else
+#define GANN_CHECK_READER(name) \
+  unsigned name() { return 0; }
+#define GANN_CHECK(c) \
+  do {                \
+  } while (0)
+#define GANN_CHECKED_ONLY(x)
+#endif
+
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 constexpr uint64_t kMaxKey = 0xFFFFFFFFFFFFFFFFull;
 
@@ -174,6 +205,31 @@ __device__ __forceinline__ uint32_t lower_bound_steps_u64(const uint64_t* a, uin
     if (j <= n && a[j - 1] < k) pos = j;
   }
   return pos;
+}
+
+// Sum U per-lane partials over the LPR lanes of a row group so that lane
+// (sub mod U) ends up holding the total of row `sub mod U` (U <= LPR, both
+// powers of two): plain butterflies for the lane bits above U, then a
+// transposed butterfly that halves the live values each step — LPR=U=8 costs
+// 4+2+1 shuffles for 8 rows instead of 3 per row.
+template <int LPR, int U, typename T>
+__device__ __forceinline__ T transpose_reduce(T (&v)[U], int sub) {
+#pragma unroll
+  for (int o = LPR / 2; o >= U; o >>= 1) {
+#pragma unroll
+    for (int u = 0; u < U; u++) v[u] += __shfl_xor_sync(0xFFFFFFFFu, v[u], o);
+  }
+#pragma unroll
+  for (int w = U / 2; w >= 1; w >>= 1) {
+    const bool hi = (sub & w) != 0;
+#pragma unroll
+    for (int i = 0; i < w; i++) {
+      const T send = hi ? v[i] : v[i + w];
+      const T keep = hi ? v[i + w] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xFFFFFFFFu, send, w);
+    }
+  }
+  return v[0];
 }
 
 }  // namespace gann

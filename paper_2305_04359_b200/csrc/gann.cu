@@ -536,16 +536,28 @@ void prune_binned(gann_index* idx, PruneArgs p, uint32_t maxlen, bool fine = fal
   else
     bounds = {bin0 ? bin0 : 80, 128, 192, 256, 512};
   const int nb = static_cast<int>(bounds.size());
-  idx->bins.ensure(size_t(p.count) * (nb + 1) * 4 + 64 + 16 * 4);
+  // back-edge re-prunes of a row prefix plus a few entries: the warp kernel
+  // (integer rows, R <= 64; GANN_SMALL_REPRUNE=0 sends them to the bins)
+  static const bool small_on = env_u32("GANN_SMALL_REPRUNE", 1) != 0;
+  const bool small = mma && p.row_lists && p.spre && idx->R <= 64 && small_on;
+  p.small_u = small ? reprune_small_max_u() : 0u;
+  idx->bins.ensure(size_t(p.count) * (nb + 2) * 4 + 64 * 4);
   uint32_t* d_counts = idx->bins.as<uint32_t>();
-  uint32_t* d_bounds = d_counts + 8;
-  uint32_t* d_lists = d_counts + 16;
+  uint32_t* d_bounds = d_counts + 16;
+  uint32_t* d_lists = d_counts + 64;
   cu(cudaMemcpyAsync(d_bounds, bounds.data(), bounds.size() * 4, cudaMemcpyHostToDevice, idx->stream), "bins");
   cu(launch_bin_lists(p, d_bounds, nb, d_counts, d_lists, idx->stream), "bin lists");
-  uint32_t counts[8] = {};
-  cu(cudaMemcpyAsync(counts, d_counts, nb * 4, cudaMemcpyDeviceToHost, idx->stream), "bin counts");
+  uint32_t counts[16] = {};
+  cu(cudaMemcpyAsync(counts, d_counts, (nb + 1) * 4, cudaMemcpyDeviceToHost, idx->stream), "bin counts");
   sync(idx);
   uint32_t lo = 0, total = 0;
+  if (counts[nb]) {
+    PruneArgs q = p;
+    q.list_index = d_lists + size_t(nb) * p.count;
+    q.count = counts[nb];
+    cu(launch_reprune_small(q, idx->elem, idx->metric, idx->geom, idx->stream), "re-prune (warp)");
+    total += counts[nb];
+  }
   for (int b = 0; b < nb; b++) {
     total += counts[b];
     if (counts[b]) {
@@ -759,6 +771,7 @@ void apply_back(gann_index* idx, const uint32_t* bsrc, uint32_t B, const uint32_
   p.out_adj = idx->adj;
   p.out_base = idx->part_base;
   p.row_lists = 1;  // merged lists start with the target's current row
+  cu(cudaMemsetAsync(idx->flags + 1, 0, 4, idx->stream), "memset flags");
   if (nps) {
     p.count = nps;
     p.list_index = b.plist_small;
@@ -773,7 +786,10 @@ void apply_back(gann_index* idx, const uint32_t* bsrc, uint32_t B, const uint32_
     p.mcap = 0xFFFFFFFFu;
     cu(launch_prune(p, idx->elem, idx->metric, idx->geom, 256, idx->stream), "reprune big");
   }
+  uint32_t tl = 0;  // a re-prune list the kernels could not take (must not happen)
+  cu(cudaMemcpyAsync(&tl, idx->flags + 1, 4, cudaMemcpyDeviceToHost, idx->stream), "read flags");
   sync(idx);
+  if (tl) fail(GANN_ECUDA, "re-prune: " + std::to_string(tl) + " list(s) not taken by any prune kernel");
   tp.stop(idx, timed ? 5 : -1);
 }
 
@@ -1196,6 +1212,23 @@ int gann_search_device(gann_index* idx, const void* d_queries, uint32_t nq, uint
     a.n_visited = d_n_visited;
     a.dist_comps = d_dist_comps;
     run_search(idx, a, s);
+  });
+}
+
+int gann_debug_check(int device, uint32_t* failed_line, int* checked_build) {
+  return guarded([&] {
+    cu(cudaSetDevice(device), "cudaSetDevice");
+    cu(cudaDeviceSynchronize(), "sync");
+    unsigned v = 0;
+    for (unsigned (*f)() : {check_line_search_u8, check_line_search_i8, check_line_search_f32, check_line_prune,
+                            check_line_backedge, check_line_misc})
+      v = std::max(v, f());
+    if (failed_line) *failed_line = v;
+#ifdef GANN_CHECKED
+    if (checked_build) *checked_build = 1;
+#else
+    if (checked_build) *checked_build = 0;
+#endif
   });
 }
 

@@ -9,6 +9,14 @@
 namespace gann {
 
 void set_last_error(const std::string& msg);  // gann_last_error() text (gann.cu)
+// checked builds (common.cuh GANN_CHECK): each kernel translation unit's
+// largest failing check line (0: none, or a release build)
+unsigned check_line_search_u8();
+unsigned check_line_search_i8();
+unsigned check_line_search_f32();
+unsigned check_line_prune();
+unsigned check_line_backedge();
+unsigned check_line_misc();
 
 // Row geometry: LPR lanes per row, up to CPL 16-byte chunks per lane.
 struct Geometry {
@@ -135,6 +143,9 @@ struct PruneArgs {
   uint8_t* spre;
   int row_lists;
   PruneHandoff* hand;          // host pointer: the calling index's hand-off region
+  // bin_lists: re-prune lists (row_lists) whose row prefix leaves at most
+  // small_u other entries go to an extra bin (index nb) for the warp kernel
+  uint32_t small_u;
 };
 // threads = 32 for short lists, larger for hubs; smem from prune_smem_bytes.
 size_t prune_smem_bytes(uint32_t mcap, uint32_t R);
@@ -143,6 +154,10 @@ cudaError_t launch_prune(const PruneArgs& a, int elem, int metric, const Geometr
 // Length bins: lists[b * count + i] for i < counts[b], b over bounds (last bin: longer).
 cudaError_t launch_bin_lists(const PruneArgs& a, const uint32_t* d_bounds, int nb, uint32_t* d_counts,
                              uint32_t* d_lists, cudaStream_t s);
+// Re-prunes of a row prefix plus <= small_u entries (integer rows, R <= 64):
+// one warp per list (prune.cu reprune_small_kernel).
+uint32_t reprune_small_max_u();
+cudaError_t launch_reprune_small(const PruneArgs& a, int elem, int metric, const Geometry& g, cudaStream_t s);
 // Integer lists up to 512 candidates run on the tensor cores (IMMA tiles).
 bool prune_uses_mma(int elem, uint32_t mcap, uint64_t stride, uint32_t R);
 // Allocate the tensor-core prune's hand-off region up front for launches of

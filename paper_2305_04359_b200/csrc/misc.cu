@@ -453,4 +453,6 @@ cudaError_t launch_validate_rows(const uint32_t* adj, uint64_t rows, uint32_t R,
   return cudaGetLastError();
 }
 
+GANN_CHECK_READER(check_line_misc)
+
 }  // namespace gann

@@ -453,6 +453,7 @@ __global__ void __launch_bounds__(PrepThreads<W>::value)
 #pragma unroll
         for (int u = 0; u < GU; u++) {
           const uint32_t r = r0 + u * step;
+          GANN_CHECK(r >= rows_g || r <= mc);
           if (r < rows_g) *reinterpret_cast<uint4*>((r < m ? X + size_t(r) * xs : Xp) + c * 16) = v[u];
         }
       }
@@ -855,14 +856,18 @@ __global__ void bin_lists_kernel(const PruneArgs a, const uint32_t* bounds, int 
   const bool valid = li < a.count;
   const uint32_t l = valid ? (a.list_index ? a.list_index[li] : li) : 0u;
   const uint32_t m = valid ? a.lengths[l] : 0u;
-  int b = nb;
+  int b = nb + 1;  // longer than every bound
   if (valid)
     for (int i = 0; i < nb; i++)
       if (m <= bounds[i]) {
         b = i;
         break;
       }
-  for (int i = 0; i < nb; i++) {  // warp-aggregated append per bin
+  if (valid && a.small_u && a.row_lists && a.spre) {  // the warp re-prune's class (bin nb)
+    const uint32_t S = min(static_cast<uint32_t>(a.spre[a.points[l] - a.out_base]), m);
+    if (S <= 64 && m - S <= a.small_u) b = nb;
+  }
+  for (int i = 0; i <= nb; i++) {  // warp-aggregated append per bin
     const uint32_t mask = __ballot_sync(0xFFFFFFFFu, b == i);
     if (!mask) continue;
     const int lane = threadIdx.x & 31;
@@ -876,10 +881,292 @@ __global__ void bin_lists_kernel(const PruneArgs a, const uint32_t* bounds, int 
 
 cudaError_t launch_bin_lists(const PruneArgs& a, const uint32_t* d_bounds, int nb, uint32_t* d_counts,
                              uint32_t* d_lists, cudaStream_t s) {
-  cudaError_t e = cudaMemsetAsync(d_counts, 0, sizeof(uint32_t) * nb, s);
+  cudaError_t e = cudaMemsetAsync(d_counts, 0, sizeof(uint32_t) * (nb + 1), s);  // + the warp re-prune class
   if (e != cudaSuccess || a.count == 0) return e;
   bin_lists_kernel<<<(a.count + 255) / 256, 256, 0, s>>>(a, d_bounds, nb, d_counts, d_lists, a.count);
   return cudaGetLastError();
+}
+
+// ---- back-edge re-prunes of a row plus a few sources: one warp per list -------
+// apply_back_edges (src/builder_common.cpp:109-140) re-prunes a target t whose
+// merged list (its row ++ new sources) outgrew R. The row's first spre
+// entries are a previous prune's output under the same alpha and rule:
+// sorted by (d(t, .), id) and mutually non-culling (no earlier entry of it
+// culls a later one). With u = m - spre <= kSmallU other entries, the greedy
+// of src/prune.cpp:25-43 only needs the tests that involve those u entries:
+//   * u_k is culled iff a selected entry before it (an S entry, or an earlier
+//     selected u) culls it;
+//   * an S entry is culled iff a selected u before it culls it;
+// and the selection stops at R. So one warp computes d(t, x) for the m rows
+// and d(u_i, s) for the u x spre pairs — every S row gathered once, its norm,
+// its dot products with t and the u rows reduced across the row's lanes — and
+// walks the u entries in key order. No shared memory, no block barrier, no
+// tensor-core tile (the prep kernel's Gram tile was 3.8% tensor-pipe busy on
+// these lists, barrier stalls 24%: profiles/r01e_prune_prep_reprune_c1.txt).
+constexpr int kSmallU = 4;
+
+template <int E>
+__device__ __forceinline__ int dot_chunk(const uint4& a, const uint4& b, int acc) {
+  if (E == kI8) {
+    acc = __dp4a(static_cast<int>(a.x), static_cast<int>(b.x), acc);
+    acc = __dp4a(static_cast<int>(a.y), static_cast<int>(b.y), acc);
+    acc = __dp4a(static_cast<int>(a.z), static_cast<int>(b.z), acc);
+    return __dp4a(static_cast<int>(a.w), static_cast<int>(b.w), acc);
+  }
+  uint32_t u = static_cast<uint32_t>(acc);
+  u = __dp4a(a.x, b.x, u);
+  u = __dp4a(a.y, b.y, u);
+  u = __dp4a(a.z, b.z, u);
+  return static_cast<int>(__dp4a(a.w, b.w, u));
+}
+
+// The exact pair distance from norms and the dot product (integer kinds):
+// |x|^2 + |y|^2 - 2 x.y is the int32 sum the reference accumulates
+// (src/metric.cpp:38-59); IP is -x.y.
+template <int M>
+__device__ __forceinline__ float pair_dist(int nx, int ny, int dot) {
+  if (M == kIP) return -__int2float_rn(dot);
+  return __int2float_rn(nx + ny - 2 * dot);
+}
+
+// cull(i -> j) of src/prune.cpp:36-39 (i selected, j later; di = d(t, i),
+// dj = d(t, j), via = d(i, j)); a zero-distance pick culls nothing (:32).
+__device__ __forceinline__ bool cull_test(int rule, float alpha, float di, float dj, float via) {
+  if (di == 0.0f) return false;
+  return rule == 0 ? __fmul_rn(alpha, via) <= dj : via < __fmul_rn(alpha, di);
+}
+
+template <int E, int M, int LPR, int CPL>
+__global__ void __launch_bounds__(128) reprune_small_kernel(const PruneArgs a) {
+  constexpr int RPP = 32 / LPR;  // rows per warp pass (one per lane group)
+  const int lane = threadIdx.x & 31;
+  const int sub = lane & (LPR - 1), grp = lane / LPR;
+  const uint32_t nch = static_cast<uint32_t>(a.stride >> 4);
+  const uint32_t R = a.R;
+  const float alpha = a.alpha;
+  const uint32_t FULL = 0xFFFFFFFFu;
+  const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t li = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; li < a.count; li += warps) {
+    const uint32_t l = a.list_index ? a.list_index[li] : li;
+    const uint32_t m = a.lengths[l];
+    const uint32_t p = a.points[l];
+    const uint64_t beg = a.begins ? a.begins[l] : uint64_t(l) * a.fixed_stride;
+    const uint32_t S = min(static_cast<uint32_t>(a.spre[p - a.out_base]), m);
+    const uint32_t nu = m - S;  // <= kSmallU (binned by the host), S <= 64
+    // ids: S entries two per lane (index lane, lane + 32); the u entries in every lane
+    const uint32_t s0 = lane < S ? __ldg(a.cand_ids + beg + lane) : kNone;
+    const uint32_t s1 = lane + 32 < S ? __ldg(a.cand_ids + beg + 32 + lane) : kNone;
+    uint32_t uid[kSmallU];
+#pragma unroll
+    for (int i = 0; i < kSmallU; i++) uid[i] = i < static_cast<int>(nu) ? __ldg(a.cand_ids + beg + S + i) : kNone;
+    // the lane's chunks of t's row and of the u rows, their norms and d(t, u_i)
+    uint4 qt[CPL], qu[kSmallU][CPL];
+    bool chv[CPL];
+#pragma unroll
+    for (int c = 0; c < CPL; c++) {
+      const uint32_t ch = sub + c * LPR;
+      chv[c] = ch < nch;
+      qt[c] = chv[c] ? __ldg(reinterpret_cast<const uint4*>(a.data + uint64_t(p) * a.stride) + ch) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int i = 0; i < kSmallU; i++)
+        qu[i][c] = (chv[c] && uid[i] != kNone)
+                       ? __ldg(reinterpret_cast<const uint4*>(a.data + uint64_t(uid[i]) * a.stride) + ch)
+                       : make_uint4(0, 0, 0, 0);
+    }
+    int nt = 0, nuv[kSmallU], dtu[kSmallU], duu[kSmallU][kSmallU];
+#pragma unroll
+    for (int c = 0; c < CPL; c++) nt = dot_chunk<E>(qt[c], qt[c], nt);
+    nt = group_sum<LPR>(nt);
+#pragma unroll
+    for (int i = 0; i < kSmallU; i++) {
+      int n = 0, d = 0;
+#pragma unroll
+      for (int c = 0; c < CPL; c++) {
+        n = dot_chunk<E>(qu[i][c], qu[i][c], n);
+        d = dot_chunk<E>(qt[c], qu[i][c], d);
+      }
+      nuv[i] = group_sum<LPR>(n);
+      dtu[i] = group_sum<LPR>(d);
+#pragma unroll
+      for (int j = 0; j < kSmallU; j++) {
+        int x = 0;
+        if (j > i) {
+#pragma unroll
+          for (int c = 0; c < CPL; c++) x = dot_chunk<E>(qu[i][c], qu[j][c], x);
+          x = group_sum<LPR>(x);
+        }
+        duu[i][j] = x;
+      }
+    }
+    float du_t[kSmallU];  // d(t, u_i)
+#pragma unroll
+    for (int i = 0; i < kSmallU; i++) du_t[i] = pair_dist<M>(nt, nuv[i], dtu[i]);
+    // S rows: lane group g takes rows g, g + RPP, ...; per row the norm and the
+    // dots with t and the u rows, reduced over the group's lanes; lane
+    // (row & 31) keeps the row's values (rows r and r + 32 of the same lane)
+    float dts[2] = {0.0f, 0.0f};              // d(t, s)
+    float dus[2][kSmallU];                     // d(u_i, s)
+#pragma unroll
+    for (int h = 0; h < 2; h++)
+#pragma unroll
+      for (int i = 0; i < kSmallU; i++) dus[h][i] = 0.0f;
+    for (uint32_t r0 = 0; r0 < S; r0 += RPP) {  // (RPP divides 32: a pass never straddles lane 32)
+      const uint32_t r = r0 + grp;
+      const bool have = r < S;
+      const uint32_t id = __shfl_sync(FULL, r0 < 32 ? s0 : s1, r & 31);
+      int ns = 0, dt = 0, du[kSmallU];
+#pragma unroll
+      for (int i = 0; i < kSmallU; i++) du[i] = 0;
+      if (have) {
+#pragma unroll
+        for (int c = 0; c < CPL; c++) {
+          if (!chv[c]) continue;
+          const uint4 x = __ldg(reinterpret_cast<const uint4*>(a.data + uint64_t(id) * a.stride) + sub + c * LPR);
+          ns = dot_chunk<E>(x, x, ns);
+          dt = dot_chunk<E>(qt[c], x, dt);
+#pragma unroll
+          for (int i = 0; i < kSmallU; i++) du[i] = dot_chunk<E>(qu[i][c], x, du[i]);
+        }
+      }
+      ns = group_sum<LPR>(ns);
+      dt = group_sum<LPR>(dt);
+#pragma unroll
+      for (int i = 0; i < kSmallU; i++) du[i] = group_sum<LPR>(du[i]);
+      // lane (row & 31) takes row's sums from the first lane of its group
+      const int g_me = lane - static_cast<int>(r0 & 31u);
+      const bool mine = g_me >= 0 && g_me < RPP && r0 + g_me < S;
+      const int src = mine ? g_me * LPR : 0;
+      const int ns_r = __shfl_sync(FULL, ns, src), dt_r = __shfl_sync(FULL, dt, src);
+      int du_r[kSmallU];
+#pragma unroll
+      for (int i = 0; i < kSmallU; i++) du_r[i] = __shfl_sync(FULL, du[i], src);
+      if (mine) {  // (static indices: the arrays stay in registers)
+        if (r0 >= 32) {
+          dts[1] = pair_dist<M>(nt, ns_r, dt_r);
+#pragma unroll
+          for (int i = 0; i < kSmallU; i++) dus[1][i] = pair_dist<M>(nuv[i], ns_r, du_r[i]);
+        } else {
+          dts[0] = pair_dist<M>(nt, ns_r, dt_r);
+#pragma unroll
+          for (int i = 0; i < kSmallU; i++) dus[0][i] = pair_dist<M>(nuv[i], ns_r, du_r[i]);
+        }
+      }
+    }
+    // keys; S must be ascending (a prune's output): else leave the list to
+    // the general kernel (flagged through too_long; never seen in the tests)
+    const uint64_t ks0 = lane < S ? make_key(dts[0], s0) : kMaxKey;
+    const uint64_t ks1 = lane + 32 < S ? make_key(dts[1], s1) : kMaxKey;
+    uint64_t ku[kSmallU];
+#pragma unroll
+    for (int i = 0; i < kSmallU; i++) ku[i] = uid[i] != kNone && uid[i] != p ? make_key(du_t[i], uid[i]) : kMaxKey;
+    {
+      const uint64_t nx = __shfl_down_sync(FULL, ks0, 1);
+      const uint64_t n32 = __shfl_sync(FULL, ks1, 0);
+      const uint64_t nx1 = __shfl_down_sync(FULL, ks1, 1);
+      const bool bad = (lane + 1 < S && (lane < 31 ? nx : n32) <= ks0) || (lane + 33 < S && nx1 <= ks1);
+      if (__any_sync(FULL, bad)) {
+        if (lane == 0) atomicAdd(a.too_long, 1u);
+        continue;
+      }
+    }
+    // u entries in key order; each one's count of S keys below it
+    int ord[kSmallU];
+    uint32_t below[kSmallU];
+#pragma unroll
+    for (int i = 0; i < kSmallU; i++) {
+      int r = 0;
+#pragma unroll
+      for (int j = 0; j < kSmallU; j++) r += ku[j] < ku[i] ? 1 : 0;
+      ord[i] = r;
+      below[i] = __popc(__ballot_sync(FULL, ks0 < ku[i])) + __popc(__ballot_sync(FULL, ks1 < ku[i]));
+    }
+    // the walk: u entries in key order; S entries culled only by selected u's
+    bool cs0 = lane >= S, cs1 = lane + 32 >= S;  // culled (or absent)
+    bool selu[kSmallU];
+#pragma unroll
+    for (int i = 0; i < kSmallU; i++) selu[i] = false;
+    bool full = false;
+#pragma unroll
+    for (int o = 0; o < kSmallU; o++) {
+#pragma unroll
+      for (int k = 0; k < kSmallU; k++) {  // k: the u entry of rank o (warp-uniform test)
+        if (ord[k] != o || ku[k] == kMaxKey || full) continue;
+        const uint32_t bk = below[k];
+        // selected S entries before it (S index < bk), and whether one culls it
+        const bool e0 = !cs0 && static_cast<uint32_t>(lane) < bk;
+        const bool e1 = !cs1 && static_cast<uint32_t>(lane) + 32 < bk;
+        bool c = (e0 && cull_test(a.rule, alpha, dts[0], du_t[k], dus[0][k])) ||
+                 (e1 && cull_test(a.rule, alpha, dts[1], du_t[k], dus[1][k]));
+        uint32_t before = __popc(__ballot_sync(FULL, e0)) + __popc(__ballot_sync(FULL, e1));
+        c = __any_sync(FULL, c);
+#pragma unroll
+        for (int j = 0; j < kSmallU; j++) {
+          if (j == k || !selu[j] || ord[j] >= o) continue;
+          before++;
+          const int dij = j < k ? duu[j][k] : duu[k][j];
+          c = c || cull_test(a.rule, alpha, du_t[j], du_t[k], pair_dist<M>(nuv[j], nuv[k], dij));
+        }
+        if (before >= R) {
+          full = true;
+          continue;
+        }
+        if (c) continue;
+        selu[k] = true;
+        // it culls the S entries after it
+        if (du_t[k] != 0.0f) {
+          if (!cs0 && static_cast<uint32_t>(lane) >= bk && cull_test(a.rule, alpha, du_t[k], dts[0], dus[0][k]))
+            cs0 = true;
+          if (!cs1 && static_cast<uint32_t>(lane) + 32 >= bk && cull_test(a.rule, alpha, du_t[k], dts[1], dus[1][k]))
+            cs1 = true;
+        }
+      }
+    }
+    // output: selected entries in key order, the first R of them
+    uint32_t* orow = a.out_rows ? a.out_rows + uint64_t(l) * R : a.out_adj + uint64_t(p - a.out_base) * R;
+    const uint32_t b0 = __ballot_sync(FULL, !cs0), b1 = __ballot_sync(FULL, !cs1);
+    const uint32_t lt = (1u << lane) - 1u;
+    uint32_t nsel = __popc(b0) + __popc(b1);
+#pragma unroll
+    for (int i = 0; i < kSmallU; i++) nsel += selu[i] ? 1u : 0u;
+    nsel = min(nsel, R);
+    auto selu_before = [&](uint32_t sidx) {  // selected u entries sorting before S index sidx
+      uint32_t n = 0;
+#pragma unroll
+      for (int i = 0; i < kSmallU; i++) n += (selu[i] && below[i] <= sidx) ? 1u : 0u;
+      return n;
+    };
+    GANN_CHECK(S <= 64 && nu <= kSmallU);
+    if (!cs0) {
+      const uint32_t oi = __popc(b0 & lt) + selu_before(lane);
+      if (oi < R) orow[oi] = s0;
+    }
+    if (!cs1) {
+      const uint32_t oi = __popc(b0) + __popc(b1 & lt) + selu_before(lane + 32);
+      if (oi < R) orow[oi] = s1;
+    }
+    if (lane == 0) {
+      auto lowmask = [](uint32_t k) { return k >= 32 ? 0xFFFFFFFFu : (1u << k) - 1u; };
+#pragma unroll
+      for (int i = 0; i < kSmallU; i++) {
+        if (!selu[i]) continue;
+        uint32_t oi = 0;  // selected S below it + selected u before it
+        oi += __popc(b0 & lowmask(below[i]));
+        oi += below[i] > 32 ? __popc(b1 & lowmask(below[i] - 32)) : 0u;
+#pragma unroll
+        for (int j = 0; j < kSmallU; j++) oi += (selu[j] && ord[j] < ord[i]) ? 1u : 0u;
+        if (oi < R) orow[oi] = uid[i];
+      }
+      if (a.stats) {
+        atomicAdd(a.stats + kStPruneLists, 1ull);
+        atomicAdd(a.stats + kStPruneCands, static_cast<unsigned long long>(m));
+      }
+    }
+    for (uint32_t i = nsel + lane; i < R; i += 32) orow[i] = kNone;
+    if (lane == 0) {
+      if (a.n_out) a.n_out[l] = nsel;
+      if (a.spre && !a.out_rows) a.spre[p - a.out_base] = static_cast<uint8_t>(nsel < 255 ? nsel : 255);
+    }
+  }
 }
 
 // ---- long lists: chunked prune ------------------------------------------------
@@ -1131,6 +1418,37 @@ __global__ void __launch_bounds__(NT) prune_chunked_kernel(const PruneArgs a) {
   }
 }
 
+uint32_t reprune_small_max_u() { return kSmallU; }
+
+namespace {
+template <int E, int M, int LPR, int CPL>
+cudaError_t launch_small_geom(const PruneArgs& a, cudaStream_t s) {
+  if (a.count == 0) return cudaSuccess;
+  const uint32_t blocks = std::min<uint32_t>((a.count + 3) / 4, 148u * 16u);
+  reprune_small_kernel<E, M, LPR, CPL><<<blocks, 128, 0, s>>>(a);
+  return cudaGetLastError();
+}
+template <int E, int M>
+cudaError_t launch_small_e(const PruneArgs& a, const Geometry& g, cudaStream_t s) {
+  switch (g.lpr) {
+    case 1: return launch_small_geom<E, M, 1, 1>(a, s);
+    case 2: return launch_small_geom<E, M, 2, 1>(a, s);
+    case 4: return launch_small_geom<E, M, 4, 1>(a, s);
+    case 8: return launch_small_geom<E, M, 8, 1>(a, s);
+    case 16: return launch_small_geom<E, M, 16, 1>(a, s);
+    default:
+      if (g.cpl == 1) return launch_small_geom<E, M, 32, 1>(a, s);
+      if (g.cpl == 2) return launch_small_geom<E, M, 32, 2>(a, s);
+      return launch_small_geom<E, M, 32, 4>(a, s);
+  }
+}
+}  // namespace
+
+cudaError_t launch_reprune_small(const PruneArgs& a, int elem, int metric, const Geometry& g, cudaStream_t s) {
+  if (metric == kL2) return elem == kU8 ? launch_small_e<kU8, kL2>(a, g, s) : launch_small_e<kI8, kL2>(a, g, s);
+  return elem == kU8 ? launch_small_e<kU8, kIP>(a, g, s) : launch_small_e<kI8, kIP>(a, g, s);
+}
+
 namespace {
 template <int E, int M, int LPR, int CPL>
 cudaError_t launch_nt(const PruneArgs& a, int threads, cudaStream_t s) {
@@ -1293,6 +1611,7 @@ namespace {
 template <int E, int M, int LPR, int CPL>
 void preload_prune_one() {
   touch_kernel(prune_kernel<E, M, LPR, CPL, 32>);
+  if (E != kF32) touch_kernel(reprune_small_kernel<E, M, LPR, CPL>);
   touch_kernel(prune_chunked_kernel<E, M, LPR, CPL, 256>);
   if (E != kF32) {
     touch_kernel(prune_prep_kernel<E, M, 4, 0>);
@@ -1354,5 +1673,7 @@ cudaError_t launch_prune(const PruneArgs& a, int elem, int metric, const Geometr
   if (elem == kI8) return dispatch<kI8, kIP>(a, g, threads, s);
   return dispatch<kF32, kIP>(a, g, threads, s);
 }
+
+GANN_CHECK_READER(check_line_prune)
 
 }  // namespace gann

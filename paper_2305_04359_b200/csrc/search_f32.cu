@@ -16,4 +16,6 @@ void preload_search_f32(int metric, const Geometry& g) {
     preload_geom<kF32, kIP>(g);
 }
 
+GANN_CHECK_READER(check_line_search_f32)
+
 }  // namespace gann

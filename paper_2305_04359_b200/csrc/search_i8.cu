@@ -16,4 +16,6 @@ void preload_search_i8(int metric, const Geometry& g) {
     preload_geom<kI8, kIP>(g);
 }
 
+GANN_CHECK_READER(check_line_search_i8)
+
 }  // namespace gann

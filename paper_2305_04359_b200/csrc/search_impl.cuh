@@ -61,31 +61,6 @@ struct Unroll {
   static constexpr int U = (raw / CPL) < 1 ? 1 : (raw / CPL);
 };
 
-// Sum U per-lane partials over the LPR lanes of a row group so that lane
-// (sub mod U) ends up holding the total of row `sub mod U` (U <= LPR, both
-// powers of two): plain butterflies for the lane bits above U, then a
-// transposed butterfly that halves the live values each step — LPR=U=8 costs
-// 4+2+1 shuffles for 8 rows instead of 3 per row.
-template <int LPR, int U, typename T>
-__device__ __forceinline__ T transpose_reduce(T (&v)[U], int sub) {
-#pragma unroll
-  for (int o = LPR / 2; o >= U; o >>= 1) {
-#pragma unroll
-    for (int u = 0; u < U; u++) v[u] += __shfl_xor_sync(0xFFFFFFFFu, v[u], o);
-  }
-#pragma unroll
-  for (int w = U / 2; w >= 1; w >>= 1) {
-    const bool hi = (sub & w) != 0;
-#pragma unroll
-    for (int i = 0; i < w; i++) {
-      const T send = hi ? v[i] : v[i + w];
-      const T keep = hi ? v[i + w] : v[i];
-      v[i] = keep + __shfl_xor_sync(0xFFFFFFFFu, send, w);
-    }
-  }
-  return v[0];
-}
-
 // Chunk `base` of row `id`: one IMAD.WIDE.U32 (id * stride + the 64-bit
 // per-lane chunk base); the compiler's own lowering of size_t(id) * stride +
 // base took three instructions per row.
@@ -141,6 +116,7 @@ __device__ __forceinline__ void eval_pass(uint32_t b0, const uint32_t* ids, uint
   if (sub < UU && r < m) key = make_key(Op::finish(tot), ids[r]);
   const bool keep = key < worst;
   const uint32_t bal = __ballot_sync(0xFFFFFFFFu, keep);
+  GANN_CHECK(!keep || n_out + __popc(bal & ((1u << lane) - 1u)) < m);
   if (keep) out[n_out + __popc(bal & ((1u << lane) - 1u))] = key;
   n_out += __popc(bal);
 }
@@ -455,10 +431,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_M
           }
         }
         const uint32_t bal = __ballot_sync(FULL, fresh);
+        GANN_CHECK(!fresh || m + __popc(bal & lanemask_lt(lane)) < Rp);
         if (fresh) cid[m + __popc(bal & lanemask_lt(lane))] = nb;
         m += __popc(bal);
       }
       if (m == 0) continue;
+      GANN_CHECK(((m + 31) & ~31u) <= Rp);
       if (m + lane < ((m + 31) & ~31u)) cid[m + lane] = cur;  // pad to a whole pass
       __syncwarp();
       evals += m;
@@ -485,6 +463,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_M
         const uint32_t bal = __ballot_sync(FULL, keep);
         if (keep) {
           const uint32_t o = s + __popc(bal & lanemask_lt(lane));
+          GANN_CHECK(o < Rp && pb <= size);
           ck[o] = k;
           posb[o] = pb;
         }
@@ -507,6 +486,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_M
             r += (p2.x < k ? 1u : 0u) + (p2.y < k ? 1u : 0u);
           }
           if (t < s) r += ck[t] < k ? 1u : 0u;
+          GANN_CHECK(r < s);
           srt[r] = k;
           p0 = min(p0, posb[j]);
           const uint32_t fin = posb[j] + r;
@@ -546,6 +526,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_M
           }
           __syncwarp();  // every read of this chunk's old entries precedes its writes
           if (act) {
+            GANN_CHECK(t < L && (mine ? before < s : t - before < size));
             beam[t] = key;
             fl[t] = f;
           }

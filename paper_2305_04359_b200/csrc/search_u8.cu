@@ -16,4 +16,6 @@ void preload_search_u8(int metric, const Geometry& g) {
     preload_geom<kU8, kIP>(g);
 }
 
+GANN_CHECK_READER(check_line_search_u8)
+
 }  // namespace gann

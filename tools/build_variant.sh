@@ -23,6 +23,6 @@ for f in *.cu; do
   objs="$objs ${f%.cu}.o"
 done
 wait
-nvcc -gencode arch=compute_100a,code=sm_100a -shared $objs -o "$root/paper_2305_04359_b200/$name" -lcudart
+nvcc -gencode arch=compute_100a,code=sm_100a -shared $objs -o "$root/paper_2305_04359_b200/$name" -lcudart -ldl
 rm -rf "$tmp"
 echo "built paper_2305_04359_b200/$name from $rev $*"
