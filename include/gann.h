@@ -212,7 +212,9 @@ int gann_hnsw_search(gann_hnsw* h, const void* queries, uint32_t nq, uint32_t k_
 void gann_hnsw_free(gann_hnsw* h);
 
 /* ---- next-row helpers --------------------------------------
- * Exact top-k by (dist, id): graphann::compute_groundtruth (src/dataset.cpp:172-217). */
+ * Exact top-k by (dist, id): graphann::compute_groundtruth (src/dataset.cpp:172-217).
+ * k <= 64, rows up to 1568 bytes (integer kinds: distances identical to the
+ * reference's; f32: FMA partial sums, within the search's f32 tolerance). */
 int gann_groundtruth(gann_index* idx, const void* queries, uint32_t nq, uint32_t k,
                      uint32_t* ids, float* dists);
 int gann_groundtruth_device(gann_index* idx, const void* d_queries, uint32_t nq, uint32_t k,

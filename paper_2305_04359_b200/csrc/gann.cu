@@ -30,6 +30,8 @@
 #include <set>
 #include <thread>
 #include <tuple>
+#include <unordered_map>
+#include <unordered_set>
 #include <vector>
 
 #include "../../include/gann.h"
@@ -674,7 +676,7 @@ void apply_back(gann_index* idx, const uint32_t* bsrc, uint32_t B, const uint32_
                 const uint32_t* psource, uint64_t npairs, float alpha, int rule, bool timed,
                 uint32_t* out_keys = nullptr, uint32_t* out_vals = nullptr,
                 uint64_t* ngroups_out = nullptr, const uint32_t* key_of_target = nullptr,
-                const uint32_t* pordinal = nullptr, uint32_t pstride = 1) {
+                const uint32_t* pordinal = nullptr, uint32_t pstride = 1, bool explicit_distinct = false) {
   if (npairs == 0) {
     if (ngroups_out) *ngroups_out = 0;
     return;
@@ -694,13 +696,14 @@ void apply_back(gann_index* idx, const uint32_t* bsrc, uint32_t B, const uint32_
   b.ptarget = ptarget;
   b.psource = psource;
   b.npairs = npairs;
-  b.sources_distinct = bsrc != nullptr;
+  b.sources_distinct = bsrc != nullptr || explicit_distinct;
   b.tcount = idx->tcount;
   b.tgroup = idx->tgroup;
   b.counters = idx->counters;
-  b.small_group_cap = kSmallGroupCap;
+  // groups above small_group_cap sources take the hub merge, which assumes
+  // the merged list overflows R: so the cap is at least R (R up to 1024)
+  b.small_group_cap = std::max<uint32_t>(kSmallGroupCap, idx->R);
   b.big_group_cap = kSortedGroupCap;
-  if (idx->R > kSmallGroupCap) fail(GANN_EINVAL, "degree bound above 256 is not supported by the back-edge merge");
   b.prune_small_cap = kPruneSmallCap;
   b.small_dists = !prune_uses_mma(idx->elem, kPruneSmallCap, idx->stride, R) || std::getenv("GANN_NO_MMA");
   b.key_of_target = key_of_target;
@@ -827,12 +830,12 @@ uint32_t choose_start_dev(gann_index* idx) {
 // Brute force over padded query rows — compute_groundtruth (src/dataset.cpp:172-217).
 void run_groundtruth(gann_index* idx, const uint8_t* q, uint32_t nq, uint32_t k, uint32_t* d_ids,
                      float* d_dists, cudaStream_t s) {
-  if (k == 0 || k > 16) fail(GANN_EINVAL, "groundtruth: k must lie in [1, 16]");
+  if (k == 0 || k > 64) fail(GANN_EINVAL, "groundtruth: k must lie in [1, 64]");
   if (k > idx->n) fail(GANN_EINVAL, "groundtruth: k=" + std::to_string(k) + " exceeds n");
-  if (idx->stride > 256) fail(GANN_EINVAL, "groundtruth: rows above 256 bytes are not supported");
+  if (idx->stride > 1568) fail(GANN_EINVAL, "groundtruth: rows above 1568 bytes are not supported");
   if (nq == 0) return;
   const uint32_t splits = groundtruth_splits(idx->n, nq);
-  idx->gt.ensure(size_t(nq) * splits * 16 * 8);
+  idx->gt.ensure(size_t(nq) * splits * (k <= 16 ? 16 : 64) * 8);
   cu(launch_groundtruth(idx->points, idx->stride, idx->n, q, nq, k, idx->elem, idx->metric,
                         static_cast<uint32_t>(idx->stride / 16), idx->gt.as<unsigned long long>(),
                         splits, d_ids, d_dists, s),
@@ -1427,6 +1430,46 @@ int gann_group_by_key(const uint32_t* keys, const uint32_t* vals, uint64_t m, in
       cu(cudaMemcpyAsync(idx->ps.p, vals, m * 4, cudaMemcpyHostToDevice, idx->stream), "upload");
       cu(launch_hash_keys(idx->qids.as<uint32_t>(), m, idx->misc.as<uint32_t>(), tbits,
                           idx->pt.as<uint32_t>(), idx->stream), "hash keys");
+      // a key with more pairs than the counting group-by orders in one block:
+      // a stable radix sort of (slot, input index) instead (semisort.cpp:15-73
+      // keeps input order inside a group; group order is unspecified)
+      uint64_t maxg = 0;
+      {
+        std::unordered_map<uint32_t, uint64_t> cnt;
+        cnt.reserve(m);
+        for (uint64_t i = 0; i < m; i++) maxg = std::max(maxg, ++cnt[keys[i]]);
+      }
+      if (maxg > kSortedGroupCap) {
+        std::vector<uint32_t> iota(m);
+        for (uint64_t i = 0; i < m; i++) iota[i] = static_cast<uint32_t>(i);
+        idx->ok.ensure(m * 4);
+        idx->ov.ensure(m * 4);
+        cu(cudaMemcpyAsync(idx->ps.p, iota.data(), m * 4, cudaMemcpyHostToDevice, idx->stream), "upload");
+        void* tmp = nullptr;
+        size_t tmp_bytes = 0;
+        const cudaError_t e = stable_sort_pairs_u32(idx->pt.as<uint32_t>(), idx->ok.as<uint32_t>(),
+                                                    idx->ps.as<uint32_t>(), idx->ov.as<uint32_t>(), m,
+                                                    static_cast<int>(tbits), &tmp, &tmp_bytes, idx->stream);
+        std::vector<uint32_t> perm(m);
+        if (e == cudaSuccess)
+          cu(cudaMemcpyAsync(perm.data(), idx->ov.p, m * 4, cudaMemcpyDeviceToHost, idx->stream), "download");
+        cudaStreamSynchronize(idx->stream);
+        if (tmp) cudaFree(tmp);
+        cu(e, "stable radix sort");
+        uint64_t g = 0;
+        for (uint64_t j = 0; j < m; j++) {
+          out_keys[j] = keys[perm[j]];
+          out_vals[j] = vals[perm[j]];
+          if (j == 0 || out_keys[j] != out_keys[j - 1]) {
+            if (offsets) offsets[g] = j;
+            g++;
+          }
+        }
+        if (offsets) offsets[g] = m;
+        if (n_groups) *n_groups = g;
+        gann_index_free(idx);
+        return;
+      }
       uint64_t ng = 0;
       apply_back(idx, nullptr, 0, idx->pt.as<uint32_t>(), idx->ps.as<uint32_t>(), m, 1.0f, 0, false,
                  idx->ok.as<uint32_t>(), idx->ov.as<uint32_t>(), &ng, idx->misc.as<uint32_t>());
@@ -1490,12 +1533,39 @@ int gann_apply_back_edges(gann_index* idx, const uint32_t* targets, const uint32
       if (targets[i] >= idx->n || sources[i] >= idx->n) fail(GANN_EINVAL, "pair id out of range");
       if (targets[i] == sources[i]) fail(GANN_EINVAL, "self loop at vertex " + std::to_string(targets[i]));
     }
+    // A repeated (target, source) pair changes nothing after its first
+    // occurrence (builder_common.cpp:124-128, first occurrence wins), so it is
+    // dropped here, keeping the input order: the sources of a target are then
+    // distinct, which is what the group merge needs for groups of any size
+    // (a group too large to sort by ordinal always overflows R and is
+    // re-pruned, where pair order does not matter).
+    std::vector<uint32_t> t2, s2;
+    {
+      std::vector<uint64_t> seen;
+      seen.reserve(m);
+      for (uint64_t i = 0; i < m; i++) seen.push_back((uint64_t(targets[i]) << 32) | sources[i]);
+      std::vector<uint64_t> sorted = seen;
+      std::sort(sorted.begin(), sorted.end());
+      if (std::adjacent_find(sorted.begin(), sorted.end()) != sorted.end()) {
+        std::unordered_set<uint64_t> first;
+        first.reserve(m * 2);
+        for (uint64_t i = 0; i < m; i++)
+          if (first.insert(seen[i]).second) {
+            t2.push_back(targets[i]);
+            s2.push_back(sources[i]);
+          }
+        targets = t2.data();
+        sources = s2.data();
+        m = t2.size();
+      }
+    }
     set_device(idx);
     idx->pt.ensure(m * 4);
     idx->ps.ensure(m * 4);
     cu(cudaMemcpyAsync(idx->pt.p, targets, m * 4, cudaMemcpyHostToDevice, idx->stream), "upload");
     cu(cudaMemcpyAsync(idx->ps.p, sources, m * 4, cudaMemcpyHostToDevice, idx->stream), "upload");
-    apply_back(idx, nullptr, 0, idx->pt.as<uint32_t>(), idx->ps.as<uint32_t>(), m, alpha, rule, false);
+    apply_back(idx, nullptr, 0, idx->pt.as<uint32_t>(), idx->ps.as<uint32_t>(), m, alpha, rule, false, nullptr,
+               nullptr, nullptr, nullptr, nullptr, 1, true);
   });
 }
 

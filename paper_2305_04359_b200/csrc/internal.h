@@ -247,6 +247,9 @@ cudaError_t launch_groundtruth(const uint8_t* data, uint64_t stride, uint64_t n,
                                int metric, uint32_t nch, unsigned long long* partial,
                                uint32_t splits, uint32_t* ids, float* dists, cudaStream_t s);
 uint32_t groundtruth_splits(uint64_t n, uint32_t nq);
+cudaError_t stable_sort_pairs_u32(const uint32_t* keys_in, uint32_t* keys_out, const uint32_t* vals_in,
+                                  uint32_t* vals_out, uint64_t m, int bits, void** tmp, size_t* tmp_bytes,
+                                  cudaStream_t s);
 // Validate rows [0, rows) of an n-vertex graph (row r is vertex row0 + r):
 // *bad = ~0 if fine, else (first bad row << 3) | code (1 id after padding,
 // 2 id out of range, 3 self loop, 4 repeated id).

@@ -1,5 +1,6 @@
 // misc.cu — start vertex, synthetic data generator, brute-force ground truth.
 #include <algorithm>
+#include <cub/device/device_radix_sort.cuh>
 #include <cmath>
 #include <mutex>
 #include <vector>
@@ -144,14 +145,15 @@ __global__ void gen_f32_kernel(float* out, uint64_t n, uint32_t d, uint32_t clus
 // One thread per query (its row in registers), a shared-memory tile of points
 // broadcast to the block; the point range is split across blockIdx.y and the
 // per-split top-16 lists are merged by gt_merge_kernel.
-constexpr int kGtK = 16;
+constexpr int kGtMaxK = 64;  // the largest k (gann_groundtruth)
 constexpr int kGtThreads = 128;
 constexpr int kGtTile = 128;
 
-template <int E, int M, int NCH>
+template <int E, int M, int NCH, int K>
 __global__ void __launch_bounds__(kGtThreads)
     gt_kernel(const uint8_t* data, uint64_t stride, uint64_t n, const uint8_t* queries,
               uint32_t nq, uint32_t nch, uint32_t splits, unsigned long long* partial) {
+  constexpr int kGtK = K;
   using Op = DistOp<E, M>;
   extern __shared__ __align__(16) uint4 tile[];
   const uint32_t q = blockIdx.x * kGtThreads + threadIdx.x;
@@ -199,8 +201,54 @@ __global__ void __launch_bounds__(kGtThreads)
   }
 }
 
+// Rows above 256 bytes: the block's 128 query rows live in shared memory
+// (thread = query, as above), the point tile beside them.
+template <int E, int M, int K>
+__global__ void __launch_bounds__(kGtThreads)
+    gt_wide_kernel(const uint8_t* data, uint64_t stride, uint64_t n, const uint8_t* queries, uint32_t nq,
+                   uint32_t nch, uint32_t splits, uint32_t tile_pts, unsigned long long* partial) {
+  using Op = DistOp<E, M>;
+  extern __shared__ __align__(16) uint4 sm[];
+  uint4* qs = sm;                           // kGtThreads rows of nch chunks
+  uint4* tile = sm + size_t(kGtThreads) * nch;  // tile_pts rows
+  const uint32_t q = blockIdx.x * kGtThreads + threadIdx.x;
+  const uint64_t lo = n * blockIdx.y / splits, hi = n * (blockIdx.y + 1) / splits;
+  for (uint32_t t = threadIdx.x; t < kGtThreads * nch; t += kGtThreads) {
+    const uint32_t qq = blockIdx.x * kGtThreads + t / nch, c = t % nch;
+    qs[t] = qq < nq ? __ldg(reinterpret_cast<const uint4*>(queries + uint64_t(qq) * stride) + c) : make_uint4(0, 0, 0, 0);
+  }
+  uint64_t top[K];
+  for (int i = 0; i < K; i++) top[i] = kMaxKey;
+  const uint4* my = qs + size_t(threadIdx.x) * nch;
+  for (uint64_t p0 = lo; p0 < hi; p0 += tile_pts) {
+    const uint32_t cnt = static_cast<uint32_t>((hi - p0) < tile_pts ? (hi - p0) : uint64_t(tile_pts));
+    __syncthreads();
+    for (uint32_t t = threadIdx.x; t < cnt * nch; t += kGtThreads) {
+      const uint32_t pp = t / nch, c = t - pp * nch;
+      tile[t] = __ldg(reinterpret_cast<const uint4*>(data + (p0 + pp) * stride) + c);
+    }
+    __syncthreads();
+    for (uint32_t pp = 0; pp < cnt; pp++) {
+      typename Op::acc_t acc = Op::zero();
+      for (uint32_t c = 0; c < nch; c++) acc = Op::chunk(my[c], tile[pp * nch + c], acc);
+      const uint64_t key = make_key(Op::finish(acc), static_cast<uint32_t>(p0 + pp));
+      if (key < top[K - 1]) {
+        int i = K - 1;
+        for (; i > 0 && top[i - 1] > key; i--) top[i] = top[i - 1];
+        top[i] = key;
+      }
+    }
+  }
+  if (q < nq) {
+    unsigned long long* out = partial + (uint64_t(q) * splits + blockIdx.y) * K;
+    for (int i = 0; i < K; i++) out[i] = top[i];
+  }
+}
+
+template <int K>
 __global__ void gt_merge_kernel(const unsigned long long* partial, uint32_t nq, uint32_t splits,
                                 uint32_t k, uint32_t* ids, float* dists) {
+  constexpr int kGtK = K;
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= nq) return;
   uint64_t top[kGtK];
@@ -230,12 +278,12 @@ __global__ void gt_merge_kernel(const unsigned long long* partial, uint32_t nq, 
   }
 }
 
-template <int E, int M, int NCH>
+template <int E, int M, int NCH, int K>
 cudaError_t gt_launch(const uint8_t* data, uint64_t stride, uint64_t n, const uint8_t* queries,
                       uint32_t nq, uint32_t nch, uint32_t splits, unsigned long long* partial,
                       cudaStream_t s) {
   const size_t smem = size_t(kGtTile) * NCH * 16;
-  auto k = gt_kernel<E, M, NCH>;
+  auto k = gt_kernel<E, M, NCH, K>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
   dim3 grid((nq + kGtThreads - 1) / kGtThreads, splits);
@@ -243,15 +291,31 @@ cudaError_t gt_launch(const uint8_t* data, uint64_t stride, uint64_t n, const ui
   return cudaGetLastError();
 }
 
+template <int E, int M, int K>
+cudaError_t gt_dispatch_k(const uint8_t* data, uint64_t stride, uint64_t n, const uint8_t* queries,
+                          uint32_t nq, uint32_t nch, uint32_t splits, unsigned long long* partial,
+                          cudaStream_t s) {
+  if (nch <= 1) return gt_launch<E, M, 1, K>(data, stride, n, queries, nq, nch, splits, partial, s);
+  if (nch <= 2) return gt_launch<E, M, 2, K>(data, stride, n, queries, nq, nch, splits, partial, s);
+  if (nch <= 4) return gt_launch<E, M, 4, K>(data, stride, n, queries, nq, nch, splits, partial, s);
+  if (nch <= 8) return gt_launch<E, M, 8, K>(data, stride, n, queries, nq, nch, splits, partial, s);
+  if (nch <= 16) return gt_launch<E, M, 16, K>(data, stride, n, queries, nq, nch, splits, partial, s);
+  // wide rows: query rows in shared memory, a point tile beside them
+  const uint32_t tile_pts = 16;
+  const size_t smem = (size_t(kGtThreads) + tile_pts) * nch * 16;  // <= 227 KB for rows up to 1568 B
+  auto kw = gt_wide_kernel<E, M, K>;
+  cudaError_t e = cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return e;
+  dim3 grid((nq + kGtThreads - 1) / kGtThreads, splits);
+  kw<<<grid, kGtThreads, smem, s>>>(data, stride, n, queries, nq, nch, splits, tile_pts, partial);
+  return cudaGetLastError();
+}
 template <int E, int M>
 cudaError_t gt_dispatch(const uint8_t* data, uint64_t stride, uint64_t n, const uint8_t* queries,
-                        uint32_t nq, uint32_t nch, uint32_t splits, unsigned long long* partial,
+                        uint32_t nq, uint32_t nch, uint32_t k, uint32_t splits, unsigned long long* partial,
                         cudaStream_t s) {
-  if (nch <= 1) return gt_launch<E, M, 1>(data, stride, n, queries, nq, nch, splits, partial, s);
-  if (nch <= 2) return gt_launch<E, M, 2>(data, stride, n, queries, nq, nch, splits, partial, s);
-  if (nch <= 4) return gt_launch<E, M, 4>(data, stride, n, queries, nq, nch, splits, partial, s);
-  if (nch <= 8) return gt_launch<E, M, 8>(data, stride, n, queries, nq, nch, splits, partial, s);
-  return gt_launch<E, M, 16>(data, stride, n, queries, nq, nch, splits, partial, s);
+  return k <= 16 ? gt_dispatch_k<E, M, 16>(data, stride, n, queries, nq, nch, splits, partial, s)
+                 : gt_dispatch_k<E, M, kGtMaxK>(data, stride, n, queries, nq, nch, splits, partial, s);
 }
 
 }  // namespace
@@ -390,7 +454,7 @@ cudaError_t launch_groundtruth(const uint8_t* data, uint64_t stride, uint64_t n,
                                uint32_t splits, uint32_t* ids, float* dists, cudaStream_t s) {
   if (nq == 0) return cudaSuccess;
   cudaError_t e;
-#define GANN_GT(E, M) e = gt_dispatch<E, M>(data, stride, n, queries, nq, nch, splits, partial, s)
+#define GANN_GT(E, M) e = gt_dispatch<E, M>(data, stride, n, queries, nq, nch, k, splits, partial, s)
   if (metric == kL2) {
     if (elem == kU8) GANN_GT(kU8, kL2); else if (elem == kI8) GANN_GT(kI8, kL2); else GANN_GT(kF32, kL2);
   } else {
@@ -398,7 +462,10 @@ cudaError_t launch_groundtruth(const uint8_t* data, uint64_t stride, uint64_t n,
   }
 #undef GANN_GT
   if (e != cudaSuccess) return e;
-  gt_merge_kernel<<<(nq + 127) / 128, 128, 0, s>>>(partial, nq, splits, k, ids, dists);
+  if (k <= 16)
+    gt_merge_kernel<16><<<(nq + 127) / 128, 128, 0, s>>>(partial, nq, splits, k, ids, dists);
+  else
+    gt_merge_kernel<kGtMaxK><<<(nq + 127) / 128, 128, 0, s>>>(partial, nq, splits, k, ids, dists);
   return cudaGetLastError();
 }
 
@@ -451,6 +518,27 @@ cudaError_t launch_validate_rows(const uint32_t* adj, uint64_t rows, uint32_t R,
   const uint64_t blocks = std::min<uint64_t>((rows + 7) / 8, 148ull * 16);
   validate_rows_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(adj, rows, R, n, row0, bad);
   return cudaGetLastError();
+}
+
+// Stable LSD radix sort of (key, value) u32 pairs over the low `bits` key
+// bits (CUB): the semisort for groups too large for the counting group-by's
+// in-block ordinal sort. `tmp` is grown as needed (caller-owned).
+cudaError_t stable_sort_pairs_u32(const uint32_t* keys_in, uint32_t* keys_out, const uint32_t* vals_in,
+                                  uint32_t* vals_out, uint64_t m, int bits, void** tmp, size_t* tmp_bytes,
+                                  cudaStream_t s) {
+  size_t need = 0;
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, need, keys_in, keys_out, vals_in, vals_out,
+                                                  static_cast<int64_t>(m), 0, bits, s);
+  if (e != cudaSuccess) return e;
+  if (need > *tmp_bytes) {
+    if (*tmp) cudaFree(*tmp);
+    *tmp = nullptr;
+    *tmp_bytes = 0;
+    if ((e = cudaMalloc(tmp, need)) != cudaSuccess) return e;
+    *tmp_bytes = need;
+  }
+  return cub::DeviceRadixSort::SortPairs(*tmp, need, keys_in, keys_out, vals_in, vals_out, static_cast<int64_t>(m), 0,
+                                         bits, s);
 }
 
 GANN_CHECK_READER(check_line_misc)

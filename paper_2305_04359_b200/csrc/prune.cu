@@ -1010,36 +1010,49 @@ __global__ void __launch_bounds__(128) reprune_small_kernel(const PruneArgs a) {
     for (int h = 0; h < 2; h++)
 #pragma unroll
       for (int i = 0; i < kSmallU; i++) dus[h][i] = 0.0f;
-    for (uint32_t r0 = 0; r0 < S; r0 += RPP) {  // (RPP divides 32: a pass never straddles lane 32)
-      const uint32_t r = r0 + grp;
-      const bool have = r < S;
-      const uint32_t id = __shfl_sync(FULL, r0 < 32 ? s0 : s1, r & 31);
-      int ns = 0, dt = 0, du[kSmallU];
+    // UU rows per lane group in flight; the sums reduced with the transposed
+    // butterfly (lane sub of group g ends with row g*UU + (sub mod UU))
+    constexpr int UU = LPR >= 4 ? 4 : LPR;
+    constexpr int PASS = RPP * UU;  // rows per warp pass (divides 32 for LPR >= 4)
+    for (uint32_t r0 = 0; r0 < S; r0 += PASS) {
+      uint4 x[UU][CPL];
 #pragma unroll
-      for (int i = 0; i < kSmallU; i++) du[i] = 0;
-      if (have) {
+      for (int u = 0; u < UU; u++) {
+        const uint32_t r = r0 + grp * UU + u;
+        const uint32_t id = __shfl_sync(FULL, r0 < 32 ? s0 : s1, r & 31);
+#pragma unroll
+        for (int c = 0; c < CPL; c++)
+          x[u][c] = (r < S && chv[c]) ? __ldg(reinterpret_cast<const uint4*>(a.data + uint64_t(id) * a.stride) + sub + c * LPR)
+                                      : make_uint4(0, 0, 0, 0);
+      }
+      int ns[UU], dt[UU], du[kSmallU][UU];
+#pragma unroll
+      for (int u = 0; u < UU; u++) {
+        ns[u] = 0;
+        dt[u] = 0;
+#pragma unroll
+        for (int i = 0; i < kSmallU; i++) du[i][u] = 0;
 #pragma unroll
         for (int c = 0; c < CPL; c++) {
-          if (!chv[c]) continue;
-          const uint4 x = __ldg(reinterpret_cast<const uint4*>(a.data + uint64_t(id) * a.stride) + sub + c * LPR);
-          ns = dot_chunk<E>(x, x, ns);
-          dt = dot_chunk<E>(qt[c], x, dt);
+          ns[u] = dot_chunk<E>(x[u][c], x[u][c], ns[u]);
+          dt[u] = dot_chunk<E>(qt[c], x[u][c], dt[u]);
 #pragma unroll
-          for (int i = 0; i < kSmallU; i++) du[i] = dot_chunk<E>(qu[i][c], x, du[i]);
+          for (int i = 0; i < kSmallU; i++) du[i][u] = dot_chunk<E>(qu[i][c], x[u][c], du[i][u]);
         }
       }
-      ns = group_sum<LPR>(ns);
-      dt = group_sum<LPR>(dt);
+      const int ns_g = transpose_reduce<LPR, UU>(ns, sub);
+      const int dt_g = transpose_reduce<LPR, UU>(dt, sub);
+      int du_g[kSmallU];
 #pragma unroll
-      for (int i = 0; i < kSmallU; i++) du[i] = group_sum<LPR>(du[i]);
-      // lane (row & 31) takes row's sums from the first lane of its group
-      const int g_me = lane - static_cast<int>(r0 & 31u);
-      const bool mine = g_me >= 0 && g_me < RPP && r0 + g_me < S;
-      const int src = mine ? g_me * LPR : 0;
-      const int ns_r = __shfl_sync(FULL, ns, src), dt_r = __shfl_sync(FULL, dt, src);
+      for (int i = 0; i < kSmallU; i++) du_g[i] = transpose_reduce<LPR, UU>(du[i], sub);
+      // lane (row & 31) takes its row's sums (row r0 + g*UU + u sits in lane g*LPR + u)
+      const int j = lane - static_cast<int>(r0 & 31u);
+      const bool mine = j >= 0 && j < PASS && r0 + j < S;
+      const int src = mine ? (j / UU) * LPR + (j % UU) : 0;
+      const int ns_r = __shfl_sync(FULL, ns_g, src), dt_r = __shfl_sync(FULL, dt_g, src);
       int du_r[kSmallU];
 #pragma unroll
-      for (int i = 0; i < kSmallU; i++) du_r[i] = __shfl_sync(FULL, du[i], src);
+      for (int i = 0; i < kSmallU; i++) du_r[i] = __shfl_sync(FULL, du_g[i], src);
       if (mine) {  // (static indices: the arrays stay in registers)
         if (r0 >= 32) {
           dts[1] = pair_dist<M>(nt, ns_r, dt_r);

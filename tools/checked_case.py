@@ -47,7 +47,9 @@ def small():
     dl = [((data[i].astype(np.int64) - data[0]) ** 2).sum(1).astype(np.float32) for i in ids]
     OUT["small_prune"] = sha(np.concatenate(idx.alpha_prune_many([0, 0], ids, dl, g.PruneParams(24, 1.2))))
     keys = rng.integers(0, 50, 5000).astype(np.uint32)
-    OUT["small_groups"] = sha(g.group_by_key(keys, np.arange(5000, dtype=np.uint32)).vals)
+    gp = g.group_by_key(keys, np.arange(5000, dtype=np.uint32))
+    order = np.argsort(gp.keys, kind="stable")  # group order is unspecified: canonical by key
+    OUT["small_groups"] = sha(np.stack([gp.keys[order], gp.vals[order]]))
     # f32 rows: the warp prune and CUDA-core distances
     f = rng.normal(0, 1, (1500, 24)).astype(np.float32)
     fi = g.build_diskann(f, "l2", g.DiskannParams(16, 32, 1.2))
