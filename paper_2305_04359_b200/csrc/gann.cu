@@ -204,6 +204,9 @@ struct gann_index {
   uint32_t bL = 0, brule = 0;
   float balpha = 0.0f;
   DevBuf pair_out, pair_cnt, lids, pair_in;
+  DevBuf gtab, gtab_busy;  // second-level visited tables of large-beam searches (search_impl.cuh)
+  uint32_t gtab_regions = 0;
+  std::mutex gtab_mu;
   PruneHandoff hand;  // the tensor-core prune's hand-off region (this index only)
   std::atomic<uint32_t> max_beam{0};  // search_max_beam, computed once
 };
@@ -411,6 +414,28 @@ SearchArgs base_search_args(gann_index* idx, uint32_t L, uint32_t k_gate, uint32
   // streams may run concurrently (up to kQueryCounters in flight)
   a.next_query = idx->qctr + (idx->qslot.fetch_add(1) % kQueryCounters);
   a.stats = idx->stats;
+  // beams from GANN_GTAB_MIN_L (default 0 = never) also use the
+  // second-level visited table: one 32 KB region per resident warp, twice
+  // the device's warp slots so concurrent launches find free regions
+  const uint32_t gmin = env_u32("GANN_GTAB_MIN_L", 0);  // read per call (A/B runs flip it)
+  if (mode == GANN_VISITED_FAST && gmin && L >= gmin && idx->n <= (uint64_t(1) << 27)) {
+    std::lock_guard<std::mutex> lk(idx->gtab_mu);
+    if (!idx->gtab_regions) {
+      int sms = 148, warps = 64;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, idx->device);
+      cudaDeviceGetAttribute(&warps, cudaDevAttrMaxThreadsPerMultiProcessor, idx->device);
+      const uint32_t regions = 2u * static_cast<uint32_t>(sms) * static_cast<uint32_t>(warps / 32);
+      idx->gtab.ensure(size_t(regions) << (kGtabLog2 + 3));
+      idx->gtab_busy.ensure(size_t((regions + 31) / 32) * 4);
+      cu(cudaMemsetAsync(idx->gtab_busy.p, 0, size_t((regions + 31) / 32) * 4, idx->stream), "memset");
+      cu(cudaStreamSynchronize(idx->stream), "sync");
+      idx->gtab_regions = regions;
+    }
+    a.gtab = idx->gtab.as<uint64_t>();
+    a.gtab_busy = idx->gtab_busy.as<uint32_t>();
+    a.gtab_regions = idx->gtab_regions;
+    a.gtab_log2 = kGtabLog2;
+  }
   return a;
 }
 
@@ -898,7 +923,8 @@ void gann_index_free(gann_index* idx) {
   for (void* p : idx->ipc_open)
     if (p) cudaIpcCloseMemHandle(p);
   if (idx->d_parts) cudaFree(idx->d_parts);
-  for (DevBuf* b : {&idx->pair_out, &idx->pair_cnt, &idx->lids, &idx->pair_in}) b->release();
+  for (DevBuf* b : {&idx->pair_out, &idx->pair_cnt, &idx->lids, &idx->pair_in, &idx->gtab, &idx->gtab_busy})
+    b->release();
   for (void* p : {static_cast<void*>(idx->points), static_cast<void*>(idx->adj),
                   static_cast<void*>(idx->tcount), static_cast<void*>(idx->tgroup),
                   static_cast<void*>(idx->stats), static_cast<void*>(idx->counters),

@@ -84,7 +84,16 @@ struct SearchArgs {
   uint32_t* overflow;        // count of searches whose |V| exceeded vcap
   uint32_t* next_query;      // persistent warps: dynamic query counter (zeroed per launch)
   unsigned long long* stats; // kStCount counters (nullable)
+  // second-level visited tables (fast mode, large beams; nullable): regions of
+  // 2^gtab_log2 u64 buckets (4 u16 remainders each) in global memory, mostly
+  // L2-resident; a warp claims a free region through the gtab_busy bitmap
+  // (gtab_regions bits) and searches without one if none is free
+  uint64_t* gtab;
+  uint32_t* gtab_busy;
+  uint32_t gtab_regions;
+  uint32_t gtab_log2;
 };
+constexpr uint32_t kGtabLog2 = 12;  // 4096 buckets x 4 slots = 16k ids, 32 KB a region
 size_t search_smem_per_warp(uint32_t L, uint32_t R, uint32_t hash_log2, bool hash16);
 constexpr int kSearchWarpsPerBlock = 4;  // one query per warp
 size_t search_smem_min_block(uint32_t L, uint32_t R, uint32_t hash_log2, bool hash16);

@@ -52,6 +52,9 @@ constexpr int kWarpsPerBlock = kSearchWarpsPerBlock;
 
 // Rows in flight per lane group per pass: U <= LPR so the transposed
 // reduction can hand every lane of the group (at most) one finished row.
+#ifndef GANN_SEARCH_RB
+#define GANN_SEARCH_RB 4  // beam chunks rebuilt per batch after a merge (see the loop)
+#endif
 #ifndef GANN_SEARCH_U
 #define GANN_SEARCH_U 8  // rows in flight per lane group (registers: U * CPL * 4)
 #endif
@@ -205,12 +208,48 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_M
   uint8_t* fl = reinterpret_cast<uint8_t*>(bm + Lp / 32);
   const uint32_t FULL = 0xFFFFFFFFu;
 
+  // Second-level visited table (large beams, fast mode): the ids the shared
+  // table has forgotten are looked up in a 16k-slot table of this warp's own
+  // region in global memory before their rows are gathered again (c1, L = 832:
+  // 40.8k evaluations per query with the 1024-slot shared table against 9.1k
+  // distinct ids). Exact-positive like the shared table (u16 remainders of a
+  // bijective hash, n <= 2^27), so results do not depend on it.
+  uint64_t* g2 = nullptr;
+  uint32_t g2_region = kNone;
+  if (F16 && a.gtab && a.n <= (1u << 27)) {
+    if (lane == 0) {
+      const uint32_t words = (a.gtab_regions + 31) / 32;
+      uint32_t w0 = (blockIdx.x * 32 + (threadIdx.x >> 5)) % words;
+      for (uint32_t t = 0; t < words && g2_region == kNone; t++) {
+        const uint32_t w = (w0 + t) % words;
+        uint32_t cur = a.gtab_busy[w];
+        while (cur != 0xFFFFFFFFu) {
+          const int b = __ffs(~cur) - 1;
+          if (w * 32 + b >= a.gtab_regions) break;
+          const uint32_t old = atomicOr(a.gtab_busy + w, 1u << b);
+          if (!(old & (1u << b))) {
+            g2_region = w * 32 + b;
+            break;
+          }
+          cur = old | (1u << b);
+        }
+      }
+    }
+    g2_region = __shfl_sync(FULL, g2_region, 0);
+    if (g2_region != kNone) g2 = a.gtab + (static_cast<uint64_t>(g2_region) << a.gtab_log2);
+  }
+  const uint32_t g2mask = (1u << (a.gtab_log2 + 15)) - 1u;
+
   // Persistent warps: a resident grid pulls queries from a global counter, so
   // slow queries do not leave whole CTAs idle at the end of a wave.
   uint32_t q = 0;
   if (lane == 0) q = atomicAdd(a.next_query, 1u);
   q = __shfl_sync(0xFFFFFFFFu, q, 0);
   for (; q < a.nq;) {
+    if (g2) {  // an empty table for this query (0xFFFF: no remainder)
+      for (uint32_t i = lane; i < (1u << a.gtab_log2) / 2; i += 32)
+        reinterpret_cast<uint4*>(g2)[i] = make_uint4(kNone, kNone, kNone, kNone);
+    }
     const uint8_t* qp = a.query_rows ? a.data + static_cast<uint64_t>(a.query_rows[q]) * a.stride
                                      : a.queries + static_cast<uint64_t>(q) * a.stride;
     const int sub = lane & (LPR - 1);
@@ -430,6 +469,17 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_M
             evict += old != kNone ? 1u : 0u;
           }
         }
+        if (F16 && g2 && __any_sync(FULL, fresh)) {
+          // not in the shared table: the second level decides (and learns it)
+          const uint32_t h = (nb * 0x85EBCA6Bu) & g2mask;
+          const uint32_t bucket = h >> 15, rem = h & 0x7FFFu;
+          const uint64_t w = fresh ? __ldcg(g2 + bucket) : 0ull;
+          const uint32_t rr = rem | (rem << 16);
+          if (fresh && (__vcmpeq2(static_cast<uint32_t>(w), rr) | __vcmpeq2(static_cast<uint32_t>(w >> 32), rr)))
+            fresh = false;
+          else if (fresh)
+            __stcg(g2 + bucket, (w << 16) | rem);
+        }
         const uint32_t bal = __ballot_sync(FULL, fresh);
         GANN_CHECK(!fresh || m + __popc(bal & lanemask_lt(lane)) < Rp);
         if (fresh) cid[m + __popc(bal & lanemask_lt(lane))] = nb;
@@ -506,33 +556,54 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_M
       // position t holds survivor #before(t) if its bit is set, else the old
       // entry t - before(t); sources never lie above t, so descending chunks
       // read only entries not yet overwritten
+      //
+      // GANN_SEARCH_RB chunks at a time: their sources are all read (independent
+      // loads in flight together) before any of them is written — sources lie
+      // at or below their target, so a batch only reads entries of its own
+      // chunks or lower ones, none written yet. One chunk at a time made the
+      // rebuild a chain of dependent shared-memory round trips, O(L / 32) per
+      // expansion, which dominated large beams.
       {
+        constexpr int RB = GANN_SEARCH_RB;
         const uint32_t nsz = min(L, size + s);
+        const int c_lo = static_cast<int>(p0 >> 5);
         uint32_t running = kept;
-        for (int c = static_cast<int>((nsz - 1) >> 5); c >= static_cast<int>(p0 >> 5); c--) {
-          const uint32_t w = bm[c];
-          running -= __popc(w);
-          const uint32_t t = static_cast<uint32_t>(c) * 32 + lane;
-          const uint32_t before = running + __popc(w & lanemask_lt(lane));
-          const bool act = t >= p0 && t < nsz;
-          // one load from either source (no divergent branch)
-          const bool mine = (w >> lane) & 1u;
-          const uint64_t* src = mine ? srt + before : beam + (t - before);
-          uint64_t key = 0;
-          uint8_t f = 0;
-          if (act) {
-            key = *src;
-            f = mine ? 0 : fl[t - before];
+        for (int cb = static_cast<int>((nsz - 1) >> 5); cb >= c_lo; cb -= RB) {
+          uint64_t key[RB];
+          uint8_t f[RB];
+          bool act[RB];
+#pragma unroll
+          for (int j = 0; j < RB; j++) {
+            const int c = cb - j;
+            const uint32_t w = c >= c_lo ? bm[c] : 0u;
+            running -= __popc(w);
+            const uint32_t t = static_cast<uint32_t>(c) * 32 + lane;
+            const uint32_t before = running + __popc(w & lanemask_lt(lane));
+            act[j] = c >= c_lo && t >= p0 && t < nsz;
+            // one load from either source (no divergent branch)
+            const bool mine = (w >> lane) & 1u;
+            const uint64_t* src = mine ? srt + before : beam + (t - before);
+            key[j] = 0;
+            f[j] = 0;
+            if (act[j]) {
+              GANN_CHECK(t < L && (mine ? before < s : t - before < size));
+              key[j] = *src;
+              f[j] = mine ? 0 : fl[t - before];
+            }
           }
-          __syncwarp();  // every read of this chunk's old entries precedes its writes
-          if (act) {
-            GANN_CHECK(t < L && (mine ? before < s : t - before < size));
-            beam[t] = key;
-            fl[t] = f;
+          __syncwarp();  // every read of these chunks' old entries precedes their writes
+#pragma unroll
+          for (int j = 0; j < RB; j++) {
+            const int c = cb - j;
+            const uint32_t t = static_cast<uint32_t>(c) * 32 + lane;
+            if (act[j]) {
+              beam[t] = key[j];
+              fl[t] = f[j];
+            }
+            if (lane == 0 && c >= c_lo) bm[c] = 0;
           }
-          if (lane == 0) bm[c] = 0;
-          // no second sync: the next (lower) chunk reads only positions below
-          // this chunk, none written yet
+          // no second sync: the next (lower) batch reads only positions below
+          // these chunks, none written yet
         }
       }
       size = min(L, size + s);
@@ -576,6 +647,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_M
     if (lane == 0) q = atomicAdd(a.next_query, 1u);
     q = __shfl_sync(0xFFFFFFFFu, q, 0);
   }
+  if (g2 && lane == 0) atomicAnd(a.gtab_busy + g2_region / 32, ~(1u << (g2_region % 32)));
 }
 
 namespace {
