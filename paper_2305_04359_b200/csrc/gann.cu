@@ -414,10 +414,10 @@ SearchArgs base_search_args(gann_index* idx, uint32_t L, uint32_t k_gate, uint32
   // streams may run concurrently (up to kQueryCounters in flight)
   a.next_query = idx->qctr + (idx->qslot.fetch_add(1) % kQueryCounters);
   a.stats = idx->stats;
-  // beams from GANN_GTAB_MIN_L (default 0 = never) also use the
+  // beams from GANN_GTAB_MIN_L (default 768; 0 = never) also use the
   // second-level visited table: one 32 KB region per resident warp, twice
   // the device's warp slots so concurrent launches find free regions
-  const uint32_t gmin = env_u32("GANN_GTAB_MIN_L", 0);  // read per call (A/B runs flip it)
+  const uint32_t gmin = env_u32("GANN_GTAB_MIN_L", 768);  // read per call (A/B runs flip it)
   if (mode == GANN_VISITED_FAST && gmin && L >= gmin && idx->n <= (uint64_t(1) << 27)) {
     std::lock_guard<std::mutex> lk(idx->gtab_mu);
     if (!idx->gtab_regions) {
