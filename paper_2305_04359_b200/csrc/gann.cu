@@ -384,6 +384,7 @@ void validate_search(const gann_index* idx, uint32_t k_out, uint32_t L, uint32_t
   if (mode != GANN_VISITED_FAST && mode != GANN_VISITED_REF && mode != GANN_VISITED_EXACT)
     fail(GANN_EINVAL, "unknown visited mode");
   if (idx->n > 0 && idx->start >= idx->n) fail(GANN_EINVAL, "start vertex out of range");
+  if (idx->n > 0x7FFFFFFFull) fail(GANN_EINVAL, "search holds ids in 31 bits: n must be below 2^31");
   if (L > 32) {
     const uint32_t mx = search_max_beam(idx);
     if (L > mx)
@@ -960,6 +961,7 @@ int gann_build(gann_index* idx, uint32_t L, float alpha, int rule, uint64_t seed
     // src/diskann.cpp:33-42
     if (idx->n == 0) fail(GANN_EINVAL, "cannot build over an empty dataset");
     if (L == 0 || idx->R == 0) fail(GANN_EINVAL, "build beam and degree bound must be positive");
+    if (idx->n > 0x7FFFFFFFull) fail(GANN_EINVAL, "search holds ids in 31 bits: n must be below 2^31");
     if (L > 32 && L > search_max_beam(idx))
       fail(GANN_EINVAL, "build beam " + std::to_string(L) + " exceeds the on-chip beam limit " +
                             std::to_string(search_max_beam(idx)));

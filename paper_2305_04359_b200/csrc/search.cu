@@ -33,11 +33,11 @@
 
 namespace gann {
 
-// Per-warp shared memory: beam keys + flags (single buffer, merged in place),
+// Per-warp shared memory: beam keys (expanded flag in bit 0, merged in place),
 // candidate scratch, and the direct-mapped visited table.
 size_t search_smem_per_warp(uint32_t L, uint32_t R, uint32_t hash_log2, bool hash16) {
   const size_t Lp = (L + 31) & ~31u, Rp = (R + 31) & ~31u;
-  size_t b = Lp * 8 + 2 * Rp * 8 + Rp * 4 + (size_t(1) << hash_log2) * (hash16 ? 2 : 4) + Lp / 8 + Lp;
+  size_t b = Lp * 8 + 2 * Rp * 8 + Rp * 4 + (size_t(1) << hash_log2) * (hash16 ? 2 : 4) + Lp / 8;
   return (b + 15) & ~size_t(15);
 }
 

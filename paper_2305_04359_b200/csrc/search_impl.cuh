@@ -64,6 +64,16 @@ struct Unroll {
   static constexpr int U = (raw / CPL) < 1 ? 1 : (raw / CPL);
 };
 
+// Beam keys: (order-preserving f32 dist) << 32 | id << 1 | expanded. The flag
+// is the least significant bit, so key order is still (dist, id) order
+// (neighbor_less) and a u64 compare needs no mask; ids are below 2^31 (the
+// host checks n). The flag bit replaced a byte array of L flags per warp:
+// less shared memory per query and no flag copy in the tail rebuild.
+__device__ __forceinline__ uint64_t make_bkey(float d, uint32_t id) {
+  return (static_cast<uint64_t>(f2ord(d)) << 32) | (static_cast<uint64_t>(id) << 1);
+}
+__device__ __forceinline__ uint32_t bkey_id(uint64_t k) { return static_cast<uint32_t>(k) >> 1; }
+
 // Chunk `base` of row `id`: one IMAD.WIDE.U32 (id * stride + the 64-bit
 // per-lane chunk base); the compiler's own lowering of size_t(id) * stride +
 // base took three instructions per row.
@@ -116,7 +126,7 @@ __device__ __forceinline__ void eval_pass(uint32_t b0, const uint32_t* ids, uint
   // keys below the L-th beam key are appended to out (candidate order is not
   // needed: the merge ranks them)
   uint64_t key = kMaxKey;
-  if (sub < UU && r < m) key = make_key(Op::finish(tot), ids[r]);
+  if (sub < UU && r < m) key = make_bkey(Op::finish(tot), ids[r]);
   const bool keep = key < worst;
   const uint32_t bal = __ballot_sync(0xFFFFFFFFu, keep);
   GANN_CHECK(!keep || n_out + __popc(bal & ((1u << lane) - 1u)) < m);
@@ -176,7 +186,9 @@ size_t search_smem_per_warp(uint32_t L, uint32_t R, uint32_t hash_log2, bool has
 // them (GANN_SEARCH_DIAG=1 selects it for the fast mode too)
 // R64: the degree bound is 64 (every BASELINE config), fixed at compile time
 // FIT: rows are exactly LPR * CPL chunks (no chunk predicate in the gather)
-template <int E, int M, int LPR, int CPL, bool F16, bool R64 = false, bool FIT = false>
+// G2: the second-level visited table (large beams; its own instance so the
+// registers it takes, 72 -> 79, do not cost the small beams a resident CTA)
+template <int E, int M, int LPR, int CPL, bool F16, bool R64 = false, bool FIT = false, bool G2 = false>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_MINB_WIDE : GANN_SEARCH_MINB)
     search_kernel(const SearchArgs a, const uint32_t per_warp) {
   using Op = DistOp<E, M>;
@@ -205,7 +217,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_M
   const int vmode = F16 ? 0 : a.visited_mode;
   const uint32_t hmask = hbits ? (1u << hbits) - 1u : 0u;
   uint32_t* bm = hash + (hbits ? H / 2 : H);  // Lp bits: final positions of a merge's survivors
-  uint8_t* fl = reinterpret_cast<uint8_t*>(bm + Lp / 32);
+  // (no flag array: a beam key's lowest bit is its expanded flag, make_bkey)
   const uint32_t FULL = 0xFFFFFFFFu;
 
   // Second-level visited table (large beams, fast mode): the ids the shared
@@ -216,7 +228,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_M
   // bijective hash, n <= 2^27), so results do not depend on it.
   uint64_t* g2 = nullptr;
   uint32_t g2_region = kNone;
-  if (F16 && a.gtab && a.n <= (1u << 27)) {
+  if (G2 && F16 && a.gtab && a.n <= (1u << 27)) {
     if (lane == 0) {
       const uint32_t words = (a.gtab_regions + 31) / 32;
       uint32_t w0 = (blockIdx.x * 32 + (threadIdx.x >> 5)) % words;
@@ -246,7 +258,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_M
   if (lane == 0) q = atomicAdd(a.next_query, 1u);
   q = __shfl_sync(0xFFFFFFFFu, q, 0);
   for (; q < a.nq;) {
-    if (g2) {  // an empty table for this query (0xFFFF: no remainder)
+    if (G2 && g2) {  // an empty table for this query (0xFFFF: no remainder)
       for (uint32_t i = lane; i < (1u << a.gtab_log2) / 2; i += 32)
         reinterpret_cast<uint4*>(g2)[i] = make_uint4(kNone, kNone, kNone, kNone);
     }
@@ -285,7 +297,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_M
     __syncwarp();
     if (lane == 0) {
       beam[0] = ck[0];
-      fl[0] = 0;
       if (vmode == 2)
         table[(start * 0x9E3779B1u) & (TS - 1)] = start;
       else if (vmode == 1)
@@ -319,7 +330,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_M
       uint32_t fbal = 0, fb0 = 0;
       for (uint32_t b0 = hint & ~31u; b0 < size; b0 += 32) {
         const uint32_t i = b0 + lane;
-        const uint32_t bal = __ballot_sync(FULL, i >= hint && i < size && fl[i] == 0);
+        const uint32_t bal = __ballot_sync(FULL, i >= hint && i < size && (beam[i] & 1ull) == 0);
         if (bal) {
           fu = static_cast<int>(b0 + __ffs(bal) - 1);
           fbal = bal;
@@ -334,7 +345,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_M
         const float lim = __fadd_rn(bk, __fmul_rn(a.eps, fabsf(bk)));
         if (key_dist(fk) > lim) break;
       }
-      const uint32_t cur = key_id(fk);
+      const uint32_t cur = bkey_id(fk);
       hint = fu + 1;
       const uint32_t* row = graph_row(a.graph, cur, R);
       uint32_t nb0 = kNone, nb1 = kNone;
@@ -352,10 +363,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_M
         int gi = above ? static_cast<int>(fb0 + __ffs(above) - 1) : -1;
         if (gi < 0 && fb0 + 32 < size) {
           const uint32_t i = fb0 + 32 + lane;
-          const uint32_t bal = __ballot_sync(FULL, i < size && fl[i] == 0);
+          const uint32_t bal = __ballot_sync(FULL, i < size && (beam[i] & 1ull) == 0);
           if (bal) gi = static_cast<int>(fb0 + 32 + __ffs(bal) - 1);
         }
-        pf_id = gi >= 0 ? key_id(beam[gi]) : kNone;
+        pf_id = gi >= 0 ? bkey_id(beam[gi]) : kNone;
         if (pf_id != kNone) {
           const uint32_t* prow = graph_row(a.graph, pf_id, R);
           pf0 = lane < R ? __ldg(prow + lane) : kNone;
@@ -364,7 +375,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_M
       }
       __syncwarp();
       if (lane == 0) {
-        fl[fu] = 1;
+        beam[fu] = fk | 1ull;  // expanded
         if (a.vis_ids && nvis < a.vcap) {
           a.vis_ids[static_cast<uint64_t>(q) * a.vcap + nvis] = cur;
           a.vis_dists[static_cast<uint64_t>(q) * a.vcap + nvis] = key_dist(fk);
@@ -469,7 +480,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_M
             evict += old != kNone ? 1u : 0u;
           }
         }
-        if (F16 && g2 && __any_sync(FULL, fresh)) {
+        if (G2 && F16 && g2 && __any_sync(FULL, fresh)) {
           // not in the shared table: the second level decides (and learns it)
           const uint32_t h = (nb * 0x85EBCA6Bu) & g2mask;
           const uint32_t bucket = h >> 15, rem = h & 0x7FFFu;
@@ -505,7 +516,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_M
         uint32_t pb = 0;
         if (keep) {
           pb = lower_bound_steps_u64(beam, size, k);
-          if (pb < size && beam[pb] == k) {
+          if (pb < size && (beam[pb] | 1ull) == (k | 1ull)) {  // the same (dist, id), expanded or not
             keep = false;
             if (!F16) dups++;
           }
@@ -560,50 +571,62 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_M
       // GANN_SEARCH_RB chunks at a time: their sources are all read (independent
       // loads in flight together) before any of them is written — sources lie
       // at or below their target, so a batch only reads entries of its own
-      // chunks or lower ones, none written yet. One chunk at a time made the
-      // rebuild a chain of dependent shared-memory round trips, O(L / 32) per
-      // expansion, which dominated large beams.
+      // chunks or lower ones, none written yet (one chunk at a time is a chain
+      // of dependent shared-memory round trips: -2.7% at c1, L = 832). The
+      // low remainder goes one chunk at a time (small beams rebuild 1-3
+      // chunks: whole batches there cost the build's L = 128 searches 12%).
       {
         constexpr int RB = GANN_SEARCH_RB;
         const uint32_t nsz = min(L, size + s);
         const int c_lo = static_cast<int>(p0 >> 5);
         uint32_t running = kept;
-        for (int cb = static_cast<int>((nsz - 1) >> 5); cb >= c_lo; cb -= RB) {
+        int cb = static_cast<int>((nsz - 1) >> 5);
+        for (; cb - c_lo + 1 >= RB; cb -= RB) {  // whole batches from the top
           uint64_t key[RB];
-          uint8_t f[RB];
           bool act[RB];
 #pragma unroll
           for (int j = 0; j < RB; j++) {
             const int c = cb - j;
-            const uint32_t w = c >= c_lo ? bm[c] : 0u;
+            const uint32_t w = bm[c];
             running -= __popc(w);
             const uint32_t t = static_cast<uint32_t>(c) * 32 + lane;
             const uint32_t before = running + __popc(w & lanemask_lt(lane));
-            act[j] = c >= c_lo && t >= p0 && t < nsz;
+            act[j] = t >= p0 && t < nsz;
             // one load from either source (no divergent branch)
             const bool mine = (w >> lane) & 1u;
             const uint64_t* src = mine ? srt + before : beam + (t - before);
             key[j] = 0;
-            f[j] = 0;
             if (act[j]) {
               GANN_CHECK(t < L && (mine ? before < s : t - before < size));
-              key[j] = *src;
-              f[j] = mine ? 0 : fl[t - before];
+              key[j] = *src;  // (a survivor's flag bit is 0: unexpanded)
             }
           }
           __syncwarp();  // every read of these chunks' old entries precedes their writes
 #pragma unroll
           for (int j = 0; j < RB; j++) {
             const int c = cb - j;
-            const uint32_t t = static_cast<uint32_t>(c) * 32 + lane;
-            if (act[j]) {
-              beam[t] = key[j];
-              fl[t] = f[j];
-            }
-            if (lane == 0 && c >= c_lo) bm[c] = 0;
+            if (act[j]) beam[static_cast<uint32_t>(c) * 32 + lane] = key[j];
+            if (lane == 0) bm[c] = 0;
           }
           // no second sync: the next (lower) batch reads only positions below
           // these chunks, none written yet
+        }
+        for (; cb >= c_lo; cb--) {  // the rest (small beams: usually all of it) one chunk at a time
+          const uint32_t w = bm[cb];
+          running -= __popc(w);
+          const uint32_t t = static_cast<uint32_t>(cb) * 32 + lane;
+          const uint32_t before = running + __popc(w & lanemask_lt(lane));
+          const bool act = t >= p0 && t < nsz;
+          const bool mine = (w >> lane) & 1u;
+          const uint64_t* src = mine ? srt + before : beam + (t - before);
+          uint64_t key = 0;
+          if (act) {
+            GANN_CHECK(t < L && (mine ? before < s : t - before < size));
+            key = *src;
+          }
+          __syncwarp();
+          if (act) beam[t] = key;
+          if (lane == 0) bm[cb] = 0;
         }
       }
       size = min(L, size + s);
@@ -617,7 +640,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_M
     if (a.out_ids) {
       for (uint32_t i = lane; i < a.k_out; i += 32) {
         const bool have = i < size;
-        a.out_ids[static_cast<uint64_t>(q) * a.k_out + i] = have ? key_id(beam[i]) : kNone;
+        a.out_ids[static_cast<uint64_t>(q) * a.k_out + i] = have ? bkey_id(beam[i]) : kNone;
         a.out_dists[static_cast<uint64_t>(q) * a.k_out + i] =
             have ? key_dist(beam[i]) : __int_as_float(0x7f800000);
       }
@@ -647,7 +670,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_M
     if (lane == 0) q = atomicAdd(a.next_query, 1u);
     q = __shfl_sync(0xFFFFFFFFu, q, 0);
   }
-  if (g2 && lane == 0) atomicAnd(a.gtab_busy + g2_region / 32, ~(1u << (g2_region % 32)));
+  if (G2 && g2 && lane == 0) atomicAnd(a.gtab_busy + g2_region / 32, ~(1u << (g2_region % 32)));
 }
 
 namespace {
@@ -675,10 +698,15 @@ cudaError_t launch_one(const SearchArgs& a, cudaStream_t s) {
   const char* rv = std::getenv("GANN_SEARCH_R64");
   const bool r64 = a.R == 64 && (rv && *rv ? *rv == '1' : LPR >= 16);
   const bool fit = a.stride == uint64_t(16) * LPR * CPL;
+  const bool g2 = a.gtab != nullptr;
   auto k = !f16 ? search_kernel<E, M, LPR, CPL, false>
-                : (r64 ? (fit ? search_kernel<E, M, LPR, CPL, true, true, true> : search_kernel<E, M, LPR, CPL, true, true>)
-                       : (fit ? search_kernel<E, M, LPR, CPL, true, false, true>
-                              : search_kernel<E, M, LPR, CPL, true, false>));
+         : g2 ? (r64 ? (fit ? search_kernel<E, M, LPR, CPL, true, true, true, true>
+                            : search_kernel<E, M, LPR, CPL, true, true, false, true>)
+                     : (fit ? search_kernel<E, M, LPR, CPL, true, false, true, true>
+                            : search_kernel<E, M, LPR, CPL, true, false, false, true>))
+              : (r64 ? (fit ? search_kernel<E, M, LPR, CPL, true, true, true> : search_kernel<E, M, LPR, CPL, true, true>)
+                     : (fit ? search_kernel<E, M, LPR, CPL, true, false, true>
+                            : search_kernel<E, M, LPR, CPL, true, false>));
   if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 size_t(per_warp) * wpb > 48 * 1024 ? static_cast<int>(size_t(per_warp) * wpb)
                                                                    : 48 * 1024)) != cudaSuccess)
@@ -730,6 +758,10 @@ void preload_one() {
   touch_kernel(search_kernel<E, M, LPR, CPL, true, true>);
   touch_kernel(search_kernel<E, M, LPR, CPL, true, false, true>);
   touch_kernel(search_kernel<E, M, LPR, CPL, true, true, true>);
+  touch_kernel(search_kernel<E, M, LPR, CPL, true, false, false, true>);
+  touch_kernel(search_kernel<E, M, LPR, CPL, true, true, false, true>);
+  touch_kernel(search_kernel<E, M, LPR, CPL, true, false, true, true>);
+  touch_kernel(search_kernel<E, M, LPR, CPL, true, true, true, true>);
 }
 template <int E, int M>
 void preload_geom(const Geometry& g) {
