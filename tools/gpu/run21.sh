@@ -1,0 +1,5 @@
+set -x
+python -m pytest tests/test_gpu_baseline.py tests/test_gpu_search.py tests/test_gpu_checked.py -m gpu -q -x -p no:cacheprovider > gpurun_out/t_s.log 2>&1; tail -2 gpurun_out/t_s.log
+for lib in libgann_prev.so libgann_b200.so; do
+GANN_LIB=$lib python tools/ab_search.py --L 832,1024 --rounds 2 > gpurun_out/ab_$lib.log 2>&1; grep -E "MQPS" gpurun_out/ab_$lib.log
+done
