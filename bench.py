@@ -87,8 +87,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c1")
-    ap.add_argument("--n", type=int, default=0, help="override the config's n (debug)")
-    ap.add_argument("--nq", type=int, default=0, help="queries per GPU (default: the config's)")
+    # (--points / --queries: torchrun's own argument parser claims --n / --nq prefixes)
+    ap.add_argument("--n", "--points", dest="n", type=int, default=0, help="override the config's n (debug)")
+    ap.add_argument("--nq", "--queries", dest="nq", type=int, default=0, help="queries per GPU (default: the config's)")
     ap.add_argument("--target-recall", type=float, default=0.95)
     ap.add_argument("--L", type=int, default=0, help="force the search beam")
     ap.add_argument("--L-max", type=int, default=200, help="largest beam of the sweep (BASELINE: 10..200)")
@@ -307,12 +308,20 @@ def setup(args):
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
+    # GANN_BENCH_BACKEND=gloo: a check of the N>1 logic on a one-GPU box (ranks
+    # share the device, collectives staged through the host); never a number
+    backend = os.environ.get("GANN_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     # a dedicated stream: torch's legacy default stream has handle 0, which the C
     # ABI reads as "the index's own stream"
     torch.cuda.set_stream(torch.cuda.Stream())
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     import paper_2305_04359_b200 as g
     from paper_2305_04359_b200._lib import check, lib
@@ -327,7 +336,7 @@ def setup(args):
         torch.cuda.synchronize()
 
     def allreduce(x, op="max"):
-        return distutil.reduce_scalar(x, op, dist if world > 1 else None, "cuda")
+        return distutil.reduce_scalar(x, op, dist if world > 1 else None, "cuda" if backend == "nccl" else "cpu")
 
     # ---- data: generated straight into HBM ------------------------------------------
     # (N>1, partitioned build of rows that need no padding: straight into the
@@ -348,7 +357,7 @@ def setup(args):
         # (gann_part_build) with the library's NCCL transport; peer rows over
         # NVLink (CUDA IPC). The batch cap is the config's, shrunk to what the
         # free device memory holds (0.2-0.5% of n at 1B).
-        from paper_2305_04359_b200.partition import NcclExchange, PartitionedIndex
+        from paper_2305_04359_b200.partition import DistExchange, NcclExchange, PartitionedIndex
         pidx = PartitionedIndex(base.data_ptr() if base is not None else 0, cfg.metric, cfg.R, dist, device=dev,
                                 shape=(n, d), dtype=cfg.np_dtype)
         if base is None:
@@ -366,15 +375,17 @@ def setup(args):
             mem_cap = pidx.batch_cap(cfg.L, int(0.8 * free_b))
             cap = int(allreduce(min(cfg.max_batch or n, mem_cap), "min"))
             params = g.DiskannParams(cfg.R, cfg.L, cfg.alpha, seed=42, max_batch=cap)
-            xch = NcclExchange(dist, dev)
+            xch = NcclExchange(dist, dev) if backend == "nccl" else DistExchange(dist, dev)
             barrier()
             t0 = time.perf_counter()
             info = pidx.build_native(params, xch)
             torch.cuda.synchronize()
             build_s = allreduce(time.perf_counter() - t0)
-            xch.close()
+            if backend == "nccl":
+                xch.close()
             bstats = pidx.stats()  # this rank's share of the build
-            build_mode = f"vertex-partitioned over {world} GPUs (gann_part_build, NCCL send/recv exchange)"
+            build_mode = (f"vertex-partitioned over {world} GPUs (gann_part_build, "
+                          + ("NCCL send/recv exchange)" if backend == "nccl" else f"{backend} exchange: logic check)"))
             build_extra = {"max_batch_used": cap, "max_batch_memory_cap": mem_cap, "pairs_sent": info["pairs_sent"],
                            "search_on": search_on}
             if search_on == "replica":
@@ -382,7 +393,12 @@ def setup(args):
                 rows = torch.full((P * cfg.R,), -1, dtype=torch.int32, device="cuda")
                 rows[: pidx.rows * cfg.R] = pidx.device_rows()
                 full = torch.empty((world * P * cfg.R,), dtype=torch.int32, device="cuda")
-                dist.all_gather_into_tensor(full, rows)
+                if backend == "nccl":
+                    dist.all_gather_into_tensor(full, rows)
+                else:  # host-staged
+                    parts = [torch.empty(P * cfg.R, dtype=torch.int32) for _ in range(world)]
+                    dist.all_gather(parts, rows.cpu())
+                    full.copy_(torch.cat(parts).cuda())
                 idx = g.Index.from_device(base.data_ptr(), n, d, cfg.np_dtype, cfg.metric, cfg.R, dev)
                 check(lib().gann_import_graph_device(idx._h, ctypes.c_void_p(full.data_ptr()), pidx.start()))
                 del full, rows
