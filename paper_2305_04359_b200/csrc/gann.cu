@@ -415,11 +415,19 @@ SearchArgs base_search_args(gann_index* idx, uint32_t L, uint32_t k_gate, uint32
   // streams may run concurrently (up to kQueryCounters in flight)
   a.next_query = idx->qctr + (idx->qslot.fetch_add(1) % kQueryCounters);
   a.stats = idx->stats;
-  // beams from GANN_GTAB_MIN_L (default 768; 0 = never) also use the
-  // second-level visited table: one 32 KB region per resident warp, twice
-  // the device's warp slots so concurrent launches find free regions
-  const uint32_t gmin = env_u32("GANN_GTAB_MIN_L", 768);  // read per call (A/B runs flip it)
-  if (mode == GANN_VISITED_FAST && gmin && L >= gmin && idx->n <= (uint64_t(1) << 27)) {
+  // Large beams use the second-level visited table instead of the shared one
+  // (launch_one drops the shared table then): one 32 KB region per resident
+  // warp, twice the device's warp slots so concurrent launches find free
+  // regions. Where it pays was measured per beam at c1 (serial launch of
+  // 10k queries, shared table only -> second level only, ms): 640: 13.4 ->
+  // 12.9, 704: 14.7 -> 13.9, 768: 17.0 -> 14.7, 832: 18.4 -> 15.5, 896: 19.7 ->
+  // 21.1, 960: 20.9 -> 22.1, 1024: 22.6 -> 24.2, 1280: 29.4 -> 26.9, 1600: 41.8
+  // -> 34.7 (the shared memory it frees is worth a resident CTA at some
+  // beams and not at others); 400 / 512: 7.9 / 10.0 with the shared table
+  // alone. So from GANN_GTAB_MIN_L (default 576; 0 = never) except 896-1151.
+  const uint32_t gmin = env_u32("GANN_GTAB_MIN_L", 576);  // read per call (A/B runs flip it)
+  const bool gband = L >= 896 && L < 1152 && !env_u32("GANN_GTAB_NO_BAND", 0);
+  if (mode == GANN_VISITED_FAST && gmin && L >= gmin && !gband && idx->n <= (uint64_t(1) << 27)) {
     std::lock_guard<std::mutex> lk(idx->gtab_mu);
     if (!idx->gtab_regions) {
       int sms = 148, warps = 64;
@@ -436,6 +444,7 @@ SearchArgs base_search_args(gann_index* idx, uint32_t L, uint32_t k_gate, uint32
     a.gtab_busy = idx->gtab_busy.as<uint32_t>();
     a.gtab_regions = idx->gtab_regions;
     a.gtab_log2 = kGtabLog2;
+
   }
   return a;
 }

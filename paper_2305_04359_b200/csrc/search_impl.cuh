@@ -301,7 +301,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_M
         table[(start * 0x9E3779B1u) & (TS - 1)] = start;
       else if (vmode == 1)
         table[mix64(static_cast<uint64_t>(start) ^ seed) % LL] = start;
-      else if ((F16 || hbits) && a.hash_ways == 4) {
+      else if (G2 && a.hash_log2 == 0) {
+        // no shared table (the second level alone): nothing to enter
+      } else if ((F16 || hbits) && a.hash_ways == 4) {
         const uint32_t h = (start * 0x9E3779B1u) & hmask;
         reinterpret_cast<uint64_t*>(hash)[h >> 15] = 0xFFFFFFFFFFFF0000ull | (h & 0x7FFFu);
       } else if ((F16 || hbits) && a.hash_ways == 2) {
@@ -414,6 +416,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_M
           if (valid && last) table[slot] = nb;
           __syncwarp();
           fresh = valid && !seen;
+        } else if (G2 && a.hash_log2 == 0) {
+          fresh = valid;  // no shared table: the second level alone decides
         } else if ((F16 || hbits) && a.hash_ways == 4) {
           // 4-way buckets of u16 slots in one u64 (newest in the low half
           // word), as the 2-way case below
@@ -675,7 +679,17 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_M
 
 namespace {
 template <int E, int M, int LPR, int CPL>
-cudaError_t launch_one(const SearchArgs& a, cudaStream_t s) {
+cudaError_t launch_one(const SearchArgs& a0, cudaStream_t s) {
+  // read per launch (A/B runs flip them between launches)
+  const char* dv = std::getenv("GANN_SEARCH_DIAG");
+  const bool diag = dv && *dv && *dv != '0';
+  const bool f16 = a0.visited_mode == 0 && a0.hash_bits != 0 && !diag;
+  // with the second level (G2), no shared table: its 2 KB per warp go to
+  // resident warps and the second level answers every neighbour
+  // (GANN_GTAB_ONLY=0 keeps both levels)
+  const char* go = std::getenv("GANN_GTAB_ONLY");
+  SearchArgs a = a0;
+  if (f16 && a.gtab && !(go && *go == '0')) a.hash_log2 = 0;
   const uint32_t per_warp = static_cast<uint32_t>(search_smem_per_warp(a.L, a.R, a.hash_log2, a.hash_bits != 0));
   int dev = 0, optin = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -687,10 +701,6 @@ cudaError_t launch_one(const SearchArgs& a, cudaStream_t s) {
   // warps at 59 KB each waste 50 KB that 1-warp CTAs use)
   int wpb = kWarpsPerBlock;
   while (wpb > 1 && size_t(per_warp) * wpb > static_cast<size_t>(optin)) wpb >>= 1;
-  // read per launch (A/B runs flip it between launches)
-  const char* dv = std::getenv("GANN_SEARCH_DIAG");
-  const bool diag = dv && *dv && *dv != '0';
-  const bool f16 = a.visited_mode == 0 && a.hash_bits != 0 && !diag;
   // R = 64 fixed at compile time (measured): 16-lane rows -5% at L=200 (c2)
   // and a faster build search; 8-lane rows (c1): -1% for a serial launch at
   // L=200 but -1% bench QPS (pipelined), +1.4% at L=64, +4.5% for the build's
