@@ -427,7 +427,9 @@ SearchArgs base_search_args(gann_index* idx, uint32_t L, uint32_t k_gate, uint32
   // alone. So from GANN_GTAB_MIN_L (default 576; 0 = never) except 896-1151.
   const uint32_t gmin = env_u32("GANN_GTAB_MIN_L", 576);  // read per call (A/B runs flip it)
   const bool gband = L >= 896 && L < 1152 && !env_u32("GANN_GTAB_NO_BAND", 0);
-  if (mode == GANN_VISITED_FAST && gmin && L >= gmin && !gband && idx->n <= (uint64_t(1) << 27)) {
+  const uint32_t glog2 = std::min<uint32_t>(kGtabLog2, std::max<uint32_t>(8, env_u32("GANN_GTAB_LOG2", kGtabLog2Default)));
+  a.next_pf = static_cast<int>(env_u32("GANN_SEARCH_NEXTPF", 1));
+  if (mode == GANN_VISITED_FAST && gmin && L >= gmin && !gband && idx->n <= (uint64_t(1) << (glog2 + 15))) {
     std::lock_guard<std::mutex> lk(idx->gtab_mu);
     if (!idx->gtab_regions) {
       int sms = 148, warps = 64;
@@ -443,7 +445,8 @@ SearchArgs base_search_args(gann_index* idx, uint32_t L, uint32_t k_gate, uint32
     a.gtab = idx->gtab.as<uint64_t>();
     a.gtab_busy = idx->gtab_busy.as<uint32_t>();
     a.gtab_regions = idx->gtab_regions;
-    a.gtab_log2 = kGtabLog2;
+    a.gtab_log2 = glog2;
+    a.gtab_keep = static_cast<int>(env_u32("GANN_GTAB_KEEP", 1));
 
   }
   return a;

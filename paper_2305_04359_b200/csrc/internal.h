@@ -92,8 +92,11 @@ struct SearchArgs {
   uint32_t* gtab_busy;
   uint32_t gtab_regions;
   uint32_t gtab_log2;
+  int gtab_keep;             // second-level table accesses carry an L2 evict_last policy
+  int next_pf;               // prefetch the next expansion's row before the merge
 };
-constexpr uint32_t kGtabLog2 = 12;  // 4096 buckets x 4 slots = 16k ids, 32 KB a region
+constexpr uint32_t kGtabLog2 = 12;  // largest region: 4096 buckets x 4 slots = 16k ids, 32 KB
+constexpr uint32_t kGtabLog2Default = 11;  // 8k ids, 16 KB: c1 L=832 evaluations 9.5k -> 11.9k per query, DRAM 36 -> 23 GB per launch, -2%
 size_t search_smem_per_warp(uint32_t L, uint32_t R, uint32_t hash_log2, bool hash16);
 constexpr int kSearchWarpsPerBlock = 4;  // one query per warp
 size_t search_smem_min_block(uint32_t L, uint32_t R, uint32_t hash_log2, bool hash16);

@@ -228,7 +228,17 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_M
   // bijective hash, n <= 2^27), so results do not depend on it.
   uint64_t* g2 = nullptr;
   uint32_t g2_region = kNone;
-  if (G2 && F16 && a.gtab && a.n <= (1u << 27)) {
+  // L2 policy of the second-level table's accesses: evict_last keeps the
+  // resident warps' regions in L2 against the stream of gathered rows
+  // (GANN_GTAB_KEEP=0: evict_normal)
+  uint64_t g2pol = 0;
+  if (G2) {
+    if (a.gtab_keep)
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(g2pol));
+    else
+      asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(g2pol));
+  }
+  if (G2 && F16 && a.gtab && a.n <= (1u << (a.gtab_log2 + 15))) {
     if (lane == 0) {
       const uint32_t words = (a.gtab_regions + 31) / 32;
       uint32_t w0 = (blockIdx.x * 32 + (threadIdx.x >> 5)) % words;
@@ -260,7 +270,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_M
   for (; q < a.nq;) {
     if (G2 && g2) {  // an empty table for this query (0xFFFF: no remainder)
       for (uint32_t i = lane; i < (1u << a.gtab_log2) / 2; i += 32)
-        reinterpret_cast<uint4*>(g2)[i] = make_uint4(kNone, kNone, kNone, kNone);
+        asm volatile("st.global.cg.L2::cache_hint.v4.u32 [%0], {%1, %1, %1, %1}, %2;"
+                     :: "l"(reinterpret_cast<uint4*>(g2) + i), "r"(kNone), "l"(g2pol) : "memory");
     }
     const uint8_t* qp = a.query_rows ? a.data + static_cast<uint64_t>(a.query_rows[q]) * a.stride
                                      : a.queries + static_cast<uint64_t>(q) * a.stride;
@@ -324,6 +335,26 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_M
     // (R <= 64: two ids per lane); used when the guess turns out right
     const bool pf_ok = R <= 64;
     uint32_t pf_id = kNone, pf0 = kNone, pf1 = kNone;
+    uint64_t pf_key = kMaxKey;  // the guess's beam key (large beams)
+    // second-level table words of the guess's neighbours, read behind this
+    // step's gather so the next step's filter does not wait on L2 (pw_id: the
+    // vertex they belong to)
+    uint64_t pw0 = 0, pw1 = 0;
+    uint32_t pw_id = kNone;
+    // the guess's second-level words (its row has arrived by the time this
+    // runs: behind a gather, or it is waited for)
+    auto g2_prefetch = [&]() {
+      if (G2 && g2 && pf_id != kNone && pw_id != pf_id) {
+        const uint32_t b0 = ((pf0 * 0x85EBCA6Bu) & g2mask) >> 15, b1 = ((pf1 * 0x85EBCA6Bu) & g2mask) >> 15;
+        pw0 = 0ull;
+        pw1 = 0ull;
+        if (pf0 != kNone)
+          asm volatile("ld.global.cg.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(pw0) : "l"(g2 + b0), "l"(g2pol) : "memory");
+        if (pf1 != kNone)
+          asm volatile("ld.global.cg.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(pw1) : "l"(g2 + b1), "l"(g2pol) : "memory");
+        pw_id = pf_id;
+      }
+    };
     __syncwarp();
 
     while (true) {
@@ -351,11 +382,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_M
       hint = fu + 1;
       const uint32_t* row = graph_row(a.graph, cur, R);
       uint32_t nb0 = kNone, nb1 = kNone;
+      bool use_pw = false;
       if (pf_ok) {
         if (pf_id == cur) {
           nb0 = pf0;
           nb1 = pf1;
           if (!F16) ghits++;
+          use_pw = G2 && g2 && pw_id == cur;
         } else {
           nb0 = lane < R ? __ldg(row + lane) : kNone;
           nb1 = lane + 32 < R ? __ldg(row + 32 + lane) : kNone;
@@ -368,7 +401,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_M
           const uint32_t bal = __ballot_sync(FULL, i < size && (beam[i] & 1ull) == 0);
           if (bal) gi = static_cast<int>(fb0 + 32 + __ffs(bal) - 1);
         }
-        pf_id = gi >= 0 ? bkey_id(beam[gi]) : kNone;
+        const uint64_t gk = gi >= 0 ? beam[gi] : kMaxKey;
+        if (G2) pf_key = gk;
+        pf_id = gi >= 0 ? bkey_id(gk) : kNone;
         if (pf_id != kNone) {
           const uint32_t* prow = graph_row(a.graph, pf_id, R);
           pf0 = lane < R ? __ldg(prow + lane) : kNone;
@@ -488,19 +523,27 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_M
           // not in the shared table: the second level decides (and learns it)
           const uint32_t h = (nb * 0x85EBCA6Bu) & g2mask;
           const uint32_t bucket = h >> 15, rem = h & 0x7FFFu;
-          const uint64_t w = fresh ? __ldcg(g2 + bucket) : 0ull;
+          uint64_t w = 0ull;
+          if (use_pw)
+            w = t0 == 0 ? pw0 : pw1;  // read behind the previous step's gather (no insert since)
+          else if (fresh)
+            asm volatile("ld.global.cg.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(w) : "l"(g2 + bucket), "l"(g2pol) : "memory");
           const uint32_t rr = rem | (rem << 16);
           if (fresh && (__vcmpeq2(static_cast<uint32_t>(w), rr) | __vcmpeq2(static_cast<uint32_t>(w >> 32), rr)))
             fresh = false;
           else if (fresh)
-            __stcg(g2 + bucket, (w << 16) | rem);
+            asm volatile("st.global.cg.L2::cache_hint.u64 [%0], %1, %2;" :: "l"(g2 + bucket), "l"((w << 16) | rem), "l"(g2pol) : "memory");
         }
         const uint32_t bal = __ballot_sync(FULL, fresh);
         GANN_CHECK(!fresh || m + __popc(bal & lanemask_lt(lane)) < Rp);
         if (fresh) cid[m + __popc(bal & lanemask_lt(lane))] = nb;
         m += __popc(bal);
       }
-      if (m == 0) continue;
+      pw_id = kNone;  // this step's inserts made any earlier read stale
+      if (m == 0) {
+        if (G2 && a.next_pf) g2_prefetch();
+        continue;
+      }
       GANN_CHECK(((m + 31) & ~31u) <= Rp);
       if (m + lane < ((m + 31) & ~31u)) cid[m + lane] = cur;  // pad to a whole pass
       __syncwarp();
@@ -508,11 +551,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_M
       // distances; keys below the L-th beam key go to tmpk (c1 of them)
       const uint64_t worst = size == L ? beam[L - 1] : kMaxKey;
       const uint32_t c1 = eval_rows<Op, LPR, CPL, FIT>(a.data, stride32, nch, cid, m, tmpk, qr, lane, worst);
+      if (G2 && a.next_pf) g2_prefetch();
       if (c1 == 0) continue;
       __syncwarp();
       // ---- merge: top-L of beam U new, exact duplicates dropped ----
       // insertion points; exact (dist, id) duplicates of beam keys drop
       uint32_t s = 0;
+      uint64_t mk = kMaxKey;  // the smallest survivor (large beams)
       for (uint32_t j0 = 0; j0 < c1; j0 += 32) {
         const uint32_t j = j0 + lane;
         bool keep = j < c1;
@@ -526,6 +571,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_M
           }
         }
         const uint32_t bal = __ballot_sync(FULL, keep);
+        if (G2 && keep) mk = min(mk, k);
         if (keep) {
           const uint32_t o = s + __popc(bal & lanemask_lt(lane));
           GANN_CHECK(o < Rp && pb <= size);
@@ -535,6 +581,26 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_M
         s += __popc(bal);
       }
       if (s == 0) continue;
+      if (G2 && pf_ok && a.next_pf) {
+        // The next expansion is known before the rest of the merge: the
+        // smaller of the guess (the first unexpanded key after fu) and the
+        // smallest survivor. When a survivor beats the guess its row is
+        // loaded now, behind the merge, instead of at the top of the next
+        // step (which still checks pf_id == cur before using it). Survivors,
+        // not new keys: re-evaluated beam keys (the filter forgets) would
+        // point it at expanded vertices.
+        const uint32_t mh = __reduce_min_sync(FULL, static_cast<uint32_t>(mk >> 32));
+        const uint32_t ml =
+            __reduce_min_sync(FULL, static_cast<uint32_t>(mk >> 32) == mh ? static_cast<uint32_t>(mk) : kNone);
+        mk = (static_cast<uint64_t>(mh) << 32) | ml;
+        if (mk < pf_key) {
+          pf_key = mk;
+          pf_id = bkey_id(mk);
+          const uint32_t* prow = graph_row(a.graph, pf_id, R);
+          pf0 = lane < R ? __ldg(prow + lane) : kNone;
+          pf1 = lane + 32 < R ? __ldg(prow + 32 + lane) : kNone;
+        }
+      }
       __syncwarp();
       // survivors sorted (srt), final positions fin = insertion point + rank
       // marked in a bitmap of beam positions (only fin < L is kept)
