@@ -50,6 +50,11 @@ constexpr int kWarpsPerBlock = kSearchWarpsPerBlock;
                                  // registers, 6 CTAs, and c2 ran 7% slower than at 7 CTAs
 #endif
 
+#ifndef GANN_SEARCH_MINB_G2
+#define GANN_SEARCH_MINB_G2 6  // large beams, rows <= 256 B: 7 (72 registers; shared memory allows 7 CTAs) measured
+                               // 33% slower at c1 L=832 (19.8 vs 14.8 ms)
+#endif
+
 // Rows in flight per lane group per pass: U <= LPR so the transposed
 // reduction can hand every lane of the group (at most) one finished row.
 #ifndef GANN_SEARCH_RB
@@ -189,7 +194,8 @@ size_t search_smem_per_warp(uint32_t L, uint32_t R, uint32_t hash_log2, bool has
 // G2: the second-level visited table (large beams; its own instance so the
 // registers it takes, 72 -> 79, do not cost the small beams a resident CTA)
 template <int E, int M, int LPR, int CPL, bool F16, bool R64 = false, bool FIT = false, bool G2 = false>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, LPR >= 16 ? GANN_SEARCH_MINB_WIDE : GANN_SEARCH_MINB)
+__global__ void __launch_bounds__(kWarpsPerBlock * 32,
+                                  G2 && LPR * CPL <= 16 ? GANN_SEARCH_MINB_G2 : (LPR >= 16 ? GANN_SEARCH_MINB_WIDE : GANN_SEARCH_MINB))
     search_kernel(const SearchArgs a, const uint32_t per_warp) {
   using Op = DistOp<E, M>;
   extern __shared__ __align__(16) uint8_t smem[];

@@ -108,5 +108,7 @@ for L in [int(x) for x in args.L.split(",")]:
     os.environ["GANN_SEARCH_DIAG"] = "0"
     nq = max(1, st["queries"])
     print(f"L={L} diag: exp/q {st['expansions'] / nq:.1f} evals/q {st['evaluations'] / nq:.1f} "
-          f"guess_hits/exp {st['guess_hits'] / max(1, st['expansions']):.3f} dups/q {st['duplicates'] / nq:.1f}",
+          f"guess_hits/exp {st['guess_hits'] / max(1, st['expansions']):.3f} dups/q {st['duplicates'] / nq:.1f} "
+          f"merges/q {st['merges'] / nq:.1f} survivors/merge {st['survivors'] / max(1, st['merges']):.2f} "
+          f"moved/merge {st['moved'] / max(1, st['merges']):.1f}",
           flush=True)
