@@ -429,7 +429,20 @@ SearchArgs base_search_args(gann_index* idx, uint32_t L, uint32_t k_gate, uint32
   const bool gband = L >= 896 && L < 1152 && !env_u32("GANN_GTAB_NO_BAND", 0);
   const uint32_t glog2 = std::min<uint32_t>(kGtabLog2, std::max<uint32_t>(8, env_u32("GANN_GTAB_LOG2", kGtabLog2Default)));
   a.next_pf = static_cast<int>(env_u32("GANN_SEARCH_NEXTPF", 1));
-  if (mode == GANN_VISITED_FAST && gmin && L >= gmin && !gband && idx->n <= (uint64_t(1) << (glog2 + 15))) {
+  // Several expansions per step (search_batch.cuh): the Alg. 1 form in the
+  // fast mode, R <= 64, ids within the visited table's remainders.
+  // GANN_BATCH_EB = 0 turns it off; GANN_BATCH_MIN_L is the smallest beam it takes.
+  const uint32_t beb = std::min<uint32_t>(env_u32("GANN_BATCH_EB", 8), 8);
+  const uint32_t bcm = std::min<uint32_t>(256, std::max<uint32_t>(64, env_u32("GANN_BATCH_CM", 64) & ~31u));
+  const bool batch = beb && mode == GANN_VISITED_FAST && k_gate == L && idx->R <= 64 && L < 65536 &&
+                     L >= env_u32("GANN_BATCH_MIN_L", 320) && idx->n <= (uint64_t(1) << (glog2 + 15)) &&
+                     search_batch_smem_per_warp(L, bcm) <= 200 * 1024;
+  if (batch) {
+    a.batch_eb = beb;
+    a.batch_cm = bcm;
+    a.batch_policy = static_cast<int>(env_u32("GANN_BATCH_POLICY", 1));
+  }
+  if (batch || (mode == GANN_VISITED_FAST && gmin && L >= gmin && !gband && idx->n <= (uint64_t(1) << (glog2 + 15)))) {
     std::lock_guard<std::mutex> lk(idx->gtab_mu);
     if (!idx->gtab_regions) {
       int sms = 148, warps = 64;

@@ -94,12 +94,17 @@ struct SearchArgs {
   uint32_t gtab_log2;
   int gtab_keep;             // second-level table accesses carry an L2 evict_last policy
   int next_pf;               // prefetch the next expansion's row before the merge
+  // several expansions per step (search_batch.cuh; Alg. 1 form, fast mode, R <= 64):
+  uint32_t batch_eb;         // expansions tried per step (0: one per step, search_kernel)
+  uint32_t batch_cm;         // fresh ids a step holds (multiple of 32, <= 256)
+  int batch_policy;          // 0: always batch_eb; 1: committed + 1; 2: batch_eb after a full commit, else committed + 1
 };
 constexpr uint32_t kGtabLog2 = 12;  // largest region: 4096 buckets x 4 slots = 16k ids, 32 KB
 constexpr uint32_t kGtabLog2Default = 11;  // 8k ids, 16 KB: c1 L=832 evaluations 9.5k -> 11.9k per query, DRAM 36 -> 23 GB per launch, -2%
 size_t search_smem_per_warp(uint32_t L, uint32_t R, uint32_t hash_log2, bool hash16);
 constexpr int kSearchWarpsPerBlock = 4;  // one query per warp
 size_t search_smem_min_block(uint32_t L, uint32_t R, uint32_t hash_log2, bool hash16);
+size_t search_batch_smem_per_warp(uint32_t L, uint32_t cm);  // search_batch_kernel (search_batch.cuh)
 
 // Kernel preloading. CUDA loads a kernel's code at its first launch (lazy
 // module loading), which put 15-200 ms of one-time stalls into the first

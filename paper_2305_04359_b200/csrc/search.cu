@@ -47,6 +47,14 @@ size_t search_smem_min_block(uint32_t L, uint32_t R, uint32_t hash_log2, bool ha
   return search_smem_per_warp(L, R, hash_log2, hash16);
 }
 
+// Per-warp shared memory of search_batch_kernel: beam, candidate keys / ids /
+// insertion points / expansion tags for cm candidates per step, merge bitmap.
+size_t search_batch_smem_per_warp(uint32_t L, uint32_t cm) {
+  const size_t Lp = (L + 31) & ~31u;
+  const size_t b = Lp * 8 + size_t(cm) * 8 + size_t(cm) * 4 + 32 + Lp / 8 + size_t(cm) * 2 + size_t(cm) * 2;
+  return (b + 15) & ~size_t(15);
+}
+
 cudaError_t launch_search_u8(const SearchArgs& a, int metric, const Geometry& g, cudaStream_t s);
 cudaError_t launch_search_i8(const SearchArgs& a, int metric, const Geometry& g, cudaStream_t s);
 cudaError_t launch_search_f32(const SearchArgs& a, int metric, const Geometry& g, cudaStream_t s);

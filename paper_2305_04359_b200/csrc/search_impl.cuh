@@ -749,9 +749,14 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32,
   if (G2 && g2 && lane == 0) atomicAnd(a.gtab_busy + g2_region / 32, ~(1u << (g2_region % 32)));
 }
 
+}  // namespace gann
+#include "search_batch.cuh"
+namespace gann {
+
 namespace {
 template <int E, int M, int LPR, int CPL>
 cudaError_t launch_one(const SearchArgs& a0, cudaStream_t s) {
+  if (a0.batch_eb) return launch_batch<E, M, LPR, CPL>(a0, s);  // several expansions per step (search_batch.cuh)
   // read per launch (A/B runs flip them between launches)
   const char* dv = std::getenv("GANN_SEARCH_DIAG");
   const bool diag = dv && *dv && *dv != '0';
@@ -794,11 +799,15 @@ cudaError_t launch_one(const SearchArgs& a0, cudaStream_t s) {
                                                                    : 48 * 1024)) != cudaSuccess)
     return e;
   if (a.nq == 0) return cudaSuccess;
+  if (const char* cv = std::getenv("GANN_SEARCH_CARVE"))  // experiment: shared-memory carve-out, percent
+    if ((e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(cv))) != cudaSuccess) return e;
   int per_sm = 0, sms = 0;
   if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, wpb * 32, size_t(per_warp) * wpb)) !=
       cudaSuccess)
     return e;
+  if (const char* dv = std::getenv("GANN_BATCH_DEBUG"))
+    if (*dv == '1') std::fprintf(stderr, "search launch: L %u per_warp %u wpb %d per_sm %d g2 %d\n", a.L, per_warp, wpb, per_sm, int(g2));
   for (int w = wpb >> 1; w >= 1; w >>= 1) {
     int ps = 0;
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, k, w * 32, size_t(per_warp) * w)) != cudaSuccess)
@@ -844,6 +853,8 @@ void preload_one() {
   touch_kernel(search_kernel<E, M, LPR, CPL, true, true, false, true>);
   touch_kernel(search_kernel<E, M, LPR, CPL, true, false, true, true>);
   touch_kernel(search_kernel<E, M, LPR, CPL, true, true, true, true>);
+  touch_kernel(search_batch_kernel<E, M, LPR, CPL, false>);
+  touch_kernel(search_batch_kernel<E, M, LPR, CPL, true>);
 }
 template <int E, int M>
 void preload_geom(const Geometry& g) {

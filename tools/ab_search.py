@@ -84,19 +84,21 @@ for L in [int(x) for x in args.L.split(",")]:
     res = {i: [] for i in range(len(combos))}
     ref_ids = None
     evq = {}
+    stq = {}
     for r in range(args.rounds):
         for i, c in enumerate(combos):
             idx.reset_stats()
             ms, ids = run(L, c)
             st = idx.stats()
             evq[i] = st["evaluations"] / max(1, st["queries"])
+            stq[i] = (st["merges"] / max(1, st["queries"]), st["guess_hits"] / max(1, st["expansions"]))
             res[i].append(ms)
             if ref_ids is None:
                 ref_ids = ids
             assert (ids == ref_ids).all(), f"ids differ under {c}"
     for i, c in enumerate(combos):
         ms = min(res[i])
-        print(f"L={L} {c}: {ms:.3f} ms  {args.nq / ms * 1e3 / 1e6:.3f} MQPS  evals/q {evq[i]:.1f}  "
+        print(f"L={L} {c}: {ms:.3f} ms  {args.nq / ms * 1e3 / 1e6:.3f} MQPS  evals/q {evq[i]:.1f}  steps/q {stq[i][0]:.1f} dropped/exp {stq[i][1]:.3f}  "
               f"(runs {[round(x, 3) for x in res[i]]})")
     # diagnostic counters (general kernel) for the first combo
     os.environ["GANN_SEARCH_DIAG"] = "1"
