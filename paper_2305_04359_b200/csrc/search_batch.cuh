@@ -396,18 +396,41 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_BATCH_MINB)
       eb = a.batch_policy == 0 ? static_cast<uint32_t>(EB)
                                : (a.batch_policy == 2 && P == nsel ? static_cast<uint32_t>(EB) : min(static_cast<uint32_t>(EB), P + 1u));
       eb = min(eb, a.batch_eb);
-      // their fresh ids enter the visited table (newest remainder in the low half word)
+      // their fresh ids enter the visited table (newest remainder in the low
+      // half word). Up to 64 of them (the default step): the buckets are read
+      // here and written at the end of the step, behind the merge, so the L2
+      // round trip is not waited for (the next step's probes come after it)
+      uint64_t tw[2] = {0ull, 0ull};
+      uint32_t tb[2] = {kNone, kNone}, tr[2] = {0u, 0u};
+      if (m <= 64) {
+#pragma unroll
+        for (int t = 0; t < 2; t++) {
+          const uint32_t j = static_cast<uint32_t>(t) * 32 + lane;
+          if (j < m && cex[j] < P) {
+            const uint32_t h = (cid[j] * 0x85EBCA6Bu) & g2mask;
+            tb[t] = h >> 15;
+            tr[t] = h & 0x7FFFu;
+            tw[t] = probe_ld(g2 + tb[t], g2pol);
+          }
+        }
+      } else {
 #pragma unroll 1
-      for (uint32_t j0 = 0; j0 < m; j0 += 32) {
-        const uint32_t j = j0 + lane;
-        if (j < m && cex[j] < P) {
-          const uint32_t h = (cid[j] * 0x85EBCA6Bu) & g2mask;
-          const uint32_t bucket = h >> 15, rem = h & 0x7FFFu;
-          uint64_t wv;
-          wv = probe_ld(g2 + bucket, g2pol);
-          asm volatile("st.global.cg.L2::cache_hint.u64 [%0], %1, %2;" :: "l"(g2 + bucket), "l"((wv << 16) | rem), "l"(g2pol) : "memory");
+        for (uint32_t j0 = 0; j0 < m; j0 += 32) {
+          const uint32_t j = j0 + lane;
+          if (j < m && cex[j] < P) {
+            const uint32_t h = (cid[j] * 0x85EBCA6Bu) & g2mask;
+            const uint32_t bucket = h >> 15, rem = h & 0x7FFFu;
+            const uint64_t wv = probe_ld(g2 + bucket, g2pol);
+            asm volatile("st.global.cg.L2::cache_hint.u64 [%0], %1, %2;" :: "l"(g2 + bucket), "l"((wv << 16) | rem), "l"(g2pol) : "memory");
+          }
         }
       }
+      auto table_commit = [&]() {
+#pragma unroll
+        for (int t = 0; t < 2; t++)
+          if (tb[t] != kNone)
+            asm volatile("st.global.cg.L2::cache_hint.u64 [%0], %1, %2;" :: "l"(g2 + tb[t]), "l"((tw[t] << 16) | tr[t]), "l"(g2pol) : "memory");
+      };
       hint = xlast + 1;
       __syncwarp();
       // survivors of dropped expansions leave (kMaxKey sorts behind every key)
@@ -422,7 +445,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_BATCH_MINB)
         }
         __syncwarp();
       }
-      if (sreal == 0) continue;
+      if (sreal == 0) {
+        table_commit();
+        continue;
+      }
 
       // ---- survivors ranked ----
       // Fast path: ranks by a 32-bit window of the keys (cd, 4 per shared
@@ -582,6 +608,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_BATCH_MINB)
       }
       size = min(L, size + sreal);
       hint = min(hint, p0);
+      table_commit();
       __syncwarp();
     }
 
