@@ -1238,7 +1238,13 @@ int gann_search(gann_index* idx, const void* queries, uint32_t nq, uint32_t k_ou
       d2h(vis_ids, a.vis_ids, size_t(nq) * vcap * 4);
       d2h(vis_dists, a.vis_dists, size_t(nq) * vcap * 4);
     }
+    uint32_t no_region = 0;  // search_batch_kernel: warps that found no visited-table region
+    d2h(&no_region, idx->flags + 2, 4);
     sync(idx);
+    if (no_region) {
+      cu(cudaMemsetAsync(idx->flags + 2, 0, 4, idx->stream), "memset flags");
+      fail(GANN_ECUDA, "search: no free visited-table region for " + std::to_string(no_region) + " warps");
+    }
   });
 }
 

@@ -196,9 +196,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_BATCH_MINB)
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(g2pol));
   else
     asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(g2pol));
-  if (lane == 0) {
+  // (a region per resident warp of two launches exists, so a free one is
+  // found at once; the retries only cover a warp that has not released yet)
+  for (uint32_t attempt = 0; lane == 0 && g2_region == kNone && attempt < (1u << 16); attempt++) {
     const uint32_t words = (a.gtab_regions + 31) / 32;
-    const uint32_t w0 = (blockIdx.x * 32 + (threadIdx.x >> 5)) % words;
+    const uint32_t w0 = (blockIdx.x * 32 + (threadIdx.x >> 5) + attempt) % words;
     for (uint32_t t = 0; t < words && g2_region == kNone; t++) {
       const uint32_t w = (w0 + t) % words;
       uint32_t cur = a.gtab_busy[w];
@@ -215,7 +217,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_BATCH_MINB)
     }
   }
   g2_region = __shfl_sync(FULL, g2_region, 0);
-  if (g2_region == kNone) return;  // the host sizes the regions for every resident warp of two launches
+  if (g2_region == kNone) {  // cannot happen with the host's region count; loud if it does
+    if (lane == 0) atomicAdd(a.overflow + 2, 1u);
+    return;
+  }
   g2 = a.gtab + (static_cast<uint64_t>(g2_region) << a.gtab_log2);
   const uint32_t g2mask = (1u << (a.gtab_log2 + 15)) - 1u;
 
