@@ -435,8 +435,11 @@ SearchArgs base_search_args(gann_index* idx, uint32_t L, uint32_t k_gate, uint32
   const uint32_t beb = std::min<uint32_t>(env_u32("GANN_BATCH_EB", 8), 8);
   const uint32_t bcm = std::min<uint32_t>(256, std::max<uint32_t>(64, env_u32("GANN_BATCH_CM", 64) & ~31u));
   const bool batch = beb && mode == GANN_VISITED_FAST && k_gate == L && idx->R <= 64 && L < 65536 &&
-                     L >= env_u32("GANN_BATCH_MIN_L", 320) && idx->n <= (uint64_t(1) << (glog2 + 15)) &&
-                     search_batch_smem_per_warp(L, bcm) <= 200 * 1024;
+                     L >= env_u32("GANN_BATCH_MIN_L", 320) && search_batch_smem_per_warp(L, bcm) <= 200 * 1024;
+  // ids beyond the u16 remainders' reach (n > 2^(log2 + 15): 67M at the default
+  // region size): the batch kernel's buckets hold two whole ids instead, in
+  // the largest regions (GANN_GTAB_WIDE=1 forces it: tests)
+  const bool wide = batch && (idx->n > (uint64_t(1) << (glog2 + 15)) || env_u32("GANN_GTAB_WIDE", 0));
   if (batch) {
     a.batch_eb = beb;
     a.batch_cm = bcm;
@@ -458,7 +461,8 @@ SearchArgs base_search_args(gann_index* idx, uint32_t L, uint32_t k_gate, uint32
     a.gtab = idx->gtab.as<uint64_t>();
     a.gtab_busy = idx->gtab_busy.as<uint32_t>();
     a.gtab_regions = idx->gtab_regions;
-    a.gtab_log2 = glog2;
+    a.gtab_log2 = wide ? kGtabLog2 : glog2;
+    a.gtab_wide = wide ? 1 : 0;
     a.gtab_keep = static_cast<int>(env_u32("GANN_GTAB_KEEP", 1));
 
   }

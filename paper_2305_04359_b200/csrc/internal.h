@@ -93,6 +93,7 @@ struct SearchArgs {
   uint32_t gtab_regions;
   uint32_t gtab_log2;
   int gtab_keep;             // second-level table accesses carry an L2 evict_last policy
+  int gtab_wide;             // search_batch_kernel: buckets of two u32 ids (n beyond the remainders' reach)
   int next_pf;               // prefetch the next expansion's row before the merge
   // several expansions per step (search_batch.cuh; Alg. 1 form, fast mode, R <= 64):
   uint32_t batch_eb;         // expansions tried per step (0: one per step, search_kernel)

@@ -81,6 +81,29 @@ __device__ __forceinline__ uint64_t probe_ld(const uint64_t* p, uint64_t pol) {
   return v;
 }
 
+// The visited table's buckets. Narrow (n <= 2^(log2 + 15)): four u16 slots per
+// u64 bucket holding the 15-bit remainders of a bijective hash of the id, so a
+// match is the same id (0xFFFF: empty); the bucket is the hash's upper bits.
+// Wide (larger n, up to 2^32 - 2): two u32 slots holding whole ids (0xFFFFFFFF:
+// empty). An insert shifts the bucket and drops its oldest slot.
+__device__ __forceinline__ uint32_t tab_bucket(uint32_t id, bool wide, uint32_t mask, uint32_t log2) {
+  const uint32_t h = id * 0x85EBCA6Bu;
+  return wide ? h >> (32u - log2) : (h & mask) >> 15;
+}
+__device__ __forceinline__ bool tab_hit(uint64_t w, uint32_t id, bool wide) {
+  if (wide) return static_cast<uint32_t>(w) == id || static_cast<uint32_t>(w >> 32) == id;
+  const uint32_t rem = (id * 0x85EBCA6Bu) & 0x7FFFu;
+  const uint32_t rr = rem | (rem << 16);
+  // a u16 slot equal to rem <=> a zero half word in w ^ rr (exact as a yes/no:
+  // a borrow only ever follows a true zero)
+  const uint32_t y0 = static_cast<uint32_t>(w) ^ rr, y1 = static_cast<uint32_t>(w >> 32) ^ rr;
+  return ((((y0 - 0x00010001u) & ~y0) | ((y1 - 0x00010001u) & ~y1)) & 0x80008000u) != 0u;
+}
+__device__ __forceinline__ uint64_t tab_insert(uint64_t w, uint32_t id, bool wide) {
+  if (wide) return (w << 32) | id;
+  return (w << 16) | ((id * 0x85EBCA6Bu) & 0x7FFFu);
+}
+
 // One gather pass (eval_pass) that also carries each row's expansion index
 // next to its key.
 template <class Op, int LPR, int CPL, int UU, bool FIT>
@@ -223,6 +246,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_BATCH_MINB)
   }
   g2 = a.gtab + (static_cast<uint64_t>(g2_region) << a.gtab_log2);
   const uint32_t g2mask = (1u << (a.gtab_log2 + 15)) - 1u;
+  const bool wide = a.gtab_wide != 0;
 
   uint32_t q = 0;
   if (lane == 0) q = atomicAdd(a.next_query, 1u);
@@ -298,7 +322,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_BATCH_MINB)
         for (int h = 0; h < 2; h++) {
           w[e][h] = 0ull;
           if (nb[e][h] != kNone) {
-            const uint32_t bucket = ((nb[e][h] * 0x85EBCA6Bu) & g2mask) >> 15;
+            const uint32_t bucket = tab_bucket(nb[e][h], wide, g2mask, a.gtab_log2);
             w[e][h] = probe_ld(g2 + bucket, g2pol);
           }
         }
@@ -312,13 +336,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_BATCH_MINB)
           bool fr[2];
 #pragma unroll
           for (int h = 0; h < 2; h++) {
-            const uint32_t rem = (nb[e][h] * 0x85EBCA6Bu) & 0x7FFFu;
-            const uint32_t rr = rem | (rem << 16);
-            // a u16 slot equal to rem <=> a zero half word in w ^ rr (exact as a
-            // yes/no: a borrow only ever follows a true zero)
-            const uint32_t y0 = static_cast<uint32_t>(w[e][h]) ^ rr, y1 = static_cast<uint32_t>(w[e][h] >> 32) ^ rr;
-            const uint32_t z = (((y0 - 0x00010001u) & ~y0) | ((y1 - 0x00010001u) & ~y1)) & 0x80008000u;
-            fr[h] = nb[e][h] != kNone && z == 0u;
+            fr[h] = nb[e][h] != kNone && !tab_hit(w[e][h], nb[e][h], wide);
           }
           const uint32_t b0 = __ballot_sync(FULL, fr[0]), b1 = __ballot_sync(FULL, fr[1]);
           const uint32_t c = __popc(b0) + __popc(b1);
@@ -406,15 +424,14 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_BATCH_MINB)
       // here and written at the end of the step, behind the merge, so the L2
       // round trip is not waited for (the next step's probes come after it)
       uint64_t tw[2] = {0ull, 0ull};
-      uint32_t tb[2] = {kNone, kNone}, tr[2] = {0u, 0u};
+      uint32_t tb[2] = {kNone, kNone}, tr[2] = {0u, 0u};  // bucket, id
       if (m <= 64) {
 #pragma unroll
         for (int t = 0; t < 2; t++) {
           const uint32_t j = static_cast<uint32_t>(t) * 32 + lane;
           if (j < m && cex[j] < P) {
-            const uint32_t h = (cid[j] * 0x85EBCA6Bu) & g2mask;
-            tb[t] = h >> 15;
-            tr[t] = h & 0x7FFFu;
+            tr[t] = cid[j];
+            tb[t] = tab_bucket(tr[t], wide, g2mask, a.gtab_log2);
             tw[t] = probe_ld(g2 + tb[t], g2pol);
           }
         }
@@ -423,10 +440,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_BATCH_MINB)
         for (uint32_t j0 = 0; j0 < m; j0 += 32) {
           const uint32_t j = j0 + lane;
           if (j < m && cex[j] < P) {
-            const uint32_t h = (cid[j] * 0x85EBCA6Bu) & g2mask;
-            const uint32_t bucket = h >> 15, rem = h & 0x7FFFu;
+            const uint32_t bucket = tab_bucket(cid[j], wide, g2mask, a.gtab_log2);
             const uint64_t wv = probe_ld(g2 + bucket, g2pol);
-            asm volatile("st.global.cg.L2::cache_hint.u64 [%0], %1, %2;" :: "l"(g2 + bucket), "l"((wv << 16) | rem), "l"(g2pol) : "memory");
+            asm volatile("st.global.cg.L2::cache_hint.u64 [%0], %1, %2;" :: "l"(g2 + bucket), "l"(tab_insert(wv, cid[j], wide)), "l"(g2pol) : "memory");
           }
         }
       }
@@ -434,7 +450,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_BATCH_MINB)
 #pragma unroll
         for (int t = 0; t < 2; t++)
           if (tb[t] != kNone)
-            asm volatile("st.global.cg.L2::cache_hint.u64 [%0], %1, %2;" :: "l"(g2 + tb[t]), "l"((tw[t] << 16) | tr[t]), "l"(g2pol) : "memory");
+            asm volatile("st.global.cg.L2::cache_hint.u64 [%0], %1, %2;" :: "l"(g2 + tb[t]), "l"(tab_insert(tw[t], tr[t], wide)), "l"(g2pol) : "memory");
       };
       hint = xlast + 1;
       __syncwarp();
@@ -691,7 +707,8 @@ cudaError_t launch_batch(const SearchArgs& a, cudaStream_t s) {
   {
     static const int kCarveKB[] = {8, 16, 32, 64, 100, 132, 164, 196, 228};
     const size_t cta = size_t(per_warp) * wpb + 1024;
-    const uint32_t l1_per_warp = 4096;
+    uint32_t l1_per_warp = 4096;
+    if (const char* lv = std::getenv("GANN_BATCH_L1KB")) l1_per_warp = static_cast<uint32_t>(std::atoi(lv)) * 1024u;  // experiment
     int c = std::max(1, per_sm), carve = 228;
     for (; c >= 1; c--) {
       carve = 228;

@@ -22,7 +22,7 @@ def _g():
 
 @pytest.fixture()
 def batch_env():
-    keys = ("GANN_BATCH_MIN_L", "GANN_BATCH_EB", "GANN_BATCH_CM", "GANN_BATCH_POLICY")
+    keys = ("GANN_BATCH_MIN_L", "GANN_BATCH_EB", "GANN_BATCH_CM", "GANN_BATCH_POLICY", "GANN_GTAB_WIDE")
     old = {k: os.environ.get(k) for k in keys}
     os.environ["GANN_BATCH_MIN_L"] = "0"
     yield os.environ
@@ -117,3 +117,19 @@ def test_batch_build_bit_identical(oracle, batch_env, cap):
     ref_adj, ref_start = oracle.build(data, 32, 64, 1.2, cap=cap, workers=4)
     assert start == ref_start
     assert int((adj != ref_adj).any(axis=1).sum()) == 0
+
+
+@pytest.mark.parametrize("L", [48, 330])
+def test_batch_wide_table(oracle, batch_env, L):
+    """The visited table's whole-id buckets (taken when n exceeds the u16
+    remainders' reach, 2^26 at the default region size; forced here)."""
+    g = _g()
+    batch_env["GANN_GTAB_WIDE"] = "1"
+    data, qs = mixture(26, 5000, 96, clusters=10, nq=200)
+    adj, start = oracle.build(data, 48, 64, 1.2, workers=4)
+    idx = g.Index(data, "l2", adj.shape[1])
+    idx.import_graph(adj, start)
+    vcap = 4 * L + 64
+    want = oracle.beam_search(adj, start, data, qs, L, L, 0.0, visited_mode=1, vcap=vcap, workers=4)
+    got = idx.search(qs, g.SearchParams(L, L, 0.0), vcap=vcap)
+    _check(got, want, len(qs))
