@@ -166,6 +166,11 @@ int gann_apply_back_edges(gann_index* idx, const uint32_t* targets, const uint32
  * batch_ranges — graphann::batch_ranges (src/builder_common.cpp:13-20) with the
  *   optional cap; returns the number of ranges (writes at most max_ranges). */
 void gann_shuffled_order(uint32_t n, uint64_t seed, uint32_t front, uint32_t* out);
+/* std::shuffle's swap log for (n, seed): log[i] is the position the same
+ * libstdc++ call swaps element i with (log[0] = 0), i.e. shuffled_order before
+ * its front swap is `a = iota; for i in 1..n-1: swap(a[i], a[log[i]])`. gann_build
+ * draws this log on the host and resolves the permutation on the device. */
+void gann_shuffle_swap_log(uint32_t n, uint64_t seed, uint32_t* log);
 uint32_t gann_batch_ranges(uint64_t n, uint32_t max_batch, uint32_t* lo, uint32_t* hi,
                            uint32_t max_ranges);
 /* The seed build_diskann derives for shuffled_order: mix64(seed, "insert"). */

@@ -8,7 +8,7 @@ if it is missing — there is no CPU fallback.
 from ._lib import GANN_NONE, GannError, LIB_PATH, lib
 from .api import (DiskannParams, GroupedPairs, HnswIndex, Index, PruneParams, SearchParams, SearchResult,
                   alpha_prune, apply_back_edges, batch_ranges, beam_search, build_diskann,
-                  choose_start, group_by_key, insert_point, insert_seed, search_hnsw, shuffled_order)
+                  choose_start, group_by_key, insert_point, insert_seed, search_hnsw, shuffle_swap_log, shuffled_order)
 
 lib()  # load now: a missing/unbuildable extension is an import error, not a silent fallback
 
@@ -16,5 +16,5 @@ __all__ = [
     "GANN_NONE", "GannError", "LIB_PATH", "DiskannParams", "GroupedPairs", "HnswIndex", "Index", "PruneParams",
     "SearchParams", "SearchResult", "alpha_prune", "apply_back_edges", "batch_ranges", "beam_search",
     "build_diskann", "choose_start", "group_by_key", "insert_point", "insert_seed", "search_hnsw",
-    "shuffled_order",
+    "shuffle_swap_log", "shuffled_order",
 ]

@@ -73,6 +73,7 @@ SIGNATURES = {
     "gann_insert_batch": (_i, [_vp, _vp, _u32, _u32, _f, _i, _vp]),
     "gann_apply_back_edges": (_i, [_vp, _vp, _vp, _u64, _f, _i]),
     "gann_shuffled_order": (None, [_u32, _u64, _u32, _vp]),
+    "gann_shuffle_swap_log": (None, [_u32, _u64, _vp]),
     "gann_batch_ranges": (_u32, [_u64, _u32, _vp, _vp, _u32]),
     "gann_insert_seed": (_u64, [_u64]),
     "gann_groundtruth": (_i, [_vp, _vp, _u32, _u32, _vp, _vp]),

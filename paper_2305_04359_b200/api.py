@@ -453,6 +453,13 @@ def shuffled_order(n: int, seed: int, front: int) -> np.ndarray:
     return out
 
 
+def shuffle_swap_log(n: int, seed: int) -> np.ndarray:
+    """std::shuffle's swap log for (n, seed) (gann_shuffle_swap_log): element i swaps with log[i]."""
+    out = np.empty(n, np.uint32)
+    lib().gann_shuffle_swap_log(n, seed, _p(out))
+    return out
+
+
 def insert_seed(seed: int) -> int:
     """The seed build_diskann passes to shuffled_order (src/diskann.cpp:51)."""
     return int(lib().gann_insert_seed(seed))

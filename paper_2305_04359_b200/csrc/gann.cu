@@ -22,6 +22,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
+#include <iterator>
 #include <random>
 #include <stdexcept>
 #include <string>
@@ -158,6 +159,64 @@ void hash_config(uint32_t L, uint64_t n, uint32_t* log2, uint32_t* bits, uint32_
 }
 
 }  // namespace
+
+// std::shuffle's swap log. libstdc++'s shuffle touches its range only through
+// iter_swap(i, first + pos) for i = first + 1 .. last - 1 (bits/stl_algo.h, both
+// its one-draw-two-swaps path and the plain one). Run over this iterator it
+// draws from the generator exactly as over a vector, but a "swap" only records
+// log[i] = pos — sequential writes instead of random ones — and the permutation
+// is resolved on the device (misc.cu launch_shuffle_from_log). Same library
+// call, same draws, so the order equals shuffled_order's (src/builder_common.cpp:99-107).
+namespace swaplog {
+struct Val {
+  uint32_t src;
+};
+struct Ref {
+  uint32_t idx;
+  uint32_t* log;
+  operator Val() const { return Val{idx}; }
+  const Ref& operator=(const Ref& o) const {  // *a = *b inside a three-step swap: a receives b's element
+    log[idx] = o.idx;
+    return *this;
+  }
+  const Ref& operator=(const Val&) const { return *this; }  // *b = tmp: the other half of the same swap
+  friend void swap(Ref a, Ref b) { a.log[a.idx] = b.idx; }
+};
+struct It {
+  using iterator_category = std::random_access_iterator_tag;
+  using value_type = Val;
+  using difference_type = int64_t;
+  using pointer = void;
+  using reference = Ref;
+  int64_t i;
+  uint32_t* log;
+  Ref operator*() const { return Ref{static_cast<uint32_t>(i), log}; }
+  Ref operator[](difference_type k) const { return Ref{static_cast<uint32_t>(i + k), log}; }
+  It& operator++() { ++i; return *this; }
+  It operator++(int) { It t = *this; ++i; return t; }
+  It& operator--() { --i; return *this; }
+  It operator--(int) { It t = *this; --i; return t; }
+  It& operator+=(difference_type k) { i += k; return *this; }
+  It& operator-=(difference_type k) { i -= k; return *this; }
+  friend It operator+(It a, difference_type k) { a.i += k; return a; }
+  friend It operator+(difference_type k, It a) { a.i += k; return a; }
+  friend It operator-(It a, difference_type k) { a.i -= k; return a; }
+  friend difference_type operator-(It a, It b) { return a.i - b.i; }
+  friend bool operator==(It a, It b) { return a.i == b.i; }
+  friend bool operator!=(It a, It b) { return a.i != b.i; }
+  friend bool operator<(It a, It b) { return a.i < b.i; }
+  friend bool operator>(It a, It b) { return a.i > b.i; }
+  friend bool operator<=(It a, It b) { return a.i <= b.i; }
+  friend bool operator>=(It a, It b) { return a.i >= b.i; }
+};
+}  // namespace swaplog
+
+// log[i] = the position std::shuffle(first, first + n, mt19937_64(seed)) swaps element i with (log[0] = 0)
+static void shuffle_swap_log(uint64_t n, uint64_t seed, uint32_t* log) {
+  for (uint64_t i = 0; i < n; i++) log[i] = static_cast<uint32_t>(i);
+  std::mt19937_64 rng(seed);
+  std::shuffle(swaplog::It{0, log}, swaplog::It{static_cast<int64_t>(n), log}, rng);
+}
 
 constexpr uint32_t kQueryCounters = 64;  // per-launch query counters per index
 
@@ -1011,8 +1070,11 @@ int gann_build(gann_index* idx, uint32_t L, float alpha, int rule, uint64_t seed
     // the shuffle does not depend on the start vertex (only the final swap
     // does), so it runs on a host thread while the device picks the start
     // and the batch scratch is allocated
-    std::vector<uint32_t> order(n);
+    // (GANN_HOST_SHUFFLE=1: std::shuffle over the array itself, as round 1 did)
+    const bool host_shuffle = env_u32("GANN_HOST_SHUFFLE", 0) != 0;
+    std::vector<uint32_t> order(n);  // the host shuffle's array, or the swap log
     std::thread shuffler([&] {
+      if (!host_shuffle) return shuffle_swap_log(n, mix64(seed, 0x696e73657274ULL), order.data());
       for (uint64_t i = 0; i < n; i++) order[i] = static_cast<uint32_t>(i);
       std::mt19937_64 rng(mix64(seed, 0x696e73657274ULL));
       std::shuffle(order.begin(), order.end(), rng);
@@ -1057,9 +1119,25 @@ int gann_build(gann_index* idx, uint32_t L, float alpha, int rule, uint64_t seed
       throw;
     }
     shuffler.join();
-    std::iter_swap(order.begin(), std::find(order.begin(), order.end(), start));
-    cu(cudaMemcpyAsync(idx->order.p, order.data(), n * 4, cudaMemcpyHostToDevice, idx->stream),
-       "upload order");
+    if (host_shuffle) {
+      std::iter_swap(order.begin(), std::find(order.begin(), order.end(), start));
+      cu(cudaMemcpyAsync(idx->order.p, order.data(), n * 4, cudaMemcpyHostToDevice, idx->stream),
+         "upload order");
+    } else {
+      // the permutation from the swap log, on the device (5 n u32 of scratch, freed again)
+      DevBuf work;
+      work.ensure(n * 5 * 4);
+      uint32_t* d_log = work.as<uint32_t>();
+      cu(cudaMemcpyAsync(d_log, order.data(), n * 4, cudaMemcpyHostToDevice, idx->stream), "upload swap log");
+      void* tmp = nullptr;
+      size_t tmp_bytes = 0;
+      const cudaError_t e = launch_shuffle_from_log(d_log, n, start, d_log + n, idx->order.as<uint32_t>(), &tmp,
+                                                    &tmp_bytes, idx->stream);
+      if (e == cudaSuccess) cudaStreamSynchronize(idx->stream);
+      if (tmp) cudaFree(tmp);
+      work.release();
+      cu(e, "shuffle from log");
+    }
     t0.stop(idx, 0);
     const uint32_t* d_order = idx->order.as<uint32_t>();
     const bool trace = env_u32("GANN_TRACE", 0) != 0;
@@ -1697,6 +1775,8 @@ int gann_generate_f32(void* d_out, uint64_t n, uint32_t d, uint32_t clusters, fl
     cu(cudaDeviceSynchronize(), "generate sync");
   });
 }
+
+void gann_shuffle_swap_log(uint32_t n, uint64_t seed, uint32_t* log) { shuffle_swap_log(n, seed, log); }
 
 void gann_shuffled_order(uint32_t n, uint64_t seed, uint32_t front, uint32_t* out) {
   std::vector<uint32_t> order(n);

@@ -268,6 +268,10 @@ uint32_t groundtruth_splits(uint64_t n, uint32_t nq);
 cudaError_t stable_sort_pairs_u32(const uint32_t* keys_in, uint32_t* keys_out, const uint32_t* vals_in,
                                   uint32_t* vals_out, uint64_t m, int bits, void** tmp, size_t* tmp_bytes,
                                   cudaStream_t s);
+// The shuffled insertion order from std::shuffle's swap log r (misc.cu): out[0..n), front in slot 0;
+// work: 4 n u32 of device scratch.
+cudaError_t launch_shuffle_from_log(const uint32_t* r, uint64_t n, uint32_t front, uint32_t* work, uint32_t* out,
+                                    void** tmp, size_t* tmp_bytes, cudaStream_t s);
 // Validate rows [0, rows) of an n-vertex graph (row r is vertex row0 + r):
 // *bad = ~0 if fine, else (first bad row << 3) | code (1 id after padding,
 // 2 id out of range, 3 self loop, 4 repeated id).

@@ -541,6 +541,79 @@ cudaError_t stable_sort_pairs_u32(const uint32_t* keys_in, uint32_t* keys_out, c
                                          bits, s);
 }
 
+// ---- std::shuffle's result from its swap log --------------------------------
+// libstdc++'s std::shuffle over n elements is the swap sequence
+//   for i = 1 .. n-1: swap(a[i], a[r_i]),  r_i <= i drawn from the generator
+// (bits/stl_algo.h; the host records r with an iterator that logs the swaps
+// instead of doing them: gann.cu shuffle_swap_log). On iota, a[i] is untouched
+// before step i, so step i places value i at position r_i and moves that
+// position's occupant to position i. With T_p = the steps that target p in
+// ascending order (r_0 := 0 makes 0 the first step of T_0):
+//   * the final occupant of p is the last step of T_p, or, when nothing
+//     targets p, the first occupant of p;
+//   * the first occupant of p (at time p) is the occupant of r_p just before
+//     step p: the step before p in T_{r_p}, or, when p is that list's first
+//     step, the first occupant of r_p (r_p < p: the chain walks down).
+// The lists come from one stable radix sort of (r_i, i); a thread per
+// position then follows its chain (expected length O(log n)).
+namespace {
+__global__ void iota_kernel(uint32_t* v, uint64_t n) {
+  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (i < n) v[i] = static_cast<uint32_t>(i);
+}
+// sorted by target: prev[step] = the step before it on the same target (kNone: first), last[target] = its last step
+__global__ void shuffle_lists_kernel(const uint32_t* tgt, const uint32_t* step, uint64_t n, uint32_t* prev,
+                                     uint32_t* last) {
+  const uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (j >= n) return;
+  const uint32_t t = tgt[j], st = step[j];
+  prev[st] = (j > 0 && tgt[j - 1] == t) ? step[j - 1] : kNone;
+  if (j + 1 == n || tgt[j + 1] != t) last[t] = st;
+}
+__global__ void shuffle_resolve_kernel(const uint32_t* r, const uint32_t* prev, const uint32_t* last, uint64_t n,
+                                       uint32_t* out, uint32_t front, uint32_t* front_pos) {
+  const uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (p >= n) return;
+  uint32_t v = last[p];
+  if (v == kNone) {
+    uint32_t q = static_cast<uint32_t>(p);
+    while ((v = prev[q]) == kNone) q = r[q];
+  }
+  out[p] = v;
+  if (v == front) *front_pos = static_cast<uint32_t>(p);
+}
+// shuffled_order's last step (src/builder_common.cpp:104-105): the front vertex swaps into slot 0
+__global__ void shuffle_front_kernel(uint32_t* out, const uint32_t* front_pos) {
+  const uint32_t p = *front_pos, a = out[0];
+  out[0] = out[p];
+  out[p] = a;
+}
+}  // namespace
+
+// out[0..n) = the shuffled insertion order for the swap log r (device, r[0] = 0), with `front` moved to slot 0.
+// work: 4 n u32 of scratch (device).
+cudaError_t launch_shuffle_from_log(const uint32_t* r, uint64_t n, uint32_t front, uint32_t* work, uint32_t* out,
+                                    void** tmp, size_t* tmp_bytes, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  uint32_t* iota = work;
+  uint32_t* tgt = work + n;
+  uint32_t* step = work + 2 * n;
+  uint32_t* prev = work + 3 * n;
+  uint32_t* last = iota;  // iota is dead after the sort
+  const unsigned blocks = static_cast<unsigned>((n + 255) / 256);
+  iota_kernel<<<blocks, 256, 0, s>>>(iota, n);
+  int bits = 1;
+  while (bits < 32 && (uint64_t(1) << bits) < n) bits++;
+  cudaError_t e = stable_sort_pairs_u32(r, tgt, iota, step, n, bits, tmp, tmp_bytes, s);
+  if (e != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(last, 0xFF, n * 4, s)) != cudaSuccess) return e;
+  shuffle_lists_kernel<<<blocks, 256, 0, s>>>(tgt, step, n, prev, last);
+  // the sorted targets are dead once the lists are built: tgt[0] holds front's position
+  shuffle_resolve_kernel<<<blocks, 256, 0, s>>>(r, prev, last, n, out, front, tgt);
+  shuffle_front_kernel<<<1, 1, 0, s>>>(out, tgt);
+  return cudaGetLastError();
+}
+
 GANN_CHECK_READER(check_line_misc)
 
 }  // namespace gann

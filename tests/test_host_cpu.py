@@ -56,6 +56,25 @@ def test_host_schedule_matches_reference(orc):
     assert g.insert_seed(42) == 16503569613174706033
 
 
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 7, 1000, 1001, 65536, 300_001])
+def test_shuffle_swap_log_replays_to_the_reference_order(orc, n):
+    """gann_build draws std::shuffle's swap log on the host (the same libstdc++
+    call over a logging iterator) and resolves the permutation on the device;
+    here the log is replayed sequentially and must give shuffled_order
+    (src/builder_common.cpp:99-107) before its front swap — odd and even n
+    (libstdc++ pairs the swaps and does an extra first one for even n)."""
+    import paper_2305_04359_b200 as g
+    seed = g.insert_seed(42)
+    log = g.shuffle_swap_log(n, seed)
+    assert log[0] == 0 and (log <= np.arange(n)).all()
+    a = list(range(n))
+    for i in range(1, n):
+        j = int(log[i])
+        a[i], a[j] = a[j], a[i]
+    want = orc.shuffled_order(n, seed, a[0])  # front = the element already first: no front swap
+    assert (np.array(a, np.uint32) == want).all()
+
+
 def test_datagen_is_deterministic_and_prefix_stable():
     from paper_2305_04359_b200 import datagen
     a = datagen.gen_u8_numpy(500, 128, 1000, 20.0, 0.0, 1, 2)
