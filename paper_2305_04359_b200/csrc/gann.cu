@@ -315,7 +315,7 @@ gann_index* new_index(uint64_t n, uint32_t d, int elem, int metric, uint32_t R, 
       parts[rank] = idx->adj;
       cu(cudaMemcpy(idx->d_parts, parts.data(), sizeof(uint32_t*) * nparts, cudaMemcpyHostToDevice), "parts");
     }
-    cu(cudaMalloc(&idx->stats, sizeof(unsigned long long) * kStCount), "cudaMalloc stats");
+    cu(cudaMalloc(&idx->stats, sizeof(unsigned long long) * kStCount * kStatSlots), "cudaMalloc stats");
     cu(cudaMalloc(&idx->counters, sizeof(unsigned long long) * kCntNum), "cudaMalloc counters");
     cu(cudaMalloc(&idx->flags, 16), "cudaMalloc flags");
     cu(cudaMalloc(&idx->qctr, kQueryCounters * 4), "cudaMalloc query counters");
@@ -323,7 +323,7 @@ gann_index* new_index(uint64_t n, uint32_t d, int elem, int metric, uint32_t R, 
     cu(cudaMemsetAsync(idx->adj, 0xFF, rows * std::max<uint32_t>(R, 1) * 4, idx->stream), "memset");
     cu(cudaMemsetAsync(idx->spre, 0, std::max<uint64_t>(rows, 1), idx->stream), "memset");
     cu(cudaMemsetAsync(idx->tcount, 0, rows * 4, idx->stream), "memset");
-    cu(cudaMemsetAsync(idx->stats, 0, sizeof(unsigned long long) * kStCount, idx->stream), "memset");
+    cu(cudaMemsetAsync(idx->stats, 0, sizeof(unsigned long long) * kStCount * kStatSlots, idx->stream), "memset");
     cu(cudaMemsetAsync(idx->flags, 0, 16, idx->stream), "memset");
     // load the kernels this index will launch now rather than at their first
     // launch inside a timed build (internal.h); once per process and kind
@@ -657,6 +657,9 @@ void prune_binned(gann_index* idx, PruneArgs p, uint32_t maxlen, bool fine = fal
   static const bool small_on = env_u32("GANN_SMALL_REPRUNE", 1) != 0;
   const bool small = mma && p.row_lists && p.spre && idx->R <= 64 && small_on;
   p.small_u = small ? reprune_small_max_u() : 0u;
+  // ... in two classes: lists with at most 2 such entries run a smaller instance (GANN_SMALL_U2=0: one class)
+  static const bool small2_on = env_u32("GANN_SMALL_U2", 1) != 0;
+  p.small_u2 = small && small2_on ? reprune_small_low_u() : 0u;
   idx->bins.ensure(size_t(p.count) * (nb + 2) * 4 + 64 * 4);
   uint32_t* d_counts = idx->bins.as<uint32_t>();
   uint32_t* d_bounds = d_counts + 16;
@@ -664,15 +667,24 @@ void prune_binned(gann_index* idx, PruneArgs p, uint32_t maxlen, bool fine = fal
   cu(cudaMemcpyAsync(d_bounds, bounds.data(), bounds.size() * 4, cudaMemcpyHostToDevice, idx->stream), "bins");
   cu(launch_bin_lists(p, d_bounds, nb, d_counts, d_lists, idx->stream), "bin lists");
   uint32_t counts[16] = {};
-  cu(cudaMemcpyAsync(counts, d_counts, (nb + 1) * 4, cudaMemcpyDeviceToHost, idx->stream), "bin counts");
+  cu(cudaMemcpyAsync(counts, d_counts, (nb + 2) * 4, cudaMemcpyDeviceToHost, idx->stream), "bin counts");
   sync(idx);
   uint32_t lo = 0, total = 0;
-  if (counts[nb]) {
+  if (p.small_u && std::getenv("GANN_PRUNE_DEBUG")) {
+    static unsigned long long acc[3] = {0, 0, 0};
+    acc[0] += counts[nb];
+    acc[1] += counts[nb + 1];
+    acc[2] += p.count;
+    std::fprintf(stderr, "re-prune lists so far: %llu with <= 2 extra entries, %llu with 3-4, %llu in all\n", acc[0], acc[1], acc[2]);
+  }
+  for (int c = nb; c <= nb + 1; c++) {
+    if (!counts[c]) continue;
     PruneArgs q = p;
-    q.list_index = d_lists + size_t(nb) * p.count;
-    q.count = counts[nb];
+    q.list_index = d_lists + size_t(c) * p.count;
+    q.count = counts[c];
+    q.small_u = c == nb ? p.small_u2 : p.small_u;  // selects the instance
     cu(launch_reprune_small(q, idx->elem, idx->metric, idx->geom, idx->stream), "re-prune (warp)");
-    total += counts[nb];
+    total += counts[c];
   }
   for (int b = 0; b < nb; b++) {
     total += counts[b];
@@ -2370,8 +2382,10 @@ int gann_get_stats(const gann_index* idx, gann_stats* out) {
     if (!idx || !out) fail(GANN_EINVAL, "NULL argument");
     cudaSetDevice(idx->device);
     cu(cudaDeviceSynchronize(), "device sync");  // launches on any stream have counted
-    unsigned long long s[kStCount];
-    cu(cudaMemcpy(s, idx->stats, sizeof(s), cudaMemcpyDeviceToHost), "read stats");
+    unsigned long long slots[kStCount * kStatSlots], s[kStCount] = {};
+    cu(cudaMemcpy(slots, idx->stats, sizeof(slots), cudaMemcpyDeviceToHost), "read stats");
+    for (uint32_t t = 0; t < kStatSlots; t++)
+      for (uint32_t i = 0; i < kStCount; i++) s[i] += slots[t * kStCount + i];
     out->queries = s[kStQueries];
     out->expansions = s[kStExpansions];
     out->evaluations = s[kStEvals];
@@ -2398,7 +2412,7 @@ int gann_reset_stats(gann_index* idx) {
     set_device(idx);
     // launches queued on other streams (any caller stream) count before the reset
     cu(cudaDeviceSynchronize(), "device sync");
-    cu(cudaMemsetAsync(idx->stats, 0, sizeof(unsigned long long) * kStCount, idx->stream), "memset");
+    cu(cudaMemsetAsync(idx->stats, 0, sizeof(unsigned long long) * kStCount * kStatSlots, idx->stream), "memset");
     sync(idx);
   });
 }

@@ -50,6 +50,20 @@ enum StatIdx {
   kStPruneLists, kStPruneCands, kStPruneEvals, kStMerges, kStSurvivors, kStMoved, kStDups, kStGuess, kStCount
 };
 
+// The counters are replicated kStatSlots times (a prune CTA adds to slot
+// blockIdx % kStatSlots; gann_get_stats sums the slots): one set of addresses
+// took every list's atomics, and at ~130M lists per c1 build their
+// serialisation at L2 cost the re-prune phase 15% (797 -> 679 ms). The search
+// kernels (three adds per query) stay on slot 0: the slot arithmetic cost
+// search_kernel its 72nd-register budget (73 registers: 6 CTAs instead of 7,
+// build search phase 1447 -> 1594 ms).
+constexpr uint32_t kStatSlots = 64;
+#ifdef __CUDACC__
+__device__ __forceinline__ unsigned long long* stat_slot(unsigned long long* stats) {
+  return stats + (blockIdx.x % kStatSlots) * kStCount;
+}
+#endif
+
 struct SearchArgs {
   const uint8_t* data;       // n rows of `stride` bytes
   uint64_t stride;
@@ -164,6 +178,7 @@ struct PruneArgs {
   // bin_lists: re-prune lists (row_lists) whose row prefix leaves at most
   // small_u other entries go to an extra bin (index nb) for the warp kernel
   uint32_t small_u;
+  uint32_t small_u2;           // ... and those with at most small_u2 of them to bin nb, the rest of the class to nb + 1
 };
 // threads = 32 for short lists, larger for hubs; smem from prune_smem_bytes.
 size_t prune_smem_bytes(uint32_t mcap, uint32_t R);
@@ -175,6 +190,7 @@ cudaError_t launch_bin_lists(const PruneArgs& a, const uint32_t* d_bounds, int n
 // Re-prunes of a row prefix plus <= small_u entries (integer rows, R <= 64):
 // one warp per list (prune.cu reprune_small_kernel).
 uint32_t reprune_small_max_u();
+uint32_t reprune_small_low_u();
 cudaError_t launch_reprune_small(const PruneArgs& a, int elem, int metric, const Geometry& g, cudaStream_t s);
 // Integer lists up to 512 candidates run on the tensor cores (IMMA tiles).
 bool prune_uses_mma(int elem, uint32_t mcap, uint64_t stride, uint32_t R);

@@ -196,9 +196,9 @@ __global__ void __launch_bounds__(NT) prune_kernel(const PruneArgs a, const uint
       if (a.n_out) a.n_out[l] = nsel;
       if (a.spre && !a.out_rows) a.spre[p - a.out_base] = static_cast<uint8_t>(nsel < 255 ? nsel : 255);
       if (a.stats) {
-        atomicAdd(a.stats + kStPruneLists, 1ull);
-        atomicAdd(a.stats + kStPruneCands, static_cast<unsigned long long>(m));
-        atomicAdd(a.stats + kStPruneEvals, static_cast<unsigned long long>(evals));
+        atomicAdd(stat_slot(a.stats) + kStPruneLists, 1ull);
+        atomicAdd(stat_slot(a.stats) + kStPruneCands, static_cast<unsigned long long>(m));
+        atomicAdd(stat_slot(a.stats) + kStPruneEvals, static_cast<unsigned long long>(evals));
       }
     }
     cta_sync<NT>();
@@ -768,10 +768,10 @@ __global__ void __launch_bounds__(PrepThreads<W>::value)
     const uint4* srcm = reinterpret_cast<const uint4*>(cm);
     for (uint32_t i = tid; i < m2 * (W / 4); i += NT) dst[i] = srcm[i];
     if (tid == 0 && a.stats) {
-      atomicAdd(a.stats + kStPruneLists, 1ull);
-      atomicAdd(a.stats + kStPruneCands, static_cast<unsigned long long>(m));
+      atomicAdd(stat_slot(a.stats) + kStPruneLists, 1ull);
+      atomicAdd(stat_slot(a.stats) + kStPruneCands, static_cast<unsigned long long>(m));
       // pair tests evaluated on the tensor cores
-      atomicAdd(a.stats + kStPruneEvals, static_cast<unsigned long long>(m2) * (m2 - (m2 > 0)) / 2);
+      atomicAdd(stat_slot(a.stats) + kStPruneEvals, static_cast<unsigned long long>(m2) * (m2 - (m2 > 0)) / 2);
     }
   }
 }
@@ -856,18 +856,18 @@ __global__ void bin_lists_kernel(const PruneArgs a, const uint32_t* bounds, int 
   const bool valid = li < a.count;
   const uint32_t l = valid ? (a.list_index ? a.list_index[li] : li) : 0u;
   const uint32_t m = valid ? a.lengths[l] : 0u;
-  int b = nb + 1;  // longer than every bound
+  int b = nb + 2;  // longer than every bound
   if (valid)
     for (int i = 0; i < nb; i++)
       if (m <= bounds[i]) {
         b = i;
         break;
       }
-  if (valid && a.small_u && a.row_lists && a.spre) {  // the warp re-prune's class (bin nb)
+  if (valid && a.small_u && a.row_lists && a.spre) {  // the warp re-prune's classes (bins nb: few entries, nb + 1)
     const uint32_t S = min(static_cast<uint32_t>(a.spre[a.points[l] - a.out_base]), m);
-    if (S <= 64 && m - S <= a.small_u) b = nb;
+    if (S <= 64 && m - S <= a.small_u) b = (a.small_u2 && m - S <= a.small_u2) ? nb : nb + 1;
   }
-  for (int i = 0; i <= nb; i++) {  // warp-aggregated append per bin
+  for (int i = 0; i <= nb + 1; i++) {  // warp-aggregated append per bin
     const uint32_t mask = __ballot_sync(0xFFFFFFFFu, b == i);
     if (!mask) continue;
     const int lane = threadIdx.x & 31;
@@ -881,7 +881,7 @@ __global__ void bin_lists_kernel(const PruneArgs a, const uint32_t* bounds, int 
 
 cudaError_t launch_bin_lists(const PruneArgs& a, const uint32_t* d_bounds, int nb, uint32_t* d_counts,
                              uint32_t* d_lists, cudaStream_t s) {
-  cudaError_t e = cudaMemsetAsync(d_counts, 0, sizeof(uint32_t) * (nb + 1), s);  // + the warp re-prune class
+  cudaError_t e = cudaMemsetAsync(d_counts, 0, sizeof(uint32_t) * (nb + 2), s);  // + the warp re-prune's two classes
   if (e != cudaSuccess || a.count == 0) return e;
   bin_lists_kernel<<<(a.count + 255) / 256, 256, 0, s>>>(a, d_bounds, nb, d_counts, d_lists, a.count);
   return cudaGetLastError();
@@ -904,6 +904,7 @@ cudaError_t launch_bin_lists(const PruneArgs& a, const uint32_t* d_bounds, int n
 // tensor-core tile (the prep kernel's Gram tile was 3.8% tensor-pipe busy on
 // these lists, barrier stalls 24%: profiles/r01e_prune_prep_reprune_c1.txt).
 constexpr int kSmallU = 4;
+constexpr int kSmallU2 = 2;  // the lists with at most this many get the smaller instance
 
 template <int E>
 __device__ __forceinline__ int dot_chunk(const uint4& a, const uint4& b, int acc) {
@@ -936,7 +937,9 @@ __device__ __forceinline__ bool cull_test(int rule, float alpha, float di, float
   return rule == 0 ? __fmul_rn(alpha, via) <= dj : via < __fmul_rn(alpha, di);
 }
 
-template <int E, int M, int LPR, int CPL>
+// KU: the most non-prefix entries a list of this instance has (2 or KU: the
+// smaller instance holds fewer rows and sums in registers)
+template <int E, int M, int LPR, int CPL, int KU>
 __global__ void __launch_bounds__(128) reprune_small_kernel(const PruneArgs a) {
   constexpr int RPP = 32 / LPR;  // rows per warp pass (one per lane group)
   const int lane = threadIdx.x & 31;
@@ -952,15 +955,15 @@ __global__ void __launch_bounds__(128) reprune_small_kernel(const PruneArgs a) {
     const uint32_t p = a.points[l];
     const uint64_t beg = a.begins ? a.begins[l] : uint64_t(l) * a.fixed_stride;
     const uint32_t S = min(static_cast<uint32_t>(a.spre[p - a.out_base]), m);
-    const uint32_t nu = m - S;  // <= kSmallU (binned by the host), S <= 64
+    const uint32_t nu = m - S;  // <= KU (binned by the host), S <= 64
     // ids: S entries two per lane (index lane, lane + 32); the u entries in every lane
     const uint32_t s0 = lane < S ? __ldg(a.cand_ids + beg + lane) : kNone;
     const uint32_t s1 = lane + 32 < S ? __ldg(a.cand_ids + beg + 32 + lane) : kNone;
-    uint32_t uid[kSmallU];
+    uint32_t uid[KU];
 #pragma unroll
-    for (int i = 0; i < kSmallU; i++) uid[i] = i < static_cast<int>(nu) ? __ldg(a.cand_ids + beg + S + i) : kNone;
+    for (int i = 0; i < KU; i++) uid[i] = i < static_cast<int>(nu) ? __ldg(a.cand_ids + beg + S + i) : kNone;
     // the lane's chunks of t's row and of the u rows, their norms and d(t, u_i)
-    uint4 qt[CPL], qu[kSmallU][CPL];
+    uint4 qt[CPL], qu[KU][CPL];
     bool chv[CPL];
 #pragma unroll
     for (int c = 0; c < CPL; c++) {
@@ -968,17 +971,17 @@ __global__ void __launch_bounds__(128) reprune_small_kernel(const PruneArgs a) {
       chv[c] = ch < nch;
       qt[c] = chv[c] ? __ldg(reinterpret_cast<const uint4*>(a.data + uint64_t(p) * a.stride) + ch) : make_uint4(0, 0, 0, 0);
 #pragma unroll
-      for (int i = 0; i < kSmallU; i++)
+      for (int i = 0; i < KU; i++)
         qu[i][c] = (chv[c] && uid[i] != kNone)
                        ? __ldg(reinterpret_cast<const uint4*>(a.data + uint64_t(uid[i]) * a.stride) + ch)
                        : make_uint4(0, 0, 0, 0);
     }
-    int nt = 0, nuv[kSmallU], dtu[kSmallU], duu[kSmallU][kSmallU];
+    int nt = 0, nuv[KU], dtu[KU], duu[KU][KU];
 #pragma unroll
     for (int c = 0; c < CPL; c++) nt = dot_chunk<E>(qt[c], qt[c], nt);
     nt = group_sum<LPR>(nt);
 #pragma unroll
-    for (int i = 0; i < kSmallU; i++) {
+    for (int i = 0; i < KU; i++) {
       int n = 0, d = 0;
 #pragma unroll
       for (int c = 0; c < CPL; c++) {
@@ -988,7 +991,7 @@ __global__ void __launch_bounds__(128) reprune_small_kernel(const PruneArgs a) {
       nuv[i] = group_sum<LPR>(n);
       dtu[i] = group_sum<LPR>(d);
 #pragma unroll
-      for (int j = 0; j < kSmallU; j++) {
+      for (int j = 0; j < KU; j++) {
         int x = 0;
         if (j > i) {
 #pragma unroll
@@ -998,18 +1001,18 @@ __global__ void __launch_bounds__(128) reprune_small_kernel(const PruneArgs a) {
         duu[i][j] = x;
       }
     }
-    float du_t[kSmallU];  // d(t, u_i)
+    float du_t[KU];  // d(t, u_i)
 #pragma unroll
-    for (int i = 0; i < kSmallU; i++) du_t[i] = pair_dist<M>(nt, nuv[i], dtu[i]);
+    for (int i = 0; i < KU; i++) du_t[i] = pair_dist<M>(nt, nuv[i], dtu[i]);
     // S rows: lane group g takes rows g, g + RPP, ...; per row the norm and the
     // dots with t and the u rows, reduced over the group's lanes; lane
     // (row & 31) keeps the row's values (rows r and r + 32 of the same lane)
     float dts[2] = {0.0f, 0.0f};              // d(t, s)
-    float dus[2][kSmallU];                     // d(u_i, s)
+    float dus[2][KU];                     // d(u_i, s)
 #pragma unroll
     for (int h = 0; h < 2; h++)
 #pragma unroll
-      for (int i = 0; i < kSmallU; i++) dus[h][i] = 0.0f;
+      for (int i = 0; i < KU; i++) dus[h][i] = 0.0f;
     // UU rows per lane group in flight; the sums reduced with the transposed
     // butterfly (lane sub of group g ends with row g*UU + (sub mod UU))
     constexpr int UU = LPR >= 4 ? 4 : LPR;
@@ -1025,43 +1028,43 @@ __global__ void __launch_bounds__(128) reprune_small_kernel(const PruneArgs a) {
           x[u][c] = (r < S && chv[c]) ? __ldg(reinterpret_cast<const uint4*>(a.data + uint64_t(id) * a.stride) + sub + c * LPR)
                                       : make_uint4(0, 0, 0, 0);
       }
-      int ns[UU], dt[UU], du[kSmallU][UU];
+      int ns[UU], dt[UU], du[KU][UU];
 #pragma unroll
       for (int u = 0; u < UU; u++) {
         ns[u] = 0;
         dt[u] = 0;
 #pragma unroll
-        for (int i = 0; i < kSmallU; i++) du[i][u] = 0;
+        for (int i = 0; i < KU; i++) du[i][u] = 0;
 #pragma unroll
         for (int c = 0; c < CPL; c++) {
           ns[u] = dot_chunk<E>(x[u][c], x[u][c], ns[u]);
           dt[u] = dot_chunk<E>(qt[c], x[u][c], dt[u]);
 #pragma unroll
-          for (int i = 0; i < kSmallU; i++) du[i][u] = dot_chunk<E>(qu[i][c], x[u][c], du[i][u]);
+          for (int i = 0; i < KU; i++) du[i][u] = dot_chunk<E>(qu[i][c], x[u][c], du[i][u]);
         }
       }
       const int ns_g = transpose_reduce<LPR, UU>(ns, sub);
       const int dt_g = transpose_reduce<LPR, UU>(dt, sub);
-      int du_g[kSmallU];
+      int du_g[KU];
 #pragma unroll
-      for (int i = 0; i < kSmallU; i++) du_g[i] = transpose_reduce<LPR, UU>(du[i], sub);
+      for (int i = 0; i < KU; i++) du_g[i] = transpose_reduce<LPR, UU>(du[i], sub);
       // lane (row & 31) takes its row's sums (row r0 + g*UU + u sits in lane g*LPR + u)
       const int j = lane - static_cast<int>(r0 & 31u);
       const bool mine = j >= 0 && j < PASS && r0 + j < S;
       const int src = mine ? (j / UU) * LPR + (j % UU) : 0;
       const int ns_r = __shfl_sync(FULL, ns_g, src), dt_r = __shfl_sync(FULL, dt_g, src);
-      int du_r[kSmallU];
+      int du_r[KU];
 #pragma unroll
-      for (int i = 0; i < kSmallU; i++) du_r[i] = __shfl_sync(FULL, du_g[i], src);
+      for (int i = 0; i < KU; i++) du_r[i] = __shfl_sync(FULL, du_g[i], src);
       if (mine) {  // (static indices: the arrays stay in registers)
         if (r0 >= 32) {
           dts[1] = pair_dist<M>(nt, ns_r, dt_r);
 #pragma unroll
-          for (int i = 0; i < kSmallU; i++) dus[1][i] = pair_dist<M>(nuv[i], ns_r, du_r[i]);
+          for (int i = 0; i < KU; i++) dus[1][i] = pair_dist<M>(nuv[i], ns_r, du_r[i]);
         } else {
           dts[0] = pair_dist<M>(nt, ns_r, dt_r);
 #pragma unroll
-          for (int i = 0; i < kSmallU; i++) dus[0][i] = pair_dist<M>(nuv[i], ns_r, du_r[i]);
+          for (int i = 0; i < KU; i++) dus[0][i] = pair_dist<M>(nuv[i], ns_r, du_r[i]);
         }
       }
     }
@@ -1069,9 +1072,9 @@ __global__ void __launch_bounds__(128) reprune_small_kernel(const PruneArgs a) {
     // the general kernel (flagged through too_long; never seen in the tests)
     const uint64_t ks0 = lane < S ? make_key(dts[0], s0) : kMaxKey;
     const uint64_t ks1 = lane + 32 < S ? make_key(dts[1], s1) : kMaxKey;
-    uint64_t ku[kSmallU];
+    uint64_t ku[KU];
 #pragma unroll
-    for (int i = 0; i < kSmallU; i++) ku[i] = uid[i] != kNone && uid[i] != p ? make_key(du_t[i], uid[i]) : kMaxKey;
+    for (int i = 0; i < KU; i++) ku[i] = uid[i] != kNone && uid[i] != p ? make_key(du_t[i], uid[i]) : kMaxKey;
     {
       const uint64_t nx = __shfl_down_sync(FULL, ks0, 1);
       const uint64_t n32 = __shfl_sync(FULL, ks1, 0);
@@ -1083,26 +1086,26 @@ __global__ void __launch_bounds__(128) reprune_small_kernel(const PruneArgs a) {
       }
     }
     // u entries in key order; each one's count of S keys below it
-    int ord[kSmallU];
-    uint32_t below[kSmallU];
+    int ord[KU];
+    uint32_t below[KU];
 #pragma unroll
-    for (int i = 0; i < kSmallU; i++) {
+    for (int i = 0; i < KU; i++) {
       int r = 0;
 #pragma unroll
-      for (int j = 0; j < kSmallU; j++) r += ku[j] < ku[i] ? 1 : 0;
+      for (int j = 0; j < KU; j++) r += ku[j] < ku[i] ? 1 : 0;
       ord[i] = r;
       below[i] = __popc(__ballot_sync(FULL, ks0 < ku[i])) + __popc(__ballot_sync(FULL, ks1 < ku[i]));
     }
     // the walk: u entries in key order; S entries culled only by selected u's
     bool cs0 = lane >= S, cs1 = lane + 32 >= S;  // culled (or absent)
-    bool selu[kSmallU];
+    bool selu[KU];
 #pragma unroll
-    for (int i = 0; i < kSmallU; i++) selu[i] = false;
+    for (int i = 0; i < KU; i++) selu[i] = false;
     bool full = false;
 #pragma unroll
-    for (int o = 0; o < kSmallU; o++) {
+    for (int o = 0; o < KU; o++) {
 #pragma unroll
-      for (int k = 0; k < kSmallU; k++) {  // k: the u entry of rank o (warp-uniform test)
+      for (int k = 0; k < KU; k++) {  // k: the u entry of rank o (warp-uniform test)
         if (ord[k] != o || ku[k] == kMaxKey || full) continue;
         const uint32_t bk = below[k];
         // selected S entries before it (S index < bk), and whether one culls it
@@ -1113,7 +1116,7 @@ __global__ void __launch_bounds__(128) reprune_small_kernel(const PruneArgs a) {
         uint32_t before = __popc(__ballot_sync(FULL, e0)) + __popc(__ballot_sync(FULL, e1));
         c = __any_sync(FULL, c);
 #pragma unroll
-        for (int j = 0; j < kSmallU; j++) {
+        for (int j = 0; j < KU; j++) {
           if (j == k || !selu[j] || ord[j] >= o) continue;
           before++;
           const int dij = j < k ? duu[j][k] : duu[k][j];
@@ -1140,15 +1143,15 @@ __global__ void __launch_bounds__(128) reprune_small_kernel(const PruneArgs a) {
     const uint32_t lt = (1u << lane) - 1u;
     uint32_t nsel = __popc(b0) + __popc(b1);
 #pragma unroll
-    for (int i = 0; i < kSmallU; i++) nsel += selu[i] ? 1u : 0u;
+    for (int i = 0; i < KU; i++) nsel += selu[i] ? 1u : 0u;
     nsel = min(nsel, R);
     auto selu_before = [&](uint32_t sidx) {  // selected u entries sorting before S index sidx
       uint32_t n = 0;
 #pragma unroll
-      for (int i = 0; i < kSmallU; i++) n += (selu[i] && below[i] <= sidx) ? 1u : 0u;
+      for (int i = 0; i < KU; i++) n += (selu[i] && below[i] <= sidx) ? 1u : 0u;
       return n;
     };
-    GANN_CHECK(S <= 64 && nu <= kSmallU);
+    GANN_CHECK(S <= 64 && nu <= KU);
     if (!cs0) {
       const uint32_t oi = __popc(b0 & lt) + selu_before(lane);
       if (oi < R) orow[oi] = s0;
@@ -1160,18 +1163,18 @@ __global__ void __launch_bounds__(128) reprune_small_kernel(const PruneArgs a) {
     if (lane == 0) {
       auto lowmask = [](uint32_t k) { return k >= 32 ? 0xFFFFFFFFu : (1u << k) - 1u; };
 #pragma unroll
-      for (int i = 0; i < kSmallU; i++) {
+      for (int i = 0; i < KU; i++) {
         if (!selu[i]) continue;
         uint32_t oi = 0;  // selected S below it + selected u before it
         oi += __popc(b0 & lowmask(below[i]));
         oi += below[i] > 32 ? __popc(b1 & lowmask(below[i] - 32)) : 0u;
 #pragma unroll
-        for (int j = 0; j < kSmallU; j++) oi += (selu[j] && ord[j] < ord[i]) ? 1u : 0u;
+        for (int j = 0; j < KU; j++) oi += (selu[j] && ord[j] < ord[i]) ? 1u : 0u;
         if (oi < R) orow[oi] = uid[i];
       }
       if (a.stats) {
-        atomicAdd(a.stats + kStPruneLists, 1ull);
-        atomicAdd(a.stats + kStPruneCands, static_cast<unsigned long long>(m));
+        atomicAdd(stat_slot(a.stats) + kStPruneLists, 1ull);
+        atomicAdd(stat_slot(a.stats) + kStPruneCands, static_cast<unsigned long long>(m));
       }
     }
     for (uint32_t i = nsel + lane; i < R; i += 32) orow[i] = kNone;
@@ -1422,9 +1425,9 @@ __global__ void __launch_bounds__(NT) prune_chunked_kernel(const PruneArgs a) {
       if (a.n_out) a.n_out[l] = nsel;
       if (a.spre && !a.out_rows) a.spre[p - a.out_base] = static_cast<uint8_t>(nsel < 255 ? nsel : 255);
       if (a.stats) {
-        atomicAdd(a.stats + kStPruneLists, 1ull);
-        atomicAdd(a.stats + kStPruneCands, static_cast<unsigned long long>(m));
-        atomicAdd(a.stats + kStPruneEvals, static_cast<unsigned long long>(evals) + sh_evals);
+        atomicAdd(stat_slot(a.stats) + kStPruneLists, 1ull);
+        atomicAdd(stat_slot(a.stats) + kStPruneCands, static_cast<unsigned long long>(m));
+        atomicAdd(stat_slot(a.stats) + kStPruneEvals, static_cast<unsigned long long>(evals) + sh_evals);
       }
     }
     __syncthreads();
@@ -1432,13 +1435,17 @@ __global__ void __launch_bounds__(NT) prune_chunked_kernel(const PruneArgs a) {
 }
 
 uint32_t reprune_small_max_u() { return kSmallU; }
+uint32_t reprune_small_low_u() { return kSmallU2; }
 
 namespace {
 template <int E, int M, int LPR, int CPL>
 cudaError_t launch_small_geom(const PruneArgs& a, cudaStream_t s) {
   if (a.count == 0) return cudaSuccess;
   const uint32_t blocks = std::min<uint32_t>((a.count + 3) / 4, 148u * 16u);
-  reprune_small_kernel<E, M, LPR, CPL><<<blocks, 128, 0, s>>>(a);
+  if (a.small_u <= kSmallU2)
+    reprune_small_kernel<E, M, LPR, CPL, kSmallU2><<<blocks, 128, 0, s>>>(a);
+  else
+    reprune_small_kernel<E, M, LPR, CPL, kSmallU><<<blocks, 128, 0, s>>>(a);
   return cudaGetLastError();
 }
 template <int E, int M>
@@ -1624,7 +1631,10 @@ namespace {
 template <int E, int M, int LPR, int CPL>
 void preload_prune_one() {
   touch_kernel(prune_kernel<E, M, LPR, CPL, 32>);
-  if (E != kF32) touch_kernel(reprune_small_kernel<E, M, LPR, CPL>);
+  if (E != kF32) {
+    touch_kernel(reprune_small_kernel<E, M, LPR, CPL, kSmallU>);
+    touch_kernel(reprune_small_kernel<E, M, LPR, CPL, kSmallU2>);
+  }
   touch_kernel(prune_chunked_kernel<E, M, LPR, CPL, 256>);
   if (E != kF32) {
     touch_kernel(prune_prep_kernel<E, M, 4, 0>);
