@@ -939,8 +939,14 @@ __device__ __forceinline__ bool cull_test(int rule, float alpha, float di, float
 
 // KU: the most non-prefix entries a list of this instance has (2 or KU: the
 // smaller instance holds fewer rows and sums in registers)
+#ifndef GANN_RS_MINB4
+#define GANN_RS_MINB4 6  // resident CTAs the KU = 4 instance's registers are budgeted for (6: 80 registers, 56 B spilled; measured: 4 CTAs at 128 registers re-prune phase 681 ms, 5: 684, 6: 667)
+#endif
+#ifndef GANN_RS_MINB2
+#define GANN_RS_MINB2 8  // ... the KU = 2 instance's (8: 64 registers; 7 CTAs at 72: 681 ms, 8: 661)
+#endif
 template <int E, int M, int LPR, int CPL, int KU>
-__global__ void __launch_bounds__(128) reprune_small_kernel(const PruneArgs a) {
+__global__ void __launch_bounds__(128, KU > 2 ? GANN_RS_MINB4 : GANN_RS_MINB2) reprune_small_kernel(const PruneArgs a) {
   constexpr int RPP = 32 / LPR;  // rows per warp pass (one per lane group)
   const int lane = threadIdx.x & 31;
   const int sub = lane & (LPR - 1), grp = lane / LPR;
