@@ -133,3 +133,28 @@ def test_batch_wide_table(oracle, batch_env, L):
     want = oracle.beam_search(adj, start, data, qs, L, L, 0.0, visited_mode=1, vcap=vcap, workers=4)
     got = idx.search(qs, g.SearchParams(L, L, 0.0), vcap=vcap)
     _check(got, want, len(qs))
+
+
+@pytest.mark.parametrize("n,R", [(2, 1), (9, 3), (40, 8), (300, 33)])
+def test_batch_tiny_graphs(oracle, batch_env, n, R):
+    """Graphs smaller than the beam (it never fills), rows with one id, an odd degree bound,
+    and a vertex without neighbours: the batch kernel's edge cases against the reference."""
+    g = _g()
+    rng = np.random.default_rng(n)
+    data = rng.integers(0, 256, (n, 20)).astype(np.uint8)
+    qs = rng.integers(0, 256, (37, 20)).astype(np.uint8)
+    adj = np.full((n, R), 0xFFFFFFFF, np.uint32)
+    for v in range(n - 1):  # the last vertex keeps an empty row
+        nb = rng.permutation([u for u in range(n) if u != v])[: rng.integers(1, R + 1)]
+        adj[v, : len(nb)] = nb
+    idx = g.Index(data, "l2", R)
+    idx.import_graph(adj, 0)
+    for L in (1, 5, 64, 400):
+        want = oracle.beam_search(adj, 0, data, qs, L, L, 0.0, visited_mode=1, vcap=2 * n + 8, workers=2)
+        got = idx.search(qs, g.SearchParams(L, L, 0.0), k_out=min(L, 10), vcap=2 * n + 8)
+        kk = min(L, 10)
+        assert (got.ids == want["ids"][:, :kk]).all()
+        assert (got.n_visited == want["n_visited"]).all()
+        for i in range(len(qs)):
+            nv = int(want["n_visited"][i])
+            assert (got.visited_ids[i, :nv] == want["visited_ids"][i, :nv]).all()
