@@ -659,6 +659,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, GANN_BATCH_MINB)
     if (lane == 0) q = atomicAdd(a.next_query, 1u);
     q = __shfl_sync(FULL, q, 0);
   }
+  // the region's next owner (any warp on the device) clears it before use: this
+  // warp's last table stores must be visible device-wide before the release
+  __threadfence();
+  __syncwarp();
   if (lane == 0) atomicAnd(a.gtab_busy + g2_region / 32, ~(1u << (g2_region % 32)));
 }
 

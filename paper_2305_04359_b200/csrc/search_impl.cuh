@@ -746,7 +746,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32,
     if (lane == 0) q = atomicAdd(a.next_query, 1u);
     q = __shfl_sync(0xFFFFFFFFu, q, 0);
   }
-  if (G2 && g2 && lane == 0) atomicAnd(a.gtab_busy + g2_region / 32, ~(1u << (g2_region % 32)));
+  if (G2 && g2) {
+    // the region's next owner clears it before use: this warp's last table
+    // stores must be visible device-wide before the release
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) atomicAnd(a.gtab_busy + g2_region / 32, ~(1u << (g2_region % 32)));
+  }
 }
 
 }  // namespace gann
