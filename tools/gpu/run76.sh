@@ -1,0 +1,10 @@
+set -x
+mkdir -p gpurun_out
+python -m pytest tests -m gpu -q -rf -p no:cacheprovider > gpurun_out/t_gpu.log 2>&1; tail -3 gpurun_out/t_gpu.log
+python -c "import __graft_entry__ as e; e.smoke()" > gpurun_out/smoke.log 2>&1; tail -1 gpurun_out/smoke.log
+python bench.py --steps 20 --warmup 5 > gpurun_out/bench_c1.jsonl 2> gpurun_out/bench_c1.err; tail -2 gpurun_out/bench_c1.err
+python - <<'PY'
+import json
+d=json.loads(open('gpurun_out/bench_c1.jsonl').read().strip().splitlines()[-1])
+print(d['value'], d['ms_per_step'], d['config'].get('L_search'), d['roofline']['frac'], d['e2e']['value'], d['build']['points_per_s'], d['parity']['graph_sha256'], d['parity']['ids_sha256'])
+PY
