@@ -598,6 +598,22 @@ def run_ours(args):
     torch.cuda.synchronize()
     xstats = idx.stats()
     per_launch_bytes = search_bytes(xstats, d * s_el, nq, k)
+    # the same accounting at the last beam of the BASELINE sweep (context for the
+    # headline: the kernel's fraction of the peak falls as the beam grows)
+    sweep_end = None
+    last = next((c for c in reversed(S["curve"]) if c["L"] != chosen), None) if S.get("curve") else None
+    if last is not None:
+        idx.reset_stats()
+        tmp_ids, tmp_d = torch.empty_like(out_ids), torch.empty_like(out_d)  # (out_ids keeps the headline's ids)
+        idx.search_device(qdev.data_ptr(), nq, g.SearchParams(last["L"], last["L"], 0.0), k, tmp_ids.data_ptr(),
+                          tmp_d.data_ptr(), stream=stream, visited_mode="exact")
+        torch.cuda.synchronize()
+        lb = search_bytes(idx.stats(), d * s_el, nq, k)
+        la = lb / (last["ms_per_launch"] / 1e3) / 1e9
+        sweep_end = {"L": last["L"], "recall@10": last["recall@10"], "avg_launch_ms": last["ms_per_launch"],
+                     "algorithmic_bytes_per_launch": round(lb), "achieved": round(la, 1),
+                     "frac": round(la / peaks()[0], 4),
+                     "kernel": "search_batch_kernel" if last["L"] >= 320 else "search_kernel"}
     # sustained time per launch: the K launches' elapsed time / K (with 2
     # streams a launch's own event span includes its overlap with neighbours)
     avg_launch_s = total_ms / args.steps / 1e3
@@ -731,7 +747,9 @@ def run_ours(args):
                             "step searches its whole batch; value = K*nq / elapsed of all K" if nstreams > 1
                             else "serial launches"),
         "roofline": {
-            "bound": "hbm", "kernel": "search_kernel", "achieved": round(achieved, 1), "peak": peak,
+            "bound": "hbm",
+            "kernel": "search_batch_kernel" if sstats.get("merges", 0) else "search_kernel",  # the batch kernel counts its steps
+            "achieved": round(achieved, 1), "peak": peak,
             "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
             "frac_nominal_8tbs": round(achieved / 8000.0, 4),
             "algorithmic_bytes_per_launch": round(per_launch_bytes),
@@ -747,6 +765,7 @@ def run_ours(args):
             "distinct_evals_per_query": round(xstats["evaluations"] / nq, 1),
             "evals_per_query_fast_filter": round(sstats["evaluations"] / (nq * args.steps), 1),
             "expansions_per_query": round(xstats["expansions"] / nq, 1),
+            "at_sweep_end": sweep_end,
         },
         "cpu_baseline": cpu,
         "e2e": {"value": round(world * nq * args.steps / e2e_s, 1), "unit": "queries/s",
