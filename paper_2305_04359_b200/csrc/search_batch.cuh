@@ -676,44 +676,42 @@ cudaError_t launch_batch(const SearchArgs& a, cudaStream_t s) {
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   if ((e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess) return e;
-  int wpb = kWarpsPerBlock;
-  while (wpb > 1 && size_t(per_warp) * wpb > static_cast<size_t>(optin)) wpb >>= 1;
   const bool fit = a.stride == uint64_t(16) * LPR * CPL;
   auto k = fit ? search_batch_kernel<E, M, LPR, CPL, true> : search_batch_kernel<E, M, LPR, CPL, false>;
-  if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                size_t(per_warp) * wpb > 48 * 1024 ? static_cast<int>(size_t(per_warp) * wpb)
-                                                                   : 48 * 1024)) != cudaSuccess)
-    return e;
   if (a.nq == 0) return cudaSuccess;
-  int per_sm = 0, sms = 0;
+  int sms = 0;
   if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+  if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, optin)) != cudaSuccess) return e;
   if ((e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared)) !=
       cudaSuccess)
     return e;
-  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, wpb * 32, size_t(per_warp) * wpb)) != cudaSuccess)
-    return e;
-  for (int w = wpb >> 1; w >= 1; w >>= 1) {
-    int ps = 0;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, k, w * 32, size_t(per_warp) * w)) != cudaSuccess)
-      return e;
-    if (ps * w > per_sm * wpb) {
-      per_sm = ps;
-      wpb = w;
-    }
-  }
-  // Shared memory and L1 share the SM's 256 KB, and the rows a step gathers
-  // are in flight through L1 lines: with the carve-out the resident CTAs'
-  // beams would take (6 CTAs at L = 832: 196 or 228 KB) the 28-60 KB left for
-  // L1 throttle the gathers (measured at c1, L = 832, 24 warps: 19.6 ms at
-  // 228 KB, 12.7 at 196, and 12.2 with 5 CTAs at 164 KB). So the CTA count is
-  // lowered until L1 keeps ~4 KB per resident warp, and the carve-out is the
-  // smallest that holds those CTAs (GANN_BATCH_CARVE: percent, overrides).
-  {
-    static const int kCarveKB[] = {8, 16, 32, 64, 100, 132, 164, 196, 228};
-    const size_t cta = size_t(per_warp) * wpb + 1024;
-    uint32_t l1_per_warp = 4096;
-    if (const char* lv = std::getenv("GANN_BATCH_L1KB")) l1_per_warp = static_cast<uint32_t>(std::atoi(lv)) * 1024u;  // experiment
-    int c = std::max(1, per_sm), carve = 228;
+  // CTA width (warps = queries per CTA; the kernel works per warp at any width)
+  // and resident CTAs per SM. Shared memory and L1 share the SM's 256 KB, and
+  // the rows a step gathers are in flight through L1 lines: with the carve-out
+  // the resident CTAs' beams would take (6 CTAs of 4 warps at L = 832: 196 or
+  // 228 KB) the 28-60 KB left for L1 throttle the gathers (measured at c1, L =
+  // 832, 24 warps: 19.6 ms at 228 KB, 12.7 at 196, and 12.2 with 5 CTAs at 164
+  // KB). So for each width the CTA count is lowered until L1 keeps ~4.5 KB per
+  // resident warp, with the smallest carve-out that holds those CTAs; the
+  // width with the most resident warps wins, on a tie the one that leaves more
+  // L1, then the narrower one down to 2 warps (CTAs of a finishing launch free
+  // their slots for the next launch sooner: 9.33 -> 9.02 ms per pipelined step
+  // at L = 832; 1-warp CTAs pay the per-CTA kilobyte 4 times). GANN_BATCH_WPB / GANN_BATCH_CARVE
+  // (percent) / GANN_BATCH_L1KB override (experiments).
+  static const int kCarveKB[] = {8, 16, 32, 64, 100, 132, 164, 196, 228};
+  uint32_t l1_per_warp = 4608;  // 4.5 KB
+  if (const char* lv = std::getenv("GANN_BATCH_L1KB")) l1_per_warp = static_cast<uint32_t>(std::atoi(lv)) * 1024u;
+  int forced_w = 0;
+  if (const char* wv = std::getenv("GANN_BATCH_WPB")) forced_w = std::max(1, std::min(kWarpsPerBlock, std::atoi(wv)));
+  int wpb = 0, per_sm = 0, pct = 100, best_carve = 0;
+  for (int w = kWarpsPerBlock; w >= 1; w >>= 1) {
+    if (size_t(per_warp) * w > static_cast<size_t>(optin)) continue;
+    if (forced_w && w != forced_w && size_t(per_warp) * forced_w <= static_cast<size_t>(optin)) continue;
+    int c = 0;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k, w * 32, size_t(per_warp) * w)) != cudaSuccess) return e;
+    c = std::max(1, c);
+    const size_t cta = size_t(per_warp) * w + 1024;
+    int carve = 228;
     for (; c >= 1; c--) {
       carve = 228;
       for (int kb : kCarveKB)
@@ -721,15 +719,26 @@ cudaError_t launch_batch(const SearchArgs& a, cudaStream_t s) {
           carve = kb;
           break;
         }
-      if (c == 1 || size_t(256 - carve) * 1024 >= size_t(c) * wpb * l1_per_warp) break;
+      if (c == 1 || size_t(256 - carve) * 1024 >= size_t(c) * w * l1_per_warp) break;
     }
-    int pct = carve * 100 / 228;
-    if (const char* cv = std::getenv("GANN_BATCH_CARVE")) {
-      pct = std::atoi(cv);
-      c = per_sm;
+    // most resident warps; then most L1 left; then the narrower CTA (down to 2 warps)
+    const bool better = c * w > per_sm * wpb ||
+                        (c * w == per_sm * wpb && (carve < best_carve || (carve == best_carve && w >= 2)));
+    if (wpb == 0 || better) {
+      wpb = w;
+      per_sm = c;
+      best_carve = carve;
+      pct = carve * 100 / 228;
     }
+  }
+  if (wpb == 0) return cudaErrorInvalidValue;  // the host checked the beam against the shared memory
+  if (const char* cv = std::getenv("GANN_BATCH_CARVE")) {
+    pct = std::atoi(cv);
     if ((e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, pct)) != cudaSuccess) return e;
-    per_sm = std::min(per_sm, c);
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, wpb * 32, size_t(per_warp) * wpb)) != cudaSuccess)
+      return e;
+  } else if ((e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, pct)) != cudaSuccess) {
+    return e;
   }
   const size_t smem = size_t(per_warp) * wpb;
   const uint32_t want = (a.nq + wpb - 1) / wpb;
