@@ -1091,6 +1091,12 @@ int gann_build(gann_index* idx, uint32_t L, float alpha, int rule, uint64_t seed
       std::mt19937_64 rng(mix64(seed, 0x696e73657274ULL));
       std::shuffle(order.begin(), order.end(), rng);
     });
+    const bool trace_start = env_u32("GANN_TRACE_START", 0) != 0;  // host times of the start phase's steps
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto since = [&](std::chrono::steady_clock::time_point a) {
+      return std::chrono::duration<double, std::milli>(now() - a).count();
+    };
+    const auto ts0 = now();
     uint32_t start = 0;
     try {
       start = choose_start_dev(idx);
@@ -1099,6 +1105,8 @@ int gann_build(gann_index* idx, uint32_t L, float alpha, int rule, uint64_t seed
       throw;
     }
     idx->start = start;
+    const double t_start_vertex = since(ts0);
+    const auto ts1 = now();
     // size the per-batch scratch once, from the largest batch: a cudaFree /
     // cudaMalloc inside the loop stalls the device for tens of milliseconds
     try {
@@ -1106,7 +1114,13 @@ int gann_build(gann_index* idx, uint32_t L, float alpha, int rule, uint64_t seed
       for (auto [lo, hi] : batch_ranges(n, max_batch)) bmax = std::max(bmax, hi - lo);
       const uint32_t vcap = std::max<uint32_t>(64, 3 * L);
       const uint64_t pairs = uint64_t(bmax) * idx->R;
-      const uint64_t groups = std::min<uint64_t>(pairs, n);
+      // distinct targets of the largest batch's reverse pairs: at most min(pairs,
+      // n), but sizing for that worst case is mostly wasted allocation time (c1:
+      // 2.3-2.6M groups per 200k-point batch against a bound of 10M; 5.2 GB of
+      // merged-list scratch instead of 2.3 GB, ~100 ms of cudaMalloc in a cold
+      // build). A third of the pairs, grown on demand by apply_back / the prune
+      // launches if a batch does need more.
+      const uint64_t groups = std::min<uint64_t>(std::min<uint64_t>(pairs, n), std::max<uint64_t>(pairs / 3, bmax));
       idx->vis_ids.ensure(size_t(bmax) * vcap * 4);
       idx->vis_d.ensure(size_t(bmax) * vcap * 4);
       idx->nvis.ensure(size_t(bmax) * 4);
@@ -1130,7 +1144,11 @@ int gann_build(gann_index* idx, uint32_t L, float alpha, int rule, uint64_t seed
       shuffler.join();
       throw;
     }
+    const double t_alloc = since(ts1);
+    const auto ts2 = now();
     shuffler.join();
+    const double t_join = since(ts2);
+    const auto ts3 = now();
     if (host_shuffle) {
       std::iter_swap(order.begin(), std::find(order.begin(), order.end(), start));
       cu(cudaMemcpyAsync(idx->order.p, order.data(), n * 4, cudaMemcpyHostToDevice, idx->stream),
@@ -1151,6 +1169,9 @@ int gann_build(gann_index* idx, uint32_t L, float alpha, int rule, uint64_t seed
       cu(e, "shuffle from log");
     }
     t0.stop(idx, 0);
+    if (trace_start)
+      std::fprintf(stderr, "build start phase (host ms): start vertex %.1f, scratch allocation %.1f, wait for the swap log %.1f, order on the device %.1f\n",
+                   t_start_vertex, t_alloc, t_join, since(ts3));
     const uint32_t* d_order = idx->order.as<uint32_t>();
     const bool trace = env_u32("GANN_TRACE", 0) != 0;
     for (auto [lo, hi] : batch_ranges(n, max_batch)) {
