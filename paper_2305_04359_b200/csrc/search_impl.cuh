@@ -783,6 +783,7 @@ cudaError_t launch_one(const SearchArgs& a0, cudaStream_t s) {
   // further while that leaves more warps resident (large beams: 3 CTAs of 4
   // warps at 59 KB each waste 50 KB that 1-warp CTAs use)
   int wpb = kWarpsPerBlock;
+  if (const char* wv = std::getenv("GANN_SEARCH_WPB")) wpb = std::max(1, std::min(kWarpsPerBlock, std::atoi(wv)));  // experiment
   while (wpb > 1 && size_t(per_warp) * wpb > static_cast<size_t>(optin)) wpb >>= 1;
   // R = 64 fixed at compile time (measured): 16-lane rows -5% at L=200 (c2)
   // and a faster build search; 8-lane rows (c1): -1% for a serial launch at
@@ -818,7 +819,10 @@ cudaError_t launch_one(const SearchArgs& a0, cudaStream_t s) {
     int ps = 0;
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, k, w * 32, size_t(per_warp) * w)) != cudaSuccess)
       return e;
-    if (ps * w > per_sm * wpb) {
+    // as many resident warps in narrower CTAs: 2-warp CTAs win the tie (a
+    // finishing launch's slots free sooner for the next launch: the bench's
+    // pipelined sweep -2 to -3% per launch at L = 10..200, the build unchanged)
+    if (ps * w > per_sm * wpb || (w >= 2 && ps * w == per_sm * wpb)) {
       per_sm = ps;
       wpb = w;
     }
