@@ -498,7 +498,11 @@ SearchArgs base_search_args(gann_index* idx, uint32_t L, uint32_t k_gate, uint32
   // ids beyond the u16 remainders' reach (n > 2^(log2 + 15): 67M at the default
   // region size): the batch kernel's buckets hold two whole ids instead, in
   // the largest regions (GANN_GTAB_WIDE=1 forces it: tests)
-  const bool wide = batch && (idx->n > (uint64_t(1) << (glog2 + 15)) || env_u32("GANN_GTAB_WIDE", 0));
+  // beams from 1024 evaluate more ids than the default region remembers: the
+  // largest region there (c1, 11 -> 12: L = 1024 -2.8%, 2048 -5%, 4096 -7%, 8192 -12% per launch)
+  uint32_t blog2 = glog2;
+  if (batch && L >= 1024 && !std::getenv("GANN_GTAB_LOG2")) blog2 = kGtabLog2;
+  const bool wide = batch && (idx->n > (uint64_t(1) << (blog2 + 15)) || env_u32("GANN_GTAB_WIDE", 0));
   if (batch) {
     a.batch_eb = beb;
     a.batch_cm = bcm;
@@ -520,7 +524,7 @@ SearchArgs base_search_args(gann_index* idx, uint32_t L, uint32_t k_gate, uint32
     a.gtab = idx->gtab.as<uint64_t>();
     a.gtab_busy = idx->gtab_busy.as<uint32_t>();
     a.gtab_regions = idx->gtab_regions;
-    a.gtab_log2 = wide ? kGtabLog2 : glog2;
+    a.gtab_log2 = wide ? kGtabLog2 : (batch ? blog2 : glog2);
     a.gtab_wide = wide ? 1 : 0;
     a.gtab_keep = static_cast<int>(env_u32("GANN_GTAB_KEEP", 1));
 
